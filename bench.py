@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the Chebyshev-Hutchinson log-det hot path (BASELINE.json metric:
+probe*Chebyshev-steps/sec, HBM GB/s vs peak, log-det wall time at 25M vars).
+
+One bench "step" = one whole estimate on this GPU's probe shard: probe
+initialisation, `degree` fused Chebyshev steps per probe block, reductions, the
+moment all-reduce (N > 1) and the device accumulation of Gamma.  Default
+workload: BASELINE configs[3] (gmrf5000: d = 2.5e7, n = 100, m = 128 probes per
+GPU, k = 64) -- weak scaling over GPUs (m = 128 * N in total).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--k K]
+    python bench.py --impl reference ...    # the CPU oracle as the reference arm
+
+Under torchrun each rank drives one GPU; rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "probe*Chebyshev-steps/sec"
+UNIT = "probe-steps/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def _traffic_per_launch(workload, k):
+    """dram read+write bytes per step launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    e = j.get(f"{workload}/k{k}")
+    return float(e["dram_bytes_per_launch"]) if e else None
+
+
+def step_bytes(d, nnz, k, first=False):
+    """Algorithmic HBM bytes of one fused step launch over a block of k probes
+    (SURVEY §8(d)): matrix (val 8 + col 4 per nnz,
+    row_ptr 8 per row) once per block; W_cur read, W_prev read, W_next write
+    (8 B each per row and probe; no W_prev on the first step); sign bits."""
+    vec = (16 if first else 24) * d * k
+    return 12 * nnz + 8 * (d + 1) + vec + d * max(4, k // 8)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, bus_id=None):
+        self.rows, self.proc, self.bus_id = [], None, bus_id
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--query-gpu=pci.bus_id,{self.FIELDS}", "--format=csv,noheader,nounits",
+               "-lms", "200"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = self.rows
+        if self.bus_id is not None:
+            mine = [r for r in rows if r and self.bus_id.lower() in r[0].lower()]
+            rows = mine or rows
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) > 8 for i in range(4)
+                          if r[5 + i].lower() == "active"})
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": reasons}
+
+
+def build_workload(name):
+    wl = W.get_workload(name)
+    A, At = wl.matrices()
+    return wl, A, At
+
+
+# ------------------------------------------------------------------------- oracle (CPU) arm
+def oracle_sample(wl, A, steps_per_probe, probes, workers):
+    """Time the oracle AS IT STANDS on a bounded sample: `probes` probes x
+    `steps_per_probe` Chebyshev steps of the same workload, one probe per worker."""
+    import oracle
+    a, b = wl.a, wl.b
+    if a is None:
+        a, b = oracle.bounds_btb(A)
+    op = oracle.Op(wl.mode, A, wl.r1_c)
+    oracle.lib()
+    t0 = time.perf_counter()
+    oracle.moments(op, a, b, steps_per_probe, wl.seed, range(probes), workers=workers)
+    dt = time.perf_counter() - t0
+    return probes * steps_per_probe / dt, dt
+
+
+def _oracle_plan(wl, budget_s=20.0):
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 16 << 30
+    per_worker = 6 * 8 * wl.d  # probe + 3 work vectors (+ scratch) of d doubles
+    workers = max(1, min(cores, 64, int(0.5 * avail // max(per_worker, 1))))
+    nnz_per_row = 5 if wl.mode != "btb" else 18
+    est_step_s = wl.d * nnz_per_row * 2.5e-9 + wl.d * 3e-9  # ~single-core C loop
+    steps = int(max(1, min(wl.degree, budget_s / max(est_step_s, 1e-9))))
+    return workers, steps
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl, A, At = build_workload(args.workload)
+    workers, steps = _oracle_plan(wl, budget_s=args.ref_budget)
+    for _ in range(args.warmup):
+        oracle_sample(wl, A, 1, workers, workers)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt = oracle_sample(wl, A, steps, workers, workers)
+        vals.append(v)
+        times.append(dt)
+    value = float(np.median(vals))
+    sample = (f"{workers} probes x {steps} Chebyshev steps of {wl.name} (d={wl.d}) per bench step, "
+              f"one single-threaded oracle process per probe")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": wl.name, "d": wl.d, "degree": wl.degree,
+                                            "num_probes_per_step": workers, "steps_per_probe": steps},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_06394_b200 import dist as pdist
+    import paper_1503_06394_b200 as P
+
+    rank, world, local = pdist.init_from_env("nccl")
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    wl, A, At = build_workload(args.workload)
+    m_per_gpu = args.probes or wl.num_probes
+    m_total = m_per_gpu * world
+    k = args.k or (64 if m_per_gpu >= 64 else 32 if m_per_gpu >= 32 else 16 if m_per_gpu >= 16 else 8)
+
+    # CPU baseline first (fork-based pool before any CUDA context exists)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers, steps = _oracle_plan(wl, budget_s=args.ref_budget)
+        v, dt = oracle_sample(wl, A, steps, workers, workers)
+        cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
+               "sample": f"{workers} probes x {steps} Chebyshev steps of {wl.name} (d={wl.d}), "
+                         f"one single-threaded oracle process per probe, {dt:.1f} s"}
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dA = P.DeviceCSR.from_host(A, dev)
+    dAt = P.DeviceCSR.from_host(At, dev) if At is not None else None
+    op = P.Operator(wl.mode, dA, dAt, wl.r1_c)
+    a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+    group = None
+    sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, group=group)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        sh.run()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events on the launching stream; max over ranks)
+    clocks = ClockSampler(None)
+    if rank == 0:
+        props = torch.cuda.get_device_properties(dev)
+        bus = getattr(props, "pci_bus_id", None)
+        clocks.bus_id = None if bus is None else f":{int(bus):02X}:00."
+        clocks.start()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    n_launch0 = P.launch_count()
+    P.profile_begin()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        gp, stats = sh.run()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    step_ms_total, step_launches = P.profile_end()
+    launches = P.launch_count() - n_launch0
+    clk = clocks.stop() if rank == 0 else None
+    elapsed = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(elapsed, op=dist.ReduceOp.MAX)
+    t_ms = float(elapsed.item())
+    st = stats.cpu().numpy()
+
+    # ---- end-to-end through the public C ABI with HOST buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, torch, dist)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    units = m_total * wl.degree * args.steps
+    value = units / (t_ms / 1e3)
+    hbm, peak_kind = _peaks()
+    d, nnz = wl.d, (A.nnz + (At.nnz if At is not None else 0))
+    blocks = math.ceil(m_per_gpu / k)
+    # algorithmic bytes of all step launches in the timed region (per GPU)
+    per_est = blocks * (step_bytes(d, A.nnz if wl.mode != "btb" else At.nnz, k, first=True)
+                        + (wl.degree - 1) * step_bytes(d, A.nnz if wl.mode != "btb" else At.nnz, k))
+    avg_launch_ms = step_ms_total / max(step_launches, 1)
+    bytes_per_launch = per_est / (blocks * wl.degree)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "peak_kind": peak_kind, "kernel": f"cheb_step_kernel<{k},{wl.mode}>",
+            "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
+            "step_kernel_share": step_ms_total / t_ms,
+            "traffic": _traffic_per_launch(wl.name, k)}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": d,
+                      "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total,
+                      "probes_per_gpu": m_per_gpu, "probe_block": k, "a": a, "b": b,
+                      "parallelism": f"probe-dp{world}", "l2": "inputs larger than L2 (W blocks "
+                      f"{2 * d * k * 8 / 1e9:.1f} GB/GPU), no flush needed",
+                      "logdet_wall_s": t_ms / args.steps / 1e3, "gamma": float(st[0]),
+                      "stderr": float(st[1])},
+           "roofline": roof, "gpu_launches": int(launches),
+           "gpu_launches_per_step": launches / args.steps, "clocks": clk, "cpu_baseline": cpu,
+           "e2e": e2e}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, torch, dist):
+    """Same metric end to end: every step copies the operator from pinned host
+    memory to the device, runs the estimate through the public API and reads the
+    result back to the host."""
+    def pin(x):
+        t = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+        return t
+
+    class HostCSR:
+        pass
+
+    def host_csr(M):
+        h = HostCSR()
+        h.n_rows, h.n_cols = M.n_rows, M.n_cols
+        h.row_ptr, h.col_idx, h.val = pin(M.row_ptr), pin(M.col_idx), pin(M.val)
+        return h
+
+    hA = host_csr(A)
+    hAt = host_csr(At) if At is not None else None
+    h2d = sum(t.numel() * t.element_size() for h in (hA, hAt) if h is not None
+              for t in (h.row_ptr, h.col_idx, h.val))
+    m_total = m_per_gpu * world
+    steps = max(1, min(args.steps, args.e2e_steps))
+    if world == 1:
+        def one():
+            r = P.logdet_host(wl.mode, hA, a, b, wl.degree, m_total, seed=wl.seed, k=k, At=hAt,
+                              c=wl.r1_c)
+            return r
+        one()  # warm
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        dt = time.perf_counter() - t0
+        d2h = 8 * (3 + m_total)
+    else:
+        def one():
+            dA = P.DeviceCSR(hA.n_rows, hA.n_cols, hA.row_ptr.to(dev, non_blocking=True),
+                             hA.col_idx.to(dev, non_blocking=True), hA.val.to(dev, non_blocking=True))
+            dAt = None
+            if hAt is not None:
+                dAt = P.DeviceCSR(hAt.n_rows, hAt.n_cols, hAt.row_ptr.to(dev, non_blocking=True),
+                                  hAt.col_idx.to(dev, non_blocking=True), hAt.val.to(dev, non_blocking=True))
+            op = P.Operator(wl.mode, dA, dAt, wl.r1_c)
+            sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed)
+            gp, stats = sh.run()
+            return stats.cpu()
+        one()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        torch.cuda.synchronize()
+        dist.barrier()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dt = float(dt.item())
+        d2h = 8 * 3
+    return {"value": m_total * wl.degree * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": "cheb_logdet_host (C ABI, pinned host CSR)" if world == 1 else
+                   "ShardedEstimator after pinned H2D of the CSR",
+            "includes": "H2D CSR copy, workspace alloc, all steps, D2H result"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="gmrf5000")
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--probes", type=int, default=0, help="probes per GPU (default: the config's m)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of oracle work per sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,160 @@
+/*
+ * cheb_logdet.h -- C ABI of the B200-native Chebyshev-Hutchinson log-determinant
+ * hot path (arXiv 1503.06394).  Library: paper_1503_06394_b200/libchebld.so.
+ *
+ * What it computes (PAPER.md, "P:n" = line n):
+ *   Gamma ~= log det M for a symmetric positive-definite operator M whose
+ *   spectrum lies in [a, b]:
+ *     alpha = 2/(b-a), beta = (b+a)/(b-a), Ã = alpha*M - beta*I          (G1/G3)
+ *     c_j   = Chebyshev interpolation coefficients of log on [a,b]
+ *     v_p   = Rademacher probes, v_p[i] = -1 iff bit 63 of
+ *             splitmix64(seed, p*d + i + 1) is set                        (G6)
+ *     w_0 = v, w_1 = Ã v, w_{j+1} = 2 Ã w_j - w_{j-1}                    (Alg. 1)
+ *     mu_{p,j} = v_p^T w_j ;  Gamma_p = sum_j c_j mu_{p,j} ;
+ *     Gamma = (1/m) sum_p Gamma_p                                         (G7)
+ *   Operator modes:
+ *     CL_OP_CSR        M = A
+ *     CL_OP_CSR_RANK1  M = A + c u u^T   (u = all ones if r1_u == NULL;
+ *                      spanning trees: log tau = Gamma - log(c N^2))      (BASELINE configs[1])
+ *     CL_OP_BTB        M = B^T B applied as B^T (B w), never formed;
+ *                      log|det B| = Gamma / 2                             (Alg. 2)
+ *
+ * Conventions
+ *   - All functions return 0 (CL_OK) on success or a negative CL_E* code, never
+ *     throw, and set a thread-local message readable with cheb_last_error().
+ *   - All validation runs before any device work; outputs are written only on
+ *     success (device outputs of the asynchronous calls: on successful launch).
+ *   - The caller owns every buffer passed in; the library never frees or keeps
+ *     a pointer past the call.  Only cheb_logdet / cheb_logdet_host /
+ *     cheb_probes / cheb_bounds_btb allocate (and free) device memory.
+ *   - Matrices are canonical CSR: row_ptr int64[n_rows+1] (row_ptr[0] = 0),
+ *     col_idx int32[nnz] sorted & unique within a row, val fp64[nnz].
+ *   - Probe-block layout on the device: W[d][k] fp64 row-major, the k probes of a
+ *     block contiguous; k in {8, 16, 32, 64}.
+ */
+#ifndef CHEB_LOGDET_H
+#define CHEB_LOGDET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CL_OK 0
+#define CL_EINVAL (-1)     /* bad scalar argument / NULL pointer / bad k          */
+#define CL_EDIM (-2)       /* non-square M, B^T not the transpose shape, d >= 2^31 */
+#define CL_ENOMEM (-3)     /* workspace too small or cudaMalloc failed             */
+#define CL_ECUDA (-4)      /* CUDA runtime error (message has the CUDA string)     */
+#define CL_ENONFINITE (-5) /* a moment / estimate is not finite: [a,b] does not
+                              enclose the spectrum (|T_j| blow-up)     */
+
+typedef struct {
+    int64_t n_rows, n_cols, nnz;
+    const int64_t *row_ptr; /* [n_rows+1] */
+    const int32_t *col_idx; /* [nnz]      */
+    const double *val;      /* [nnz]      */
+} cl_csr;
+
+typedef enum { CL_OP_CSR = 0, CL_OP_CSR_RANK1 = 1, CL_OP_BTB = 2 } cl_op_kind;
+
+typedef struct {
+    int32_t kind;      /* cl_op_kind                                              */
+    cl_csr A;          /* A (CSR, RANK1) or B (BTB); d = A.n_cols                 */
+    cl_csr At;         /* BTB only: exact CSR of B^T (n_rows = B.n_cols)          */
+    double r1_c;       /* RANK1 only: weight c                                    */
+    const double *r1_u;/* RANK1 only: u[d], NULL = all ones                       */
+} cl_operator;
+
+typedef struct {
+    double logdet;        /* Gamma: estimate of log det M (BTB: of B^T B)         */
+    double stderr_;       /* sample sd(Gamma_p) / sqrt(m)                          */
+    int64_t num_probes;   /* m                                                      */
+    int32_t degree;       /* n                                                      */
+    int32_t probe_block;  /* k actually used                                        */
+    double *per_probe;    /* caller-owned HOST array [m] or NULL: Gamma_p           */
+    double *moments;      /* caller-owned HOST array [m*(n+1)] or NULL: mu_{p,j}    */
+    double elapsed_s;     /* wall time of the call                                  */
+} cl_result;
+
+/* Chebyshev interpolation coefficients c_0..c_n of f(x) = log(((b-a)x+(b+a))/2)
+ * on [-1,1] at the n+1 first-kind nodes x_k = cos(pi(k+1/2)/(n+1))
+ * (Alg. 1 line 4 P:225-227 in [a,b] form).  Host fp64 routine; c_out
+ * is a HOST array of degree+1 doubles.  CL_EINVAL if !(0 < a < b), non-finite, or
+ * degree < 0. */
+int cheb_coeffs_log(double a, double b, int32_t degree, double *c_out);
+
+/* Device workspace bytes cheb_moments needs for operator `op` and probe block k
+ * on the current device.  Returns 0 on invalid input (see cheb_last_error). */
+size_t cheb_workspace_bytes(const cl_operator *op, int32_t probe_block);
+
+/* Shard-level, stream-ordered, ASYNCHRONOUS moments: for global probes
+ * p in [probe_begin, probe_end) writes mu_out[(p-probe_begin)*(degree+1) + j]
+ * = v_p^T T_j(Ã) v_p, j = 0..degree (DEVICE array).  All CSR / u pointers are
+ * DEVICE pointers.  Probes are addressed by global index, so sharding never
+ * changes a probe.  `stream` is a cudaStream_t (NULL = legacy default).
+ * Allocates nothing; `workspace` must hold cheb_workspace_bytes(op, k) bytes.
+ * Non-finite moments are NOT detected here (see cheb_finalize / cheb_logdet). */
+int cheb_moments(const cl_operator *op, double a, double b, int32_t degree,
+                 int64_t probe_begin, int64_t probe_end, uint64_t seed,
+                 int32_t probe_block, void *workspace, size_t ws_bytes,
+                 double *mu_out, void *stream);
+
+/* ASYNCHRONOUS device accumulation (reading G7):
+ *   gamma_p[p] = sum_{j=0..n} c[j] mu[p*(n+1)+j] (ascending j),
+ *   stats[0] = Gamma = (sum_p gamma_p, ascending p)/m,
+ *   stats[1] = sample sd(gamma_p)/sqrt(m) (0 if m == 1),
+ *   stats[2] = 1.0 if every gamma_p is finite else 0.0.
+ * mu, c, gamma_p, stats are DEVICE arrays. */
+int cheb_finalize(const double *mu, const double *c, int64_t m, int32_t degree,
+                  double *gamma_p, double *stats, void *stream);
+
+/* Synchronous single-GPU estimate in BASELINE's shape; operator pointers are
+ * DEVICE pointers.  probe_block = 0 picks k automatically.  Allocates its own
+ * workspace.  CL_ENONFINITE if any estimate is not finite. */
+int cheb_logdet(const cl_operator *op, double a, double b, int32_t degree,
+                int32_t num_probes, uint64_t seed, int32_t probe_block,
+                cl_result *out);
+
+/* As cheb_logdet, but every operator pointer is a HOST pointer: the call copies
+ * the matrix (and u) to the device, runs, copies the result back, and frees. */
+int cheb_logdet_host(const cl_operator *op, double a, double b, int32_t degree,
+                     int32_t num_probes, uint64_t seed, int32_t probe_block,
+                     cl_result *out);
+
+/* Spectral interval of B^T B for Algorithm 2, computed on the device
+ * from B and B^T (DEVICE CSRs in op, kind must be CL_OP_BTB):
+ *   ab_out[0] = a = (min_i |b_ii| - (r_i + c_i)/2)^2   (Johnson lower bound on
+ *               sigma_min; r_i, c_i off-diagonal absolute row/column sums)
+ *   ab_out[1] = b = ||B||_1 ||B||_inf
+ * ab_out is a HOST array[2]; synchronous on `stream`.  CL_EINVAL if the Johnson
+ * bound is not positive (B not diagonally dominant enough). */
+int cheb_bounds_btb(const cl_operator *op, double *ab_out, void *stream);
+
+/* The probes the path uses: writes v_p[i] (+1.0 / -1.0) for p in
+ * [probe_begin, probe_begin+k), into v_out[i*k + (p-probe_begin)] (DEVICE, d*k
+ * doubles), running the same probe-initialisation kernel as cheb_moments. */
+int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_block,
+                double *v_out, void *stream);
+
+/* Kernel accounting for benchmarks.  cheb_launch_count(): cumulative number of
+ * this library's kernel launches in the process.  cheb_profile_begin(): start
+ * recording CUDA events around every Chebyshev-step launch on its stream;
+ * cheb_profile_end(): synchronise, return the summed step-kernel milliseconds,
+ * the number of step launches, and stop recording. */
+int64_t cheb_launch_count(void);
+int cheb_profile_begin(void);
+int cheb_profile_end(double *step_ms, int64_t *step_launches);
+
+/* Thread-local message for the last failing call on this thread. */
+const char *cheb_last_error(void);
+
+/* ABI version (major*10000 + minor*100 + patch). */
+int cheb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHEB_LOGDET_H */

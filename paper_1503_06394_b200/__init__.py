@@ -1,0 +1,17 @@
+"""B200-native Chebyshev-Hutchinson log-determinant hot path (arXiv 1503.06394).
+
+The compute lives in libchebld.so (include/cheb_logdet.h, csrc/); this package
+is the thin Python binding (api.py) and the multi-GPU probe-sharding driver
+(dist.py).  There is no CPU fallback: importing the API without the built
+library raises.
+"""
+from .api import (DeviceCSR, Operator, Result, Estimator, coeffs_log, workspace_bytes,
+                  alloc_workspace, moments, finalize, logdet, logdet_host, bounds_btb, probes,
+                  launch_count, profile_begin, profile_end, log_abs_det_from_btb,
+                  log_tau_from_rank1)
+from ._lib import ChebError, load as load_library
+
+__all__ = ["DeviceCSR", "Operator", "Result", "Estimator", "coeffs_log", "workspace_bytes",
+           "alloc_workspace", "moments", "finalize", "logdet", "logdet_host", "bounds_btb",
+           "probes", "launch_count", "profile_begin", "profile_end", "log_abs_det_from_btb",
+           "log_tau_from_rank1", "ChebError", "load_library"]

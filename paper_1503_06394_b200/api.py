@@ -1,0 +1,277 @@
+"""Python face of the C ABI (include/cheb_logdet.h).
+
+PyTorch is plumbing here: it owns device memory and streams.  Every arithmetic
+step of the path (probes, Chebyshev steps, reductions, accumulation, bounds)
+runs in libchebld.so's CUDA kernels; this module only marshals pointers.
+"""
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import CLCsr, CLOperator, CLResult, OP_KIND, check
+
+
+@dataclass
+class DeviceCSR:
+    """CSR resident on a CUDA device: row_ptr int64, col_idx int32, val float64."""
+    n_rows: int
+    n_cols: int
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    val: torch.Tensor
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @classmethod
+    def from_host(cls, csr, device="cuda"):
+        """Upload any object with n_rows, n_cols, row_ptr, col_idx, val (numpy)."""
+        return cls(int(csr.n_rows), int(csr.n_cols),
+                   torch.from_numpy(np.ascontiguousarray(csr.row_ptr, dtype=np.int64)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(csr.col_idx, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(csr.val, dtype=np.float64)).to(device))
+
+    def struct(self) -> CLCsr:
+        for t, dt in ((self.row_ptr, torch.int64), (self.col_idx, torch.int32), (self.val, torch.float64)):
+            if t.dtype != dt or not t.is_contiguous() or not t.is_cuda:
+                raise TypeError("DeviceCSR tensors must be contiguous CUDA int64/int32/float64")
+        return CLCsr(self.n_rows, self.n_cols, self.nnz, self.row_ptr.data_ptr(),
+                     self.col_idx.data_ptr(), self.val.data_ptr())
+
+
+def _host_ptr(x, np_dtype, torch_dtype, keep):
+    """Host pointer of a numpy array or a (pinned) CPU torch tensor, no copy if
+    already contiguous with the right dtype."""
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda or x.dtype != torch_dtype or not x.is_contiguous():
+            raise TypeError("host CSR tensors must be contiguous CPU tensors of the right dtype")
+        keep.append(x)
+        return x.data_ptr(), x.numel()
+    a = np.ascontiguousarray(x, dtype=np_dtype)
+    keep.append(a)
+    return a.ctypes.data, a.size
+
+
+def _host_csr_struct(csr, keep):
+    rp, _ = _host_ptr(csr.row_ptr, np.int64, torch.int64, keep)
+    ci, nnz = _host_ptr(csr.col_idx, np.int32, torch.int32, keep)
+    va, _ = _host_ptr(csr.val, np.float64, torch.float64, keep)
+    return CLCsr(int(csr.n_rows), int(csr.n_cols), int(nnz), rp, ci, va)
+
+
+@dataclass
+class Operator:
+    """M = A (kind "csr"), A + c u u^T ("rank1", u None = ones), or B^T B ("btb",
+    A = B, At = exact CSR of B^T)."""
+    kind: str
+    A: DeviceCSR
+    At: Optional[DeviceCSR] = None
+    c: float = 0.0
+    u: Optional[torch.Tensor] = None
+
+    @property
+    def d(self) -> int:
+        return self.A.n_cols
+
+    def struct(self) -> CLOperator:
+        s = CLOperator()
+        s.kind = OP_KIND[self.kind]
+        s.A = self.A.struct()
+        if self.kind == "btb":
+            if self.At is None:
+                raise ValueError("btb operator needs At (CSR of B^T)")
+            s.At = self.At.struct()
+        s.r1_c = float(self.c)
+        s.r1_u = self.u.data_ptr() if (self.kind == "rank1" and self.u is not None) else None
+        return s
+
+
+@dataclass
+class Result:
+    logdet: float          # Gamma: estimate of log det M
+    stderr: float
+    num_probes: int
+    degree: int
+    probe_block: int
+    gamma_p: np.ndarray
+    moments: Optional[np.ndarray]
+    elapsed_s: float
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def coeffs_log(a: float, b: float, degree: int) -> np.ndarray:
+    """Host fp64 Chebyshev coefficients of log on [a,b] (library routine)."""
+    c = np.empty(degree + 1 if degree >= 0 else 1)
+    check(_lib.load().cheb_coeffs_log(float(a), float(b), int(degree), c.ctypes.data))
+    return c
+
+
+def workspace_bytes(op: Operator, k: int) -> int:
+    L = _lib.load()
+    s = op.struct()
+    n = L.cheb_workspace_bytes(ctypes.byref(s), int(k))
+    if n == 0:
+        raise _lib.ChebError(-1, L.cheb_last_error().decode())
+    return int(n)
+
+
+def alloc_workspace(op: Operator, k: int) -> torch.Tensor:
+    n = workspace_bytes(op, k)
+    return torch.empty(n, dtype=torch.uint8, device=op.A.val.device)
+
+
+def moments(op: Operator, a: float, b: float, degree: int, probe_begin: int, probe_end: int,
+            seed: int, k: int, mu_out: Optional[torch.Tensor] = None,
+            workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Asynchronous: mu[(p - probe_begin), j] = v_p^T T_j(Ã) v_p on the device."""
+    dev = op.A.val.device
+    if mu_out is None:
+        mu_out = torch.empty((probe_end - probe_begin, degree + 1), dtype=torch.float64, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(op, k)
+    s = op.struct()
+    check(_lib.load().cheb_moments(ctypes.byref(s), float(a), float(b), int(degree), int(probe_begin),
+                                   int(probe_end), int(seed) & (2 ** 64 - 1), int(k),
+                                   workspace.data_ptr(), workspace.numel(), mu_out.data_ptr(),
+                                   _stream_ptr(stream)))
+    return mu_out
+
+
+def finalize(mu: torch.Tensor, c: torch.Tensor, stream=None):
+    """Asynchronous device accumulation: returns (gamma_p[m], stats[3]) tensors;
+    stats = (Gamma, stderr, all-finite flag)."""
+    m, n1 = mu.shape
+    gp = torch.empty(m, dtype=torch.float64, device=mu.device)
+    stats = torch.empty(3, dtype=torch.float64, device=mu.device)
+    check(_lib.load().cheb_finalize(mu.data_ptr(), c.data_ptr(), int(m), int(n1 - 1), gp.data_ptr(),
+                                    stats.data_ptr(), _stream_ptr(stream)))
+    return gp, stats
+
+
+def _result(r: CLResult, gp, mu) -> Result:
+    return Result(r.logdet, r.stderr_, int(r.num_probes), int(r.degree), int(r.probe_block), gp, mu,
+                  r.elapsed_s)
+
+
+def logdet(op: Operator, a: float, b: float, degree: int = 15, num_probes: int = 30, seed: int = 1,
+           k: int = 0, want_moments: bool = False) -> Result:
+    """Synchronous estimate of log det M (cheb_logdet; device-resident operator)."""
+    gp = np.empty(num_probes)
+    mu = np.empty((num_probes, degree + 1)) if want_moments else None
+    r = CLResult()
+    r.per_probe = gp.ctypes.data
+    r.moments = mu.ctypes.data if mu is not None else None
+    s = op.struct()
+    check(_lib.load().cheb_logdet(ctypes.byref(s), float(a), float(b), int(degree), int(num_probes),
+                                  int(seed) & (2 ** 64 - 1), int(k), ctypes.byref(r)))
+    return _result(r, gp, mu)
+
+
+def logdet_host(kind: str, A, a: float, b: float, degree: int = 15, num_probes: int = 30,
+                seed: int = 1, k: int = 0, At=None, c: float = 0.0, u: Optional[np.ndarray] = None,
+                want_moments: bool = False) -> Result:
+    """Synchronous estimate from HOST (numpy) CSR arrays: the library copies the
+    operator to the device inside the call (cheb_logdet_host)."""
+    keep = []
+    s = CLOperator()
+    s.kind = OP_KIND[kind]
+    s.A = _host_csr_struct(A, keep)
+    if kind == "btb":
+        s.At = _host_csr_struct(At, keep)
+    s.r1_c = float(c)
+    if kind == "rank1" and u is not None:
+        uu = np.ascontiguousarray(u, dtype=np.float64)
+        keep.append(uu)
+        s.r1_u = uu.ctypes.data
+    gp = np.empty(num_probes)
+    mu = np.empty((num_probes, degree + 1)) if want_moments else None
+    r = CLResult()
+    r.per_probe = gp.ctypes.data
+    r.moments = mu.ctypes.data if mu is not None else None
+    check(_lib.load().cheb_logdet_host(ctypes.byref(s), float(a), float(b), int(degree),
+                                       int(num_probes), int(seed) & (2 ** 64 - 1), int(k),
+                                       ctypes.byref(r)))
+    return _result(r, gp, mu)
+
+
+def bounds_btb(op: Operator, stream=None):
+    """(a, b) spectral interval of B^T B from the device kernel."""
+    ab = np.empty(2)
+    s = op.struct()
+    check(_lib.load().cheb_bounds_btb(ctypes.byref(s), ab.ctypes.data, _stream_ptr(stream)))
+    return float(ab[0]), float(ab[1])
+
+
+def probes(d: int, seed: int, probe_begin: int, k: int, device="cuda") -> torch.Tensor:
+    """The path's probes v_p[i] for p in [probe_begin, probe_begin+k): tensor [d, k]."""
+    v = torch.empty((d, k), dtype=torch.float64, device=device)
+    check(_lib.load().cheb_probes(int(d), int(seed) & (2 ** 64 - 1), int(probe_begin), int(k),
+                                  v.data_ptr(), _stream_ptr()))
+    return v
+
+
+def launch_count() -> int:
+    return int(_lib.load().cheb_launch_count())
+
+
+def profile_begin():
+    check(_lib.load().cheb_profile_begin())
+
+
+def profile_end():
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    check(_lib.load().cheb_profile_end(ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
+
+
+class Estimator:
+    """Reusable device state for repeated estimates on one operator (bench,
+    multi-GPU driver): workspace, coefficients and moment buffer stay resident."""
+
+    def __init__(self, op: Operator, a: float, b: float, degree: int, num_probes: int,
+                 k: int, seed: int = 1, probe_begin: int = 0, probe_end: Optional[int] = None):
+        self.op, self.a, self.b, self.degree, self.k, self.seed = op, a, b, degree, k, seed
+        self.m = num_probes
+        self.probe_begin = probe_begin
+        self.probe_end = num_probes if probe_end is None else probe_end
+        dev = op.A.val.device
+        self.workspace = alloc_workspace(op, k)
+        self.c = torch.from_numpy(coeffs_log(a, b, degree)).to(dev)
+        self.mu = torch.zeros((num_probes, degree + 1), dtype=torch.float64, device=dev)
+
+    def enqueue_moments(self, stream=None):
+        """Fill this shard's rows [probe_begin, probe_end) of mu (others untouched)."""
+        if self.probe_end > self.probe_begin:
+            moments(self.op, self.a, self.b, self.degree, self.probe_begin, self.probe_end, self.seed,
+                    self.k, mu_out=self.mu[self.probe_begin:self.probe_end], workspace=self.workspace,
+                    stream=stream)
+        return self.mu
+
+    def enqueue_finalize(self, stream=None):
+        return finalize(self.mu, self.c, stream=stream)
+
+    def run(self, stream=None):
+        self.enqueue_moments(stream)
+        return self.enqueue_finalize(stream)
+
+
+def log_abs_det_from_btb(gamma: float) -> float:
+    """Alg. 2: log|det B| = 1/2 log det B^T B ([a,b] form: the
+    d log(s) shift is already inside c_0)."""
+    return 0.5 * gamma
+
+
+def log_tau_from_rank1(gamma: float, c: float, n_vertices: int) -> float:
+    """Spanning trees via M = L + c 11^T: log tau = log det M - log(c N^2)."""
+    return gamma - math.log(c * n_vertices * n_vertices)

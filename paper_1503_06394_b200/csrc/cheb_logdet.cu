@@ -1,0 +1,538 @@
+// cheb_logdet.cu -- host side of the C ABI (include/cheb_logdet.h): validation,
+// fp64 coefficient routine, workspace planning, stream-ordered launch sequence,
+// kernel accounting.  Device kernels live in cheb_kernels.cuh.
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "cheb_logdet.h"
+#include "cheb_kernels.cuh"
+
+using namespace chebld;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CL_CUDA(call)                                                                 \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(CL_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                        __FILE__, __LINE__);                                          \
+    } while (0)
+
+// ---- step-kernel profiling (CUDA events on the launching stream) ------------
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // recorded pairs
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+} g_prof;
+
+struct ProfScope {
+    cudaStream_t s;
+    std::pair<cudaEvent_t, cudaEvent_t> pr{nullptr, nullptr};
+    explicit ProfScope(cudaStream_t st) : s(st) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        if (!g_prof.on) return;
+        if (!g_prof.pool.empty()) {
+            pr = g_prof.pool.back();
+            g_prof.pool.pop_back();
+        } else {
+            cudaEventCreate(&pr.first);
+            cudaEventCreate(&pr.second);
+        }
+        cudaEventRecord(pr.first, s);
+    }
+    ~ProfScope() {
+        if (!pr.first) return;
+        cudaEventRecord(pr.second, s);
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.ev.push_back(pr);
+    }
+};
+
+int sm_count() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+constexpr int kMaxCtasPerSm = 8;  // partial buffers are sized for this
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64; }
+
+struct Layout {
+    size_t w0, w1, y, sbits, part_mu, part_s, sbuf, ticket, total;
+};
+
+Layout plan(int64_t d, int k, int kind, int sms) {
+    Layout L{};
+    size_t off = 0;
+    const size_t wbytes = align256((size_t)d * k * sizeof(double));
+    const int words = k >= 32 ? k / 32 : 1;
+    const size_t maxgrid = (size_t)sms * kMaxCtasPerSm;
+    L.w0 = off; off += wbytes;
+    L.w1 = off; off += wbytes;
+    L.y = off; if (kind == CL_OP_BTB) off += wbytes;
+    L.sbits = off; off += align256((size_t)d * words * sizeof(uint32_t));
+    L.part_mu = off; off += align256(maxgrid * k * sizeof(double));
+    L.part_s = off; off += align256(maxgrid * k * sizeof(double));
+    L.sbuf = off; off += align256(2 * (size_t)k * sizeof(double));
+    L.ticket = off; off += 256;
+    L.total = off;
+    return L;
+}
+
+int check_csr(const cl_csr& A, const char* name) {
+    if (A.n_rows < 0 || A.n_cols < 0 || A.nnz < 0)
+        return fail(CL_EINVAL, "%s: negative dimension", name);
+    if (A.n_rows > 0 && (!A.row_ptr || (A.nnz > 0 && (!A.col_idx || !A.val))))
+        return fail(CL_EINVAL, "%s: NULL pointer", name);
+    if (A.n_cols >= (int64_t(1) << 31) || A.n_rows >= (int64_t(1) << 31))
+        return fail(CL_EDIM, "%s: dimension >= 2^31 (int32 column indices)", name);
+    return CL_OK;
+}
+
+int check_op(const cl_operator* op) {
+    if (!op) return fail(CL_EINVAL, "operator is NULL");
+    if (op->kind != CL_OP_CSR && op->kind != CL_OP_CSR_RANK1 && op->kind != CL_OP_BTB)
+        return fail(CL_EINVAL, "unknown operator kind %d", op->kind);
+    int rc = check_csr(op->A, "A");
+    if (rc) return rc;
+    if (op->A.n_rows == 0) return fail(CL_EDIM, "empty operator (d = 0)");
+    if (op->A.n_rows != op->A.n_cols) return fail(CL_EDIM, "A must be square (%lld x %lld)",
+                                                  (long long)op->A.n_rows, (long long)op->A.n_cols);
+    if (op->kind == CL_OP_BTB) {
+        if ((rc = check_csr(op->At, "At"))) return rc;
+        if (op->At.n_rows != op->A.n_cols || op->At.n_cols != op->A.n_rows || op->At.nnz != op->A.nnz)
+            return fail(CL_EDIM, "At is not shaped as the transpose of B");
+    }
+    if (op->kind == CL_OP_CSR_RANK1 && !std::isfinite(op->r1_c))
+        return fail(CL_EINVAL, "rank-1 weight is not finite");
+    return CL_OK;
+}
+
+int check_ab(double a, double b, int32_t degree) {
+    if (!std::isfinite(a) || !std::isfinite(b) || !(a > 0.0) || !(b > a))
+        return fail(CL_EINVAL, "need finite 0 < a < b (got a=%g b=%g)", a, b);
+    if (degree < 0) return fail(CL_EINVAL, "degree < 0");
+    return CL_OK;
+}
+
+template <typename Kern>
+int grid_for(Kern kern, int64_t ntiles, int sms) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0);
+    if (occ < 1) occ = 1;
+    if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
+    int64_t g = (int64_t)sms * occ;
+    if (g > ntiles) g = ntiles;
+    return (int)(g < 1 ? 1 : g);
+}
+
+// ---- one probe block: K1, then n x ([K3] K2) --------------------------------
+template <int K, int MODE>
+int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
+              int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
+              int64_t mu_stride, cudaStream_t st, int sms) {
+    using G = Geo<K>;
+    const int64_t d = op->A.n_cols;
+    double* w[2] = {(double*)(ws + L.w0), (double*)(ws + L.w1)};
+    double* y = (double*)(ws + L.y);
+    uint32_t* sbits = (uint32_t*)(ws + L.sbits);
+    double* sbuf = (double*)(ws + L.sbuf);
+
+    StepArgs a{};
+    a.d = d;
+    a.sbits = sbits;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.r1c = op->r1_c;
+    a.r1u = (MODE == MODE_RANK1) ? op->r1_u : nullptr;
+    a.part_mu = (double*)(ws + L.part_mu);
+    a.part_s = (double*)(ws + L.part_s);
+    a.ticket = (unsigned int*)(ws + L.ticket);
+    a.mu_out = mu_rows;
+    a.mu_stride = mu_stride;
+    a.kvalid = kvalid;
+
+    // K1
+    {
+        const int64_t niter = (d + G::GROUPS - 1) / G::GROUPS;
+        const int grid = grid_for(probe_init_kernel<K, MODE>, niter, sms);
+        a.mu_col = 0;
+        a.s_next = sbuf;
+        probe_init_kernel<K, MODE><<<grid, kThreads, 0, st>>>(a, seed, (uint64_t)p0, w[0], sbits);
+        g_launches++;
+    }
+    if (n < 1) return CL_OK;
+
+    const cl_csr& G2 = (MODE == MODE_BTB) ? op->At : op->A;  // gather matrix of K2
+    a.rp = G2.row_ptr;
+    a.ci = G2.col_idx;
+    a.va = G2.val;
+    a.ntiles = (d + G::TILE - 1) / G::TILE;
+    const int grid_first = grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms);
+    const int grid_step = grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms);
+    int grid_spmm = 1;
+    int64_t ntiles_b = 0;
+    if (MODE == MODE_BTB) {
+        ntiles_b = (op->A.n_rows + G::TILE - 1) / G::TILE;
+        grid_spmm = grid_for(spmm_kernel<K>, ntiles_b, sms);
+    }
+    for (int32_t j = 1; j <= n; j++) {
+        const double* cur = w[(j - 1) & 1];
+        double* nxt = w[j & 1];
+        if (MODE == MODE_BTB) {
+            spmm_kernel<K><<<grid_spmm, kThreads, 0, st>>>(op->A.n_rows, ntiles_b, op->A.row_ptr,
+                                                          op->A.col_idx, op->A.val, cur, y);
+            g_launches++;
+        }
+        a.xg = (MODE == MODE_BTB) ? y : cur;
+        a.wcur = cur;
+        a.wnext = nxt;
+        a.s_cur = sbuf + ((j - 1) & 1) * K;
+        a.s_next = sbuf + (j & 1) * K;
+        a.mu_col = j;
+        ProfScope ps(st);
+        if (j == 1)
+            cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, 0, st>>>(a);
+        else
+            cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, 0, st>>>(a);
+        g_launches++;
+    }
+    return CL_OK;
+}
+
+template <int K>
+int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
+                   int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
+                   int64_t mu_stride, cudaStream_t st, int sms) {
+    switch (op->kind) {
+        case CL_OP_CSR:
+            return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
+        case CL_OP_CSR_RANK1:
+            return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
+        default:
+            return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
+    }
+}
+
+int pick_k(int64_t m) {
+    // Largest block the probe count fills; matrix bytes amortise over k.
+    if (m >= 64) return 64;
+    if (m > 16) return 32;
+    if (m > 8) return 16;
+    return 8;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int cheb_version(void) { return 100; }
+
+const char* cheb_last_error(void) { return g_err.c_str(); }
+
+int64_t cheb_launch_count(void) { return g_launches.load(); }
+
+int cheb_profile_begin(void) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (auto& p : g_prof.ev) g_prof.pool.push_back(p);
+    g_prof.ev.clear();
+    g_prof.on = true;
+    return CL_OK;
+}
+
+int cheb_profile_end(double* step_ms, int64_t* step_launches) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = false;
+    double tot = 0.0;
+    for (auto& p : g_prof.ev) {
+        cudaError_t e = cudaEventSynchronize(p.second);
+        if (e != cudaSuccess) return fail(CL_ECUDA, "event sync: %s", cudaGetErrorString(e));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        tot += ms;
+    }
+    if (step_ms) *step_ms = tot;
+    if (step_launches) *step_launches = (int64_t)g_prof.ev.size();
+    for (auto& p : g_prof.ev) g_prof.pool.push_back(p);
+    g_prof.ev.clear();
+    return CL_OK;
+}
+
+// Host fp64 coefficient routine: accumulate, node by node, f(x_k)
+// times T_j(x_k) for all j with the scalar recurrence, then scale.
+int cheb_coeffs_log(double a, double b, int32_t degree, double* c_out) {
+    int rc = check_ab(a, b, degree);
+    if (rc) return rc;
+    if (!c_out) return fail(CL_EINVAL, "c_out is NULL");
+    const int n = degree;
+    std::vector<double> acc((size_t)n + 1, 0.0);
+    const double half_w = 0.5 * (b - a), mid = 0.5 * (b + a);
+    for (int k = 0; k <= n; k++) {
+        const double x = std::cos(M_PI * (k + 0.5) / (n + 1.0));
+        const double f = std::log(half_w * x + mid);
+        double tm1 = 1.0, t = x;
+        acc[0] += f;
+        if (n >= 1) acc[1] += f * x;
+        for (int j = 2; j <= n; j++) {
+            const double tn = 2.0 * x * t - tm1;
+            acc[j] += f * tn;
+            tm1 = t;
+            t = tn;
+        }
+    }
+    const double s0 = 1.0 / (n + 1.0), s1 = 2.0 / (n + 1.0);
+    for (int j = 0; j <= n; j++) {
+        const double cj = (j == 0 ? s0 : s1) * acc[j];
+        if (!std::isfinite(cj)) return fail(CL_ENONFINITE, "coefficient %d not finite", j);
+        c_out[j] = cj;
+    }
+    return CL_OK;
+}
+
+size_t cheb_workspace_bytes(const cl_operator* op, int32_t probe_block) {
+    if (check_op(op)) return 0;
+    if (!valid_k(probe_block)) {
+        fail(CL_EINVAL, "probe_block must be 8, 16, 32 or 64 (got %d)", probe_block);
+        return 0;
+    }
+    return plan(op->A.n_cols, probe_block, op->kind, sm_count()).total;
+}
+
+int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
+                 int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                 void* workspace, size_t ws_bytes, double* mu_out, void* stream) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if ((rc = check_ab(a, b, degree))) return rc;
+    if (probe_begin < 0 || probe_end <= probe_begin)
+        return fail(CL_EINVAL, "need 0 <= probe_begin < probe_end");
+    if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32 or 64");
+    if (!workspace || !mu_out) return fail(CL_EINVAL, "NULL workspace or mu_out");
+    const int sms = sm_count();
+    const Layout L = plan(op->A.n_cols, probe_block, op->kind, sms);
+    if (ws_bytes < L.total)
+        return fail(CL_ENOMEM, "workspace too small: %zu < %zu", ws_bytes, L.total);
+    if ((uintptr_t)workspace & 255) return fail(CL_EINVAL, "workspace must be 256-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    const double alpha = 2.0 / (b - a), beta = (b + a) / (b - a);
+    const int64_t stride = (int64_t)degree + 1;
+    CL_CUDA(cudaGetLastError());
+    CL_CUDA(cudaMemsetAsync(ws + L.ticket, 0, 256, st));
+    for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
+        const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
+        double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
+        switch (probe_block) {
+            case 8: rc = run_block_mode<8>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+            case 16: rc = run_block_mode<16>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+            case 32: rc = run_block_mode<32>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+            default: rc = run_block_mode<64>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+        }
+        if (rc) return rc;
+    }
+    CL_CUDA(cudaGetLastError());
+    return CL_OK;
+}
+
+int cheb_finalize(const double* mu, const double* c, int64_t m, int32_t degree,
+                  double* gamma_p, double* stats, void* stream) {
+    if (!mu || !c || !gamma_p || !stats) return fail(CL_EINVAL, "NULL pointer");
+    if (m < 1 || degree < 0) return fail(CL_EINVAL, "need m >= 1, degree >= 0");
+    finalize_kernel<<<1, kThreads, 0, (cudaStream_t)stream>>>(mu, c, m, degree, gamma_p, stats);
+    g_launches++;
+    CL_CUDA(cudaGetLastError());
+    return CL_OK;
+}
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+};
+
+int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
+                  uint64_t seed, int32_t probe_block, cl_result* out, cudaStream_t st) {
+    const int k = probe_block ? probe_block : pick_k(num_probes);
+    if (!valid_k(k)) return fail(CL_EINVAL, "probe_block must be 0, 8, 16, 32 or 64");
+    const size_t ws_bytes = plan(op->A.n_cols, k, op->kind, sm_count()).total;
+    const size_t mu_n = (size_t)num_probes * (degree + 1);
+    DevBuf ws, aux;
+    CL_CUDA(cudaMalloc(&ws.p, ws_bytes));
+    const size_t aux_bytes = sizeof(double) * (mu_n + (degree + 1) + num_probes + 4);
+    CL_CUDA(cudaMalloc(&aux.p, aux_bytes));
+    double* mu = (double*)aux.p;
+    double* c = mu + mu_n;
+    double* gp = c + degree + 1;
+    double* stats = gp + num_probes;
+    std::vector<double> ch((size_t)degree + 1);
+    int rc = cheb_coeffs_log(a, b, degree, ch.data());
+    if (rc) return rc;
+    CL_CUDA(cudaMemcpyAsync(c, ch.data(), ch.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    rc = cheb_moments(op, a, b, degree, 0, num_probes, seed, k, ws.p, ws_bytes, mu, st);
+    if (rc) return rc;
+    rc = cheb_finalize(mu, c, num_probes, degree, gp, stats, st);
+    if (rc) return rc;
+    double hstats[3];
+    CL_CUDA(cudaMemcpyAsync(hstats, stats, sizeof(hstats), cudaMemcpyDeviceToHost, st));
+    if (out->per_probe)
+        CL_CUDA(cudaMemcpyAsync(out->per_probe, gp, sizeof(double) * num_probes, cudaMemcpyDeviceToHost, st));
+    if (out->moments)
+        CL_CUDA(cudaMemcpyAsync(out->moments, mu, sizeof(double) * mu_n, cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    out->logdet = hstats[0];
+    out->stderr_ = hstats[1];
+    out->num_probes = num_probes;
+    out->degree = degree;
+    out->probe_block = k;
+    if (hstats[2] != 1.0 || !std::isfinite(hstats[0]))
+        return fail(CL_ENONFINITE, "non-finite estimate: [a,b]=[%g,%g] likely does not enclose the spectrum", a, b);
+    return CL_OK;
+}
+
+}  // namespace
+
+int cheb_logdet(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
+                uint64_t seed, int32_t probe_block, cl_result* out) {
+    auto t0 = std::chrono::steady_clock::now();
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if ((rc = check_ab(a, b, degree))) return rc;
+    if (num_probes < 1) return fail(CL_EINVAL, "num_probes < 1");
+    if (!out) return fail(CL_EINVAL, "out is NULL");
+    cudaStream_t st;
+    CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    rc = logdet_device(op, a, b, degree, num_probes, seed, probe_block, out, st);
+    cudaStreamDestroy(st);
+    out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
+                     uint64_t seed, int32_t probe_block, cl_result* out) {
+    auto t0 = std::chrono::steady_clock::now();
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if ((rc = check_ab(a, b, degree))) return rc;
+    if (num_probes < 1) return fail(CL_EINVAL, "num_probes < 1");
+    if (!out) return fail(CL_EINVAL, "out is NULL");
+    cudaStream_t st;
+    CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cl_operator dop = *op;
+    DevBuf bufs[8];
+    int nb = 0;
+    auto up = [&](const void* h, size_t bytes, const void** dptr) -> int {
+        if (!h || bytes == 0) return CL_OK;
+        CL_CUDA(cudaMalloc(&bufs[nb].p, bytes));
+        CL_CUDA(cudaMemcpyAsync(bufs[nb].p, h, bytes, cudaMemcpyHostToDevice, st));
+        *dptr = bufs[nb++].p;
+        return CL_OK;
+    };
+    auto up_csr = [&](cl_csr& A) -> int {
+        int r;
+        if ((r = up(A.row_ptr, sizeof(int64_t) * (A.n_rows + 1), (const void**)&A.row_ptr))) return r;
+        if ((r = up(A.col_idx, sizeof(int32_t) * A.nnz, (const void**)&A.col_idx))) return r;
+        return up(A.val, sizeof(double) * A.nnz, (const void**)&A.val);
+    };
+    rc = up_csr(dop.A);
+    if (!rc && dop.kind == CL_OP_BTB) rc = up_csr(dop.At);
+    if (!rc && dop.kind == CL_OP_CSR_RANK1 && dop.r1_u)
+        rc = up(dop.r1_u, sizeof(double) * dop.A.n_cols, (const void**)&dop.r1_u);
+    if (!rc) rc = logdet_device(&dop, a, b, degree, num_probes, seed, probe_block, out, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+int cheb_bounds_btb(const cl_operator* op, double* ab_out, void* stream) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if (op->kind != CL_OP_BTB) return fail(CL_EINVAL, "cheb_bounds_btb needs a CL_OP_BTB operator");
+    if (!ab_out) return fail(CL_EINVAL, "ab_out is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf buf;
+    CL_CUDA(cudaMalloc(&buf.p, 3 * sizeof(unsigned long long)));
+    unsigned long long init[3] = {~0ull, 0ull, 0ull};
+    CL_CUDA(cudaMemcpyAsync(buf.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const int64_t d = op->A.n_rows;
+    int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    bounds_btb_kernel<<<grid, kThreads, 0, st>>>(d, op->A.row_ptr, op->A.col_idx, op->A.val,
+                                                  op->At.row_ptr, op->At.col_idx, op->At.val,
+                                                  (unsigned long long*)buf.p);
+    g_launches++;
+    CL_CUDA(cudaGetLastError());
+    unsigned long long h[3];
+    CL_CUDA(cudaMemcpyAsync(h, buf.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    auto unkey = [](unsigned long long k) {
+        unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        double x;
+        memcpy(&x, &b, sizeof(x));
+        return x;
+    };
+    const double smin = unkey(h[0]), rmax = unkey(h[1]), cmax = unkey(h[2]);
+    if (!(smin > 0.0))
+        return fail(CL_EINVAL, "Johnson lower bound on sigma_min is not positive (%g); supply [a,b]", smin);
+    ab_out[0] = smin * smin;
+    ab_out[1] = cmax * rmax;
+    return CL_OK;
+}
+
+int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_block,
+                double* v_out, void* stream) {
+    if (d < 1 || d >= (int64_t(1) << 31)) return fail(CL_EDIM, "bad d");
+    if (probe_begin < 0 || !valid_k(probe_block) || !v_out) return fail(CL_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    cl_operator op{};
+    op.kind = CL_OP_CSR;
+    op.A.n_rows = op.A.n_cols = d;
+    const int sms = sm_count();
+    const Layout L = plan(d, probe_block, CL_OP_CSR, sms);
+    DevBuf ws, mu;
+    CL_CUDA(cudaMalloc(&ws.p, L.total));
+    CL_CUDA(cudaMalloc(&mu.p, sizeof(double) * probe_block));
+    CL_CUDA(cudaMemsetAsync((char*)ws.p + L.ticket, 0, 256, st));
+    int rc;
+    switch (probe_block) {
+        case 8: rc = run_block<8, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 8, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+        case 16: rc = run_block<16, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 16, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+        case 32: rc = run_block<32, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 32, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+        default: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+    }
+    if (rc) return rc;
+    CL_CUDA(cudaMemcpyAsync(v_out, (char*)ws.p + L.w0, sizeof(double) * d * probe_block,
+                            cudaMemcpyDeviceToDevice, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    return CL_OK;
+}
+
+}  // extern "C"

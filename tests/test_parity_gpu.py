@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the pinned CPU oracle on
+identical seeded inputs.
+
+Tolerances (BASELINE north_star):
+  * probes: bit-exact (integer/bit work);
+  * Gamma: |Gamma_gpu - Gamma_oracle| <= 1e-10 |Gamma_oracle|;
+  * diagnostics: |d mu_{p,j}| <= 1e-11 * d, per-probe |d Gamma_p| <= 1e-10 |Gamma_p| + 1e-12 d.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes only with -m gpu
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_1503_06394_b200 as P  # noqa: E402
+
+GAMMA_RTOL = 1e-10
+
+
+def _mats(wl):
+    A, At = wl.matrices()
+    return A, At
+
+
+def _dev_op(kind, A, At=None, c=0.0, u=None):
+    return P.Operator(kind, P.DeviceCSR.from_host(A),
+                      P.DeviceCSR.from_host(At) if At is not None else None, c,
+                      torch.from_numpy(u).cuda() if u is not None else None)
+
+
+def _check_moments(mu_gpu, mu_orc, d):
+    mu_gpu = np.asarray(mu_gpu)
+    assert mu_gpu.shape == mu_orc.shape
+    assert np.all(np.isfinite(mu_gpu))
+    err = np.abs(mu_gpu - mu_orc).max()
+    assert err <= 1e-11 * d, err
+
+
+def _check_gamma(g_gpu, g_orc):
+    assert abs(g_gpu - g_orc) <= GAMMA_RTOL * abs(g_orc), (g_gpu, g_orc)
+
+
+# ------------------------------------------------------------------ probes (a2)
+@pytest.mark.parametrize("d,p0,k", [(1, 0, 8), (1000, 0, 8), (1027, 5, 16), (4099, 33, 32),
+                                    (65536, 64, 64), (3, 1 << 40, 64)])
+def test_probes_bit_identical(orc, d, p0, k):
+    v = P.probes(d, 0x1234, p0, k).cpu().numpy()
+    for j in range(k):
+        assert np.array_equal(v[:, j], orc.rademacher(0x1234, p0 + j, d)), (j,)
+
+
+# ------------------------------------------------------------------ small configs, every k
+SMALL = ["gmrf32", "gmrf_s", "torus_s", "btb_s"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+def test_moments_and_gamma_small(orc, name, k):
+    wl = W.get_workload(name)
+    A, At = _mats(wl)
+    op = _dev_op(wl.mode, A, At, wl.r1_c)
+    a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+    m = wl.num_probes  # 12/20/64: ragged last block for most k
+    r = P.logdet(op, a, b, wl.degree, m, seed=wl.seed, k=k, want_moments=True)
+    mu = orc.moments(orc.Op(wl.mode, A, wl.r1_c), a, b, wl.degree, wl.seed, range(m), workers=4)
+    _check_moments(r.moments, mu, wl.d)
+    g, gp, se = orc.gamma_from_moments(orc.coeffs_log(a, b, wl.degree), mu)
+    _check_gamma(r.logdet, g)
+    assert np.all(np.abs(r.gamma_p - gp) <= 1e-10 * np.abs(gp) + 1e-12 * wl.d)
+    assert abs(r.stderr - se) <= 1e-8 * se
+
+
+def test_rank1_explicit_u(orc):
+    T = W.torus_laplacian(21)
+    u = np.linspace(0.5, 1.5, T.n_rows)
+    op = _dev_op("rank1", T, None, 1e-3, u)
+    a, b = 1e-3, 8.5
+    r = P.logdet(op, a, b, 50, 10, seed=3, k=16, want_moments=True)
+    mu = orc.moments(orc.Op("rank1", T, 1e-3, u), a, b, 50, 3, range(10))
+    _check_moments(r.moments, mu, T.n_rows)
+
+
+def test_general_csr_without_diagonal_entries(orc):
+    """Rows without a stored diagonal and empty rows (the -beta*w term must still apply)."""
+    S = W.random_spd(3000, 4)
+    rows = np.repeat(np.arange(S.n_rows), np.diff(S.row_ptr))
+    keep = (rows != S.col_idx) | (rows % 7 != 0)
+    keep &= ~((rows % 101) == 5)  # some rows become empty
+    C = W.csr.from_coo(S.n_rows, S.n_cols, rows[keep], S.col_idx[keep], S.val[keep])
+    lam = 1.0 + np.abs(C.val).max() * 40
+    op = _dev_op("csr", C)
+    mu_g = P.moments(op, 0.05, lam, 25, 0, 9, 11, 8).cpu().numpy()
+    mu = orc.moments(orc.Op("csr", C), 0.05, lam, 25, 11, range(9))
+    # the spectrum leaves [a,b] (no stored diagonal in some rows): compare relative
+    scale = np.maximum(np.abs(mu).max(axis=0), C.n_rows)
+    assert np.all(np.abs(mu_g - mu) <= 1e-11 * scale)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2])
+def test_degenerate_degrees(orc, n):
+    wl = W.get_workload("gmrf_s")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    r = P.logdet(op, wl.a, wl.b, n, 5, seed=2, k=8, want_moments=True)
+    mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, 2, range(5))
+    _check_moments(r.moments, mu, wl.d)
+    if n == 0:
+        assert np.all(r.moments[:, 0] == wl.d)
+        assert r.logdet == coeffs0(wl) * wl.d
+
+
+def coeffs0(wl):
+    return P.coeffs_log(wl.a, wl.b, 0)[0]
+
+
+def test_single_row_and_single_probe(orc):
+    A = W.csr.from_coo(1, 1, [0], [0], [0.7])
+    op = _dev_op("csr", A)
+    r = P.logdet(op, 0.5, 1.0, 10, 1, seed=4, k=8, want_moments=True)
+    mu = orc.moments(orc.Op("csr", A), 0.5, 1.0, 10, 4, [0])
+    _check_moments(r.moments, mu, 1)
+    assert r.stderr == 0.0
+    assert abs(r.logdet - math.log(0.7)) < 1e-6
+
+
+def test_shard_offsets_do_not_change_probes(orc):
+    """Global probe addressing: moments of probes [5, 21) computed as a shard equal
+    the same rows of a [0, 32) run bit for bit (fixed k)."""
+    wl = W.get_workload("gmrf_s")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    full = P.moments(op, wl.a, wl.b, 12, 0, 32, 9, 16).cpu().numpy()
+    part = P.moments(op, wl.a, wl.b, 12, 5, 21, 9, 16).cpu().numpy()
+    assert np.array_equal(full[5:21], part)
+    again = P.moments(op, wl.a, wl.b, 12, 0, 32, 9, 16).cpu().numpy()
+    assert np.array_equal(full, again)  # deterministic reductions
+
+
+def test_host_entry_point_matches_device(orc):
+    wl = W.get_workload("torus_s")
+    A, _ = _mats(wl)
+    rd = P.logdet(_dev_op("rank1", A, None, wl.r1_c), wl.a, wl.b, wl.degree, wl.num_probes, seed=5,
+                  k=8, want_moments=True)
+    rh = P.logdet_host("rank1", A, wl.a, wl.b, wl.degree, wl.num_probes, seed=5, k=8, c=wl.r1_c,
+                       want_moments=True)
+    assert np.array_equal(rd.moments, rh.moments) and rd.logdet == rh.logdet
+
+
+def test_bounds_btb_match_oracle(orc):
+    for d, seed in ((5003, 3), (20000, 8)):
+        B = W.random_nonsingular(d, seed)
+        op = _dev_op("btb", B, W.transpose(B))
+        a, b = P.bounds_btb(op)
+        oa, ob = orc.bounds_btb(B)
+        assert abs(a - oa) <= 1e-13 * oa and abs(b - ob) <= 1e-13 * ob
+
+
+def test_nonfinite_detected():
+    """b below lambda_max: |T_j| grows geometrically and overflows -> CL_ENONFINITE."""
+    A = W.csr.from_coo(50, 50, np.arange(50), np.arange(50), np.full(50, 1e6))
+    op = _dev_op("csr", A)
+    with pytest.raises(P.ChebError) as ei:
+        P.logdet(op, 0.5, 1.0, 200, 8, seed=1, k=8)
+    assert ei.value.code == -5
+
+
+def test_launch_count_increases():
+    wl = W.get_workload("gmrf32")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    n0 = P.launch_count()
+    P.logdet(op, wl.a, wl.b, 10, 16, k=16)
+    assert P.launch_count() - n0 == 1 + 10 + 1  # init + 10 steps + finalize
+
+
+# ------------------------------------------------------------------ estimate vs truth
+def test_config0_estimate_vs_closed_form():
+    from oracle import closed_forms as cf
+    wl = W.get_workload("gmrf32")
+    A, _ = _mats(wl)
+    r = P.logdet(_dev_op("csr", A), wl.a, wl.b, wl.degree, wl.num_probes, seed=wl.seed, k=64)
+    assert abs(r.logdet - cf.grid_logdet(32, 0.2)) <= 4 * r.stderr
+
+
+# ------------------------------------------------------------------ BASELINE full sizes, sampled
+def _full_size(orc, name, k, sample, workers=None):
+    wl = W.get_workload(name)
+    A, At = _mats(wl)
+    op = _dev_op(wl.mode, A, At, wl.r1_c)
+    a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+    est = P.Estimator(op, a, b, wl.degree, wl.num_probes, k, seed=wl.seed)
+    gp, stats = est.run()
+    torch.cuda.synchronize()
+    mu = est.mu.cpu().numpy()
+    st = stats.cpu().numpy()
+    assert st[2] == 1.0
+    omu = orc.moments(orc.Op(wl.mode, A, wl.r1_c), a, b, wl.degree, wl.seed, sample,
+                      workers=workers or len(sample))
+    _check_moments(mu[list(sample)], omu, wl.d)
+    c = orc.coeffs_log(a, b, wl.degree)
+    gpn = gp.cpu().numpy()
+    for i, p in enumerate(sample):
+        og = orc.gamma_from_moments(c, omu[i:i + 1])[0]
+        assert abs(gpn[p] - og) <= GAMMA_RTOL * abs(og) + 1e-12 * wl.d
+    return wl, st, a, b
+
+
+def test_full_config1_torus256(orc):
+    from oracle import closed_forms as cf
+    wl, st, a, b = _full_size(orc, "torus256", 32, [0, 31])
+    log_tau = P.log_tau_from_rank1(st[0], wl.r1_c, wl.d)
+    assert abs(log_tau - cf.torus_log_tau(256)) <= 4 * st[1]
+
+
+def test_full_config2_gmrf1000(orc):
+    from oracle import closed_forms as cf
+    wl, st, a, b = _full_size(orc, "gmrf1000", 64, [0, 37, 63])
+    assert abs(st[0] - cf.grid_logdet(1000, 0.24)) <= 4 * st[1]
+
+
+@pytest.mark.slow
+def test_full_config3_gmrf5000_bench_launch(orc):
+    """The bench launch configuration (k = 64, m = 128, two probe blocks)."""
+    from oracle import closed_forms as cf
+    wl, st, a, b = _full_size(orc, "gmrf5000", 64, [0, 127])
+    assert abs(st[0] - cf.grid_logdet(5000, 0.24)) <= 4 * st[1]
+
+
+@pytest.mark.slow
+def test_full_config4_btb4m(orc):
+    _full_size(orc, "btb4m", 64, [0, 63])
