@@ -30,7 +30,7 @@
  *   - Matrices are canonical CSR: row_ptr int64[n_rows+1] (row_ptr[0] = 0),
  *     col_idx int32[nnz] sorted & unique within a row, val fp64[nnz].
  *   - Probe-block layout on the device: W[d][k] fp64 row-major, the k probes of a
- *     block contiguous; k in {8, 16, 32, 64}.
+ *     block contiguous; k in {8, 16, 32, 64, 128}.
  */
 #ifndef CHEB_LOGDET_H
 #define CHEB_LOGDET_H

@@ -1,24 +1,27 @@
 // cheb_kernels.cuh -- sm_100a device kernels of the Chebyshev-Hutchinson hot path.
 //
-// Layout (DESIGN.md "Data layout in HBM"):
-//   W[d][K]  fp64, the K probes of a block contiguous per row (row = 8K bytes);
-//   each row is handled by a "group" of L = K/2 lanes, lane l owning probes
-//   2l, 2l+1 as one 16-byte double2 (fully coalesced 8K-byte row accesses).
-//   S[d][WORDS] uint32 packed probe signs (bit p%32 of word p/32 = 1 <=> v_p[i] = -1).
+// Layout (DESIGN.md §6):
+//   W[d][K]  fp64, the K probes of a block contiguous per row (row = 8K bytes).
+//   S[d][WORDS] uint32 packed probe signs (bit p%32 of word p/32 set <=> v_p[i] = -1).
 //
 // Kernels
+//   prep_kernel<MODE>               per-estimate operator prep: Ã's alpha/beta folded into a
+//                                   padded value copy, padded col/row_ptr copies for 16-byte
+//                                   bulk copies, "row has no stored diagonal" bitmap
 //   probe_init_kernel<K,MODE>       K1: v -> W_cur, S; mu_0 = v^T v; rank-1 s_0 = u^T v
-//   cheb_step_kernel<K,MODE,FIRST>  K2: fused CSR-SpMM x K probes + three-term
-//                                   recurrence + Ã scaling + rank-1 term + per-probe
-//                                   dot v^T w_j, deterministic last-CTA reduction (K4)
+//   cheb_step_kernel<K,MODE,FIRST>  K2: fused CSR-SpMM x K probes + three-term recurrence +
+//                                   Ã scaling + rank-1 term + per-probe dot v^T w_j, with a
+//                                   deterministic last-CTA reduction (K4)
 //   spmm_kernel<K>                  K3: Y = B W (first half of a B^T B application)
 //   finalize_kernel                 Gamma_p, Gamma, stderr
 //   bounds_btb_kernel               Johnson / norm bounds of B^T B
 //
-// Every kernel is a persistent grid (a multiple of the SM count) walking row
-// tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... in increasing order, so the
-// rows being processed chip-wide form one narrow moving window: the W_cur halo
-// rows i +- N of a stencil are re-read from L2, not HBM (SURVEY §7 "hard parts").
+// The step kernel is a persistent grid (SMs x resident CTAs) walking row tiles
+// t = blockIdx.x + i*gridDim.x in increasing order, so the rows in flight chip-wide form one
+// narrow window and the W_cur halo rows i +- N of a stencil are re-read from L2, not HBM.
+// Each CTA double-buffers its tiles in shared memory: one thread issues TMA bulk copies
+// (cp.async.bulk, mbarrier completion) of the NEXT tile's row_ptr slice, col/val range,
+// W_prev rows and sign words while all warps gather W_cur rows for the current tile.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -26,22 +29,101 @@
 namespace chebld {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 2;  // rows per group processed concurrently (memory-level parallelism)
 #ifndef CHEB_MIN_CTAS
-#define CHEB_MIN_CTAS 3     // resident CTAs per SM the step kernel is register-budgeted for
+#define CHEB_MIN_CTAS 4  // resident CTAs per SM the step kernel is register-budgeted for
 #endif
 
 enum { MODE_CSR = 0, MODE_RANK1 = 1, MODE_BTB = 2 };
 
+__host__ __device__ constexpr int words_for(int K) { return K >= 32 ? K / 32 : 1; }
+
+// Geometry of the step / spmm kernels: each lane owns PPL = 4 consecutive probes
+// (two 16-byte double2), L = K/4 lanes own a row; RPG rows per group per tile.
 template <int K>
 struct Geo {
-    static_assert(K == 8 || K == 16 || K == 32 || K == 64, "K in {8,16,32,64}");
-    static constexpr int L = K / 2;               // lanes per row
-    static constexpr int GROUPS = kThreads / L;   // row groups per CTA
-    static constexpr int WORDS = K >= 32 ? K / 32 : 1;
-    static constexpr int TILE = GROUPS * kUnroll; // rows per tile
-    static constexpr int RED_T = kThreads / K;    // threads per probe in the final reduction
+    static_assert(K == 8 || K == 16 || K == 32 || K == 64 || K == 128, "K in {8,...,128}");
+    static constexpr int PPL = 4;
+    static constexpr int L = K / PPL;               // lanes per row: 2..32
+    static constexpr int GROUPS = kThreads / L;     // rows in flight per CTA
+    static constexpr int RPG = 2;                   // rows per group per tile
+    static constexpr int TILE = GROUPS * RPG;       // rows per tile: 256 .. 16
+    static constexpr int WORDS = words_for(K);
+    static constexpr int CAP = TILE * 8;            // staged nnz capacity (avg 8 per row)
+    static constexpr int RED_T = kThreads / K;      // threads per probe in the final reduction
+    // shared-memory stage layout (bytes, every field 16-byte aligned)
+    static constexpr int WBYTES = TILE * K * 8;     // 16 KB
+    static constexpr int RPBYTES = (TILE + 2) * 8;
+    static constexpr int COLBYTES = (CAP + 8) * 4;
+    static constexpr int VALBYTES = (CAP + 4) * 8;
+    static constexpr int SGNBYTES = ((TILE * WORDS * 4 + 15) / 16) * 16;
+    static constexpr int UBYTES = ((TILE * 8 + 15) / 16) * 16;
 };
+
+template <int K, int MODE>
+struct StageLayout {
+    using G = Geo<K>;
+    static constexpr int OFF_WPREV = 0;
+    static constexpr int OFF_WCUR = OFF_WPREV + G::WBYTES;                       // BTB only
+    static constexpr int OFF_VAL = OFF_WCUR + (MODE == MODE_BTB ? G::WBYTES : 0);
+    static constexpr int OFF_RP = OFF_VAL + G::VALBYTES;
+    static constexpr int OFF_COL = OFF_RP + G::RPBYTES;
+    static constexpr int OFF_SGN = OFF_COL + G::COLBYTES;
+    static constexpr int OFF_U = OFF_SGN + G::SGNBYTES;                          // RANK1 only
+    static constexpr int BYTES = OFF_U + (MODE == MODE_RANK1 ? G::UBYTES : 0);
+    static constexpr int SMEM = 2 * BYTES;                                       // double buffer
+};
+
+// ---------------------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP)
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+        "[%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 
 // SplitMix64 at flat counter t of the stream seeded `seed` (reading G6).
 __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t t) {
@@ -51,71 +133,66 @@ __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t t) {
     return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ double2 ld_nc2(const double* p) {
+__device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
+
+__device__ __forceinline__ double2 ldg2(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
-}
-__device__ __forceinline__ double2 ld_cs2(const double* p) {
-    return __ldcs(reinterpret_cast<const double2*>(p));
-}
-__device__ __forceinline__ void st2(double* p, double2 v) {
-    *reinterpret_cast<double2*>(p) = v;
 }
 
 struct StepArgs {
-    int64_t d;          // rows of the gather matrix (= dimension of M)
+    int64_t d;            // rows of the gather matrix (= dimension of M)
     int64_t ntiles;
-    const int64_t* rp;  // gather matrix: A (csr/rank1) or B^T (btb)
-    const int32_t* ci;
-    const double* va;
-    const double* xg;   // gather source: W_cur (csr/rank1) or Y = B W_cur (btb)
-    const double* wcur; // W_cur (the -beta*w term)
-    double* wnext;      // in: W_prev (unless FIRST); out: W_next (in place)
+    const int64_t* rp;    // prepped gather matrix: padded row_ptr copy
+    const int32_t* ci;    //   padded col copy
+    const double* va;     //   padded scaled values (alpha*a, diagonal alpha*a_ii - beta)
+    const uint32_t* nodiag;  // bit i: row i has no stored diagonal (csr/rank1)
+    const double* xg;     // gather source: W_cur (csr/rank1) or Y = B W_cur (btb)
+    const double* wcur;   // W_cur
+    double* wnext;        // in: W_prev (unless FIRST); out: W_next (in place)
     const uint32_t* sbits;
-    double alpha, beta;
-    double r1c;          // rank-1 weight
-    const double* r1u;   // rank-1 u (nullptr = ones)
-    const double* s_cur; // [K] u^T w_{j-1}
-    double* s_next;      // [K] u^T w_j
-    double* part_mu;     // [gridDim.x][K]
-    double* part_s;      // [gridDim.x][K]
+    double beta;          // for rows without a stored diagonal (csr/rank1) and for btb
+    double r1c_alpha;     // alpha * c (rank-1)
+    const double* r1u;    // padded u copy (nullptr = ones)
+    const double* s_cur;  // [K] u^T w_{j-1}
+    double* s_next;       // [K] u^T w_j
+    double* part_mu;      // [gridDim.x][K]
+    double* part_s;       // [gridDim.x][K]
     unsigned int* ticket;
-    double* mu_out;      // mu_out[p*mu_stride + mu_col]
+    double* mu_out;       // mu_out[p*mu_stride + mu_col]
     int64_t mu_stride;
     int32_t mu_col;
-    int32_t kvalid;      // probes of this block that exist (<= K)
+    int32_t kvalid;       // probes of this block that exist (<= K)
 };
 
-// ---------------------------------------------------------------------------
-// Deterministic CTA + grid reduction of two per-thread double2 accumulators
-// (probes 2l, 2l+1).  Order: fixed shuffle tree inside a warp, warps in index
-// order, CTAs in a fixed strided order -- independent of timing.  The last CTA
-// to finish (atomic ticket) produces the final sums.
-// ---------------------------------------------------------------------------
-template <int K, bool HAS_S>
-__device__ __forceinline__ void grid_reduce_finish(double2 mu, double2 s, const StepArgs& a) {
-    using G = Geo<K>;
+// ---------------------------------------------------------------------------------------
+// Deterministic CTA + grid reduction of per-lane accumulators for probes pl..pl+PPL-1
+// (lane group size LG = K/PPL).  Fixed shuffle tree in a warp, warps in index order, CTAs
+// in a fixed strided order; the last CTA to finish (atomic ticket) writes the result.
+// ---------------------------------------------------------------------------------------
+template <int K, int PPL, bool HAS_S>
+__device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s)[PPL], const StepArgs& a) {
+    constexpr int LG = K / PPL;
+    constexpr int RED_T = kThreads / K;
     __shared__ double red_mu[kThreads / 32][K];
     __shared__ double red_s[HAS_S ? kThreads / 32 : 1][K];
-    __shared__ double fin_mu[G::RED_T][K];
-    __shared__ double fin_s[HAS_S ? G::RED_T : 1][K];
+    __shared__ double fin_mu[RED_T][K];
+    __shared__ double fin_s[HAS_S ? RED_T : 1][K];
     __shared__ bool is_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int lg = lane % G::L;
+    const int pl = (lane % LG) * PPL;
 #pragma unroll
-    for (int off = G::L; off < 32; off <<= 1) {
-        mu.x += __shfl_xor_sync(0xffffffffu, mu.x, off);
-        mu.y += __shfl_xor_sync(0xffffffffu, mu.y, off);
-        if (HAS_S) {
-            s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
-            s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+    for (int off = LG; off < 32; off <<= 1) {
+#pragma unroll
+        for (int q = 0; q < PPL; q++) {
+            mu[q] += __shfl_xor_sync(0xffffffffu, mu[q], off);
+            if (HAS_S) s[q] += __shfl_xor_sync(0xffffffffu, s[q], off);
         }
     }
-    if (lane < G::L) {
-        red_mu[warp][2 * lg] = mu.x;
-        red_mu[warp][2 * lg + 1] = mu.y;
-        if (HAS_S) {
-            red_s[warp][2 * lg] = s.x;
-            red_s[warp][2 * lg + 1] = s.y;
+    if (lane < LG) {
+#pragma unroll
+        for (int q = 0; q < PPL; q++) {
+            red_mu[warp][pl + q] = mu[q];
+            if (HAS_S) red_s[warp][pl + q] = s[q];
         }
     }
     __syncthreads();
@@ -132,7 +209,7 @@ __device__ __forceinline__ void grid_reduce_finish(double2 mu, double2 s, const 
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-        unsigned int prev = atomicAdd(a.ticket, 1u);
+        const unsigned int prev = atomicAdd(a.ticket, 1u);
         is_last = (prev == gridDim.x - 1);
     }
     __syncthreads();
@@ -141,7 +218,7 @@ __device__ __forceinline__ void grid_reduce_finish(double2 mu, double2 s, const 
     {
         const int p = tid % K, r = tid / K;
         double m = 0.0, t = 0.0;
-        for (int c = r; c < (int)gridDim.x; c += G::RED_T) {
+        for (int c = r; c < (int)gridDim.x; c += RED_T) {
             m += __ldcg(a.part_mu + (size_t)c * K + p);
             if (HAS_S) t += __ldcg(a.part_s + (size_t)c * K + p);
         }
@@ -152,7 +229,7 @@ __device__ __forceinline__ void grid_reduce_finish(double2 mu, double2 s, const 
     if (tid < K) {
         double m = 0.0, t = 0.0;
 #pragma unroll
-        for (int r = 0; r < G::RED_T; r++) {
+        for (int r = 0; r < RED_T; r++) {
             m += fin_mu[r][tid];
             if (HAS_S) t += fin_s[r][tid];
         }
@@ -162,231 +239,374 @@ __device__ __forceinline__ void grid_reduce_finish(double2 mu, double2 s, const 
     if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch (stream-ordered)
 }
 
-// ---------------------------------------------------------------------------
-// K1: probe initialisation.  W_cur[i][p] = v_p[i] = +-1 (global probe p0+p),
-// sign bits, mu_0 = v^T v (= d exactly), rank-1 s_0 = u^T v.
-// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Operator prep (once per estimate): padded copies for 16-byte bulk copies and the Ã map
+// folded into the values:  val'_e = alpha*a_e (- beta if e is row i's diagonal, csr/rank1).
+// ---------------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads)
+prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+            const double* __restrict__ va, double alpha, double beta, int64_t* __restrict__ rp2,
+            int64_t rp2_len, int32_t* __restrict__ ci2, double* __restrict__ va2,
+            uint32_t* __restrict__ nodiag, const double* __restrict__ u, double* __restrict__ u2) {
+    const int64_t nnz = rp[d];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of 32
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < d; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        bool has = true;
+        if (i < d) {
+            const int64_t e0 = rp[i], e1 = rp[i + 1];
+            rp2[i] = e0;
+            has = (MODE == MODE_BTB);
+            for (int64_t e = e0; e < e1; e++) {
+                const int32_t c = ci[e];
+                double v = alpha * va[e];
+                if (MODE != MODE_BTB && c == i) {
+                    v = fma(alpha, va[e], -beta);
+                    has = true;
+                }
+                ci2[e] = c;
+                va2[e] = v;
+            }
+            if (u2) u2[i] = u ? u[i] : 1.0;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, !has);
+        if ((threadIdx.x & 31) == 0 && i < d) nodiag[i >> 5] = m;
+    }
+    if (blockIdx.x == 0) {
+        for (int64_t k = d + threadIdx.x; k < rp2_len; k += blockDim.x) rp2[k] = nnz;
+        if (threadIdx.x < 8) ci2[nnz + threadIdx.x] = 0;
+        if (threadIdx.x < 4) va2[nnz + threadIdx.x] = 0.0;
+        if (u2 && threadIdx.x < 2) u2[d + threadIdx.x] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1: probe initialisation.  W_cur[i][p] = v_p[i] = +-1 (global probe p0+p), sign bits,
+// mu_0 = v^T v (= d exactly), rank-1 s_0 = u^T v.
+// ---------------------------------------------------------------------------------------
 template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads)
 probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* sbits) {
-    using G = Geo<K>;
+    constexpr int PPL = K <= 64 ? 2 : 4;
+    constexpr int LG = K / PPL;               // <= 32
+    constexpr int GROUPS = kThreads / LG;
+    constexpr int WORDS = words_for(K);
     constexpr bool HAS_S = (MODE == MODE_RANK1);
-    const int lg = threadIdx.x % G::L;
-    const int group = threadIdx.x / G::L;
-    const int p2 = 2 * lg;
+    const int lg = threadIdx.x % LG;
+    const int group = threadIdx.x / LG;
+    const int pl = PPL * lg;
     const uint64_t d = (uint64_t)a.d;
-    double2 mu = make_double2(0.0, 0.0), s = make_double2(0.0, 0.0);
-    const int64_t rows_per_iter = (int64_t)G::GROUPS;
-    const int64_t niter = (a.d + rows_per_iter - 1) / rows_per_iter;
+    double mu[PPL], s[PPL];
+#pragma unroll
+    for (int q = 0; q < PPL; q++) mu[q] = s[q] = 0.0;
+    const int64_t niter = (a.d + GROUPS - 1) / GROUPS;
     for (int64_t t = blockIdx.x; t < niter; t += gridDim.x) {
-        const int64_t i = t * rows_per_iter + group;
+        const int64_t i = t * GROUPS + group;
         const bool ok = i < a.d;
         uint32_t bits = 0;
-        double v0 = 1.0, v1 = 1.0;
         if (ok) {
-            const uint64_t z0 = splitmix64_at(seed, (p0 + p2) * d + (uint64_t)i + 1ull);
-            const uint64_t z1 = splitmix64_at(seed, (p0 + p2 + 1) * d + (uint64_t)i + 1ull);
-            const uint32_t b0 = (uint32_t)(z0 >> 63), b1 = (uint32_t)(z1 >> 63);
-            v0 = b0 ? -1.0 : 1.0;
-            v1 = b1 ? -1.0 : 1.0;
-            bits = (b0 << (p2 & 31)) | (b1 << ((p2 + 1) & 31));
-            st2(w0 + (size_t)i * K + p2, make_double2(v0, v1));
-            mu.x += v0 * v0;
-            mu.y += v1 * v1;
+            double v[PPL];
+#pragma unroll
+            for (int q = 0; q < PPL; q++) {
+                const uint64_t z = splitmix64_at(seed, (p0 + pl + q) * d + (uint64_t)i + 1ull);
+                const uint32_t bq = (uint32_t)(z >> 63);
+                v[q] = bq ? -1.0 : 1.0;
+                bits |= bq << ((pl + q) & 31);
+                mu[q] += v[q] * v[q];
+            }
+#pragma unroll
+            for (int q = 0; q < PPL; q += 2)
+                *reinterpret_cast<double2*>(w0 + (size_t)i * K + pl + q) = make_double2(v[q], v[q + 1]);
             if (HAS_S) {
-                const double u = a.r1u ? __ldg(a.r1u + i) : 1.0;
-                s.x += u * v0;
-                s.y += u * v1;
+                const double u = a.r1u ? a.r1u[i] : 1.0;
+#pragma unroll
+                for (int q = 0; q < PPL; q++) s[q] += u * v[q];
             }
         }
-        // OR the bits of the (up to) 16 lanes that share one 32-bit word
-        constexpr int WL = G::L < 16 ? G::L : 16;
+        // OR the bits of the lanes that share one 32-bit word
+        constexpr int LW = (32 / PPL) < LG ? (32 / PPL) : LG;
 #pragma unroll
-        for (int off = 1; off < WL; off <<= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, off);
-        if (ok && (lg % 16) == 0) sbits[(size_t)i * G::WORDS + (p2 >> 5)] = bits;
+        for (int off = 1; off < LW; off <<= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, off);
+        if (ok && (lg % LW) == 0) sbits[(size_t)i * WORDS + (pl >> 5)] = bits;
     }
-    grid_reduce_finish<K, HAS_S>(mu, s, a);
+    grid_reduce_finish<K, PPL, HAS_S>(mu, s, a);
 }
 
-// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
 // K2: the fused Chebyshev step (w_j from w_{j-1}, w_{j-2}):
-//   y    = alpha * (G xg)_i [+ alpha*c*u_i*s_cur] - beta * wcur_i
-//   w_j  = FIRST ? y : 2y - w_{j-2}          (written over w_{j-2})
-//   mu_j += v_i * w_j ; rank-1: s_j += u_i * w_j
-// ---------------------------------------------------------------------------
+//   y    = sum_e val'_e xg[col_e]  [- beta*wcur_i if no stored diagonal / btb]
+//          [+ alpha*c*u_i*s_cur]                    (Ã w_{j-1}, alpha/beta folded in val')
+//   w_j  = FIRST ? y : 2y - w_{j-2}                 (written over w_{j-2})
+//   mu_j += v_i * w_j ;  rank-1: s_j += u_i * w_j
+// ---------------------------------------------------------------------------------------
+template <int K, int MODE, bool FIRST, bool STAGED>
+__device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
+                                          int64_t base_c, int64_t base_v, double2 r1a, double2 r1b,
+                                          double (&mu)[4], double (&s)[4]) {
+    using G = Geo<K>;
+    using SL = StageLayout<K, MODE>;
+    constexpr bool HAS_S = (MODE == MODE_RANK1);
+    const int lg = threadIdx.x % G::L;
+    const int grp = threadIdx.x / G::L;
+    const int pl = 4 * lg;
+    const int64_t* rp_s = reinterpret_cast<const int64_t*>(st + SL::OFF_RP);
+    const int32_t* col_s = reinterpret_cast<const int32_t*>(st + SL::OFF_COL);
+    const double* val_s = reinterpret_cast<const double*>(st + SL::OFF_VAL);
+    const double* wp_s = reinterpret_cast<const double*>(st + SL::OFF_WPREV);
+    const double* wc_s = reinterpret_cast<const double*>(st + SL::OFF_WCUR);
+    const uint32_t* sg_s = reinterpret_cast<const uint32_t*>(st + SL::OFF_SGN);
+    const double* u_s = reinterpret_cast<const double*>(st + SL::OFF_U);
+#pragma unroll
+    for (int rr = 0; rr < G::RPG; rr++) {
+        const int lr = grp + rr * G::GROUPS;
+        if (lr >= rows) break;
+        const int64_t i = r0 + lr;
+        const int64_t e_lo = rp_s[lr], e_hi = rp_s[lr + 1];
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int64_t e = e_lo;
+        for (; e + 4 <= e_hi; e += 4) {
+            int32_t c[4];
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                c[q] = STAGED ? col_s[e + q - base_c] : __ldg(a.ci + e + q);
+                v[q] = STAGED ? val_s[e + q - base_v] : __ldg(a.va + e + q);
+            }
+            double2 x0[4], x1[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const double* p = a.xg + (size_t)(uint32_t)c[q] * K + pl;
+                x0[q] = ldg2(p);
+                x1[q] = ldg2(p + 2);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                acc0.x = fma(v[q], x0[q].x, acc0.x);
+                acc0.y = fma(v[q], x0[q].y, acc0.y);
+                acc1.x = fma(v[q], x1[q].x, acc1.x);
+                acc1.y = fma(v[q], x1[q].y, acc1.y);
+            }
+        }
+        for (; e < e_hi; e++) {
+            const int32_t c = STAGED ? col_s[e - base_c] : __ldg(a.ci + e);
+            const double v = STAGED ? val_s[e - base_v] : __ldg(a.va + e);
+            const double* p = a.xg + (size_t)(uint32_t)c * K + pl;
+            const double2 x0 = ldg2(p), x1 = ldg2(p + 2);
+            acc0.x = fma(v, x0.x, acc0.x);
+            acc0.y = fma(v, x0.y, acc0.y);
+            acc1.x = fma(v, x1.x, acc1.x);
+            acc1.y = fma(v, x1.y, acc1.y);
+        }
+        // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
+        if (MODE == MODE_BTB) {
+            const double2 w0 = *reinterpret_cast<const double2*>(wc_s + lr * K + pl);
+            const double2 w1 = *reinterpret_cast<const double2*>(wc_s + lr * K + pl + 2);
+            acc0.x = fma(-a.beta, w0.x, acc0.x);
+            acc0.y = fma(-a.beta, w0.y, acc0.y);
+            acc1.x = fma(-a.beta, w1.x, acc1.x);
+            acc1.y = fma(-a.beta, w1.y, acc1.y);
+        } else if ((__ldg(a.nodiag + (i >> 5)) >> (i & 31)) & 1u) {
+            const double2 w0 = ldg2(a.wcur + (size_t)i * K + pl);
+            const double2 w1 = ldg2(a.wcur + (size_t)i * K + pl + 2);
+            acc0.x = fma(-a.beta, w0.x, acc0.x);
+            acc0.y = fma(-a.beta, w0.y, acc0.y);
+            acc1.x = fma(-a.beta, w1.x, acc1.x);
+            acc1.y = fma(-a.beta, w1.y, acc1.y);
+        }
+        double ui = 1.0;
+        if (HAS_S) {
+            ui = a.r1u ? u_s[lr] : 1.0;
+            acc0.x = fma(ui, r1a.x, acc0.x);
+            acc0.y = fma(ui, r1a.y, acc0.y);
+            acc1.x = fma(ui, r1b.x, acc1.x);
+            acc1.y = fma(ui, r1b.y, acc1.y);
+        }
+        double2 n0, n1;
+        if (FIRST) {
+            n0 = acc0;
+            n1 = acc1;
+        } else {
+            const double2 p0 = *reinterpret_cast<const double2*>(wp_s + lr * K + pl);
+            const double2 p1 = *reinterpret_cast<const double2*>(wp_s + lr * K + pl + 2);
+            n0 = make_double2(2.0 * acc0.x - p0.x, 2.0 * acc0.y - p0.y);
+            n1 = make_double2(2.0 * acc1.x - p1.x, 2.0 * acc1.y - p1.y);
+        }
+        double* out = a.wnext + (size_t)i * K + pl;
+        __stcs(reinterpret_cast<double2*>(out), n0);
+        __stcs(reinterpret_cast<double2*>(out + 2), n1);
+        const uint32_t b = sg_s[lr * G::WORDS + (pl >> 5)] >> (pl & 31);
+        mu[0] += (b & 1u) ? -n0.x : n0.x;
+        mu[1] += (b & 2u) ? -n0.y : n0.y;
+        mu[2] += (b & 4u) ? -n1.x : n1.x;
+        mu[3] += (b & 8u) ? -n1.y : n1.y;
+        if (HAS_S) {
+            s[0] = fma(ui, n0.x, s[0]);
+            s[1] = fma(ui, n0.y, s[1]);
+            s[2] = fma(ui, n1.x, s[2]);
+            s[3] = fma(ui, n1.y, s[3]);
+        }
+    }
+}
+
+// resident CTAs per SM each mode is register-budgeted for (BTB is smem-limited to 2)
+__host__ __device__ constexpr int min_ctas(int mode) {
+    return mode == MODE_CSR ? CHEB_MIN_CTAS : (mode == MODE_RANK1 ? 3 : 2);
+}
+
 template <int K, int MODE, bool FIRST>
-__global__ void __launch_bounds__(kThreads, CHEB_MIN_CTAS)
+__global__ void __launch_bounds__(kThreads, min_ctas(MODE))
 cheb_step_kernel(StepArgs a) {
     using G = Geo<K>;
+    using SL = StageLayout<K, MODE>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
-    constexpr int U = kUnroll;
-    const int lg = threadIdx.x % G::L;
-    const int group = threadIdx.x / G::L;
-    const int p2 = 2 * lg;
-    const int sh = p2 & 31, wsel = p2 >> 5;
-    double2 mu = make_double2(0.0, 0.0), s = make_double2(0.0, 0.0);
-    double2 r1 = make_double2(0.0, 0.0);
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int64_t s_base_c[2], s_base_v[2];
+    __shared__ int s_fit[2];
+
+    const int tid = threadIdx.x;
+    const int pl = 4 * (tid % G::L);
+    double mu[4] = {0.0, 0.0, 0.0, 0.0}, s[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
     if (HAS_S) {
-        const double2 sc = *reinterpret_cast<const double2*>(a.s_cur + p2);
-        r1 = make_double2(a.alpha * a.r1c * sc.x, a.alpha * a.r1c * sc.y);
+        r1a = make_double2(a.r1c_alpha * a.s_cur[pl], a.r1c_alpha * a.s_cur[pl + 1]);
+        r1b = make_double2(a.r1c_alpha * a.s_cur[pl + 2], a.r1c_alpha * a.s_cur[pl + 3]);
     }
-    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        int64_t row[U], rs[U], len[U];
-        bool ok[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            row[u] = t * G::TILE + u * G::GROUPS + group;
-            ok[u] = row[u] < a.d;
-            rs[u] = ok[u] ? __ldg(a.rp + row[u]) : 0;
-            len[u] = ok[u] ? __ldg(a.rp + row[u] + 1) - rs[u] : 0;
+    const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    // ---- producer (thread 0): issue the bulk copies of tile t into stage b
+    uint64_t pol = 0;
+    auto issue = [&](int64_t t, int b, int64_t e0, int64_t e1) {
+        unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
+        const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+        const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
+        s_fit[b] = fit;
+        s_base_c[b] = c0;
+        s_base_v[b] = v0;
+        const uint32_t wbytes = (uint32_t)rows * K * 8;
+        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+        uint32_t bytes = G::RPBYTES + sgbytes;
+        if (!FIRST) bytes += wbytes;
+        if (MODE == MODE_BTB) bytes += wbytes;
+        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+        const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
+        if (HAS_S && a.r1u) bytes += ubytes;
+        mbar_expect_tx(&bar[b], bytes);
+        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
+        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        if (!FIRST) bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], pol);
+        if (MODE == MODE_BTB) bulk_g2s(st + SL::OFF_WCUR, a.wcur + (size_t)r0 * K, wbytes, &bar[b]);
+        if (fit) {
+            bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
+            bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
         }
-        double2 wp[U];
-        uint32_t sw[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            wp[u] = make_double2(0.0, 0.0);
-            if (!FIRST && ok[u]) wp[u] = ld_cs2(a.wnext + (size_t)row[u] * K + p2);
-            sw[u] = ok[u] ? __ldg(a.sbits + (size_t)row[u] * G::WORDS + wsel) : 0u;
-        }
-        double2 acc[U], xd[U];
-        bool found[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            acc[u] = make_double2(0.0, 0.0);
-            xd[u] = make_double2(0.0, 0.0);
-            found[u] = false;
-        }
-        int64_t maxlen = len[0];
-#pragma unroll
-        for (int u = 1; u < U; u++) maxlen = len[u] > maxlen ? len[u] : maxlen;
-        for (int64_t e0 = 0; e0 < maxlen; e0 += 4) {
-            int c[U][4];
-            double v[U][4];
-            double2 x[U][4];
-#pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const bool in = e0 + q < len[u];
-                    c[u][q] = in ? __ldg(a.ci + rs[u] + e0 + q) : -1;
-                    v[u][q] = in ? __ldg(a.va + rs[u] + e0 + q) : 0.0;
-                }
-#pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int q = 0; q < 4; q++)
-                    x[u][q] = c[u][q] >= 0 ? ld_nc2(a.xg + (size_t)c[u][q] * K + p2)
-                                           : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    acc[u].x = fma(v[u][q], x[u][q].x, acc[u].x);
-                    acc[u].y = fma(v[u][q], x[u][q].y, acc[u].y);
-                    if (MODE != MODE_BTB && c[u][q] == row[u]) {
-                        xd[u] = x[u][q];
-                        found[u] = true;
-                    }
-                }
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (!ok[u]) continue;
-            if (MODE == MODE_BTB || !found[u]) xd[u] = ld_nc2(a.wcur + (size_t)row[u] * K + p2);
-            double yx = a.alpha * acc[u].x - a.beta * xd[u].x;
-            double yy = a.alpha * acc[u].y - a.beta * xd[u].y;
-            double ui = 1.0;
-            if (HAS_S) {
-                ui = a.r1u ? __ldg(a.r1u + row[u]) : 1.0;
-                yx = fma(ui, r1.x, yx);
-                yy = fma(ui, r1.y, yy);
-            }
-            double2 wn;
-            if (FIRST) {
-                wn = make_double2(yx, yy);
-            } else {
-                wn = make_double2(2.0 * yx - wp[u].x, 2.0 * yy - wp[u].y);
-            }
-            __stcs(reinterpret_cast<double2*>(a.wnext + (size_t)row[u] * K + p2), wn);
-            const uint32_t b = sw[u] >> sh;
-            mu.x += (b & 1u) ? -wn.x : wn.x;
-            mu.y += (b & 2u) ? -wn.y : wn.y;
-            if (HAS_S) {
-                s.x = fma(ui, wn.x, s.x);
-                s.y = fma(ui, wn.y, s.y);
-            }
+        if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
+    };
+    auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
+    auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
+        const int64_t r0 = t * G::TILE;
+        e0 = __ldg(a.rp + r0);
+        e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+    };
+
+    int64_t ne0 = 0, ne1 = 0;
+    if (tid == 0) {
+        pol = policy_evict_first();
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        for (int64_t i = 0; i < 2 && i < nmine; i++) {
+            int64_t e0, e1;
+            bounds(tile_of(i), e0, e1);
+            issue(tile_of(i), (int)i, e0, e1);
         }
     }
-    grid_reduce_finish<K, HAS_S>(mu, s, a);
+    __syncthreads();
+
+    for (int64_t it = 0; it < nmine; it++) {
+        const int b = (int)(it & 1);
+        const uint32_t phase = (uint32_t)((it >> 1) & 1);
+        const int64_t t = tile_of(it);
+        if (tid == 0 && it + 2 < nmine) bounds(tile_of(it + 2), ne0, ne1);  // consumed below
+        mbar_wait(&bar[b], phase);
+        const unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        if (s_fit[b])
+            step_tile<K, MODE, FIRST, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu, s);
+        else
+            step_tile<K, MODE, FIRST, false>(a, st, r0, rows, 0, 0, r1a, r1b, mu, s);
+        __syncthreads();  // every warp is done with stage b
+        if (tid == 0 && it + 2 < nmine) issue(tile_of(it + 2), b, ne0, ne1);
+    }
+    grid_reduce_finish<K, 4, HAS_S>(mu, s, a);
 }
 
-// ---------------------------------------------------------------------------
-// K3: Y = B W (first half of applying B^T B; Alg. 2 via P:312-314)
-// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// K3: Y = B W (first half of applying B^T B; Alg. 2 via P:312-314).  Plain gather SpMM.
+// ---------------------------------------------------------------------------------------
 template <int K>
 __global__ void __launch_bounds__(kThreads, CHEB_MIN_CTAS)
-spmm_kernel(int64_t d, int64_t ntiles, const int64_t* __restrict__ rp,
-            const int32_t* __restrict__ ci, const double* __restrict__ va,
-            const double* __restrict__ x, double* __restrict__ y) {
+spmm_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+            const double* __restrict__ va, const double* __restrict__ x, double* __restrict__ y) {
     using G = Geo<K>;
-    constexpr int U = kUnroll;
     const int lg = threadIdx.x % G::L;
-    const int group = threadIdx.x / G::L;
-    const int p2 = 2 * lg;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int64_t row[U], rs[U], len[U];
-        bool ok[U];
+    const int grp = threadIdx.x / G::L;
+    const int pl = 4 * lg;
+    const int64_t ngroups_total = (int64_t)gridDim.x * G::GROUPS;
+    for (int64_t i = (int64_t)blockIdx.x * G::GROUPS + grp; i < d; i += ngroups_total) {
+        const int64_t e_lo = __ldg(rp + i), e_hi = __ldg(rp + i + 1);
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int64_t e = e_lo;
+        for (; e + 4 <= e_hi; e += 4) {
+            int32_t c[4];
+            double v[4];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            row[u] = t * G::TILE + u * G::GROUPS + group;
-            ok[u] = row[u] < d;
-            rs[u] = ok[u] ? __ldg(rp + row[u]) : 0;
-            len[u] = ok[u] ? __ldg(rp + row[u] + 1) - rs[u] : 0;
+            for (int q = 0; q < 4; q++) {
+                c[q] = __ldg(ci + e + q);
+                v[q] = __ldg(va + e + q);
+            }
+            double2 x0[4], x1[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const double* p = x + (size_t)(uint32_t)c[q] * K + pl;
+                x0[q] = ldg2(p);
+                x1[q] = ldg2(p + 2);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                acc0.x = fma(v[q], x0[q].x, acc0.x);
+                acc0.y = fma(v[q], x0[q].y, acc0.y);
+                acc1.x = fma(v[q], x1[q].x, acc1.x);
+                acc1.y = fma(v[q], x1[q].y, acc1.y);
+            }
         }
-        double2 acc[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) acc[u] = make_double2(0.0, 0.0);
-        int64_t maxlen = len[0];
-#pragma unroll
-        for (int u = 1; u < U; u++) maxlen = len[u] > maxlen ? len[u] : maxlen;
-        for (int64_t e0 = 0; e0 < maxlen; e0 += 4) {
-            int c[U][4];
-            double v[U][4];
-            double2 xx[U][4];
-#pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const bool in = e0 + q < len[u];
-                    c[u][q] = in ? __ldg(ci + rs[u] + e0 + q) : -1;
-                    v[u][q] = in ? __ldg(va + rs[u] + e0 + q) : 0.0;
-                }
-#pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int q = 0; q < 4; q++)
-                    xx[u][q] = c[u][q] >= 0 ? ld_nc2(x + (size_t)c[u][q] * K + p2)
-                                            : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < U; u++)
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    acc[u].x = fma(v[u][q], xx[u][q].x, acc[u].x);
-                    acc[u].y = fma(v[u][q], xx[u][q].y, acc[u].y);
-                }
+        for (; e < e_hi; e++) {
+            const int32_t c = __ldg(ci + e);
+            const double v = __ldg(va + e);
+            const double* p = x + (size_t)(uint32_t)c * K + pl;
+            const double2 x0 = ldg2(p), x1 = ldg2(p + 2);
+            acc0.x = fma(v, x0.x, acc0.x);
+            acc0.y = fma(v, x0.y, acc0.y);
+            acc1.x = fma(v, x1.x, acc1.x);
+            acc1.y = fma(v, x1.y, acc1.y);
         }
-#pragma unroll
-        for (int u = 0; u < U; u++)
-            if (ok[u]) st2(y + (size_t)row[u] * K + p2, acc[u]);
+        double* out = y + (size_t)i * K + pl;
+        *reinterpret_cast<double2*>(out) = acc0;
+        *reinterpret_cast<double2*>(out + 2) = acc1;
     }
 }
 
-// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
 // Accumulation (reading G7): one CTA.
-// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
-finalize_kernel(const double* __restrict__ mu, const double* __restrict__ c, int64_t m,
-                int32_t n, double* __restrict__ gamma_p, double* __restrict__ stats) {
+finalize_kernel(const double* __restrict__ mu, const double* __restrict__ c, int64_t m, int32_t n,
+                double* __restrict__ gamma_p, double* __restrict__ stats) {
     for (int64_t p = threadIdx.x; p < m; p += blockDim.x) {
         const double* row = mu + (size_t)p * (n + 1);
         double g = 0.0;
@@ -414,13 +634,12 @@ finalize_kernel(const double* __restrict__ mu, const double* __restrict__ c, int
     }
 }
 
-// ---------------------------------------------------------------------------
-// Spectral interval of B^T B.  out[0] <- min_i s_i as an ordered
-// key, out[1] <- max row abs sum, out[2] <- max column abs sum (bit patterns of
-// non-negative doubles order like integers).
-// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Spectral interval of B^T B.  out[0] <- min_i s_i as an ordered key,
+// out[1] <- max row abs sum, out[2] <- max column abs sum.
+// ---------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long order_key(double x) {
-    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 

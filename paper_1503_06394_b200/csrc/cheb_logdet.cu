@@ -82,29 +82,43 @@ int sm_count() {
 constexpr int kMaxCtasPerSm = 8;  // partial buffers are sized for this
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64; }
+bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64 || k == 128; }
+
+int tile_rows(int k) { return 2 * kThreads * 4 / k; }  // Geo<K>::TILE
 
 struct Layout {
-    size_t w0, w1, y, sbits, part_mu, part_s, sbuf, ticket, total;
+    size_t w0, w1, y, sbits, part_mu, part_s, sbuf, ticket;
+    size_t rp2, ci2, va2, nodiag, u2, total;
+    int64_t rp2_len;
 };
 
-Layout plan(int64_t d, int k, int kind, int sms) {
+// Workspace of cheb_moments for dimension d, gather-matrix nnz, probe block k.
+Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     Layout L{};
     size_t off = 0;
     const size_t wbytes = align256((size_t)d * k * sizeof(double));
     const int words = k >= 32 ? k / 32 : 1;
     const size_t maxgrid = (size_t)sms * kMaxCtasPerSm;
+    const int64_t ntiles = (d + tile_rows(k) - 1) / tile_rows(k);
     L.w0 = off; off += wbytes;
     L.w1 = off; off += wbytes;
     L.y = off; if (kind == CL_OP_BTB) off += wbytes;
-    L.sbits = off; off += align256((size_t)d * words * sizeof(uint32_t));
+    L.sbits = off; off += align256((size_t)d * words * sizeof(uint32_t) + 16);
     L.part_mu = off; off += align256(maxgrid * k * sizeof(double));
     L.part_s = off; off += align256(maxgrid * k * sizeof(double));
     L.sbuf = off; off += align256(2 * (size_t)k * sizeof(double));
     L.ticket = off; off += 256;
+    L.rp2_len = ntiles * tile_rows(k) + 2;
+    L.rp2 = off; off += align256((size_t)L.rp2_len * sizeof(int64_t));
+    L.ci2 = off; off += align256(((size_t)nnz + 8) * sizeof(int32_t));
+    L.va2 = off; off += align256(((size_t)nnz + 4) * sizeof(double));
+    L.nodiag = off; off += align256(((size_t)d / 32 + 1) * sizeof(uint32_t));
+    L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
     L.total = off;
     return L;
 }
+
+int64_t gather_nnz(const cl_operator* op) { return op->kind == CL_OP_BTB ? op->At.nnz : op->A.nnz; }
 
 int check_csr(const cl_csr& A, const char* name) {
     if (A.n_rows < 0 || A.n_cols < 0 || A.nnz < 0)
@@ -143,14 +157,30 @@ int check_ab(double a, double b, int32_t degree) {
 }
 
 template <typename Kern>
-int grid_for(Kern kern, int64_t ntiles, int sms) {
+int grid_for(Kern kern, int64_t ntiles, int sms, size_t dyn_smem = 0) {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0);
+    if (dyn_smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, dyn_smem);
     if (occ < 1) occ = 1;
     if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
     int64_t g = (int64_t)sms * occ;
     if (g > ntiles) g = ntiles;
     return (int)(g < 1 ? 1 : g);
+}
+
+// ---- operator prep (once per cheb_moments call): scaled/padded gather matrix ---------
+template <int MODE>
+void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const Layout& L,
+              cudaStream_t st, int sms) {
+    const cl_csr& G2 = (MODE == MODE_BTB) ? op->At : op->A;
+    const int64_t d = G2.n_rows;
+    int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sms * 8);
+    if (grid < 1) grid = 1;
+    prep_kernel<MODE><<<grid, kThreads, 0, st>>>(
+        d, G2.row_ptr, G2.col_idx, G2.val, alpha, beta, (int64_t*)(ws + L.rp2), L.rp2_len,
+        (int32_t*)(ws + L.ci2), (double*)(ws + L.va2), (uint32_t*)(ws + L.nodiag),
+        MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr);
+    g_launches++;
 }
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
@@ -159,6 +189,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
               int64_t mu_stride, cudaStream_t st, int sms) {
     using G = Geo<K>;
+    using SL = StageLayout<K, MODE>;
     const int64_t d = op->A.n_cols;
     double* w[2] = {(double*)(ws + L.w0), (double*)(ws + L.w1)};
     double* y = (double*)(ws + L.y);
@@ -167,11 +198,14 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
 
     StepArgs a{};
     a.d = d;
+    a.rp = (const int64_t*)(ws + L.rp2);
+    a.ci = (const int32_t*)(ws + L.ci2);
+    a.va = (const double*)(ws + L.va2);
+    a.nodiag = (const uint32_t*)(ws + L.nodiag);
     a.sbits = sbits;
-    a.alpha = alpha;
     a.beta = beta;
-    a.r1c = op->r1_c;
-    a.r1u = (MODE == MODE_RANK1) ? op->r1_u : nullptr;
+    a.r1c_alpha = alpha * op->r1_c;
+    a.r1u = (MODE == MODE_RANK1 && op->r1_u) ? (const double*)(ws + L.u2) : nullptr;
     a.part_mu = (double*)(ws + L.part_mu);
     a.part_s = (double*)(ws + L.part_s);
     a.ticket = (unsigned int*)(ws + L.ticket);
@@ -181,7 +215,8 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
 
     // K1
     {
-        const int64_t niter = (d + G::GROUPS - 1) / G::GROUPS;
+        constexpr int groups = kThreads / (K <= 64 ? K / 2 : K / 4);
+        const int64_t niter = (d + groups - 1) / groups;
         const int grid = grid_for(probe_init_kernel<K, MODE>, niter, sms);
         a.mu_col = 0;
         a.s_next = sbuf;
@@ -190,25 +225,21 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     }
     if (n < 1) return CL_OK;
 
-    const cl_csr& G2 = (MODE == MODE_BTB) ? op->At : op->A;  // gather matrix of K2
-    a.rp = G2.row_ptr;
-    a.ci = G2.col_idx;
-    a.va = G2.val;
     a.ntiles = (d + G::TILE - 1) / G::TILE;
-    const int grid_first = grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms);
-    const int grid_step = grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms);
+    const size_t smem = SL::SMEM;
+    const int grid_first = grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem);
+    const int grid_step = grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem);
     int grid_spmm = 1;
-    int64_t ntiles_b = 0;
     if (MODE == MODE_BTB) {
-        ntiles_b = (op->A.n_rows + G::TILE - 1) / G::TILE;
-        grid_spmm = grid_for(spmm_kernel<K>, ntiles_b, sms);
+        const int64_t ng = (op->A.n_rows + G::GROUPS - 1) / G::GROUPS;
+        grid_spmm = grid_for(spmm_kernel<K>, ng, sms);
     }
     for (int32_t j = 1; j <= n; j++) {
         const double* cur = w[(j - 1) & 1];
         double* nxt = w[j & 1];
         if (MODE == MODE_BTB) {
-            spmm_kernel<K><<<grid_spmm, kThreads, 0, st>>>(op->A.n_rows, ntiles_b, op->A.row_ptr,
-                                                          op->A.col_idx, op->A.val, cur, y);
+            spmm_kernel<K><<<grid_spmm, kThreads, 0, st>>>(op->A.n_rows, op->A.row_ptr, op->A.col_idx,
+                                                          op->A.val, cur, y);
             g_launches++;
         }
         a.xg = (MODE == MODE_BTB) ? y : cur;
@@ -219,9 +250,9 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.mu_col = j;
         ProfScope ps(st);
         if (j == 1)
-            cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, 0, st>>>(a);
+            cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem, st>>>(a);
         else
-            cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, 0, st>>>(a);
+            cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem, st>>>(a);
         g_launches++;
     }
     return CL_OK;
@@ -241,8 +272,18 @@ int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, 
     }
 }
 
+void prep_mode(const cl_operator* op, double alpha, double beta, char* ws, const Layout& L,
+               cudaStream_t st, int sms) {
+    switch (op->kind) {
+        case CL_OP_CSR: run_prep<MODE_CSR>(op, alpha, beta, ws, L, st, sms); break;
+        case CL_OP_CSR_RANK1: run_prep<MODE_RANK1>(op, alpha, beta, ws, L, st, sms); break;
+        default: run_prep<MODE_BTB>(op, alpha, beta, ws, L, st, sms); break;
+    }
+}
+
 int pick_k(int64_t m) {
     // Largest block the probe count fills; matrix bytes amortise over k.
+    if (m >= 128) return 128;
     if (m >= 64) return 64;
     if (m > 16) return 32;
     if (m > 8) return 16;
@@ -320,10 +361,10 @@ int cheb_coeffs_log(double a, double b, int32_t degree, double* c_out) {
 size_t cheb_workspace_bytes(const cl_operator* op, int32_t probe_block) {
     if (check_op(op)) return 0;
     if (!valid_k(probe_block)) {
-        fail(CL_EINVAL, "probe_block must be 8, 16, 32 or 64 (got %d)", probe_block);
+        fail(CL_EINVAL, "probe_block must be 8, 16, 32, 64 or 128 (got %d)", probe_block);
         return 0;
     }
-    return plan(op->A.n_cols, probe_block, op->kind, sm_count()).total;
+    return plan(op->A.n_cols, gather_nnz(op), probe_block, op->kind, sm_count()).total;
 }
 
 int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
@@ -334,10 +375,10 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
     if ((rc = check_ab(a, b, degree))) return rc;
     if (probe_begin < 0 || probe_end <= probe_begin)
         return fail(CL_EINVAL, "need 0 <= probe_begin < probe_end");
-    if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32 or 64");
+    if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32, 64 or 128");
     if (!workspace || !mu_out) return fail(CL_EINVAL, "NULL workspace or mu_out");
     const int sms = sm_count();
-    const Layout L = plan(op->A.n_cols, probe_block, op->kind, sms);
+    const Layout L = plan(op->A.n_cols, gather_nnz(op), probe_block, op->kind, sms);
     if (ws_bytes < L.total)
         return fail(CL_ENOMEM, "workspace too small: %zu < %zu", ws_bytes, L.total);
     if ((uintptr_t)workspace & 255) return fail(CL_EINVAL, "workspace must be 256-byte aligned");
@@ -347,6 +388,7 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
     const int64_t stride = (int64_t)degree + 1;
     CL_CUDA(cudaGetLastError());
     CL_CUDA(cudaMemsetAsync(ws + L.ticket, 0, 256, st));
+    prep_mode(op, alpha, beta, ws, L, st, sms);
     for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
         const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
@@ -354,7 +396,8 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
             case 8: rc = run_block_mode<8>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
             case 16: rc = run_block_mode<16>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
             case 32: rc = run_block_mode<32>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
-            default: rc = run_block_mode<64>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+            case 64: rc = run_block_mode<64>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+            default: rc = run_block_mode<128>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
         }
         if (rc) return rc;
     }
@@ -382,8 +425,8 @@ struct DevBuf {
 int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
                   uint64_t seed, int32_t probe_block, cl_result* out, cudaStream_t st) {
     const int k = probe_block ? probe_block : pick_k(num_probes);
-    if (!valid_k(k)) return fail(CL_EINVAL, "probe_block must be 0, 8, 16, 32 or 64");
-    const size_t ws_bytes = plan(op->A.n_cols, k, op->kind, sm_count()).total;
+    if (!valid_k(k)) return fail(CL_EINVAL, "probe_block must be 0, 8, 16, 32, 64 or 128");
+    const size_t ws_bytes = plan(op->A.n_cols, gather_nnz(op), k, op->kind, sm_count()).total;
     const size_t mu_n = (size_t)num_probes * (degree + 1);
     DevBuf ws, aux;
     CL_CUDA(cudaMalloc(&ws.p, ws_bytes));
@@ -516,7 +559,7 @@ int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_blo
     op.kind = CL_OP_CSR;
     op.A.n_rows = op.A.n_cols = d;
     const int sms = sm_count();
-    const Layout L = plan(d, probe_block, CL_OP_CSR, sms);
+    const Layout L = plan(d, 0, probe_block, CL_OP_CSR, sms);
     DevBuf ws, mu;
     CL_CUDA(cudaMalloc(&ws.p, L.total));
     CL_CUDA(cudaMalloc(&mu.p, sizeof(double) * probe_block));
@@ -526,7 +569,8 @@ int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_blo
         case 8: rc = run_block<8, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 8, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
         case 16: rc = run_block<16, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 16, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
         case 32: rc = run_block<32, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 32, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
-        default: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+        case 64: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+        default: rc = run_block<128, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 128, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
     }
     if (rc) return rc;
     CL_CUDA(cudaMemcpyAsync(v_out, (char*)ws.p + L.w0, sizeof(double) * d * probe_block,

@@ -49,7 +49,7 @@ def _check_gamma(g_gpu, g_orc):
 
 # ------------------------------------------------------------------ probes (a2)
 @pytest.mark.parametrize("d,p0,k", [(1, 0, 8), (1000, 0, 8), (1027, 5, 16), (4099, 33, 32),
-                                    (65536, 64, 64), (3, 1 << 40, 64)])
+                                    (65536, 64, 64), (3, 1 << 40, 64), (5000, 7, 128)])
 def test_probes_bit_identical(orc, d, p0, k):
     v = P.probes(d, 0x1234, p0, k).cpu().numpy()
     for j in range(k):
@@ -61,7 +61,7 @@ SMALL = ["gmrf32", "gmrf_s", "torus_s", "btb_s"]
 
 
 @pytest.mark.parametrize("name", SMALL)
-@pytest.mark.parametrize("k", [8, 16, 32, 64])
+@pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
 def test_moments_and_gamma_small(orc, name, k):
     wl = W.get_workload(name)
     A, At = _mats(wl)
@@ -177,7 +177,7 @@ def test_launch_count_increases():
     op = _dev_op("csr", A)
     n0 = P.launch_count()
     P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-    assert P.launch_count() - n0 == 1 + 10 + 1  # init + 10 steps + finalize
+    assert P.launch_count() - n0 == 1 + 1 + 10 + 1  # prep + init + 10 steps + finalize
 
 
 # ------------------------------------------------------------------ estimate vs truth
