@@ -169,7 +169,15 @@ struct StepArgs {
 // (lane group size LG = K/PPL).  Fixed shuffle tree in a warp, warps in index order, CTAs
 // in a fixed strided order; the last CTA to finish (atomic ticket) writes the result.
 // ---------------------------------------------------------------------------------------
-template <int K, int PPL, bool HAS_S>
+// Lane lg of a row group owns probes probe_of<K,PPL,SPLIT>(lg, q), q < PPL: contiguous
+// (pl = PPL*lg + q) or, with SPLIT (PPL = 4), two pairs from the two halves of the row
+// {2lg, 2lg+1, K/2+2lg, K/2+2lg+1} so that every 16-byte access of a warp is contiguous.
+template <int K, int PPL, bool SPLIT>
+__device__ __forceinline__ int probe_of(int lg, int q) {
+    return SPLIT ? 2 * lg + (q & 1) + (q >> 1) * (K / 2) : PPL * lg + q;
+}
+
+template <int K, int PPL, bool HAS_S, bool SPLIT = false>
 __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s)[PPL], const StepArgs& a) {
     constexpr int LG = K / PPL;
     constexpr int RED_T = kThreads / K;
@@ -179,7 +187,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s
     __shared__ double fin_s[HAS_S ? RED_T : 1][K];
     __shared__ bool is_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int pl = (lane % LG) * PPL;
+    const int lg = lane % LG;
 #pragma unroll
     for (int off = LG; off < 32; off <<= 1) {
 #pragma unroll
@@ -191,8 +199,9 @@ __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s
     if (lane < LG) {
 #pragma unroll
         for (int q = 0; q < PPL; q++) {
-            red_mu[warp][pl + q] = mu[q];
-            if (HAS_S) red_s[warp][pl + q] = s[q];
+            const int p = probe_of<K, PPL, SPLIT>(lg, q);
+            red_mu[warp][p] = mu[q];
+            if (HAS_S) red_s[warp][p] = s[q];
         }
     }
     __syncthreads();
@@ -349,7 +358,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     const int lg = threadIdx.x % G::L;
     const int grp = threadIdx.x / G::L;
-    const int pl = 4 * lg;
+    const int pa = 2 * lg, pb = K / 2 + 2 * lg;  // probe pairs (first / second half of the row)
     const int64_t* rp_s = reinterpret_cast<const int64_t*>(st + SL::OFF_RP);
     const int32_t* col_s = reinterpret_cast<const int32_t*>(st + SL::OFF_COL);
     const double* val_s = reinterpret_cast<const double*>(st + SL::OFF_VAL);
@@ -376,9 +385,9 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             double2 x0[4], x1[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                const double* p = a.xg + (size_t)(uint32_t)c[q] * K + pl;
-                x0[q] = ldg2(p);
-                x1[q] = ldg2(p + 2);
+                const double* p = a.xg + (size_t)(uint32_t)c[q] * K;
+                x0[q] = ldg2(p + pa);
+                x1[q] = ldg2(p + pb);
             }
 #pragma unroll
             for (int q = 0; q < 4; q++) {
@@ -391,8 +400,8 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         for (; e < e_hi; e++) {
             const int32_t c = STAGED ? col_s[e - base_c] : __ldg(a.ci + e);
             const double v = STAGED ? val_s[e - base_v] : __ldg(a.va + e);
-            const double* p = a.xg + (size_t)(uint32_t)c * K + pl;
-            const double2 x0 = ldg2(p), x1 = ldg2(p + 2);
+            const double* p = a.xg + (size_t)(uint32_t)c * K;
+            const double2 x0 = ldg2(p + pa), x1 = ldg2(p + pb);
             acc0.x = fma(v, x0.x, acc0.x);
             acc0.y = fma(v, x0.y, acc0.y);
             acc1.x = fma(v, x1.x, acc1.x);
@@ -400,15 +409,15 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         }
         // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
         if (MODE == MODE_BTB) {
-            const double2 w0 = *reinterpret_cast<const double2*>(wc_s + lr * K + pl);
-            const double2 w1 = *reinterpret_cast<const double2*>(wc_s + lr * K + pl + 2);
+            const double2 w0 = *reinterpret_cast<const double2*>(wc_s + lr * K + pa);
+            const double2 w1 = *reinterpret_cast<const double2*>(wc_s + lr * K + pb);
             acc0.x = fma(-a.beta, w0.x, acc0.x);
             acc0.y = fma(-a.beta, w0.y, acc0.y);
             acc1.x = fma(-a.beta, w1.x, acc1.x);
             acc1.y = fma(-a.beta, w1.y, acc1.y);
         } else if ((__ldg(a.nodiag + (i >> 5)) >> (i & 31)) & 1u) {
-            const double2 w0 = ldg2(a.wcur + (size_t)i * K + pl);
-            const double2 w1 = ldg2(a.wcur + (size_t)i * K + pl + 2);
+            const double2 w0 = ldg2(a.wcur + (size_t)i * K + pa);
+            const double2 w1 = ldg2(a.wcur + (size_t)i * K + pb);
             acc0.x = fma(-a.beta, w0.x, acc0.x);
             acc0.y = fma(-a.beta, w0.y, acc0.y);
             acc1.x = fma(-a.beta, w1.x, acc1.x);
@@ -427,19 +436,20 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             n0 = acc0;
             n1 = acc1;
         } else {
-            const double2 p0 = *reinterpret_cast<const double2*>(wp_s + lr * K + pl);
-            const double2 p1 = *reinterpret_cast<const double2*>(wp_s + lr * K + pl + 2);
+            const double2 p0 = *reinterpret_cast<const double2*>(wp_s + lr * K + pa);
+            const double2 p1 = *reinterpret_cast<const double2*>(wp_s + lr * K + pb);
             n0 = make_double2(2.0 * acc0.x - p0.x, 2.0 * acc0.y - p0.y);
             n1 = make_double2(2.0 * acc1.x - p1.x, 2.0 * acc1.y - p1.y);
         }
-        double* out = a.wnext + (size_t)i * K + pl;
-        __stcs(reinterpret_cast<double2*>(out), n0);
-        __stcs(reinterpret_cast<double2*>(out + 2), n1);
-        const uint32_t b = sg_s[lr * G::WORDS + (pl >> 5)] >> (pl & 31);
-        mu[0] += (b & 1u) ? -n0.x : n0.x;
-        mu[1] += (b & 2u) ? -n0.y : n0.y;
-        mu[2] += (b & 4u) ? -n1.x : n1.x;
-        mu[3] += (b & 8u) ? -n1.y : n1.y;
+        double* out = a.wnext + (size_t)i * K;
+        __stcs(reinterpret_cast<double2*>(out + pa), n0);
+        __stcs(reinterpret_cast<double2*>(out + pb), n1);
+        const uint32_t ba = sg_s[lr * G::WORDS + (pa >> 5)] >> (pa & 31);
+        const uint32_t bb = sg_s[lr * G::WORDS + (pb >> 5)] >> (pb & 31);
+        mu[0] += (ba & 1u) ? -n0.x : n0.x;
+        mu[1] += (ba & 2u) ? -n0.y : n0.y;
+        mu[2] += (bb & 1u) ? -n1.x : n1.x;
+        mu[3] += (bb & 2u) ? -n1.y : n1.y;
         if (HAS_S) {
             s[0] = fma(ui, n0.x, s[0]);
             s[1] = fma(ui, n0.y, s[1]);
@@ -466,17 +476,16 @@ cheb_step_kernel(StepArgs a) {
     __shared__ int s_fit[2];
 
     const int tid = threadIdx.x;
-    const int pl = 4 * (tid % G::L);
+    const int pa = 2 * (tid % G::L), pb = K / 2 + pa;
     double mu[4] = {0.0, 0.0, 0.0, 0.0}, s[4] = {0.0, 0.0, 0.0, 0.0};
     double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
     if (HAS_S) {
-        r1a = make_double2(a.r1c_alpha * a.s_cur[pl], a.r1c_alpha * a.s_cur[pl + 1]);
-        r1b = make_double2(a.r1c_alpha * a.s_cur[pl + 2], a.r1c_alpha * a.s_cur[pl + 3]);
+        r1a = make_double2(a.r1c_alpha * a.s_cur[pa], a.r1c_alpha * a.s_cur[pa + 1]);
+        r1b = make_double2(a.r1c_alpha * a.s_cur[pb], a.r1c_alpha * a.s_cur[pb + 1]);
     }
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     // ---- producer (thread 0): issue the bulk copies of tile t into stage b
-    uint64_t pol = 0;
     auto issue = [&](int64_t t, int b, int64_t e0, int64_t e1) {
         unsigned char* st = smem + b * SL::BYTES;
         const int64_t r0 = t * G::TILE;
@@ -498,7 +507,7 @@ cheb_step_kernel(StepArgs a) {
         mbar_expect_tx(&bar[b], bytes);
         bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
         bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
-        if (!FIRST) bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], pol);
+        if (!FIRST) bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
         if (MODE == MODE_BTB) bulk_g2s(st + SL::OFF_WCUR, a.wcur + (size_t)r0 * K, wbytes, &bar[b]);
         if (fit) {
             bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
@@ -515,7 +524,6 @@ cheb_step_kernel(StepArgs a) {
 
     int64_t ne0 = 0, ne1 = 0;
     if (tid == 0) {
-        pol = policy_evict_first();
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_mbar_init();
@@ -543,7 +551,7 @@ cheb_step_kernel(StepArgs a) {
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + 2 < nmine) issue(tile_of(it + 2), b, ne0, ne1);
     }
-    grid_reduce_finish<K, 4, HAS_S>(mu, s, a);
+    grid_reduce_finish<K, 4, HAS_S, true>(mu, s, a);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -556,7 +564,7 @@ spmm_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
     using G = Geo<K>;
     const int lg = threadIdx.x % G::L;
     const int grp = threadIdx.x / G::L;
-    const int pl = 4 * lg;
+    const int pa = 2 * lg, pb = K / 2 + 2 * lg;
     const int64_t ngroups_total = (int64_t)gridDim.x * G::GROUPS;
     for (int64_t i = (int64_t)blockIdx.x * G::GROUPS + grp; i < d; i += ngroups_total) {
         const int64_t e_lo = __ldg(rp + i), e_hi = __ldg(rp + i + 1);
@@ -573,9 +581,9 @@ spmm_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
             double2 x0[4], x1[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                const double* p = x + (size_t)(uint32_t)c[q] * K + pl;
-                x0[q] = ldg2(p);
-                x1[q] = ldg2(p + 2);
+                const double* p = x + (size_t)(uint32_t)c[q] * K;
+                x0[q] = ldg2(p + pa);
+                x1[q] = ldg2(p + pb);
             }
 #pragma unroll
             for (int q = 0; q < 4; q++) {
@@ -588,16 +596,16 @@ spmm_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
         for (; e < e_hi; e++) {
             const int32_t c = __ldg(ci + e);
             const double v = __ldg(va + e);
-            const double* p = x + (size_t)(uint32_t)c * K + pl;
-            const double2 x0 = ldg2(p), x1 = ldg2(p + 2);
+            const double* p = x + (size_t)(uint32_t)c * K;
+            const double2 x0 = ldg2(p + pa), x1 = ldg2(p + pb);
             acc0.x = fma(v, x0.x, acc0.x);
             acc0.y = fma(v, x0.y, acc0.y);
             acc1.x = fma(v, x1.x, acc1.x);
             acc1.y = fma(v, x1.y, acc1.y);
         }
-        double* out = y + (size_t)i * K + pl;
-        *reinterpret_cast<double2*>(out) = acc0;
-        *reinterpret_cast<double2*>(out + 2) = acc1;
+        double* out = y + (size_t)i * K;
+        *reinterpret_cast<double2*>(out + pa) = acc0;
+        *reinterpret_cast<double2*>(out + pb) = acc1;
     }
 }
 
