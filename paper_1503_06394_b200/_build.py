@@ -21,13 +21,15 @@ def nvcc():
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in DEPS):
-        return SO
-    tmp = SO + f".tmp{os.getpid()}"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp] + SOURCES
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libchebld.so (or a tuning variant at `out` with extra -D defines)."""
+    so = out or SO
+    if not force and os.path.exists(so) and all(os.path.getmtime(so) >= os.path.getmtime(d) for d in DEPS):
+        return so
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = [nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-I", os.path.join(ROOT, "include"), "-o", tmp] + SOURCES
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(CSRC, "ptxas.log")
+    log = os.path.join(CSRC, "ptxas.log" if out is None else "ptxas_" + os.path.basename(so) + ".log")
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
@@ -35,8 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed: " + " ".join(cmd))
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

@@ -8,7 +8,7 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SO_PATH = os.path.join(PKG, "libchebld.so")
+SO_PATH = os.environ.get("CHEB_LIB") or os.path.join(PKG, "libchebld.so")  # CHEB_LIB: tuning builds
 HEADER = os.path.join(ROOT, "include", "cheb_logdet.h")
 
 CL_OK, CL_EINVAL, CL_EDIM, CL_ENOMEM, CL_ECUDA, CL_ENONFINITE = 0, -1, -2, -3, -4, -5

@@ -32,6 +32,9 @@ constexpr int kThreads = 256;
 #ifndef CHEB_MIN_CTAS
 #define CHEB_MIN_CTAS 4  // resident CTAs per SM the step kernel is register-budgeted for
 #endif
+#ifndef CHEB_NNZ_UNROLL
+#define CHEB_NNZ_UNROLL 5  // nnz of a row whose gathers are in flight together (5-point stencil: 1 chunk)
+#endif
 
 enum { MODE_CSR = 0, MODE_RANK1 = 1, MODE_BTB = 2 };
 
@@ -373,39 +376,35 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         const int64_t i = r0 + lr;
         const int64_t e_lo = rp_s[lr], e_hi = rp_s[lr + 1];
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-        int64_t e = e_lo;
-        for (; e + 4 <= e_hi; e += 4) {
-            int32_t c[4];
-            double v[4];
+        // all nnz of a chunk issue their gathers before any is consumed (predicated tail)
+        for (int64_t e0 = e_lo; e0 < e_hi; e0 += CHEB_NNZ_UNROLL) {
+            int32_t c[CHEB_NNZ_UNROLL];
+            double v[CHEB_NNZ_UNROLL];
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                c[q] = STAGED ? col_s[e + q - base_c] : __ldg(a.ci + e + q);
-                v[q] = STAGED ? val_s[e + q - base_v] : __ldg(a.va + e + q);
+            for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
+                const bool in = e0 + q < e_hi;
+                const int64_t e = in ? e0 + q : e_lo;
+                c[q] = STAGED ? col_s[e - base_c] : __ldg(a.ci + e);
+                v[q] = in ? (STAGED ? val_s[e - base_v] : __ldg(a.va + e)) : 0.0;
             }
-            double2 x0[4], x1[4];
+            double2 x0[CHEB_NNZ_UNROLL], x1[CHEB_NNZ_UNROLL];
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const double* p = a.xg + (size_t)(uint32_t)c[q] * K;
-                x0[q] = ldg2(p + pa);
-                x1[q] = ldg2(p + pb);
+            for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
+                if (e0 + q < e_hi) {
+                    const double* p = a.xg + (size_t)(uint32_t)c[q] * K;
+                    x0[q] = ldg2(p + pa);
+                    x1[q] = ldg2(p + pb);
+                } else {
+                    x0[q] = x1[q] = make_double2(0.0, 0.0);
+                }
             }
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
+            for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
                 acc0.x = fma(v[q], x0[q].x, acc0.x);
                 acc0.y = fma(v[q], x0[q].y, acc0.y);
                 acc1.x = fma(v[q], x1[q].x, acc1.x);
                 acc1.y = fma(v[q], x1[q].y, acc1.y);
             }
-        }
-        for (; e < e_hi; e++) {
-            const int32_t c = STAGED ? col_s[e - base_c] : __ldg(a.ci + e);
-            const double v = STAGED ? val_s[e - base_v] : __ldg(a.va + e);
-            const double* p = a.xg + (size_t)(uint32_t)c * K;
-            const double2 x0 = ldg2(p + pa), x1 = ldg2(p + pb);
-            acc0.x = fma(v, x0.x, acc0.x);
-            acc0.y = fma(v, x0.y, acc0.y);
-            acc1.x = fma(v, x1.x, acc1.x);
-            acc1.y = fma(v, x1.y, acc1.y);
         }
         // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
         if (MODE == MODE_BTB) {

@@ -1,0 +1,24 @@
+"""Build tuning variants of libchebld.so into build_variants/ (git-ignored)."""
+import os
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1503_06394_b200 import _build  # noqa: E402
+
+VARIANTS = {
+    "u4c4": ["CHEB_NNZ_UNROLL=4", "CHEB_MIN_CTAS=4"],
+    "u8c3": ["CHEB_NNZ_UNROLL=8", "CHEB_MIN_CTAS=3"],
+    "u8c2": ["CHEB_NNZ_UNROLL=8", "CHEB_MIN_CTAS=2"],
+    "u6c3": ["CHEB_NNZ_UNROLL=6", "CHEB_MIN_CTAS=3"],
+    "u5c4": ["CHEB_NNZ_UNROLL=5", "CHEB_MIN_CTAS=4"],
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    root = os.path.join(_build.ROOT, "build_variants")
+    os.makedirs(root, exist_ok=True)
+    with ThreadPoolExecutor(4) as ex:
+        for p in ex.map(lambda n: _build.build(force=True, out=os.path.join(root, f"libchebld_{n}.so"),
+                                              defines=VARIANTS[n]), names):
+            print(p)
