@@ -146,6 +146,20 @@ int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_blo
 int64_t cheb_launch_count(void);
 int cheb_profile_begin(void);
 int cheb_profile_end(double *step_ms, int64_t *step_launches);
+/* After cheb_profile_end(): summed milliseconds and launch count of the temporally fused
+ * two-step kernel (each launch = 2 Chebyshev steps). */
+int cheb_profile_fused(double *ms, int64_t *launches);
+
+/* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 2):
+ *   1 = one launch per Chebyshev step;
+ *   2 = auto: pairs of steps (w_{j+1}, w_{j+2}) in one cooperative launch when the
+ *       operator's bandwidth max|i - col| is small enough for the two-step wavefront to
+ *       stay in L2 and the matrix has enough row tiles to fill the pipeline;
+ *   3 = always fuse pairs (testing; correct for any bandwidth, slow when it is large).
+ * Results are bit-identical across modes; only the schedule changes.  With modes 2/3,
+ * cheb_moments synchronises its stream once after the operator prep (to read the
+ * bandwidth).  CL_EINVAL for other values. */
+int cheb_set_fusion(int32_t steps);
 
 /* Thread-local message for the last failing call on this thread. */
 const char *cheb_last_error(void);

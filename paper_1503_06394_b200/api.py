@@ -229,10 +229,19 @@ def profile_begin():
 
 
 def profile_end():
-    ms = ctypes.c_double()
-    n = ctypes.c_int64()
-    check(_lib.load().cheb_profile_end(ctypes.byref(ms), ctypes.byref(n)))
-    return ms.value, n.value
+    """Stop recording; returns {"single": (ms, launches), "fused": (ms, launches)} for the
+    single-step and the fused two-step kernels."""
+    L = _lib.load()
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    check(L.cheb_profile_end(ctypes.byref(ms), ctypes.byref(n)))
+    fms, fn = ctypes.c_double(), ctypes.c_int64()
+    check(L.cheb_profile_fused(ctypes.byref(fms), ctypes.byref(fn)))
+    return {"single": (ms.value, n.value), "fused": (fms.value, fn.value)}
+
+
+def set_fusion(steps: int):
+    """Temporal fusion for CSR operators: 1 (off), 2 (auto, default), 3 (always fuse pairs)."""
+    check(_lib.load().cheb_set_fusion(int(steps)))
 
 
 class Estimator:

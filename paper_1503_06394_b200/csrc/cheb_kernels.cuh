@@ -180,7 +180,7 @@ __device__ __forceinline__ int probe_of(int lg, int q) {
     return SPLIT ? 2 * lg + (q & 1) + (q >> 1) * (K / 2) : PPL * lg + q;
 }
 
-template <int K, int PPL, bool HAS_S, bool SPLIT = false>
+template <int K, int PPL, bool HAS_S, bool SPLIT = false, bool S_IS_MU = false>
 __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s)[PPL], const StepArgs& a) {
     constexpr int LG = K / PPL;
     constexpr int RED_T = kThreads / K;
@@ -246,7 +246,8 @@ __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s
             if (HAS_S) t += fin_s[r][tid];
         }
         if (tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col] = m;
-        if (HAS_S) a.s_next[tid] = t;
+        if (HAS_S && S_IS_MU && tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col + 1] = t;
+        if (HAS_S && !S_IS_MU) a.s_next[tid] = t;
     }
     if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch (stream-ordered)
 }
@@ -260,8 +261,10 @@ __global__ void __launch_bounds__(kThreads)
 prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ va, double alpha, double beta, int64_t* __restrict__ rp2,
             int64_t rp2_len, int32_t* __restrict__ ci2, double* __restrict__ va2,
-            uint32_t* __restrict__ nodiag, const double* __restrict__ u, double* __restrict__ u2) {
+            uint32_t* __restrict__ nodiag, const double* __restrict__ u, double* __restrict__ u2,
+            unsigned long long* __restrict__ bw) {
     const int64_t nnz = rp[d];
+    int64_t bwmax = 0;  // operator bandwidth max |i - col| (temporal fusion planning)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of 32
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < d; i0 += stride) {
         const int64_t i = i0 + threadIdx.x;
@@ -279,11 +282,21 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
                 }
                 ci2[e] = c;
                 va2[e] = v;
+                const int64_t dist = c > i ? c - i : i - c;
+                bwmax = dist > bwmax ? dist : bwmax;
             }
             if (u2) u2[i] = u ? u[i] : 1.0;
         }
         const unsigned m = __ballot_sync(0xffffffffu, !has);
         if ((threadIdx.x & 31) == 0 && i < d) nodiag[i >> 5] = m;
+    }
+    if (bw) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const int64_t o = __shfl_xor_sync(0xffffffffu, bwmax, off);
+            bwmax = o > bwmax ? o : bwmax;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(bw, (unsigned long long)bwmax);
     }
     if (blockIdx.x == 0) {
         for (int64_t k = d + threadIdx.x; k < rp2_len; k += blockDim.x) rp2[k] = nnz;
@@ -352,10 +365,18 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
 //   w_j  = FIRST ? y : 2y - w_{j-2}                 (written over w_{j-2})
 //   mu_j += v_i * w_j ;  rank-1: s_j += u_i * w_j
 // ---------------------------------------------------------------------------------------
-template <int K, int MODE, bool FIRST, bool STAGED>
+__device__ __forceinline__ double2 ldcg2(const double* p) {
+    return __ldcg(reinterpret_cast<const double2*>(p));
+}
+
+// One staged tile of the fused step.  xg: gather source; wcur: W_cur (for rows without a
+// stored diagonal); wout: output rows (in place over W_prev).  CG: gather through L2 only
+// (data produced earlier in the same launch by other CTAs -- temporally fused kernel).
+template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, double2 r1a, double2 r1b,
-                                          double (&mu)[4], double (&s)[4]) {
+                                          double (&mu)[4], double (&s)[4], const double* xg,
+                                          const double* wcur, double* wout) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
@@ -391,9 +412,9 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
 #pragma unroll
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
                 if (e0 + q < e_hi) {
-                    const double* p = a.xg + (size_t)(uint32_t)c[q] * K;
-                    x0[q] = ldg2(p + pa);
-                    x1[q] = ldg2(p + pb);
+                    const double* p = xg + (size_t)(uint32_t)c[q] * K;
+                    x0[q] = CG ? ldcg2(p + pa) : ldg2(p + pa);
+                    x1[q] = CG ? ldcg2(p + pb) : ldg2(p + pb);
                 } else {
                     x0[q] = x1[q] = make_double2(0.0, 0.0);
                 }
@@ -415,8 +436,8 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             acc1.x = fma(-a.beta, w1.x, acc1.x);
             acc1.y = fma(-a.beta, w1.y, acc1.y);
         } else if ((__ldg(a.nodiag + (i >> 5)) >> (i & 31)) & 1u) {
-            const double2 w0 = ldg2(a.wcur + (size_t)i * K + pa);
-            const double2 w1 = ldg2(a.wcur + (size_t)i * K + pb);
+            const double2 w0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
+            const double2 w1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
             acc0.x = fma(-a.beta, w0.x, acc0.x);
             acc0.y = fma(-a.beta, w0.y, acc0.y);
             acc1.x = fma(-a.beta, w1.x, acc1.x);
@@ -440,9 +461,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             n0 = make_double2(2.0 * acc0.x - p0.x, 2.0 * acc0.y - p0.y);
             n1 = make_double2(2.0 * acc1.x - p1.x, 2.0 * acc1.y - p1.y);
         }
-        double* out = a.wnext + (size_t)i * K;
-        __stcs(reinterpret_cast<double2*>(out + pa), n0);
-        __stcs(reinterpret_cast<double2*>(out + pb), n1);
+        double* out = wout + (size_t)i * K;
+        if (KEEP) {  // re-read from L2 later in the same launch (fused kernel, stage 1)
+            *reinterpret_cast<double2*>(out + pa) = n0;
+            *reinterpret_cast<double2*>(out + pb) = n1;
+        } else {     // streamed: next read is by a later launch
+            __stcs(reinterpret_cast<double2*>(out + pa), n0);
+            __stcs(reinterpret_cast<double2*>(out + pb), n1);
+        }
         const uint32_t ba = sg_s[lr * G::WORDS + (pa >> 5)] >> (pa & 31);
         const uint32_t bb = sg_s[lr * G::WORDS + (pb >> 5)] >> (pb & 31);
         mu[0] += (ba & 1u) ? -n0.x : n0.x;
@@ -544,13 +570,181 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu, s);
+            step_tile<K, MODE, FIRST, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu, s,
+                                            a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false>(a, st, r0, rows, 0, 0, r1a, r1b, mu, s);
+            step_tile<K, MODE, FIRST, false>(a, st, r0, rows, 0, 0, r1a, r1b, mu, s, a.xg, a.wcur, a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + 2 < nmine) issue(tile_of(it + 2), b, ne0, ne1);
     }
     grid_reduce_finish<K, 4, HAS_S, true>(mu, s, a);
+}
+
+
+// ---------------------------------------------------------------------------------------
+// K2x2: temporally fused pair of Chebyshev steps (CSR mode, banded operators).
+//   stage 1 (tile P):      w_{j+1} = 2 Ã w_j     - w_{j-1}   (A: w_{j-1} -> w_{j+1}, gathers B)
+//   stage 2 (tile P - D):  w_{j+2} = 2 Ã w_{j+1} - w_j       (B: w_j -> w_{j+2},     gathers A)
+// Every element is computed with exactly the single-step arithmetic, in the same order, so
+// results are bit-identical to two cheb_step_kernel launches; only the schedule changes.
+// Stage 2 of tile u gathers w_{j+1} rows within the operator bandwidth beta of u and
+// overwrites w_j rows of u that stage 1 of tiles u-H-1..u+H+1 read (H = ceil(beta/TILE)+1),
+// so it waits for those stage-1 tiles (per-group completion counters, release/acquire).
+// The lag D = H + 1 + gridDim.x positions means every awaited tile was assigned to its CTA
+// in an earlier iteration: with all CTAs co-resident (cooperative launch) there is no
+// deadlock.  w_{j+1} stays in L2 between the stages: per 2 steps HBM sees w_{j-1}, w_j read
+// and w_{j+1}, w_{j+2} written (4 vector streams instead of 6).
+// ---------------------------------------------------------------------------------------
+constexpr int kFlagGroup = 16;  // stage-1 tiles per completion counter
+
+struct FusedArgs {
+    double* A;                // in: w_{j-1}, out: w_{j+1}
+    double* B;                // in: w_j,     out: w_{j+2}
+    unsigned int* cnt;        // [ceil(ntiles/kFlagGroup)] stage-1 completion counters (zeroed)
+    unsigned int* err;        // dependency-wait timeout flag
+    int64_t H;                // dependency halo in tiles
+    int64_t D;                // stage-2 lag in positions
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, CHEB_MIN_CTAS)
+cheb_step2_kernel(StepArgs a, FusedArgs f) {
+    using G = Geo<K>;
+    using SL = StageLayout<K, MODE_CSR>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int64_t s_base_c[2], s_base_v[2];
+    __shared__ int s_fit[2];
+
+    const int tid = threadIdx.x;
+    const int64_t Gd = gridDim.x;
+    double mu1[4] = {0.0, 0.0, 0.0, 0.0}, mu2[4] = {0.0, 0.0, 0.0, 0.0};
+    const double2 z2 = make_double2(0.0, 0.0);
+    const int64_t npos = a.ntiles + f.D;  // positions 0 .. ntiles + D - 1
+    const int64_t M = blockIdx.x < npos ? 2 * ((npos - 1 - blockIdx.x) / Gd + 1) : 0;
+
+    auto item = [&](int64_t m, int& stg, int64_t& t) -> bool {
+        const int64_t P = (int64_t)blockIdx.x + (m >> 1) * Gd;
+        stg = (int)(m & 1);
+        t = stg ? P - f.D : P;
+        return t >= 0 && t < a.ntiles;
+    };
+    auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
+        const int64_t r0 = t * G::TILE;
+        e0 = __ldg(a.rp + r0);
+        e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+    };
+    auto issue = [&](int64_t t, int b, const double* wsrc, int64_t e0, int64_t e1) {
+        unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
+        const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+        const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
+        s_fit[b] = fit;
+        s_base_c[b] = c0;
+        s_base_v[b] = v0;
+        const uint32_t wbytes = (uint32_t)rows * K * 8;
+        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+        uint32_t bytes = G::RPBYTES + sgbytes + wbytes;
+        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+        mbar_expect_tx(&bar[b], bytes);
+        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
+        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        bulk_g2s_hint(st + SL::OFF_WPREV, wsrc + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
+        if (fit) {
+            bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
+            bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
+        }
+    };
+    auto advance = [&](int64_t& m, int& stg, int64_t& t) -> bool {
+        for (; m < M; ++m)
+            if (item(m, stg, t)) return true;
+        return false;
+    };
+
+    int64_t m_issue = 0, ne0 = 0, ne1 = 0, nt = 0;
+    int nstg = 0;
+    bool pending = false;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        for (int q = 0; q < 2; q++) {
+            int stg;
+            int64_t t, e0, e1;
+            if (!advance(m_issue, stg, t)) break;
+            bounds(t, e0, e1);
+            issue(t, q, stg ? f.B : f.A, e0, e1);
+            ++m_issue;
+        }
+    }
+    __syncthreads();
+
+    int64_t q = 0;
+    for (int64_t m = 0; m < M; ++m) {
+        int stg;
+        int64_t t;
+        if (!item(m, stg, t)) continue;
+        const int b = (int)(q & 1);
+        const uint32_t phase = (uint32_t)((q >> 1) & 1);
+        if (tid == 0) {
+            pending = advance(m_issue, nstg, nt);
+            if (pending) bounds(nt, ne0, ne1);
+        }
+        if (stg == 1 && tid < 32) {  // wait for stage 1 of tiles t-H-1 .. t+H+1
+            const int64_t lo = t - f.H - 1 < 0 ? 0 : t - f.H - 1;
+            const int64_t hi = t + f.H + 1 >= a.ntiles ? a.ntiles - 1 : t + f.H + 1;
+            for (int64_t g = lo / kFlagGroup + tid; g <= hi / kFlagGroup; g += 32) {
+                const unsigned int want = (unsigned int)imin64(kFlagGroup, a.ntiles - g * kFlagGroup);
+                uint32_t spins = 0;
+                while (ld_acquire_u32(f.cnt + g) < want) {
+                    __nanosleep(128);
+                    if ((++spins & 1023u) == 0 && (spins > (1u << 24) || ld_acquire_u32(f.err))) {
+                        atomicExch(f.err, 1u);  // ~2 s without progress: give up, never hang
+                        break;
+                    }
+                }
+            }
+            __threadfence();
+        }
+        if (stg == 1) __syncthreads();
+        mbar_wait(&bar[b], phase);
+        const unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        if (stg == 0) {
+            if (s_fit[b])
+                step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
+                                                                 mu1, mu1, f.B, f.B, f.A);
+            else
+                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, z2, mu1, mu1, f.B,
+                                                                  f.B, f.A);
+            __threadfence();  // publish this tile's w_{j+1} rows (and the end of its w_j reads)
+            __syncthreads();
+            if (tid == 0) atomicAdd(f.cnt + t / kFlagGroup, 1u);
+        } else {
+            if (s_fit[b])
+                step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
+                                                                 mu2, mu2, f.A, f.A, f.B);
+            else
+                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, z2, mu2, mu2, f.A,
+                                                                  f.A, f.B);
+        }
+        __syncthreads();  // every warp is done with stage b
+        if (tid == 0 && pending) {
+            issue(nt, b, nstg ? f.B : f.A, ne0, ne1);
+            ++m_issue;
+        }
+        ++q;
+    }
+    grid_reduce_finish<K, 4, true, true, true>(mu1, mu2, a);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -45,14 +45,19 @@ int fail(int code, const char* fmt, ...) {
 struct Profiler {
     std::mutex mu;
     bool on = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // recorded pairs
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];  // [0] single step, [1] fused pair
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+    double ms[2] = {0.0, 0.0};
+    int64_t n[2] = {0, 0};
 } g_prof;
+
+std::atomic<int> g_fusion{2};  // max Chebyshev steps fused per launch (1 = off)
 
 struct ProfScope {
     cudaStream_t s;
+    int kind;
     std::pair<cudaEvent_t, cudaEvent_t> pr{nullptr, nullptr};
-    explicit ProfScope(cudaStream_t st) : s(st) {
+    explicit ProfScope(cudaStream_t st, int k = 0) : s(st), kind(k) {
         std::lock_guard<std::mutex> lk(g_prof.mu);
         if (!g_prof.on) return;
         if (!g_prof.pool.empty()) {
@@ -68,7 +73,7 @@ struct ProfScope {
         if (!pr.first) return;
         cudaEventRecord(pr.second, s);
         std::lock_guard<std::mutex> lk(g_prof.mu);
-        g_prof.ev.push_back(pr);
+        g_prof.ev[kind].push_back(pr);
     }
 };
 
@@ -88,7 +93,7 @@ int tile_rows(int k) { return 2 * kThreads * 4 / k; }  // Geo<K>::TILE
 
 struct Layout {
     size_t w0, w1, y, sbits, part_mu, part_s, sbuf, ticket;
-    size_t rp2, ci2, va2, nodiag, u2, total;
+    size_t rp2, ci2, va2, nodiag, u2, cnt, misc, total;
     int64_t rp2_len;
 };
 
@@ -114,6 +119,8 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.va2 = off; off += align256(((size_t)nnz + 4) * sizeof(double));
     L.nodiag = off; off += align256(((size_t)d / 32 + 1) * sizeof(uint32_t));
     L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
+    L.cnt = off; off += align256(((size_t)ntiles / kFlagGroup + 1) * sizeof(unsigned int));
+    L.misc = off; off += 256;  // [0] u64 bandwidth, [8] u32 fused-wait error flag
     L.total = off;
     return L;
 }
@@ -179,15 +186,22 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
     prep_kernel<MODE><<<grid, kThreads, 0, st>>>(
         d, G2.row_ptr, G2.col_idx, G2.val, alpha, beta, (int64_t*)(ws + L.rp2), L.rp2_len,
         (int32_t*)(ws + L.ci2), (double*)(ws + L.va2), (uint32_t*)(ws + L.nodiag),
-        MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr);
+        MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr,
+        MODE == MODE_CSR ? (unsigned long long*)(ws + L.misc) : nullptr);
     g_launches++;
 }
+
+// Temporal fusion plan (CSR mode): stage-2 halo H (tiles) and lag D (positions).
+struct FusionPlan {
+    bool on = false;
+    int64_t H = 0, D = 0;
+};
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
 template <int K, int MODE>
 int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-              int64_t mu_stride, cudaStream_t st, int sms) {
+              int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp = FusionPlan()) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE>;
     const int64_t d = op->A.n_cols;
@@ -234,9 +248,30 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         const int64_t ng = (op->A.n_rows + G::GROUPS - 1) / G::GROUPS;
         grid_spmm = grid_for(spmm_kernel<K>, ng, sms);
     }
+    int grid_fused = 0;
+    if (MODE == MODE_CSR && fp.on) grid_fused = grid_for(cheb_step2_kernel<K>, a.ntiles + fp.D, sms, smem);
     for (int32_t j = 1; j <= n; j++) {
         const double* cur = w[(j - 1) & 1];
         double* nxt = w[j & 1];
+        if (MODE == MODE_CSR && fp.on && j >= 2 && j + 1 <= n) {
+            // steps j and j+1 in one launch: A = w_{j-2} -> w_j, B = w_{j-1} -> w_{j+1}
+            FusedArgs f{};
+            f.A = nxt;
+            f.B = (double*)cur;
+            f.cnt = (unsigned int*)(ws + L.cnt);
+            f.err = (unsigned int*)(ws + L.misc + 8);
+            f.H = fp.H;
+            f.D = fp.D;
+            a.mu_col = j;
+            CL_CUDA(cudaMemsetAsync(f.cnt, 0, ((size_t)a.ntiles / kFlagGroup + 1) * sizeof(unsigned int), st));
+            void* args[] = {&a, &f};
+            ProfScope ps(st, 1);
+            CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),
+                                                dim3(kThreads), args, smem, st));
+            g_launches++;
+            j++;  // consumed two steps
+            continue;
+        }
         if (MODE == MODE_BTB) {
             spmm_kernel<K><<<grid_spmm, kThreads, 0, st>>>(op->A.n_rows, op->A.row_ptr, op->A.col_idx,
                                                           op->A.val, cur, y);
@@ -261,10 +296,10 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
 template <int K>
 int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
                    int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-                   int64_t mu_stride, cudaStream_t st, int sms) {
+                   int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
     switch (op->kind) {
         case CL_OP_CSR:
-            return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
+            return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         case CL_OP_CSR_RANK1:
             return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
         default:
@@ -278,6 +313,22 @@ void prep_mode(const cl_operator* op, double alpha, double beta, char* ws, const
         case CL_OP_CSR: run_prep<MODE_CSR>(op, alpha, beta, ws, L, st, sms); break;
         case CL_OP_CSR_RANK1: run_prep<MODE_RANK1>(op, alpha, beta, ws, L, st, sms); break;
         default: run_prep<MODE_BTB>(op, alpha, beta, ws, L, st, sms); break;
+    }
+}
+
+int fused_occupancy(int k) {
+    auto occ_of = [](auto kern, size_t smem) {
+        int occ = 0;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+        return occ < 1 ? 1 : (occ > kMaxCtasPerSm ? kMaxCtasPerSm : occ);
+    };
+    switch (k) {
+        case 8: return occ_of(cheb_step2_kernel<8>, StageLayout<8, MODE_CSR>::SMEM);
+        case 16: return occ_of(cheb_step2_kernel<16>, StageLayout<16, MODE_CSR>::SMEM);
+        case 32: return occ_of(cheb_step2_kernel<32>, StageLayout<32, MODE_CSR>::SMEM);
+        case 64: return occ_of(cheb_step2_kernel<64>, StageLayout<64, MODE_CSR>::SMEM);
+        default: return occ_of(cheb_step2_kernel<128>, StageLayout<128, MODE_CSR>::SMEM);
     }
 }
 
@@ -303,8 +354,12 @@ int64_t cheb_launch_count(void) { return g_launches.load(); }
 
 int cheb_profile_begin(void) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
-    for (auto& p : g_prof.ev) g_prof.pool.push_back(p);
-    g_prof.ev.clear();
+    for (int k = 0; k < 2; k++) {
+        for (auto& p : g_prof.ev[k]) g_prof.pool.push_back(p);
+        g_prof.ev[k].clear();
+        g_prof.ms[k] = 0.0;
+        g_prof.n[k] = 0;
+    }
     g_prof.on = true;
     return CL_OK;
 }
@@ -312,18 +367,35 @@ int cheb_profile_begin(void) {
 int cheb_profile_end(double* step_ms, int64_t* step_launches) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = false;
-    double tot = 0.0;
-    for (auto& p : g_prof.ev) {
-        cudaError_t e = cudaEventSynchronize(p.second);
-        if (e != cudaSuccess) return fail(CL_ECUDA, "event sync: %s", cudaGetErrorString(e));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, p.first, p.second);
-        tot += ms;
+    for (int k = 0; k < 2; k++) {
+        double tot = 0.0;
+        for (auto& p : g_prof.ev[k]) {
+            cudaError_t e = cudaEventSynchronize(p.second);
+            if (e != cudaSuccess) return fail(CL_ECUDA, "event sync: %s", cudaGetErrorString(e));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, p.first, p.second);
+            tot += ms;
+        }
+        g_prof.ms[k] = tot;
+        g_prof.n[k] = (int64_t)g_prof.ev[k].size();
+        for (auto& p : g_prof.ev[k]) g_prof.pool.push_back(p);
+        g_prof.ev[k].clear();
     }
-    if (step_ms) *step_ms = tot;
-    if (step_launches) *step_launches = (int64_t)g_prof.ev.size();
-    for (auto& p : g_prof.ev) g_prof.pool.push_back(p);
-    g_prof.ev.clear();
+    if (step_ms) *step_ms = g_prof.ms[0];
+    if (step_launches) *step_launches = g_prof.n[0];
+    return CL_OK;
+}
+
+int cheb_profile_fused(double* ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (ms) *ms = g_prof.ms[1];
+    if (launches) *launches = g_prof.n[1];
+    return CL_OK;
+}
+
+int cheb_set_fusion(int32_t steps) {
+    if (steps < 1 || steps > 3) return fail(CL_EINVAL, "fusion mode must be 1, 2 or 3");
+    g_fusion = steps;
     return CL_OK;
 }
 
@@ -388,16 +460,34 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
     const int64_t stride = (int64_t)degree + 1;
     CL_CUDA(cudaGetLastError());
     CL_CUDA(cudaMemsetAsync(ws + L.ticket, 0, 256, st));
+    CL_CUDA(cudaMemsetAsync(ws + L.misc, 0, 256, st));
     prep_mode(op, alpha, beta, ws, L, st, sms);
+    FusionPlan fp;
+    if (op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
+        // needs the operator bandwidth computed by the prep kernel: one small D2H per call
+        unsigned long long bw = 0;
+        CL_CUDA(cudaMemcpyAsync(&bw, ws + L.misc, sizeof(bw), cudaMemcpyDeviceToHost, st));
+        CL_CUDA(cudaStreamSynchronize(st));
+        const int T = tile_rows(probe_block);
+        const int64_t ntiles = (op->A.n_cols + T - 1) / T;
+        const int64_t G = (int64_t)sms * fused_occupancy(probe_block);
+        fp.H = (int64_t)((bw + T - 1) / T) + 1;
+        fp.D = fp.H + 1 + G;
+        const double window = (double)(fp.D + fp.H + 2) * T * probe_block * 8.0 * 2.0;
+        int l2 = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        fp.on = g_fusion.load() == 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
+    }
     for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
         const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
         switch (probe_block) {
-            case 8: rc = run_block_mode<8>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
-            case 16: rc = run_block_mode<16>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
-            case 32: rc = run_block_mode<32>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
-            case 64: rc = run_block_mode<64>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
-            default: rc = run_block_mode<128>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms); break;
+            case 8: rc = run_block_mode<8>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 16: rc = run_block_mode<16>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 32: rc = run_block_mode<32>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 64: rc = run_block_mode<64>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            default: rc = run_block_mode<128>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
         }
         if (rc) return rc;
     }
@@ -445,7 +535,10 @@ int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int
     rc = cheb_finalize(mu, c, num_probes, degree, gp, stats, st);
     if (rc) return rc;
     double hstats[3];
+    unsigned int ferr = 0;
     CL_CUDA(cudaMemcpyAsync(hstats, stats, sizeof(hstats), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaMemcpyAsync(&ferr, (char*)ws.p + plan(op->A.n_cols, gather_nnz(op), k, op->kind, sm_count()).misc + 8,
+                            sizeof(ferr), cudaMemcpyDeviceToHost, st));
     if (out->per_probe)
         CL_CUDA(cudaMemcpyAsync(out->per_probe, gp, sizeof(double) * num_probes, cudaMemcpyDeviceToHost, st));
     if (out->moments)
@@ -456,6 +549,7 @@ int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int
     out->num_probes = num_probes;
     out->degree = degree;
     out->probe_block = k;
+    if (ferr) return fail(CL_ECUDA, "fused-step dependency wait timed out (CTAs not co-resident?)");
     if (hstats[2] != 1.0 || !std::isfinite(hstats[0]))
         return fail(CL_ENONFINITE, "non-finite estimate: [a,b]=[%g,%g] likely does not enclose the spectrum", a, b);
     return CL_OK;

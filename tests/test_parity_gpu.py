@@ -77,6 +77,47 @@ def test_moments_and_gamma_small(orc, name, k):
     assert abs(r.stderr - se) <= 1e-8 * se
 
 
+@pytest.fixture
+def fusion_mode():
+    """Restore the default temporal-fusion mode after a test."""
+    yield P.set_fusion
+    P.set_fusion(2)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
+@pytest.mark.parametrize("degree", [3, 4, 9, 40])
+def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, k, degree):
+    """The temporally fused two-step kernel (forced) gives moments bit-identical to one
+    launch per step, and both match the oracle (odd and even step counts)."""
+    wl = W.get_workload("gmrf_s")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    m = 11
+    fusion_mode(1)
+    single = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
+    fusion_mode(3)
+    n0 = P.launch_count()
+    fused = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
+    nl = P.launch_count() - n0
+    assert nl == 1 + 1 + 1 + (degree - 1) // 2 + (degree - 1) % 2  # prep, init, first, pairs, tail
+    assert np.array_equal(single, fused)
+    mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, degree, wl.seed, range(m), workers=4)
+    _check_moments(fused, mu, wl.d)
+
+
+def test_fused_wide_band_forced(orc, fusion_mode):
+    """Forced fusion stays correct for an operator with a wide band (random SPD:
+    bandwidth ~ d) -- the dependency wait covers the whole matrix."""
+    S = W.random_spd(20000, 6)
+    op = _dev_op("csr", S)
+    lam = 1.0 + 2.0 * np.abs(S.val).max() * 12
+    fusion_mode(3)
+    fused = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
+    fusion_mode(1)
+    single = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
+    assert np.array_equal(single, fused)
+
+
 def test_rank1_explicit_u(orc):
     T = W.torus_laplacian(21)
     u = np.linspace(0.5, 1.5, T.n_rows)
