@@ -150,7 +150,8 @@ int cheb_profile_end(double *step_ms, int64_t *step_launches);
  * two-step kernel (each launch = 2 Chebyshev steps). */
 int cheb_profile_fused(double *ms, int64_t *launches);
 
-/* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 2):
+/* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 1 -- the fused
+ * kernel is correct and bit-identical but not yet faster on B200):
  *   1 = one launch per Chebyshev step;
  *   2 = auto: pairs of steps (w_{j+1}, w_{j+2}) in one cooperative launch when the
  *       operator's bandwidth max|i - col| is small enough for the two-step wavefront to

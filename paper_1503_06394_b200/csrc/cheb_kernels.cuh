@@ -111,6 +111,24 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st2_hint(double* p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ double2 ldnc2_hint(const double* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+#ifndef CHEB_FUSED_HINTS
+#define CHEB_FUSED_HINTS 0  // fused kernel: keep the L2 window (w_j gathers, w_{j+1} stores) evict_last
+#endif
+
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -365,8 +383,13 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
 //   w_j  = FIRST ? y : 2y - w_{j-2}                 (written over w_{j-2})
 //   mu_j += v_i * w_j ;  rank-1: s_j += u_i * w_j
 // ---------------------------------------------------------------------------------------
+// Gather of data written earlier in the same launch (fused kernel, stage 2): a plain
+// L1-allocating load (not the read-only .nc path).  L1 is invalidated at launch and rows are
+// only read after they are final, so no stale line can be cached.
 __device__ __forceinline__ double2 ldcg2(const double* p) {
-    return __ldcg(reinterpret_cast<const double2*>(p));
+    double2 v;
+    asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
 }
 
 // One staged tile of the fused step.  xg: gather source; wcur: W_cur (for rows without a
@@ -413,8 +436,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
                 if (e0 + q < e_hi) {
                     const double* p = xg + (size_t)(uint32_t)c[q] * K;
-                    x0[q] = CG ? ldcg2(p + pa) : ldg2(p + pa);
-                    x1[q] = CG ? ldcg2(p + pb) : ldg2(p + pb);
+                    if (KEEP && CHEB_FUSED_HINTS) {
+                        const uint64_t pol = policy_evict_last();
+                        x0[q] = ldnc2_hint(p + pa, pol);
+                        x1[q] = ldnc2_hint(p + pb, pol);
+                    } else {
+                        x0[q] = CG ? ldcg2(p + pa) : ldg2(p + pa);
+                        x1[q] = CG ? ldcg2(p + pb) : ldg2(p + pb);
+                    }
                 } else {
                     x0[q] = x1[q] = make_double2(0.0, 0.0);
                 }
@@ -463,8 +492,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         }
         double* out = wout + (size_t)i * K;
         if (KEEP) {  // re-read from L2 later in the same launch (fused kernel, stage 1)
-            *reinterpret_cast<double2*>(out + pa) = n0;
-            *reinterpret_cast<double2*>(out + pb) = n1;
+            if (CHEB_FUSED_HINTS) {
+                const uint64_t pol = policy_evict_last();
+                st2_hint(out + pa, n0, pol);
+                st2_hint(out + pb, n1, pol);
+            } else {
+                *reinterpret_cast<double2*>(out + pa) = n0;
+                *reinterpret_cast<double2*>(out + pb) = n1;
+            }
         } else {     // streamed: next read is by a later launch
             __stcs(reinterpret_cast<double2*>(out + pa), n0);
             __stcs(reinterpret_cast<double2*>(out + pb), n1);
@@ -587,29 +622,38 @@ cheb_step_kernel(StepArgs a) {
 //   stage 2 (tile P - D):  w_{j+2} = 2 Ã w_{j+1} - w_j       (B: w_j -> w_{j+2},     gathers A)
 // Every element is computed with exactly the single-step arithmetic, in the same order, so
 // results are bit-identical to two cheb_step_kernel launches; only the schedule changes.
-// Stage 2 of tile u gathers w_{j+1} rows within the operator bandwidth beta of u and
-// overwrites w_j rows of u that stage 1 of tiles u-H-1..u+H+1 read (H = ceil(beta/TILE)+1),
-// so it waits for those stage-1 tiles (per-group completion counters, release/acquire).
-// The lag D = H + 1 + gridDim.x positions means every awaited tile was assigned to its CTA
-// in an earlier iteration: with all CTAs co-resident (cooperative launch) there is no
-// deadlock.  w_{j+1} stays in L2 between the stages: per 2 steps HBM sees w_{j-1}, w_j read
-// and w_{j+1}, w_{j+2} written (4 vector streams instead of 6).
+// CTA c handles positions P = c + k*G (k = 0, 1, ...): stage 1 of tile P, then stage 2 of
+// tile P - D.  Stage 2 of tile u gathers w_{j+1} rows within the operator bandwidth beta of
+// u and overwrites w_j rows of u that stage 1 of tiles u-H-1..u+H+1 read (H = ceil(beta/T)+1).
+// With D = (SLACK + ceil((H+2)/G)) * G those tiles all belong to iterations <= k - SLACK, so
+// stage 2 of iteration k only needs "every CTA finished stage 1 of iteration k - SLACK": one
+// counter per iteration (release add / acquire load), prefetched one item ahead so the check
+// is normally free.  D is a multiple of G, so stage-2 tile u runs on CTA u mod G exactly like
+// the single-step kernel: the per-CTA partial dot products (hence the moments) are
+// bit-identical too.  Waits point strictly backwards in k, so with all CTAs co-resident
+// (cooperative launch) there is no deadlock.  w_{j+1} stays in L2 between the stages: per
+// 2 steps HBM sees w_{j-1}, w_j read and w_{j+1}, w_{j+2} written (4 streams instead of 6).
 // ---------------------------------------------------------------------------------------
-constexpr int kFlagGroup = 16;  // stage-1 tiles per completion counter
+#ifndef CHEB_FUSED_SLACK
+#define CHEB_FUSED_SLACK 1
+#endif
+constexpr int kFusedSlack = CHEB_FUSED_SLACK;  // iterations of slack between the stages
 
 struct FusedArgs {
     double* A;                // in: w_{j-1}, out: w_{j+1}
     double* B;                // in: w_j,     out: w_{j+2}
-    unsigned int* cnt;        // [ceil(ntiles/kFlagGroup)] stage-1 completion counters (zeroed)
+    unsigned int* wave;       // [iterations] CTAs that finished stage 1 of iteration k (zeroed)
     unsigned int* err;        // dependency-wait timeout flag
-    int64_t H;                // dependency halo in tiles
-    int64_t D;                // stage-2 lag in positions
+    int64_t D;                // stage-2 lag in positions, a multiple of gridDim.x
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 template <int K>
@@ -624,6 +668,7 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
 
     const int tid = threadIdx.x;
     const int64_t Gd = gridDim.x;
+    const unsigned int nctas = gridDim.x;
     double mu1[4] = {0.0, 0.0, 0.0, 0.0}, mu2[4] = {0.0, 0.0, 0.0, 0.0};
     const double2 z2 = make_double2(0.0, 0.0);
     const int64_t npos = a.ntiles + f.D;  // positions 0 .. ntiles + D - 1
@@ -688,33 +733,43 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
     __syncthreads();
 
     int64_t q = 0;
+    int64_t waited = -1;    // thread 0: highest iteration known complete (stage 1, all CTAs)
+    int64_t peek_k = -1;    // thread 0: iteration whose counter was prefetched into peek
+    unsigned int peek = 0;
     for (int64_t m = 0; m < M; ++m) {
         int stg;
         int64_t t;
-        if (!item(m, stg, t)) continue;
+        if (!item(m, stg, t)) {
+            // an empty stage-1 slot (drain phase) still counts as "done" for iteration m/2
+            if (stg == 0 && tid == 0) red_release_add(f.wave + (m >> 1), 1u);
+            continue;
+        }
+        const int64_t k = m >> 1;
         const int b = (int)(q & 1);
         const uint32_t phase = (uint32_t)((q >> 1) & 1);
         if (tid == 0) {
             pending = advance(m_issue, nstg, nt);
             if (pending) bounds(nt, ne0, ne1);
         }
-        if (stg == 1 && tid < 32) {  // wait for stage 1 of tiles t-H-1 .. t+H+1
-            const int64_t lo = t - f.H - 1 < 0 ? 0 : t - f.H - 1;
-            const int64_t hi = t + f.H + 1 >= a.ntiles ? a.ntiles - 1 : t + f.H + 1;
-            for (int64_t g = lo / kFlagGroup + tid; g <= hi / kFlagGroup; g += 32) {
-                const unsigned int want = (unsigned int)imin64(kFlagGroup, a.ntiles - g * kFlagGroup);
+        if (stg == 1) {
+            const int64_t need = k - kFusedSlack;  // iteration whose stage 1 must be complete
+            if (tid == 0 && need > waited) {
+                unsigned int c = (peek_k == need) ? peek : 0u;
                 uint32_t spins = 0;
-                while (ld_acquire_u32(f.cnt + g) < want) {
-                    __nanosleep(128);
+                while (c < nctas) {
+                    __nanosleep(64);
+                    c = ld_acquire_u32(f.wave + need);
                     if ((++spins & 1023u) == 0 && (spins > (1u << 24) || ld_acquire_u32(f.err))) {
-                        atomicExch(f.err, 1u);  // ~2 s without progress: give up, never hang
+                        atomicExch(f.err, 1u);  // ~seconds without progress: give up, never hang
                         break;
                     }
                 }
+                waited = need;
+                peek_k = need + 1;
+                peek = ld_acquire_u32(f.wave + need + 1);  // consumed at the next stage-2 item
             }
-            __threadfence();
+            __syncthreads();
         }
-        if (stg == 1) __syncthreads();
         mbar_wait(&bar[b], phase);
         const unsigned char* st = smem + b * SL::BYTES;
         const int64_t r0 = t * G::TILE;
@@ -726,9 +781,6 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
             else
                 step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, z2, mu1, mu1, f.B,
                                                                   f.B, f.A);
-            __threadfence();  // publish this tile's w_{j+1} rows (and the end of its w_j reads)
-            __syncthreads();
-            if (tid == 0) atomicAdd(f.cnt + t / kFlagGroup, 1u);
         } else {
             if (s_fit[b])
                 step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
@@ -737,12 +789,20 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
                 step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, z2, mu2, mu2, f.A,
                                                                   f.A, f.B);
         }
-        __syncthreads();  // every warp is done with stage b
-        if (tid == 0 && pending) {
-            issue(nt, b, nstg ? f.B : f.A, ne0, ne1);
-            ++m_issue;
+        __syncthreads();  // every warp is done with stage b (and, for stage 1, with its stores)
+        if (tid == 0) {
+            if (stg == 0) red_release_add(f.wave + k, 1u);  // publish: this CTA finished stage 1 of k
+            if (pending) {
+                issue(nt, b, nstg ? f.B : f.A, ne0, ne1);
+                ++m_issue;
+            }
         }
         ++q;
+    }
+    // CTAs whose stage-1 work ended early still count towards later iterations' waits
+    if (tid == 0) {
+        const int64_t iters = (npos + Gd - 1) / Gd;
+        for (int64_t k = (M >> 1); k < iters; k++) red_release_add(f.wave + k, 1u);
     }
     grid_reduce_finish<K, 4, true, true, true>(mu1, mu2, a);
 }

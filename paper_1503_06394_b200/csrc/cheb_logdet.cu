@@ -51,7 +51,7 @@ struct Profiler {
     int64_t n[2] = {0, 0};
 } g_prof;
 
-std::atomic<int> g_fusion{2};  // max Chebyshev steps fused per launch (1 = off)
+std::atomic<int> g_fusion{1};  // temporal fusion mode: 1 off (default), 2 auto, 3 forced
 
 struct ProfScope {
     cudaStream_t s;
@@ -119,7 +119,7 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.va2 = off; off += align256(((size_t)nnz + 4) * sizeof(double));
     L.nodiag = off; off += align256(((size_t)d / 32 + 1) * sizeof(uint32_t));
     L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
-    L.cnt = off; off += align256(((size_t)ntiles / kFlagGroup + 1) * sizeof(unsigned int));
+    L.cnt = off; off += align256(((size_t)ntiles + 64) * sizeof(unsigned int));  // fused wave counters
     L.misc = off; off += 256;  // [0] u64 bandwidth, [8] u32 fused-wait error flag
     L.total = off;
     return L;
@@ -258,12 +258,12 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
             FusedArgs f{};
             f.A = nxt;
             f.B = (double*)cur;
-            f.cnt = (unsigned int*)(ws + L.cnt);
+            f.wave = (unsigned int*)(ws + L.cnt);
             f.err = (unsigned int*)(ws + L.misc + 8);
-            f.H = fp.H;
             f.D = fp.D;
             a.mu_col = j;
-            CL_CUDA(cudaMemsetAsync(f.cnt, 0, ((size_t)a.ntiles / kFlagGroup + 1) * sizeof(unsigned int), st));
+            const int64_t iters = (a.ntiles + fp.D + grid_fused - 1) / grid_fused;
+            CL_CUDA(cudaMemsetAsync(f.wave, 0, ((size_t)iters + 4) * sizeof(unsigned int), st));
             void* args[] = {&a, &f};
             ProfScope ps(st, 1);
             CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),
@@ -472,7 +472,7 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
         const int64_t ntiles = (op->A.n_cols + T - 1) / T;
         const int64_t G = (int64_t)sms * fused_occupancy(probe_block);
         fp.H = (int64_t)((bw + T - 1) / T) + 1;
-        fp.D = fp.H + 1 + G;
+        fp.D = (kFusedSlack + (fp.H + 2 + G - 1) / G) * G;
         const double window = (double)(fp.D + fp.H + 2) * T * probe_block * 8.0 * 2.0;
         int l2 = 0, dev = 0;
         cudaGetDevice(&dev);

@@ -7,6 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1503_06394_b200 import _build  # noqa: E402
 
 VARIANTS = {
+    "f_s1": ["CHEB_FUSED_SLACK=1"],
+    "f_s2": ["CHEB_FUSED_SLACK=2"],
+    "f_s1h": ["CHEB_FUSED_SLACK=1", "CHEB_FUSED_HINTS=1"],
+    "f_s2h": ["CHEB_FUSED_SLACK=2", "CHEB_FUSED_HINTS=1"],
     "u4c4": ["CHEB_NNZ_UNROLL=4", "CHEB_MIN_CTAS=4"],
     "u8c3": ["CHEB_NNZ_UNROLL=8", "CHEB_MIN_CTAS=3"],
     "u8c2": ["CHEB_NNZ_UNROLL=8", "CHEB_MIN_CTAS=2"],

@@ -81,7 +81,7 @@ def test_moments_and_gamma_small(orc, name, k):
 def fusion_mode():
     """Restore the default temporal-fusion mode after a test."""
     yield P.set_fusion
-    P.set_fusion(2)
+    P.set_fusion(1)
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
@@ -99,7 +99,8 @@ def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, k, degree):
     n0 = P.launch_count()
     fused = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
     nl = P.launch_count() - n0
-    assert nl == 1 + 1 + 1 + (degree - 1) // 2 + (degree - 1) % 2  # prep, init, first, pairs, tail
+    blocks = -(-m // k)
+    assert nl == 1 + blocks * (1 + 1 + (degree - 1) // 2 + (degree - 1) % 2)  # prep; init, first, pairs, tail
     assert np.array_equal(single, fused)
     mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, degree, wl.seed, range(m), workers=4)
     _check_moments(fused, mu, wl.d)
