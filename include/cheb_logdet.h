@@ -149,6 +149,18 @@ int cheb_profile_end(double *step_ms, int64_t *step_launches);
 /* After cheb_profile_end(): summed milliseconds and launch count of the temporally fused
  * two-step kernel (each launch = 2 Chebyshev steps). */
 int cheb_profile_fused(double *ms, int64_t *launches);
+/* After cheb_profile_end(): milliseconds and launches of the persistent kernel (each launch
+ * = all n Chebyshev steps of one probe block). */
+int cheb_profile_persistent(double *ms, int64_t *launches);
+
+/* Persistent multi-step schedule for CL_OP_CSR / CL_OP_CSR_RANK1 (process-wide):
+ *   0 = off (one launch per step);
+ *   1 = auto (default): all n steps of a probe block in one cooperative launch with a grid
+ *       barrier per step when the working set (two probe blocks + matrix) fits in half of
+ *       L2 -- there the per-step launch/drain gaps, not bandwidth, bound the step;
+ *   2 = always.
+ * Moments are bit-identical to per-step launches when both use the same grid size. */
+int cheb_set_persistent(int32_t mode);
 
 /* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 1 -- the fused
  * kernel is correct and bit-identical but not yet faster on B200):

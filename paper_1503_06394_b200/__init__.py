@@ -7,11 +7,11 @@ library raises.
 """
 from .api import (DeviceCSR, Operator, Result, Estimator, coeffs_log, workspace_bytes,
                   alloc_workspace, moments, finalize, logdet, logdet_host, bounds_btb, probes,
-                  launch_count, profile_begin, profile_end, set_fusion, log_abs_det_from_btb,
+                  launch_count, profile_begin, profile_end, set_fusion, set_persistent, log_abs_det_from_btb,
                   log_tau_from_rank1)
 from ._lib import ChebError, load as load_library
 
 __all__ = ["DeviceCSR", "Operator", "Result", "Estimator", "coeffs_log", "workspace_bytes",
            "alloc_workspace", "moments", "finalize", "logdet", "logdet_host", "bounds_btb",
-           "probes", "launch_count", "profile_begin", "profile_end", "set_fusion", "log_abs_det_from_btb",
+           "probes", "launch_count", "profile_begin", "profile_end", "set_fusion", "set_persistent", "log_abs_det_from_btb",
            "log_tau_from_rank1", "ChebError", "load_library"]

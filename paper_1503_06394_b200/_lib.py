@@ -72,6 +72,8 @@ def load():
         "cheb_profile_end": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "cheb_profile_fused": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "cheb_set_fusion": (I, [I32]),
+        "cheb_profile_persistent": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
+        "cheb_set_persistent": (I, [I32]),
         "cheb_last_error": (ctypes.c_char_p, []),
         "cheb_version": (I, []),
     }

@@ -236,7 +236,15 @@ def profile_end():
     check(L.cheb_profile_end(ctypes.byref(ms), ctypes.byref(n)))
     fms, fn = ctypes.c_double(), ctypes.c_int64()
     check(L.cheb_profile_fused(ctypes.byref(fms), ctypes.byref(fn)))
-    return {"single": (ms.value, n.value), "fused": (fms.value, fn.value)}
+    pms, pn = ctypes.c_double(), ctypes.c_int64()
+    check(L.cheb_profile_persistent(ctypes.byref(pms), ctypes.byref(pn)))
+    return {"single": (ms.value, n.value), "fused": (fms.value, fn.value),
+            "persistent": (pms.value, pn.value)}
+
+
+def set_persistent(mode: int):
+    """Persistent multi-step kernel (csr/rank-1): 0 off, 1 auto (default), 2 always."""
+    check(_lib.load().cheb_set_persistent(int(mode)))
 
 
 def set_fusion(steps: int):

@@ -807,6 +807,235 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
     grid_reduce_finish<K, 4, true, true, true>(mu1, mu2, a);
 }
 
+
+// ---------------------------------------------------------------------------------------
+// K2p: persistent multi-step kernel for small / L2-resident operators (csr, rank-1).
+// One cooperative launch runs steps j = 1..n of a probe block: each step walks the same
+// static tile schedule as cheb_step_kernel (tile t on CTA t mod G, same staged pipeline),
+// writes per-CTA partial dot products, and crosses one grid barrier.  CTA 0 then reduces
+// the partials in the same fixed order as grid_reduce_finish and publishes mu_j (and the
+// rank-1 s_j = u^T w_j, which the other CTAs await before finishing rows of step j+1), so
+// the moments are bit-identical to per-step launches with the same grid.  Removes the
+// n launch/drain gaps that dominate when one step is a few microseconds of L2 traffic.
+// ---------------------------------------------------------------------------------------
+struct PersistArgs {
+    double* w0;               // holds v (from probe_init) at entry
+    double* w1;
+    int32_t n;                // degree
+    double* part;             // [2][gridDim.x][K] mu partials (double-buffered by step parity)
+    double* part_s;           // [2][gridDim.x][K] rank-1 partials
+    double* s_buf;            // [2][K] s_j by step parity (s_0 from probe_init in s_buf[0])
+    unsigned int* bar_count;  // grid barrier arrival counter (zeroed)
+    unsigned int* bar_gen;    // grid barrier generation
+    unsigned int* s_ready;    // last step whose s_j is published (rank-1)
+    unsigned int* err;        // wait timeout flag
+};
+
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned int want, unsigned int* err) {
+    uint32_t spins = 0;
+    while (ld_acquire_u32(p) < want) {
+        __nanosleep(32);
+        if ((++spins & 1023u) == 0 && (spins > (1u << 25) || ld_acquire_u32(err))) {
+            atomicExch(err, 1u);
+            break;
+        }
+    }
+}
+
+// Sense-reversing grid barrier (all CTAs co-resident: cooperative launch).
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int g = ld_acquire_u32(gen);
+        __threadfence();
+        const unsigned int arrived = atomicAdd(count, 1u);
+        if (arrived == gridDim.x - 1) {
+            *count = 0u;
+            __threadfence();
+            st_release_u32(gen, g + 1u);
+        } else {
+            uint32_t spins = 0;
+            while (ld_acquire_u32(gen) == g) {
+                __nanosleep(32);
+                if ((++spins & 1023u) == 0 && (spins > (1u << 25) || ld_acquire_u32(err))) {
+                    atomicExch(err, 1u);
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kThreads, min_ctas(MODE))
+cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
+    using G = Geo<K>;
+    using SL = StageLayout<K, MODE>;
+    constexpr bool HAS_S = (MODE == MODE_RANK1);
+    constexpr int RED_T = kThreads / K;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int64_t s_base_c[2], s_base_v[2];
+    __shared__ int s_fit[2];
+    __shared__ double red_mu[kThreads / 32][K];
+    __shared__ double red_s[HAS_S ? kThreads / 32 : 1][K];
+    __shared__ double fin[2][RED_T][K];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lg = tid % G::L;
+    const int pa = 2 * lg, pb = K / 2 + pa;
+    const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    uint32_t uses[2] = {0u, 0u};
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    for (int32_t j = 1; j <= pa_.n; j++) {
+        const bool first = (j == 1);
+        const double* cur = (j & 1) ? pa_.w0 : pa_.w1;  // w_{j-1}
+        double* nxt = (j & 1) ? pa_.w1 : pa_.w0;        // w_{j-2} -> w_j
+        auto issue = [&](int64_t t, int b) {
+            unsigned char* st = smem + b * SL::BYTES;
+            const int64_t r0 = t * G::TILE;
+            const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+            const int64_t e0 = __ldg(a.rp + r0), e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+            const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
+            const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+            const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
+            s_fit[b] = fit;
+            s_base_c[b] = c0;
+            s_base_v[b] = v0;
+            const uint32_t wbytes = (uint32_t)rows * K * 8;
+            const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+            const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
+            uint32_t bytes = G::RPBYTES + sgbytes;
+            if (!first) bytes += wbytes;
+            if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+            if (HAS_S && a.r1u) bytes += ubytes;
+            mbar_expect_tx(&bar[b], bytes);
+            bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
+            bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+            if (!first) bulk_g2s(st + SL::OFF_WPREV, nxt + (size_t)r0 * K, wbytes, &bar[b]);
+            if (fit) {
+                bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
+                bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
+            }
+            if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
+        };
+        if (tid == 0) {
+            // w_{j-2} rows were written by generic-proxy stores of other CTAs in step j-2;
+            // order them before this CTA's async-proxy (TMA) reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (int64_t i = 0; i < 2 && i < nmine; i++) issue((int64_t)blockIdx.x + i * gridDim.x, (int)i);
+        }
+        // rank-1: the previous step's s_{j-1} (s_0 from probe_init) must be published
+        double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
+        if (HAS_S) {
+            if (j >= 2) {
+                if (tid == 0) spin_until_geq(pa_.s_ready, (unsigned int)(j - 1), pa_.err);
+                __syncthreads();
+            }
+            const double* sc = pa_.s_buf + ((j - 1) & 1) * K;
+            r1a = make_double2(a.r1c_alpha * __ldcg(sc + pa), a.r1c_alpha * __ldcg(sc + pa + 1));
+            r1b = make_double2(a.r1c_alpha * __ldcg(sc + pb), a.r1c_alpha * __ldcg(sc + pb + 1));
+        }
+        double mu[4] = {0.0, 0.0, 0.0, 0.0}, sacc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t it = 0; it < nmine; it++) {
+            const int b = (int)(it & 1);
+            mbar_wait(&bar[b], uses[b] & 1u);
+            uses[b]++;
+            const unsigned char* st = smem + b * SL::BYTES;
+            const int64_t t = (int64_t)blockIdx.x + it * gridDim.x;
+            const int64_t r0 = t * G::TILE;
+            const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+            if (first) {
+                if (s_fit[b])
+                    step_tile<K, MODE, true, true, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu,
+                                                         sacc, cur, cur, nxt);
+                else
+                    step_tile<K, MODE, true, false, true>(a, st, r0, rows, 0, 0, r1a, r1b, mu, sacc, cur, cur, nxt);
+            } else {
+                if (s_fit[b])
+                    step_tile<K, MODE, false, true, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu,
+                                                          sacc, cur, cur, nxt);
+                else
+                    step_tile<K, MODE, false, false, true>(a, st, r0, rows, 0, 0, r1a, r1b, mu, sacc, cur, cur, nxt);
+            }
+            __syncthreads();
+            if (tid == 0 && it + 2 < nmine) issue((int64_t)blockIdx.x + (it + 2) * gridDim.x, b);
+        }
+        // ---- per-CTA partials (same tree as grid_reduce_finish)
+#pragma unroll
+        for (int off = G::L; off < 32; off <<= 1) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                mu[q] += __shfl_xor_sync(0xffffffffu, mu[q], off);
+                if (HAS_S) sacc[q] += __shfl_xor_sync(0xffffffffu, sacc[q], off);
+            }
+        }
+        if (lane < G::L) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int p = probe_of<K, 4, true>(lg, q);
+                red_mu[warp][p] = mu[q];
+                if (HAS_S) red_s[warp][p] = sacc[q];
+            }
+        }
+        __syncthreads();
+        double* part = pa_.part + (size_t)(j & 1) * gridDim.x * K;
+        double* part_s = pa_.part_s + (size_t)(j & 1) * gridDim.x * K;
+        if (tid < K) {
+            double m = 0.0, t2 = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; w++) {
+                m += red_mu[w][tid];
+                if (HAS_S) t2 += red_s[w][tid];
+            }
+            part[(size_t)blockIdx.x * K + tid] = m;
+            if (HAS_S) part_s[(size_t)blockIdx.x * K + tid] = t2;
+        }
+        grid_barrier(pa_.bar_count, pa_.bar_gen, pa_.err);  // step j complete everywhere
+        if (blockIdx.x == 0) {  // fixed-order reduction of step j's partials
+            const int p = tid % K, r = tid / K;
+            double m = 0.0, t2 = 0.0;
+            for (int c = r; c < (int)gridDim.x; c += RED_T) {
+                m += __ldcg(part + (size_t)c * K + p);
+                if (HAS_S) t2 += __ldcg(part_s + (size_t)c * K + p);
+            }
+            fin[0][r][p] = m;
+            if (HAS_S) fin[1][r][p] = t2;
+            __syncthreads();
+            if (tid < K) {
+                double mm = 0.0, tt = 0.0;
+#pragma unroll
+                for (int q = 0; q < RED_T; q++) {
+                    mm += fin[0][q][tid];
+                    if (HAS_S) tt += fin[1][q][tid];
+                }
+                if (tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + j] = mm;
+                if (HAS_S) pa_.s_buf[(j & 1) * K + tid] = tt;
+            }
+            if (HAS_S) {
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    st_release_u32(pa_.s_ready, (unsigned int)j);
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // K3: Y = B W (first half of applying B^T B; Alg. 2 via P:312-314).  Plain gather SpMM.
 // ---------------------------------------------------------------------------------------

@@ -45,13 +45,15 @@ int fail(int code, const char* fmt, ...) {
 struct Profiler {
     std::mutex mu;
     bool on = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];  // [0] single step, [1] fused pair
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];  // [0] single step, [1] fused pair,
+                                                               // [2] persistent (all n steps)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
-    double ms[2] = {0.0, 0.0};
-    int64_t n[2] = {0, 0};
+    double ms[3] = {0.0, 0.0, 0.0};
+    int64_t n[3] = {0, 0, 0};
 } g_prof;
 
-std::atomic<int> g_fusion{1};  // temporal fusion mode: 1 off (default), 2 auto, 3 forced
+std::atomic<int> g_fusion{1};     // temporal fusion mode: 1 off (default), 2 auto, 3 forced
+std::atomic<int> g_persistent{1};  // persistent multi-step kernel: 0 off, 1 auto (default), 2 forced
 
 struct ProfScope {
     cudaStream_t s;
@@ -109,8 +111,8 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.w1 = off; off += wbytes;
     L.y = off; if (kind == CL_OP_BTB) off += wbytes;
     L.sbits = off; off += align256((size_t)d * words * sizeof(uint32_t) + 16);
-    L.part_mu = off; off += align256(maxgrid * k * sizeof(double));
-    L.part_s = off; off += align256(maxgrid * k * sizeof(double));
+    L.part_mu = off; off += align256(2 * maxgrid * k * sizeof(double));  // x2: persistent kernel
+    L.part_s = off; off += align256(2 * maxgrid * k * sizeof(double));
     L.sbuf = off; off += align256(2 * (size_t)k * sizeof(double));
     L.ticket = off; off += 256;
     L.rp2_len = ntiles * tile_rows(k) + 2;
@@ -120,7 +122,8 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.nodiag = off; off += align256(((size_t)d / 32 + 1) * sizeof(uint32_t));
     L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
     L.cnt = off; off += align256(((size_t)ntiles + 64) * sizeof(unsigned int));  // fused wave counters
-    L.misc = off; off += 256;  // [0] u64 bandwidth, [8] u32 fused-wait error flag
+    L.misc = off; off += 256;  // [0] u64 bandwidth, [8] u32 wait-timeout flag, [16] barrier count,
+                               // [20] barrier generation, [24] rank-1 s_ready
     L.total = off;
     return L;
 }
@@ -193,7 +196,8 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
 
 // Temporal fusion plan (CSR mode): stage-2 halo H (tiles) and lag D (positions).
 struct FusionPlan {
-    bool on = false;
+    bool on = false;          // temporally fused pairs
+    bool persistent = false;  // all steps in one persistent cooperative launch
     int64_t H = 0, D = 0;
 };
 
@@ -247,6 +251,27 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     if (MODE == MODE_BTB) {
         const int64_t ng = (op->A.n_rows + G::GROUPS - 1) / G::GROUPS;
         grid_spmm = grid_for(spmm_kernel<K>, ng, sms);
+    }
+    if (MODE != MODE_BTB && fp.persistent) {
+        const int grid_p = grid_for(cheb_persist_kernel<K, MODE>, a.ntiles, sms, smem);
+        PersistArgs pp{};
+        pp.w0 = w[0];
+        pp.w1 = w[1];
+        pp.n = n;
+        pp.part = (double*)(ws + L.part_mu);
+        pp.part_s = (double*)(ws + L.part_s);
+        pp.s_buf = sbuf;
+        pp.bar_count = (unsigned int*)(ws + L.misc + 16);
+        pp.bar_gen = (unsigned int*)(ws + L.misc + 20);
+        pp.s_ready = (unsigned int*)(ws + L.misc + 24);
+        pp.err = (unsigned int*)(ws + L.misc + 8);
+        CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
+        void* args[] = {&a, &pp};
+        ProfScope ps(st, 2);
+        CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_persist_kernel<K, MODE>, dim3(grid_p), dim3(kThreads),
+                                            args, smem, st));
+        g_launches++;
+        return CL_OK;
     }
     int grid_fused = 0;
     if (MODE == MODE_CSR && fp.on) grid_fused = grid_for(cheb_step2_kernel<K>, a.ntiles + fp.D, sms, smem);
@@ -354,7 +379,7 @@ int64_t cheb_launch_count(void) { return g_launches.load(); }
 
 int cheb_profile_begin(void) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < 3; k++) {
         for (auto& p : g_prof.ev[k]) g_prof.pool.push_back(p);
         g_prof.ev[k].clear();
         g_prof.ms[k] = 0.0;
@@ -367,7 +392,7 @@ int cheb_profile_begin(void) {
 int cheb_profile_end(double* step_ms, int64_t* step_launches) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = false;
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < 3; k++) {
         double tot = 0.0;
         for (auto& p : g_prof.ev[k]) {
             cudaError_t e = cudaEventSynchronize(p.second);
@@ -390,6 +415,19 @@ int cheb_profile_fused(double* ms, int64_t* launches) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     if (ms) *ms = g_prof.ms[1];
     if (launches) *launches = g_prof.n[1];
+    return CL_OK;
+}
+
+int cheb_profile_persistent(double* ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (ms) *ms = g_prof.ms[2];
+    if (launches) *launches = g_prof.n[2];
+    return CL_OK;
+}
+
+int cheb_set_persistent(int32_t mode) {
+    if (mode < 0 || mode > 2) return fail(CL_EINVAL, "persistent mode must be 0, 1 or 2");
+    g_persistent = mode;
     return CL_OK;
 }
 
@@ -463,7 +501,16 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
     CL_CUDA(cudaMemsetAsync(ws + L.misc, 0, 256, st));
     prep_mode(op, alpha, beta, ws, L, st, sms);
     FusionPlan fp;
-    if (op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
+    if (op->kind != CL_OP_BTB && g_persistent.load() > 0 && degree >= 1) {
+        // L2-resident working set (two probe-block buffers + matrix): the per-step launch and
+        // drain gaps dominate, so run all steps in one launch
+        int l2 = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        const double wset = 2.0 * op->A.n_cols * probe_block * 8.0 + 12.0 * op->A.nnz + 8.0 * op->A.n_cols;
+        fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
+    }
+    if (!fp.persistent && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
         // needs the operator bandwidth computed by the prep kernel: one small D2H per call
         unsigned long long bw = 0;
         CL_CUDA(cudaMemcpyAsync(&bw, ws + L.misc, sizeof(bw), cudaMemcpyDeviceToHost, st));

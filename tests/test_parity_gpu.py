@@ -60,9 +60,20 @@ def test_probes_bit_identical(orc, d, p0, k):
 SMALL = ["gmrf32", "gmrf_s", "torus_s", "btb_s"]
 
 
+@pytest.fixture
+def persistent_mode():
+    """Restore the default persistent-kernel mode after a test."""
+    yield P.set_persistent
+    P.set_persistent(1)
+
+
 @pytest.mark.parametrize("name", SMALL)
 @pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
-def test_moments_and_gamma_small(orc, name, k):
+@pytest.mark.parametrize("persist", [0, 2])
+def test_moments_and_gamma_small(orc, persistent_mode, name, k, persist):
+    """Per-step launches (persist=0) and the persistent multi-step kernel (persist=2,
+    csr/rank-1) against the oracle."""
+    persistent_mode(persist)
     wl = W.get_workload(name)
     A, At = _mats(wl)
     op = _dev_op(wl.mode, A, At, wl.r1_c)
@@ -213,13 +224,31 @@ def test_nonfinite_detected():
     assert ei.value.code == -5
 
 
-def test_launch_count_increases():
+def test_launch_count_increases(persistent_mode):
     wl = W.get_workload("gmrf32")
     A, _ = _mats(wl)
     op = _dev_op("csr", A)
+    persistent_mode(0)
     n0 = P.launch_count()
     P.logdet(op, wl.a, wl.b, 10, 16, k=16)
     assert P.launch_count() - n0 == 1 + 1 + 10 + 1  # prep + init + 10 steps + finalize
+    persistent_mode(2)
+    n0 = P.launch_count()
+    P.logdet(op, wl.a, wl.b, 10, 16, k=16)
+    assert P.launch_count() - n0 == 1 + 1 + 1 + 1  # prep + init + persistent + finalize
+
+
+@pytest.mark.parametrize("name", ["gmrf32", "torus_s", "gmrf_s"])
+def test_persistent_bit_identical_to_per_step(persistent_mode, name):
+    """Same grid, same tile schedule, same reduction order: identical moments."""
+    wl = W.get_workload(name)
+    A, _ = _mats(wl)
+    op = _dev_op(wl.mode, A, None, wl.r1_c)
+    out = {}
+    for mode in (0, 2):
+        persistent_mode(mode)
+        out[mode] = P.moments(op, wl.a, wl.b, wl.degree, 0, 24, 5, 16).cpu().numpy()
+    assert np.array_equal(out[0], out[2])
 
 
 # ------------------------------------------------------------------ estimate vs truth
