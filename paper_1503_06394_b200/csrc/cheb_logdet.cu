@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -326,7 +327,7 @@ int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, 
         case CL_OP_CSR:
             return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         case CL_OP_CSR_RANK1:
-            return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
+            return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         default:
             return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
     }
@@ -509,6 +510,7 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         const double wset = 2.0 * op->A.n_cols * probe_block * 8.0 + 12.0 * op->A.nnz + 8.0 * op->A.n_cols;
         fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
+        if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
     if (!fp.persistent && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
         // needs the operator bandwidth computed by the prep kernel: one small D2H per call
@@ -526,6 +528,10 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         fp.on = g_fusion.load() == 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
     }
+    if (getenv("CHEB_DEBUG"))
+        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d H=%lld D=%lld\n",
+                (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
+                (int)fp.on, (long long)fp.H, (long long)fp.D);
     for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
         const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;

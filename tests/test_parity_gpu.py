@@ -60,13 +60,6 @@ def test_probes_bit_identical(orc, d, p0, k):
 SMALL = ["gmrf32", "gmrf_s", "torus_s", "btb_s"]
 
 
-@pytest.fixture
-def persistent_mode():
-    """Restore the default persistent-kernel mode after a test."""
-    yield P.set_persistent
-    P.set_persistent(1)
-
-
 @pytest.mark.parametrize("name", SMALL)
 @pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
 @pytest.mark.parametrize("persist", [0, 2])
@@ -89,6 +82,13 @@ def test_moments_and_gamma_small(orc, persistent_mode, name, k, persist):
 
 
 @pytest.fixture
+def persistent_mode():
+    """Restore the default persistent-kernel mode after a test."""
+    yield P.set_persistent
+    P.set_persistent(1)
+
+
+@pytest.fixture
 def fusion_mode():
     """Restore the default temporal-fusion mode after a test."""
     yield P.set_fusion
@@ -97,9 +97,10 @@ def fusion_mode():
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
 @pytest.mark.parametrize("degree", [3, 4, 9, 40])
-def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, k, degree):
+def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, persistent_mode, k, degree):
     """The temporally fused two-step kernel (forced) gives moments bit-identical to one
     launch per step, and both match the oracle (odd and even step counts)."""
+    persistent_mode(0)
     wl = W.get_workload("gmrf_s")
     A, _ = _mats(wl)
     op = _dev_op("csr", A)
@@ -117,9 +118,10 @@ def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, k, degree):
     _check_moments(fused, mu, wl.d)
 
 
-def test_fused_wide_band_forced(orc, fusion_mode):
+def test_fused_wide_band_forced(orc, fusion_mode, persistent_mode):
     """Forced fusion stays correct for an operator with a wide band (random SPD:
     bandwidth ~ d) -- the dependency wait covers the whole matrix."""
+    persistent_mode(0)
     S = W.random_spd(20000, 6)
     op = _dev_op("csr", S)
     lam = 1.0 + 2.0 * np.abs(S.val).max() * 12
