@@ -190,6 +190,80 @@ struct StepArgs {
 // (lane group size LG = K/PPL).  Fixed shuffle tree in a warp, warps in index order, CTAs
 // in a fixed strided order; the last CTA to finish (atomic ticket) writes the result.
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Canonical (deterministic) reduction of the per-CTA partials part[c][p], c < G, for one
+// probe p:  thread t sums c = t, t+256, ... ascending; lanes combine with the xor-butterfly
+// 16, 8, 4, 2, 1 (every lane ends with the bitwise-same sum); warps 0..7 are added in order.
+// Every kernel that produces moments (per-step, fused, persistent) uses exactly this order,
+// so the result depends only on the grid size G -- not on which kernel or CTA computed it.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum_xor(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// All K probes by one CTA (last-CTA-done epilogue).  out_mu/out_s: shared arrays [K].
+template <int K, bool HAS_S>
+__device__ __forceinline__ void reduce_partials_all(const double* part, const double* part_s, int G,
+                                                    double* out_mu, double* out_s) {
+    __shared__ double wsum[2][kThreads / 32][8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int p0 = 0; p0 < K; p0 += 8) {
+        double m[8], t[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) m[q] = t[q] = 0.0;
+        for (int c = tid; c < G; c += kThreads) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                m[q] += __ldcg(part + (size_t)c * K + p0 + q);
+                if (HAS_S) t[q] += __ldcg(part_s + (size_t)c * K + p0 + q);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            m[q] = warp_sum_xor(m[q]);
+            if (HAS_S) t[q] = warp_sum_xor(t[q]);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                wsum[0][warp][q] = m[q];
+                if (HAS_S) wsum[1][warp][q] = t[q];
+            }
+        }
+        __syncthreads();
+        if (tid < 8) {
+            double mm = 0.0, tt = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; w++) {
+                mm += wsum[0][w][tid];
+                if (HAS_S) tt += wsum[1][w][tid];
+            }
+            out_mu[p0 + tid] = mm;
+            if (HAS_S) out_s[p0 + tid] = tt;
+        }
+        __syncthreads();
+    }
+}
+
+// One probe p by one CTA (persistent kernel); returns the sum in thread 0.
+__device__ __forceinline__ double reduce_partials_one(const double* part, int K, int G, int p, double* wbuf) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double m = 0.0;
+    for (int c = tid; c < G; c += kThreads) m += __ldcg(part + (size_t)c * K + p);
+    m = warp_sum_xor(m);
+    if (lane == 0) wbuf[warp] = m;
+    __syncthreads();
+    double r = 0.0;
+    if (tid == 0) {
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; w++) r += wbuf[w];
+    }
+    __syncthreads();
+    return r;
+}
+
 // Lane lg of a row group owns probes probe_of<K,PPL,SPLIT>(lg, q), q < PPL: contiguous
 // (pl = PPL*lg + q) or, with SPLIT (PPL = 4), two pairs from the two halves of the row
 // {2lg, 2lg+1, K/2+2lg, K/2+2lg+1} so that every 16-byte access of a warp is contiguous.
@@ -201,11 +275,10 @@ __device__ __forceinline__ int probe_of(int lg, int q) {
 template <int K, int PPL, bool HAS_S, bool SPLIT = false, bool S_IS_MU = false>
 __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s)[PPL], const StepArgs& a) {
     constexpr int LG = K / PPL;
-    constexpr int RED_T = kThreads / K;
     __shared__ double red_mu[kThreads / 32][K];
     __shared__ double red_s[HAS_S ? kThreads / 32 : 1][K];
-    __shared__ double fin_mu[RED_T][K];
-    __shared__ double fin_s[HAS_S ? RED_T : 1][K];
+    __shared__ double fin_mu[K];
+    __shared__ double fin_s[HAS_S ? K : 1];
     __shared__ bool is_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = lane % LG;
@@ -245,27 +318,11 @@ __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    {
-        const int p = tid % K, r = tid / K;
-        double m = 0.0, t = 0.0;
-        for (int c = r; c < (int)gridDim.x; c += RED_T) {
-            m += __ldcg(a.part_mu + (size_t)c * K + p);
-            if (HAS_S) t += __ldcg(a.part_s + (size_t)c * K + p);
-        }
-        fin_mu[r][p] = m;
-        if (HAS_S) fin_s[r][p] = t;
-    }
-    __syncthreads();
+    reduce_partials_all<K, HAS_S>(a.part_mu, a.part_s, (int)gridDim.x, fin_mu, fin_s);
     if (tid < K) {
-        double m = 0.0, t = 0.0;
-#pragma unroll
-        for (int r = 0; r < RED_T; r++) {
-            m += fin_mu[r][tid];
-            if (HAS_S) t += fin_s[r][tid];
-        }
-        if (tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col] = m;
-        if (HAS_S && S_IS_MU && tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col + 1] = t;
-        if (HAS_S && !S_IS_MU) a.s_next[tid] = t;
+        if (tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col] = fin_mu[tid];
+        if (HAS_S && S_IS_MU && tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col + 1] = fin_s[tid];
+        if (HAS_S && !S_IS_MU) a.s_next[tid] = fin_s[tid];
     }
     if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch (stream-ordered)
 }
@@ -811,12 +868,15 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
 // ---------------------------------------------------------------------------------------
 // K2p: persistent multi-step kernel for small / L2-resident operators (csr, rank-1).
 // One cooperative launch runs steps j = 1..n of a probe block: each step walks the same
-// static tile schedule as cheb_step_kernel (tile t on CTA t mod G, same staged pipeline),
-// writes per-CTA partial dot products, and crosses one grid barrier.  CTA 0 then reduces
-// the partials in the same fixed order as grid_reduce_finish and publishes mu_j (and the
-// rank-1 s_j = u^T w_j, which the other CTAs await before finishing rows of step j+1), so
-// the moments are bit-identical to per-step launches with the same grid.  Removes the
-// n launch/drain gaps that dominate when one step is a few microseconds of L2 traffic.
+// static tile schedule as cheb_step_kernel (tile t on CTA t mod G, same staged pipeline) and
+// writes per-CTA partial dot products; CTAs then arrive at a grid barrier (monotone
+// counter: step j is complete when it reaches j*G).  Before waiting, each CTA already issues
+// the TMA copies of its first tiles of step j+1 (W_prev = w_{j-1} and the matrix are final),
+// so the barrier latency overlaps the next step's staging.  After the barrier every CTA
+// reduces the rank-1 partials itself (s_j = u^T w_j, same fixed order everywhere) and CTA 0
+// reduces mu_j, in the order grid_reduce_finish uses: moments are bit-identical to per-step
+// launches with the same grid.  Removes the n launch/drain gaps that dominate when one step
+// is a few microseconds of L2 traffic.
 // ---------------------------------------------------------------------------------------
 struct PersistArgs {
     double* w0;               // holds v (from probe_init) at entry
@@ -825,51 +885,20 @@ struct PersistArgs {
     double* part;             // [2][gridDim.x][K] mu partials (double-buffered by step parity)
     double* part_s;           // [2][gridDim.x][K] rank-1 partials
     double* s_buf;            // [2][K] s_j by step parity (s_0 from probe_init in s_buf[0])
-    unsigned int* bar_count;  // grid barrier arrival counter (zeroed)
-    unsigned int* bar_gen;    // grid barrier generation
-    unsigned int* s_ready;    // last step whose s_j is published (rank-1)
+    unsigned int* bar_count;  // grid barrier arrivals (zeroed; monotone)
+    unsigned int* s_count;    // rank-1: probes whose s_j is published (zeroed; monotone)
     unsigned int* err;        // wait timeout flag
 };
-
-__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned int want, unsigned int* err) {
     uint32_t spins = 0;
     while (ld_acquire_u32(p) < want) {
-        __nanosleep(32);
+        __nanosleep(20);
         if ((++spins & 1023u) == 0 && (spins > (1u << 25) || ld_acquire_u32(err))) {
-            atomicExch(err, 1u);
+            atomicExch(err, 1u);  // ~seconds without progress: give up, never hang
             break;
         }
     }
-}
-
-// Sense-reversing grid barrier (all CTAs co-resident: cooperative launch).
-__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int* err) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned int g = ld_acquire_u32(gen);
-        __threadfence();
-        const unsigned int arrived = atomicAdd(count, 1u);
-        if (arrived == gridDim.x - 1) {
-            *count = 0u;
-            __threadfence();
-            st_release_u32(gen, g + 1u);
-        } else {
-            uint32_t spins = 0;
-            while (ld_acquire_u32(gen) == g) {
-                __nanosleep(32);
-                if ((++spins & 1023u) == 0 && (spins > (1u << 25) || ld_acquire_u32(err))) {
-                    atomicExch(err, 1u);
-                    break;
-                }
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
 }
 
 template <int K, int MODE>
@@ -878,14 +907,14 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
-    constexpr int RED_T = kThreads / K;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ int64_t s_base_c[2], s_base_v[2];
     __shared__ int s_fit[2];
     __shared__ double red_mu[kThreads / 32][K];
     __shared__ double red_s[HAS_S ? kThreads / 32 : 1][K];
-    __shared__ double fin[2][RED_T][K];
+    __shared__ double wbuf[kThreads / 32];
+    __shared__ double s_sh[HAS_S ? K : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = tid % G::L;
@@ -893,61 +922,55 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     uint32_t uses[2] = {0u, 0u};
 
+    // staging of tile t of step j into stage b (thread 0)
+    auto issue = [&](int32_t j, int64_t t, int b) {
+        const bool first = (j == 1);
+        const double* wprev = (j & 1) ? pa_.w1 : pa_.w0;  // w_{j-2}
+        unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        const int64_t e0 = __ldg(a.rp + r0), e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+        const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
+        const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+        const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
+        s_fit[b] = fit;
+        s_base_c[b] = c0;
+        s_base_v[b] = v0;
+        const uint32_t wbytes = (uint32_t)rows * K * 8;
+        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+        const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
+        uint32_t bytes = G::RPBYTES + sgbytes;
+        if (!first) bytes += wbytes;
+        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+        if (HAS_S && a.r1u) bytes += ubytes;
+        mbar_expect_tx(&bar[b], bytes);
+        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
+        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        if (!first) bulk_g2s(st + SL::OFF_WPREV, wprev + (size_t)r0 * K, wbytes, &bar[b]);
+        if (fit) {
+            bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
+            bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
+        }
+        if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
+    };
+
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_mbar_init();
+        for (int64_t i = 0; i < 2 && i < nmine; i++) issue(1, (int64_t)blockIdx.x + i * gridDim.x, (int)i);
     }
+    if (HAS_S && tid < K) s_sh[tid] = __ldcg(pa_.s_buf + tid);  // s_0
     __syncthreads();
 
     for (int32_t j = 1; j <= pa_.n; j++) {
         const bool first = (j == 1);
         const double* cur = (j & 1) ? pa_.w0 : pa_.w1;  // w_{j-1}
         double* nxt = (j & 1) ? pa_.w1 : pa_.w0;        // w_{j-2} -> w_j
-        auto issue = [&](int64_t t, int b) {
-            unsigned char* st = smem + b * SL::BYTES;
-            const int64_t r0 = t * G::TILE;
-            const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-            const int64_t e0 = __ldg(a.rp + r0), e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
-            const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
-            const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
-            const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
-            s_fit[b] = fit;
-            s_base_c[b] = c0;
-            s_base_v[b] = v0;
-            const uint32_t wbytes = (uint32_t)rows * K * 8;
-            const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
-            const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
-            uint32_t bytes = G::RPBYTES + sgbytes;
-            if (!first) bytes += wbytes;
-            if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
-            if (HAS_S && a.r1u) bytes += ubytes;
-            mbar_expect_tx(&bar[b], bytes);
-            bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
-            bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
-            if (!first) bulk_g2s(st + SL::OFF_WPREV, nxt + (size_t)r0 * K, wbytes, &bar[b]);
-            if (fit) {
-                bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
-                bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
-            }
-            if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
-        };
-        if (tid == 0) {
-            // w_{j-2} rows were written by generic-proxy stores of other CTAs in step j-2;
-            // order them before this CTA's async-proxy (TMA) reads
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            for (int64_t i = 0; i < 2 && i < nmine; i++) issue((int64_t)blockIdx.x + i * gridDim.x, (int)i);
-        }
-        // rank-1: the previous step's s_{j-1} (s_0 from probe_init) must be published
         double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
         if (HAS_S) {
-            if (j >= 2) {
-                if (tid == 0) spin_until_geq(pa_.s_ready, (unsigned int)(j - 1), pa_.err);
-                __syncthreads();
-            }
-            const double* sc = pa_.s_buf + ((j - 1) & 1) * K;
-            r1a = make_double2(a.r1c_alpha * __ldcg(sc + pa), a.r1c_alpha * __ldcg(sc + pa + 1));
-            r1b = make_double2(a.r1c_alpha * __ldcg(sc + pb), a.r1c_alpha * __ldcg(sc + pb + 1));
+            r1a = make_double2(a.r1c_alpha * s_sh[pa], a.r1c_alpha * s_sh[pa + 1]);
+            r1b = make_double2(a.r1c_alpha * s_sh[pb], a.r1c_alpha * s_sh[pb + 1]);
         }
         double mu[4] = {0.0, 0.0, 0.0, 0.0}, sacc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int64_t it = 0; it < nmine; it++) {
@@ -972,7 +995,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
                     step_tile<K, MODE, false, false, true>(a, st, r0, rows, 0, 0, r1a, r1b, mu, sacc, cur, cur, nxt);
             }
             __syncthreads();
-            if (tid == 0 && it + 2 < nmine) issue((int64_t)blockIdx.x + (it + 2) * gridDim.x, b);
+            if (tid == 0 && it + 2 < nmine) issue(j, (int64_t)blockIdx.x + (it + 2) * gridDim.x, b);
         }
         // ---- per-CTA partials (same tree as grid_reduce_finish)
 #pragma unroll
@@ -1004,34 +1027,45 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             part[(size_t)blockIdx.x * K + tid] = m;
             if (HAS_S) part_s[(size_t)blockIdx.x * K + tid] = t2;
         }
-        grid_barrier(pa_.bar_count, pa_.bar_gen, pa_.err);  // step j complete everywhere
-        if (blockIdx.x == 0) {  // fixed-order reduction of step j's partials
-            const int p = tid % K, r = tid / K;
-            double m = 0.0, t2 = 0.0;
-            for (int c = r; c < (int)gridDim.x; c += RED_T) {
-                m += __ldcg(part + (size_t)c * K + p);
-                if (HAS_S) t2 += __ldcg(part_s + (size_t)c * K + p);
+        // ---- grid barrier, split: arrive, stage step j+1, wait
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(pa_.bar_count, 1u);
+            if (j < pa_.n) {
+                // w_{j-1} (W_prev of step j+1) and the matrix are final: stage ahead.  The
+                // proxy fence orders other CTAs' generic stores of w_{j-1} (step j-1, already
+                // behind the previous barrier) before these async-proxy reads.
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                for (int64_t i = 0; i < 2 && i < nmine; i++)
+                    issue(j + 1, (int64_t)blockIdx.x + i * gridDim.x, (int)i);  // stages are all consumed
             }
-            fin[0][r][p] = m;
-            if (HAS_S) fin[1][r][p] = t2;
-            __syncthreads();
-            if (tid < K) {
-                double mm = 0.0, tt = 0.0;
-#pragma unroll
-                for (int q = 0; q < RED_T; q++) {
-                    mm += fin[0][q][tid];
-                    if (HAS_S) tt += fin[1][q][tid];
-                }
-                if (tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + j] = mm;
-                if (HAS_S) pa_.s_buf[(j & 1) * K + tid] = tt;
-            }
+            spin_until_geq(pa_.bar_count, (unsigned int)j * gridDim.x, pa_.err);
+            __threadfence();
+        }
+        __syncthreads();
+        // ---- canonical reductions of step j's partials: CTA c owns probes c, c+G, ...
+        for (int p = blockIdx.x; p < K; p += gridDim.x) {
+            const double m = reduce_partials_one(part, K, (int)gridDim.x, p, wbuf);
+            if (tid == 0 && p < a.kvalid) a.mu_out[(size_t)p * a.mu_stride + j] = m;
             if (HAS_S) {
-                __syncthreads();
-                if (tid == 0) {
-                    __threadfence();
-                    st_release_u32(pa_.s_ready, (unsigned int)j);
-                }
+                const double t2 = reduce_partials_one(part_s, K, (int)gridDim.x, p, wbuf);
+                if (tid == 0) pa_.s_buf[(j & 1) * K + p] = t2;
             }
+        }
+        if (HAS_S) {
+            if (tid == 0) {
+                const unsigned int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+                if (mine) {
+                    __threadfence();
+                    atomicAdd(pa_.s_count, mine);
+                }
+                spin_until_geq(pa_.s_count, (unsigned int)j * K, pa_.err);  // every s_j published
+                __threadfence();
+            }
+            __syncthreads();
+            if (tid < K) s_sh[tid] = __ldcg(pa_.s_buf + (j & 1) * K + tid);
+            __syncthreads();
         }
     }
 }

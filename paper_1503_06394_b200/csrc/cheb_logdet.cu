@@ -167,6 +167,17 @@ int check_ab(double a, double b, int32_t degree) {
     return CL_OK;
 }
 
+// Tiles per CTA below which a step-kernel grid is shrunk (small operators: fewer CTAs mean a
+// deeper per-CTA pipeline and cheaper grid-wide reductions/barriers).  CHEB_MIN_TILES tunes it.
+int min_tiles_per_cta() {
+    static int v = [] {
+        const char* e = getenv("CHEB_MIN_TILES");
+        const int x = e ? atoi(e) : 1;
+        return x < 1 ? 1 : x;
+    }();
+    return v;
+}
+
 template <typename Kern>
 int grid_for(Kern kern, int64_t ntiles, int sms, size_t dyn_smem = 0) {
     int occ = 0;
@@ -175,6 +186,10 @@ int grid_for(Kern kern, int64_t ntiles, int sms, size_t dyn_smem = 0) {
     if (occ < 1) occ = 1;
     if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
     int64_t g = (int64_t)sms * occ;
+    if (dyn_smem > 0) {  // staged step kernels: keep >= min_tiles_per_cta() tiles per CTA
+        const int64_t cap = (ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta();
+        if (g > cap) g = cap;
+    }
     if (g > ntiles) g = ntiles;
     return (int)(g < 1 ? 1 : g);
 }
@@ -200,6 +215,7 @@ struct FusionPlan {
     bool on = false;          // temporally fused pairs
     bool persistent = false;  // all steps in one persistent cooperative launch
     int64_t H = 0, D = 0;
+    int G = 0;                // fused grid (= the single-step grid, for bit-identical moments)
 };
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
@@ -263,8 +279,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         pp.part_s = (double*)(ws + L.part_s);
         pp.s_buf = sbuf;
         pp.bar_count = (unsigned int*)(ws + L.misc + 16);
-        pp.bar_gen = (unsigned int*)(ws + L.misc + 20);
-        pp.s_ready = (unsigned int*)(ws + L.misc + 24);
+        pp.s_count = (unsigned int*)(ws + L.misc + 20);
         pp.err = (unsigned int*)(ws + L.misc + 8);
         CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
         void* args[] = {&a, &pp};
@@ -275,7 +290,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         return CL_OK;
     }
     int grid_fused = 0;
-    if (MODE == MODE_CSR && fp.on) grid_fused = grid_for(cheb_step2_kernel<K>, a.ntiles + fp.D, sms, smem);
+    if (MODE == MODE_CSR && fp.on) grid_fused = fp.G;
     for (int32_t j = 1; j <= n; j++) {
         const double* cur = w[(j - 1) & 1];
         double* nxt = w[j & 1];
@@ -355,6 +370,16 @@ int fused_occupancy(int k) {
         case 32: return occ_of(cheb_step2_kernel<32>, StageLayout<32, MODE_CSR>::SMEM);
         case 64: return occ_of(cheb_step2_kernel<64>, StageLayout<64, MODE_CSR>::SMEM);
         default: return occ_of(cheb_step2_kernel<128>, StageLayout<128, MODE_CSR>::SMEM);
+    }
+}
+
+int step_grid_csr(int k, int64_t ntiles, int sms) {
+    switch (k) {
+        case 8: return grid_for(cheb_step_kernel<8, MODE_CSR, false>, ntiles, sms, StageLayout<8, MODE_CSR>::SMEM);
+        case 16: return grid_for(cheb_step_kernel<16, MODE_CSR, false>, ntiles, sms, StageLayout<16, MODE_CSR>::SMEM);
+        case 32: return grid_for(cheb_step_kernel<32, MODE_CSR, false>, ntiles, sms, StageLayout<32, MODE_CSR>::SMEM);
+        case 64: return grid_for(cheb_step_kernel<64, MODE_CSR, false>, ntiles, sms, StageLayout<64, MODE_CSR>::SMEM);
+        default: return grid_for(cheb_step_kernel<128, MODE_CSR, false>, ntiles, sms, StageLayout<128, MODE_CSR>::SMEM);
     }
 }
 
@@ -519,7 +544,12 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
         CL_CUDA(cudaStreamSynchronize(st));
         const int T = tile_rows(probe_block);
         const int64_t ntiles = (op->A.n_cols + T - 1) / T;
-        const int64_t G = (int64_t)sms * fused_occupancy(probe_block);
+        // same grid as the single-step kernel (bit-identical per-CTA partial sums), limited to
+        // what the fused kernel can keep co-resident
+        int64_t G = step_grid_csr(probe_block, ntiles, sms);
+        const int64_t Gmax = (int64_t)sms * fused_occupancy(probe_block);
+        if (G > Gmax) G = Gmax;
+        fp.G = (int)G;
         fp.H = (int64_t)((bw + T - 1) / T) + 1;
         fp.D = (kFusedSlack + (fp.H + 2 + G - 1) / G) * G;
         const double window = (double)(fp.D + fp.H + 2) * T * probe_block * 8.0 * 2.0;
