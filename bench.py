@@ -296,7 +296,9 @@ def run_ours(args):
             "traffic": _traffic_per_launch(wl.name, k)}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": "weak",
+           "vs_baseline": (value / wl.paper_probe_steps_per_s) if wl.paper_probe_steps_per_s else None,
+           "dtype": "f64", "data": "synthetic",
            "config": {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": d,
                       "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total,
                       "probes_per_gpu": m_per_gpu, "probe_block": k, "a": a, "b": b,

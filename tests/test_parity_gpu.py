@@ -57,7 +57,7 @@ def test_probes_bit_identical(orc, d, p0, k):
 
 
 # ------------------------------------------------------------------ small configs, every k
-SMALL = ["gmrf32", "gmrf_s", "torus_s", "btb_s"]
+SMALL = ["gmrf32", "gmrf_s", "torus_s", "btb_s", "spd_s"]
 
 
 @pytest.mark.parametrize("name", SMALL)

@@ -10,7 +10,7 @@ Recipes (BASELINE.json configs):
 * random_nonsingular(d, seed): diag 3.0 + 8 distinct off-diagonal columns per
   row drawn uniformly, values U(-0.1, 0.1) (BASELINE.json configs[4]; reading G19).
 * random_spd(d, seed): the paper's §5.1 generator: 5 U[-1,1]
-  off-diagonals per row, symmetrised, diagonal = abs row sum + 1e-3.
+  off-diagonals per row, symmetrised, diagonal = abs row sum + 1e-3 (reading G23).
 * triangular_b / complete_graph_laplacian: pin inputs with closed-form answers.
 """
 import numpy as np
@@ -125,32 +125,54 @@ def random_nonsingular(d: int, seed: int = 1, per_row: int = 8,
     return from_coo(d, d, r, c, v)
 
 
-def random_spd(d: int, seed: int = 1, per_row: int = 5, shift: float = 1e-3) -> CSR:
-    """Paper §5.1 generator: per row `per_row` off-diagonal entries
-    U[-1,1] at uniform random columns, symmetrised (C + C^T)/2-free: the pair
-    (i,j),(j,i) both get the drawn value; duplicates summed; diagonal = absolute
-    off-diagonal row sum + shift (strictly diagonally dominant => SPD)."""
-    rows = np.repeat(np.arange(d, dtype=np.int64), per_row)
-    ctr = 1 + np.arange(d * per_row, dtype=np.uint64)
-    z = splitmix64_at(seed, ctr)
-    cols = ((z >> np.uint64(32)) * np.uint64(d) >> np.uint64(32)).astype(np.int64)
+def random_spd(d: int, seed: int = 1, per_row: int = 5, shift: float = 1e-3,
+               device: str = "cpu") -> CSR:
+    """Paper §5.1 generator, reading G23: every row draws `per_row`
+    off-diagonal columns uniformly (splitmix64_at(seed, 1+t), multiply-shift) with
+    values U[-1,1] (second stream); each draw (i,j,v) also sets the transposed entry
+    (j,i) = v; coinciding draws are summed; self-draws are dropped; the diagonal is the
+    absolute off-diagonal row sum (numpy add.reduceat over the row) + `shift`, which
+    makes C strictly diagonally dominant, hence SPD.
+
+    The sort/dedupe runs in torch on `device` (a CUDA device makes d = 3e7 take
+    seconds); the arrays returned are numpy.
+    """
+    import torch
+    dev = torch.device(device)
+    n = d * per_row
+    ctr = 1 + np.arange(n, dtype=np.uint64)
+    cols = ((splitmix64_at(seed, ctr) >> np.uint64(32)) * np.uint64(d) >> np.uint64(32)).astype(np.int64)
     vals = -1.0 + 2.0 * _unit_double(splitmix64_at(np.uint64(seed) ^ np.uint64(0xA0761D6478BD642F), ctr))
-    keep = rows != cols
-    rows, cols, vals = rows[keep], cols[keep], vals[keep]
-    r = np.concatenate([rows, cols])
-    c = np.concatenate([cols, rows])
-    v = np.concatenate([vals, vals])
-    key = r * d + c
-    uk, inv = np.unique(key, return_inverse=True)
-    sv = np.zeros(uk.size)
-    np.add.at(sv, inv, v)
-    ur, uc = uk // d, uk % d
-    rowsum = np.zeros(d)
-    np.add.at(rowsum, ur, np.abs(sv))
-    r = np.concatenate([ur, np.arange(d)])
-    c = np.concatenate([uc, np.arange(d)])
-    v = np.concatenate([sv, rowsum + shift])
-    return from_coo(d, d, r, c, v)
+    del ctr
+    rows = torch.arange(d, dtype=torch.int64, device=dev).repeat_interleave(per_row)
+    cols_t = torch.from_numpy(cols).to(dev)
+    vals_t = torch.from_numpy(vals).to(dev)
+    del cols, vals
+    keep = rows != cols_t
+    rows, cols_t, vals_t = rows[keep], cols_t[keep], vals_t[keep]
+    # both orientations + a zero placeholder for every diagonal entry
+    diag = torch.arange(d, dtype=torch.int64, device=dev)
+    keys = torch.cat([rows * d + cols_t, cols_t * d + rows, diag * d + diag])
+    v = torch.cat([vals_t, vals_t, torch.zeros(d, dtype=torch.float64, device=dev)])
+    del rows, cols_t, vals_t
+    keys, order = torch.sort(keys, stable=True)
+    v = v[order]
+    del order
+    ukeys, inv = torch.unique_consecutive(keys, return_inverse=True)
+    del keys
+    sv = torch.zeros(ukeys.numel(), dtype=torch.float64, device=dev).index_add_(0, inv, v)
+    del inv, v
+    r = (ukeys // d).cpu().numpy()
+    c = (ukeys % d).cpu().numpy().astype(np.int32)
+    sv = sv.cpu().numpy()
+    del ukeys
+    counts = np.bincount(r, minlength=d)
+    rp = np.zeros(d + 1, dtype=np.int64)
+    np.cumsum(counts, out=rp[1:])
+    rowsum = np.add.reduceat(np.abs(sv), rp[:-1])  # sequential left-to-right per row
+    isdiag = c == r
+    sv[isdiag] = rowsum + shift
+    return CSR(d, d, rp, c, sv)
 
 
 def triangular_b(d: int, diag: float = 3.0, seed: int = 7, per_row: int = 3,
