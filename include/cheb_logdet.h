@@ -101,6 +101,17 @@ int cheb_moments(const cl_operator *op, double a, double b, int32_t degree,
                  int32_t probe_block, void *workspace, size_t ws_bytes,
                  double *mu_out, void *stream);
 
+/* Taylor baseline (Fig. 1(d)): power moments
+ *   mu_{p,j} = v_p^T A^j v_p,  A = I - M/s  (s > 0; s >= lambda_max(M) keeps spec(A) in [0,1)),
+ * by the power recurrence w_j = A w_{j-1} on the same fused SpMM kernels.  Arguments, layout,
+ * workspace and stream semantics as cheb_moments.  With c = cheb_taylor_coeffs(s, n)
+ * (c_0 = log s, c_k = -1/k: log det M = d log s + tr log(I - A), log(1-x) = -sum_k x^k/k),
+ * cheb_finalize gives the Taylor estimate of log det M. */
+int cheb_power_moments(const cl_operator *op, double s, int32_t degree, int64_t probe_begin,
+                       int64_t probe_end, uint64_t seed, int32_t probe_block, void *workspace,
+                       size_t ws_bytes, double *mu_out, void *stream);
+int cheb_taylor_coeffs(double s, int32_t degree, double *c_out);
+
 /* ASYNCHRONOUS device accumulation (reading G7):
  *   gamma_p[p] = sum_{j=0..n} c[j] mu[p*(n+1)+j] (ascending j),
  *   stats[0] = Gamma = (sum_p gamma_p, ascending p)/m,

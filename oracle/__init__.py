@@ -10,8 +10,10 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 """
 from .runner import (Op, build_oracle, lib, cheb_nodes, coeffs_from_values,
                      coeffs_log, cheb_eval, splitmix64, rademacher, apply_tilde,
-                     moments_vec, moments, logdet, bounds_btb, gamma_from_moments)
+                     moments_vec, moments, logdet, bounds_btb, gamma_from_moments,
+                     taylor_coeffs, power_moments_vec, taylor_logdet)
 
 __all__ = ["Op", "build_oracle", "lib", "cheb_nodes", "coeffs_from_values",
            "coeffs_log", "cheb_eval", "splitmix64", "rademacher", "apply_tilde",
-           "moments_vec", "moments", "logdet", "bounds_btb", "gamma_from_moments"]
+           "moments_vec", "moments", "logdet", "bounds_btb", "gamma_from_moments",
+           "taylor_coeffs", "power_moments_vec", "taylor_logdet"]

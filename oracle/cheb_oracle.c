@@ -339,3 +339,52 @@ int32_t orc_bounds_btb(const orc_csr *B, double *a_out, double *b_out)
     *b_out = norm1 * norminf;
     return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------- */
+/* Taylor baseline: "other polynomial approximations, e.g.  */
+/* Taylor, can also be used", the comparison of Fig. 1(d)       */
+/* (P:633-638).  log det M = d log s + tr log(I - A), A = I - M/s, with     */
+/* log(1 - x) = -sum_{k>=1} x^k / k truncated at k = n; the traces come     */
+/* from the power recurrence w_k = A w_{k-1} (reading G24: s = a + b).      */
+/* ---------------------------------------------------------------------- */
+int32_t orc_taylor_coeffs(double s, int32_t n, double *c)
+{
+    if (!(s > 0.0) || n < 0 || !c) return ORC_EINVAL;
+    c[0] = log(s);
+    for (int32_t k = 1; k <= n; k++) c[k] = -1.0 / (double)k;
+    return ORC_OK;
+}
+
+/* mu_k = v^T A^k v, k = 0..n, A = I - M/s. */
+int32_t orc_power_moments_vec(const orc_op *op, double s, int32_t n, const double *v, double *mu)
+{
+    if (!(s > 0.0) || n < 0) return ORC_EINVAL;
+    int64_t d = op_dim(op);
+    double *w = (double *)malloc(sizeof(double) * (size_t)d);
+    double *mx = (double *)malloc(sizeof(double) * (size_t)d);
+    double *tmp = (double *)malloc(sizeof(double) * (size_t)d);
+    if (!w || !mx || !tmp) { free(w); free(mx); free(tmp); return ORC_ENOMEM; }
+    for (int64_t i = 0; i < d; i++) w[i] = v[i];
+    mu[0] = dot(v, w, d);
+    for (int32_t k = 1; k <= n; k++) {
+        orc_apply_M(op, w, mx, tmp);
+        for (int64_t i = 0; i < d; i++) w[i] = w[i] - mx[i] / s;  /* w <- (I - M/s) w */
+        mu[k] = dot(v, w, d);
+    }
+    int32_t rc = ORC_OK;
+    for (int32_t k = 0; k <= n; k++)
+        if (!isfinite(mu[k])) rc = ORC_ENONFINITE;
+    free(w); free(mx); free(tmp);
+    return rc;
+}
+
+int32_t orc_power_moments_probe(const orc_op *op, double s, int32_t n, uint64_t seed, int64_t p, double *mu)
+{
+    int64_t d = op_dim(op);
+    double *v = (double *)malloc(sizeof(double) * (size_t)d);
+    if (!v) return ORC_ENOMEM;
+    orc_rademacher(seed, p, d, v);
+    int32_t rc = orc_power_moments_vec(op, s, n, v, mu);
+    free(v);
+    return rc;
+}

@@ -72,6 +72,12 @@ def lib():
         L.orc_gamma_probe.restype = D
         L.orc_bounds_btb.argtypes = [ctypes.POINTER(_CSR), P, P]
         L.orc_bounds_btb.restype = I32
+        L.orc_taylor_coeffs.argtypes = [D, I32, P]
+        L.orc_taylor_coeffs.restype = I32
+        L.orc_power_moments_vec.argtypes = [ctypes.POINTER(_OP), D, I32, P, P]
+        L.orc_power_moments_vec.restype = I32
+        L.orc_power_moments_probe.argtypes = [ctypes.POINTER(_OP), D, I32, U64, I64, P]
+        L.orc_power_moments_probe.restype = I32
         _lib = L
     return _lib
 
@@ -169,28 +175,50 @@ def moments_vec(op: Op, a: float, b: float, n: int, v: np.ndarray) -> np.ndarray
     return mu
 
 
+def taylor_coeffs(s: float, n: int) -> np.ndarray:
+    c = np.empty(n + 1)
+    if lib().orc_taylor_coeffs(s, n, _ptr(c)) != 0:
+        raise ValueError("orc_taylor_coeffs")
+    return c
+
+
+def power_moments_vec(op: Op, s: float, n: int, v: np.ndarray) -> np.ndarray:
+    """mu_k = v^T (I - M/s)^k v, k = 0..n (Taylor baseline)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    mu = np.empty(n + 1)
+    st = op._struct()
+    rc = lib().orc_power_moments_vec(ctypes.byref(st), s, n, _ptr(v), _ptr(mu))
+    if rc not in (0, -5):
+        raise RuntimeError(f"orc_power_moments_vec rc={rc}")
+    return mu
+
+
 # ---- probe-parallel pool (fork start method shares the CSR copy-on-write) ----
 _G = {}
 
 
 def _probe_task(p):
-    op, a, b, n, seed = _G["args"]
+    op, a, b, n, seed, power = _G["args"]
     mu = np.empty(n + 1)
     s = op._struct()
-    rc = lib().orc_moments_probe(ctypes.byref(s), a, b, n, seed, int(p), _ptr(mu))
+    if power:
+        rc = lib().orc_power_moments_probe(ctypes.byref(s), a, n, seed, int(p), _ptr(mu))
+    else:
+        rc = lib().orc_moments_probe(ctypes.byref(s), a, b, n, seed, int(p), _ptr(mu))
     if rc not in (0, -5):
-        raise RuntimeError(f"orc_moments_probe rc={rc}")
+        raise RuntimeError(f"oracle moments rc={rc}")
     return mu
 
 
 def moments(op: Op, a: float, b: float, n: int, seed: int, probes: Sequence[int],
-            workers: Optional[int] = None) -> np.ndarray:
-    """mu[len(probes)][n+1] for Rademacher probes with the given GLOBAL indices."""
+            workers: Optional[int] = None, power: bool = False) -> np.ndarray:
+    """mu[len(probes)][n+1] for Rademacher probes with the given GLOBAL indices.
+    power=True: Taylor-baseline power moments with scale s = a (b ignored)."""
     probes = [int(p) for p in probes]
     workers = workers or 1
     workers = max(1, min(workers, len(probes)))
     lib()
-    _G["args"] = (op, a, b, n, seed)
+    _G["args"] = (op, a, b, n, seed, power)
     if workers == 1:
         rows = [_probe_task(p) for p in probes]
     else:
@@ -228,6 +256,14 @@ def logdet(op: Op, a: float, b: float, n: int, m: int, seed: int,
     Returns dict(gamma, gamma_p, stderr, mu, c)."""
     c = coeffs_log(a, b, n)
     mu = moments(op, a, b, n, seed, range(probe_begin, probe_begin + m), workers)
+    gamma, gp, se = gamma_from_moments(c, mu)
+    return {"gamma": gamma, "gamma_p": gp, "stderr": se, "mu": mu, "c": c}
+
+
+def taylor_logdet(op: Op, s: float, n: int, m: int, seed: int, workers: Optional[int] = None):
+    """Taylor baseline over probes 0..m-1: dict(gamma, gamma_p, stderr, mu, c)."""
+    c = taylor_coeffs(s, n)
+    mu = moments(op, s, 0.0, n, seed, range(m), workers, power=True)
     gamma, gp, se = gamma_from_moments(c, mu)
     return {"gamma": gamma, "gamma_p": gp, "stderr": se, "mu": mu, "c": c}
 

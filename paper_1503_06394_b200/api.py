@@ -147,6 +147,39 @@ def moments(op: Operator, a: float, b: float, degree: int, probe_begin: int, pro
     return mu_out
 
 
+def power_moments(op: Operator, s: float, degree: int, probe_begin: int, probe_end: int, seed: int,
+                  k: int, mu_out: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Asynchronous Taylor-baseline moments mu[(p - probe_begin), j] = v_p^T (I - M/s)^j v_p."""
+    dev = op.A.val.device
+    if mu_out is None:
+        mu_out = torch.empty((probe_end - probe_begin, degree + 1), dtype=torch.float64, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(op, k)
+    st = op.struct()
+    check(_lib.load().cheb_power_moments(ctypes.byref(st), float(s), int(degree), int(probe_begin),
+                                         int(probe_end), int(seed) & (2 ** 64 - 1), int(k),
+                                         workspace.data_ptr(), workspace.numel(), mu_out.data_ptr(),
+                                         _stream_ptr(stream)))
+    return mu_out
+
+
+def taylor_coeffs(s: float, degree: int) -> np.ndarray:
+    c = np.empty(degree + 1)
+    check(_lib.load().cheb_taylor_coeffs(float(s), int(degree), c.ctypes.data))
+    return c
+
+
+def taylor_logdet(op: Operator, s: float, degree: int, num_probes: int, seed: int = 1, k: int = 16):
+    """Taylor-baseline estimate of log det M (scale s >= lambda_max): returns
+    (Gamma, stderr, mu[m][n+1]) -- all steps on the device."""
+    mu = power_moments(op, s, degree, 0, num_probes, seed, k)
+    c = torch.from_numpy(taylor_coeffs(s, degree)).to(mu.device)
+    gp, stats = finalize(mu, c)
+    st = stats.cpu().numpy()
+    return float(st[0]), float(st[1]), mu.cpu().numpy()
+
+
 def finalize(mu: torch.Tensor, c: torch.Tensor, stream=None):
     """Asynchronous device accumulation: returns (gamma_p[m], stats[3]) tensors;
     stats = (Gamma, stderr, all-finite flag)."""

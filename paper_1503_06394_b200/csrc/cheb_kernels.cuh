@@ -888,6 +888,7 @@ struct PersistArgs {
     unsigned int* bar_count;  // grid barrier arrivals (zeroed; monotone)
     unsigned int* s_count;    // rank-1: probes whose s_j is published (zeroed; monotone)
     unsigned int* err;        // wait timeout flag
+    int32_t power;            // power basis (Taylor baseline): every step is w_j = Ã w_{j-1}
 };
 
 __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned int want, unsigned int* err) {
@@ -924,7 +925,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
 
     // staging of tile t of step j into stage b (thread 0)
     auto issue = [&](int32_t j, int64_t t, int b) {
-        const bool first = (j == 1);
+        const bool first = (j == 1) || pa_.power;
         const double* wprev = (j & 1) ? pa_.w1 : pa_.w0;  // w_{j-2}
         unsigned char* st = smem + b * SL::BYTES;
         const int64_t r0 = t * G::TILE;
@@ -964,7 +965,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     __syncthreads();
 
     for (int32_t j = 1; j <= pa_.n; j++) {
-        const bool first = (j == 1);
+        const bool first = (j == 1) || pa_.power;
         const double* cur = (j & 1) ? pa_.w0 : pa_.w1;  // w_{j-1}
         double* nxt = (j & 1) ? pa_.w1 : pa_.w0;        // w_{j-2} -> w_j
         double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);

@@ -216,6 +216,7 @@ struct FusionPlan {
     bool persistent = false;  // all steps in one persistent cooperative launch
     int64_t H = 0, D = 0;
     int G = 0;                // fused grid (= the single-step grid, for bit-identical moments)
+    bool power = false;       // power basis (Taylor baseline): w_j = Ã w_{j-1}, every step "FIRST"
 };
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
@@ -281,6 +282,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         pp.bar_count = (unsigned int*)(ws + L.misc + 16);
         pp.s_count = (unsigned int*)(ws + L.misc + 20);
         pp.err = (unsigned int*)(ws + L.misc + 8);
+        pp.power = fp.power ? 1 : 0;
         CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
         void* args[] = {&a, &pp};
         ProfScope ps(st, 2);
@@ -325,7 +327,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.s_next = sbuf + (j & 1) * K;
         a.mu_col = j;
         ProfScope ps(st);
-        if (j == 1)
+        if (j == 1 || fp.power)  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
             cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem, st>>>(a);
         else
             cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem, st>>>(a);
@@ -503,12 +505,47 @@ size_t cheb_workspace_bytes(const cl_operator* op, int32_t probe_block) {
     return plan(op->A.n_cols, gather_nnz(op), probe_block, op->kind, sm_count()).total;
 }
 
+namespace {
+int moments_impl(const cl_operator* op, double alpha, double beta, bool power, int32_t degree,
+                 int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                 void* workspace, size_t ws_bytes, double* mu_out, void* stream);
+}
+
 int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
                  int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
                  void* workspace, size_t ws_bytes, double* mu_out, void* stream) {
     int rc;
     if ((rc = check_op(op))) return rc;
     if ((rc = check_ab(a, b, degree))) return rc;
+    return moments_impl(op, 2.0 / (b - a), (b + a) / (b - a), false, degree, probe_begin, probe_end, seed,
+                        probe_block, workspace, ws_bytes, mu_out, stream);
+}
+
+int cheb_power_moments(const cl_operator* op, double s, int32_t degree, int64_t probe_begin,
+                       int64_t probe_end, uint64_t seed, int32_t probe_block, void* workspace,
+                       size_t ws_bytes, double* mu_out, void* stream) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if (!std::isfinite(s) || !(s > 0.0)) return fail(CL_EINVAL, "need finite s > 0");
+    if (degree < 0) return fail(CL_EINVAL, "degree < 0");
+    // A = I - M/s = alpha*M - beta*I with alpha = -1/s, beta = -1
+    return moments_impl(op, -1.0 / s, -1.0, true, degree, probe_begin, probe_end, seed, probe_block,
+                        workspace, ws_bytes, mu_out, stream);
+}
+
+int cheb_taylor_coeffs(double s, int32_t degree, double* c_out) {
+    if (!std::isfinite(s) || !(s > 0.0)) return fail(CL_EINVAL, "need finite s > 0");
+    if (degree < 0 || !c_out) return fail(CL_EINVAL, "bad degree or NULL c_out");
+    c_out[0] = std::log(s);  // log det M = d log s + log det(M/s), log det(M/s) = tr log(I - A)
+    for (int32_t k = 1; k <= degree; k++) c_out[k] = -1.0 / (double)k;  // log(1-x) = -sum x^k/k
+    return CL_OK;
+}
+
+namespace {
+int moments_impl(const cl_operator* op, double alpha, double beta, bool power, int32_t degree,
+                 int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                 void* workspace, size_t ws_bytes, double* mu_out, void* stream) {
+    int rc;
     if (probe_begin < 0 || probe_end <= probe_begin)
         return fail(CL_EINVAL, "need 0 <= probe_begin < probe_end");
     if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32, 64 or 128");
@@ -520,13 +557,13 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
     if ((uintptr_t)workspace & 255) return fail(CL_EINVAL, "workspace must be 256-byte aligned");
     cudaStream_t st = (cudaStream_t)stream;
     char* ws = (char*)workspace;
-    const double alpha = 2.0 / (b - a), beta = (b + a) / (b - a);
     const int64_t stride = (int64_t)degree + 1;
     CL_CUDA(cudaGetLastError());
     CL_CUDA(cudaMemsetAsync(ws + L.ticket, 0, 256, st));
     CL_CUDA(cudaMemsetAsync(ws + L.misc, 0, 256, st));
     prep_mode(op, alpha, beta, ws, L, st, sms);
     FusionPlan fp;
+    fp.power = power;
     if (op->kind != CL_OP_BTB && g_persistent.load() > 0 && degree >= 1) {
         // L2-resident working set (two probe-block buffers + matrix): the per-step launch and
         // drain gaps dominate, so run all steps in one launch
@@ -537,7 +574,7 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
         fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
-    if (!fp.persistent && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
+    if (!fp.persistent && !power && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
         // needs the operator bandwidth computed by the prep kernel: one small D2H per call
         unsigned long long bw = 0;
         CL_CUDA(cudaMemcpyAsync(&bw, ws + L.misc, sizeof(bw), cudaMemcpyDeviceToHost, st));
@@ -577,6 +614,7 @@ int cheb_moments(const cl_operator* op, double a, double b, int32_t degree,
     CL_CUDA(cudaGetLastError());
     return CL_OK;
 }
+}  // namespace
 
 int cheb_finalize(const double* mu, const double* c, int64_t m, int32_t degree,
                   double* gamma_p, double* stats, void* stream) {

@@ -394,3 +394,48 @@ def test_btb_triangular_logabsdet(orc):
     c = orc.coeffs_log(a, b, n)
     half = 0.5 * orc.gamma_from_moments(c, mu[None, :])[0]
     assert abs(half - d * math.log(3)) <= 0.5 * d * cf.theorem3_bound(a / (a + b), n) + 1e-10 * d
+
+
+# ---------------------------------------------------------------- Taylor baseline
+def test_taylor_scalar_operator_closed_form(orc):
+    """M = sigma I: mu_k = d (1 - sigma/s)^k, and the estimate obeys the truncated-series
+    bound |Gamma/d - log sigma| <= x^(n+1) / ((n+1)(1-x)), x = 1 - sigma/s."""
+    d, sig, s, n = 30, 0.7, 2.0, 25
+    I = W.csr.from_coo(d, d, np.arange(d), np.arange(d), np.full(d, sig))
+    r = orc.taylor_logdet(orc.Op("csr", I), s, n, 3, 5)
+    x = 1 - sig / s
+    want = d * x ** np.arange(n + 1)
+    assert np.allclose(r["mu"], want, rtol=1e-13, atol=0)
+    assert abs(r["gamma"] / d - math.log(sig)) <= x ** (n + 1) / ((n + 1) * (1 - x)) + 1e-14
+    assert r["c"][0] == math.log(s) and r["c"][3] == -1.0 / 3
+
+
+def test_taylor_basis_probes_grid_closed_form(orc):
+    """Standard-basis probes: sum_i e_i^T A^k e_i = sum_lambda (1 - lambda/s)^k with
+    closed-form grid eigenvalues, every k (pins the power recurrence and the 1/s scaling)."""
+    N, theta, n = 12, 0.2, 20
+    s = 2.0  # = a + b for [0.2, 1.8]
+    op = orc.Op("csr", W.grid_gmrf(N, theta))
+    mu = np.zeros(n + 1)
+    e = np.zeros(op.d)
+    for i in range(op.d):
+        e[:] = 0
+        e[i] = 1
+        mu += orc.power_moments_vec(op, s, n, e)
+    lam = cf.grid_eigs(N, theta)
+    want = np.array([((1 - lam / s) ** k).sum() for k in range(n + 1)])
+    assert np.abs(mu - want).max() < 1e-12 * op.d
+
+
+def test_chebyshev_beats_taylor_exact_traces(orc):
+    """Fig. 1(d), noise-free form: with exact traces (basis probes) the
+    Chebyshev polynomial's log-det error is far below the Taylor series' at equal degree."""
+    N, theta, n = 16, 0.22, 20
+    a, b = 1 - 4 * theta, 1 + 4 * theta
+    A = W.grid_gmrf(N, theta)
+    exact = cf.grid_logdet(N, theta)
+    lt = (2 * cf.grid_eigs(N, theta) - (a + b)) / (b - a)
+    cheb = cf.cheb_poly_closed(orc.coeffs_log(a, b, n), lt).sum()
+    x = 1 - cf.grid_eigs(N, theta) / (a + b)
+    taylor = (N * N) * math.log(a + b) + sum(-(x ** k).sum() / k for k in range(1, n + 1))
+    assert abs(cheb - exact) < 0.01 * abs(taylor - exact)

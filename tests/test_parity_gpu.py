@@ -309,3 +309,39 @@ def test_full_config3_gmrf5000_bench_launch(orc):
 @pytest.mark.slow
 def test_full_config4_btb4m(orc):
     _full_size(orc, "btb4m", 64, [0, 63])
+
+
+# ------------------------------------------------------------------ Taylor baseline
+@pytest.mark.parametrize("name", ["gmrf_s", "torus_s", "btb_s", "spd_s"])
+@pytest.mark.parametrize("persist", [0, 2])
+def test_taylor_power_moments_parity(orc, persistent_mode, name, persist):
+    """Power-basis moments v^T (I - M/s)^j v through the same fused kernels vs the oracle."""
+    persistent_mode(persist)
+    wl = W.get_workload(name)
+    A, At = _mats(wl)
+    op = _dev_op(wl.mode, A, At, wl.r1_c)
+    a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+    s = a + b
+    n, m = 25, 11
+    mu = P.power_moments(op, s, n, 0, m, wl.seed, 16).cpu().numpy()
+    want = orc.moments(orc.Op(wl.mode, A, wl.r1_c), s, 0.0, n, wl.seed, range(m), workers=4, power=True)
+    _check_moments(mu, want, wl.d)
+    g, se, _ = P.taylor_logdet(op, s, n, m, wl.seed, 16)
+    og = orc.taylor_logdet(orc.Op(wl.mode, A, wl.r1_c), s, n, m, wl.seed, workers=4)
+    _check_gamma(g, og["gamma"])
+
+
+def test_chebyshev_beats_taylor_config2():
+    """Fig. 1(d) claim on the GPU path, matched (m, n, seed), BASELINE configs[2]:
+    the Chebyshev estimate is within 4 stderr of the exact log det and closer to it than
+    the Taylor estimate."""
+    from oracle import closed_forms as cf
+    wl = W.get_workload("gmrf1000")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    n, m = 30, 64
+    r = P.logdet(op, wl.a, wl.b, n, m, seed=wl.seed, k=64)
+    gt, _, _ = P.taylor_logdet(op, wl.a + wl.b, n, m, wl.seed, 64)
+    exact = cf.grid_logdet(1000, 0.24)
+    assert abs(r.logdet - exact) <= 4 * r.stderr
+    assert abs(r.logdet - exact) < abs(gt - exact)
