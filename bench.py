@@ -218,7 +218,7 @@ def run_ours(args):
     op = P.Operator(wl.mode, dA, dAt, wl.r1_c)
     a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
     group = None
-    sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, group=group)
+    sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, group=group, basis=args.basis)
 
     def barrier():
         if world > 1:
@@ -276,7 +276,7 @@ def run_ours(args):
     if p_ms > max(s_ms, f_ms):  # persistent multi-step kernel: one launch = all steps of a block
         kern = f"cheb_persist_kernel<{k},{wl.mode}>"
         bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode)
-                            + (wl.degree - 1) * step_bytes(d, gnnz, k, False, wl.mode))
+                            + (wl.degree - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode))
         avg_launch_ms, dom_ms = p_ms / max(p_n, 1), p_ms
     elif f_ms > s_ms:  # temporally fused pairs dominate
         kern = f"cheb_step2_kernel<{k}>"
@@ -286,8 +286,11 @@ def run_ours(args):
         kern = f"cheb_step_kernel<{k},{wl.mode}>"
         # per block and estimate: one FIRST launch, the rest full steps
         per_block = s_n / max(blocks * args.steps, 1)
-        tot = blocks * args.steps * (step_bytes(d, gnnz, k, True, wl.mode)
-                                     + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode))
+        if args.basis == "taylor":  # power recurrence: every launch reads w_{j-1}, writes w_j
+            tot = s_n * step_bytes(d, gnnz, k, True, wl.mode)
+        else:
+            tot = blocks * args.steps * (step_bytes(d, gnnz, k, True, wl.mode)
+                                         + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode))
         bytes_per_launch = tot / max(s_n, 1)
         avg_launch_ms, dom_ms = s_ms / max(s_n, 1), s_ms
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
@@ -310,7 +313,7 @@ def run_ours(args):
            "config": {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": d,
                       "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total,
                       "probes_per_gpu": m_per_gpu, "probe_block": k, "a": a, "b": b,
-                      "parallelism": f"probe-dp{world}", "l2": "inputs larger than L2 (W blocks "
+                      "basis": args.basis, "parallelism": f"probe-dp{world}", "l2": "inputs larger than L2 (W blocks "
                       f"{2 * d * k * 8 / 1e9:.1f} GB/GPU), no flush needed",
                       "logdet_wall_s": t_ms / args.steps / 1e3, "gamma": float(st[0]),
                       "stderr": float(st[1])},
@@ -396,6 +399,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="gmrf5000")
     ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--basis", choices=["chebyshev", "taylor"], default="chebyshev",
+                    help="taylor: the Fig. 1(d) power-series baseline on the same kernels")
     ap.add_argument("--probes", type=int, default=0, help="probes per GPU (default: the config's m)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of oracle work per sample")

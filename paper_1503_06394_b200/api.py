@@ -290,22 +290,33 @@ class Estimator:
     multi-GPU driver): workspace, coefficients and moment buffer stay resident."""
 
     def __init__(self, op: Operator, a: float, b: float, degree: int, num_probes: int,
-                 k: int, seed: int = 1, probe_begin: int = 0, probe_end: Optional[int] = None):
+                 k: int, seed: int = 1, probe_begin: int = 0, probe_end: Optional[int] = None,
+                 basis: str = "chebyshev"):
+        """basis "chebyshev" (the paper's estimator) or "taylor" (the Fig. 1(d) baseline,
+        scale s = a + b)."""
+        if basis not in ("chebyshev", "taylor"):
+            raise ValueError("basis must be 'chebyshev' or 'taylor'")
         self.op, self.a, self.b, self.degree, self.k, self.seed = op, a, b, degree, k, seed
+        self.basis = basis
         self.m = num_probes
         self.probe_begin = probe_begin
         self.probe_end = num_probes if probe_end is None else probe_end
         dev = op.A.val.device
         self.workspace = alloc_workspace(op, k)
-        self.c = torch.from_numpy(coeffs_log(a, b, degree)).to(dev)
+        c = coeffs_log(a, b, degree) if basis == "chebyshev" else taylor_coeffs(a + b, degree)
+        self.c = torch.from_numpy(c).to(dev)
         self.mu = torch.zeros((num_probes, degree + 1), dtype=torch.float64, device=dev)
 
     def enqueue_moments(self, stream=None):
         """Fill this shard's rows [probe_begin, probe_end) of mu (others untouched)."""
         if self.probe_end > self.probe_begin:
-            moments(self.op, self.a, self.b, self.degree, self.probe_begin, self.probe_end, self.seed,
-                    self.k, mu_out=self.mu[self.probe_begin:self.probe_end], workspace=self.workspace,
-                    stream=stream)
+            rows = self.mu[self.probe_begin:self.probe_end]
+            if self.basis == "chebyshev":
+                moments(self.op, self.a, self.b, self.degree, self.probe_begin, self.probe_end, self.seed,
+                        self.k, mu_out=rows, workspace=self.workspace, stream=stream)
+            else:
+                power_moments(self.op, self.a + self.b, self.degree, self.probe_begin, self.probe_end,
+                              self.seed, self.k, mu_out=rows, workspace=self.workspace, stream=stream)
         return self.mu
 
     def enqueue_finalize(self, stream=None):

@@ -223,7 +223,7 @@ struct FusionPlan {
 template <int K, int MODE>
 int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-              int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp = FusionPlan()) {
+              int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE>;
     const int64_t d = op->A.n_cols;
@@ -346,7 +346,7 @@ int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, 
         case CL_OP_CSR_RANK1:
             return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         default:
-            return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms);
+            return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
     }
 }
 
@@ -781,11 +781,11 @@ int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_blo
     CL_CUDA(cudaMemsetAsync((char*)ws.p + L.ticket, 0, 256, st));
     int rc;
     switch (probe_block) {
-        case 8: rc = run_block<8, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 8, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
-        case 16: rc = run_block<16, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 16, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
-        case 32: rc = run_block<32, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 32, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
-        case 64: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
-        default: rc = run_block<128, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 128, (char*)ws.p, L, (double*)mu.p, 1, st, sms); break;
+        case 8: rc = run_block<8, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 8, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
+        case 16: rc = run_block<16, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 16, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
+        case 32: rc = run_block<32, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 32, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
+        case 64: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
+        default: rc = run_block<128, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 128, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
     }
     if (rc) return rc;
     CL_CUDA(cudaMemcpyAsync(v_out, (char*)ws.p + L.w0, sizeof(double) * d * probe_block,

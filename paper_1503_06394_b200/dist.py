@@ -48,13 +48,13 @@ class ShardedEstimator:
     """Estimator over this rank's probe shard; `run()` enqueues moments, the
     all-reduce and the device finalisation on the current stream."""
 
-    def __init__(self, op, a, b, degree, num_probes, k, seed=1, group=None):
+    def __init__(self, op, a, b, degree, num_probes, k, seed=1, group=None, basis="chebyshev"):
         from .api import Estimator
         self.group = group
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.begin, self.end = shard_range(num_probes, world, rank)
-        self.est = Estimator(op, a, b, degree, num_probes, k, seed, self.begin, self.end)
+        self.est = Estimator(op, a, b, degree, num_probes, k, seed, self.begin, self.end, basis=basis)
 
     def run(self):
         self.est.mu.zero_()
