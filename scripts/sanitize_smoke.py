@@ -1,0 +1,42 @@
+"""Tiny invocation of every kernel variant, for compute-sanitizer (one tool per run)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+import paper_1503_06394_b200 as P  # noqa: E402
+
+
+def dev(A):
+    return P.DeviceCSR.from_host(A)
+
+
+def main():
+    G = W.grid_gmrf(23, 0.2)
+    T = W.torus_laplacian(11)
+    B = W.random_nonsingular(777, 2)
+    op_g = P.Operator("csr", dev(G))
+    op_t = P.Operator("rank1", dev(T), None, 0.01, torch.from_numpy(np.linspace(0.5, 1.5, T.n_rows)).cuda())
+    op_b = P.Operator("btb", dev(B), dev(W.transpose(B)))
+    a, b = P.bounds_btb(op_b)
+    P.probes(1000, 3, 5, 16)
+    for persist in (0, 2):
+        P.set_persistent(persist)
+        for k in (8, 64):
+            P.logdet(op_g, 0.2, 1.8, 7, 11, seed=1, k=k)
+            P.logdet(op_t, 0.01, 8.5, 7, 11, seed=1, k=k)
+            P.taylor_logdet(op_g, 2.0, 5, 9, 1, k)
+    P.set_persistent(1)
+    P.logdet(op_b, a, b, 5, 9, seed=1, k=16)
+    P.set_fusion(3)
+    P.moments(op_g, 0.2, 1.8, 6, 0, 9, 1, 16)
+    P.set_fusion(1)
+    torch.cuda.synchronize()
+    print("sanitize smoke ok")
+
+
+if __name__ == "__main__":
+    main()
