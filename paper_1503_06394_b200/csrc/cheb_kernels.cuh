@@ -23,8 +23,21 @@
 // (cp.async.bulk, mbarrier completion) of the NEXT tile's row_ptr slice, col/val range,
 // W_prev rows and sign words while all warps gather W_cur rows for the current tile.
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+// CHEB_CHECKS=1 builds (scripts/build_variants.py "checked") turn on device-side bounds
+// asserts: compute-sanitizer is not available on the B200 pool, so out-of-range gathers,
+// staging overflows and bad tile geometry trap here instead.
+#ifndef CHEB_CHECKS
+#define CHEB_CHECKS 0
+#endif
+#if CHEB_CHECKS
+#define CHEB_ASSERT(x) assert(x)
+#else
+#define CHEB_ASSERT(x) ((void)0)
+#endif
 
 namespace chebld {
 
@@ -476,6 +489,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         if (lr >= rows) break;
         const int64_t i = r0 + lr;
         const int64_t e_lo = rp_s[lr], e_hi = rp_s[lr + 1];
+        CHEB_ASSERT(rows <= G::TILE && i < a.d && e_lo <= e_hi);
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
         // all nnz of a chunk issue their gathers before any is consumed (predicated tail)
         for (int64_t e0 = e_lo; e0 < e_hi; e0 += CHEB_NNZ_UNROLL) {
@@ -485,7 +499,10 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
                 const bool in = e0 + q < e_hi;
                 const int64_t e = in ? e0 + q : e_lo;
+                CHEB_ASSERT(!STAGED || (e - base_c >= 0 && e - base_c < G::CAP + 8));
+                CHEB_ASSERT(!STAGED || (e - base_v >= 0 && e - base_v < G::CAP + 4));
                 c[q] = STAGED ? col_s[e - base_c] : __ldg(a.ci + e);
+                CHEB_ASSERT(!in || (c[q] >= 0 && (int64_t)c[q] < a.d));
                 v[q] = in ? (STAGED ? val_s[e - base_v] : __ldg(a.va + e)) : 0.0;
             }
             double2 x0[CHEB_NNZ_UNROLL], x1[CHEB_NNZ_UNROLL];

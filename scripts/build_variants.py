@@ -7,6 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1503_06394_b200 import _build  # noqa: E402
 
 VARIANTS = {
+    "checked": ["CHEB_CHECKS=1"],
     "f_s1": ["CHEB_FUSED_SLACK=1"],
     "f_s2": ["CHEB_FUSED_SLACK=2"],
     "f_s1h": ["CHEB_FUSED_SLACK=1", "CHEB_FUSED_HINTS=1"],
