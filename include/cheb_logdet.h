@@ -112,6 +112,20 @@ int cheb_power_moments(const cl_operator *op, double s, int32_t degree, int64_t 
                        size_t ws_bytes, double *mu_out, void *stream);
 int cheb_taylor_coeffs(double s, int32_t degree, double *c_out);
 
+/* Device-side spectral bounds ("one can run the power iteration to estimate a
+ * better bound"):
+ *   cheb_affine_power_moments: mu_{p,j} = v_p^T (alpha M - beta I)^j v_p (power recurrence on
+ *     the fused kernels; cheb_power_moments is alpha = -1/s, beta = -1).  Block power
+ *     iteration: mu_{j+1}/mu_j -> the dominant eigenvalue of alpha M - beta I.
+ *   cheb_norm_bound: s >= lambda_max(M) from the matrix, on the device: Gershgorin
+ *     max_i sum_j |a_ij| (+ |c| max|u|^2 d for rank-1) or ||B||_1 ||B||_inf for B^T B
+ *     (P:301-302).  s_out is a HOST double; synchronous on `stream`.
+ * Python's spectrum_estimate() combines them into (lambda_min, lambda_max) estimates. */
+int cheb_affine_power_moments(const cl_operator *op, double alpha, double beta, int32_t degree,
+                              int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                              void *workspace, size_t ws_bytes, double *mu_out, void *stream);
+int cheb_norm_bound(const cl_operator *op, double *s_out, void *stream);
+
 /* ASYNCHRONOUS device accumulation (reading G7):
  *   gamma_p[p] = sum_{j=0..n} c[j] mu[p*(n+1)+j] (ascending j),
  *   stats[0] = Gamma = (sum_p gamma_p, ascending p)/m,

@@ -11,9 +11,11 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 from .runner import (Op, build_oracle, lib, cheb_nodes, coeffs_from_values,
                      coeffs_log, cheb_eval, splitmix64, rademacher, apply_tilde,
                      moments_vec, moments, logdet, bounds_btb, gamma_from_moments,
-                     taylor_coeffs, power_moments_vec, taylor_logdet)
+                     taylor_coeffs, power_moments_vec, taylor_logdet, affine_power_moments,
+                     affine_power_moments_vec, gershgorin)
 
 __all__ = ["Op", "build_oracle", "lib", "cheb_nodes", "coeffs_from_values",
            "coeffs_log", "cheb_eval", "splitmix64", "rademacher", "apply_tilde",
            "moments_vec", "moments", "logdet", "bounds_btb", "gamma_from_moments",
-           "taylor_coeffs", "power_moments_vec", "taylor_logdet"]
+           "taylor_coeffs", "power_moments_vec", "taylor_logdet", "affine_power_moments",
+           "affine_power_moments_vec", "gershgorin"]

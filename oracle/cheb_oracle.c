@@ -388,3 +388,52 @@ int32_t orc_power_moments_probe(const orc_op *op, double s, int32_t n, uint64_t 
     free(v);
     return rc;
 }
+
+/* ---------------------------------------------------------------------- */
+/* Spectral bounds by power iteration ("one can  */
+/* run the power iteration to estimate a better bound").                   */
+/*   mu_j = v^T (alpha M - beta I)^j v  (unnormalised block power moments)  */
+/*   Gershgorin: lambda_max(M) <= max_i sum_j |m_ij| for csr.               */
+/* ---------------------------------------------------------------------- */
+int32_t orc_affine_power_moments_vec(const orc_op *op, double alpha, double beta, int32_t n,
+                                     const double *v, double *mu)
+{
+    if (n < 0) return ORC_EINVAL;
+    int64_t d = op_dim(op);
+    double *w = (double *)malloc(sizeof(double) * (size_t)d);
+    double *mx = (double *)malloc(sizeof(double) * (size_t)d);
+    double *tmp = (double *)malloc(sizeof(double) * (size_t)d);
+    if (!w || !mx || !tmp) { free(w); free(mx); free(tmp); return ORC_ENOMEM; }
+    for (int64_t i = 0; i < d; i++) w[i] = v[i];
+    mu[0] = dot(v, w, d);
+    for (int32_t j = 1; j <= n; j++) {
+        orc_apply_M(op, w, mx, tmp);
+        for (int64_t i = 0; i < d; i++) w[i] = alpha * mx[i] - beta * w[i];
+        mu[j] = dot(v, w, d);
+    }
+    free(w); free(mx); free(tmp);
+    return ORC_OK;
+}
+
+int32_t orc_affine_power_moments_probe(const orc_op *op, double alpha, double beta, int32_t n,
+                                       uint64_t seed, int64_t p, double *mu)
+{
+    int64_t d = op_dim(op);
+    double *v = (double *)malloc(sizeof(double) * (size_t)d);
+    if (!v) return ORC_ENOMEM;
+    orc_rademacher(seed, p, d, v);
+    int32_t rc = orc_affine_power_moments_vec(op, alpha, beta, n, v, mu);
+    free(v);
+    return rc;
+}
+
+double orc_gershgorin(const orc_csr *A)
+{
+    double best = 0.0;
+    for (int64_t i = 0; i < A->n_rows; i++) {
+        double s = 0.0;
+        for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; e++) s += fabs(A->val[e]);
+        if (s > best) best = s;
+    }
+    return best;
+}

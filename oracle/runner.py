@@ -78,6 +78,12 @@ def lib():
         L.orc_power_moments_vec.restype = I32
         L.orc_power_moments_probe.argtypes = [ctypes.POINTER(_OP), D, I32, U64, I64, P]
         L.orc_power_moments_probe.restype = I32
+        L.orc_affine_power_moments_vec.argtypes = [ctypes.POINTER(_OP), D, D, I32, P, P]
+        L.orc_affine_power_moments_vec.restype = I32
+        L.orc_affine_power_moments_probe.argtypes = [ctypes.POINTER(_OP), D, D, I32, U64, I64, P]
+        L.orc_affine_power_moments_probe.restype = I32
+        L.orc_gershgorin.argtypes = [ctypes.POINTER(_CSR)]
+        L.orc_gershgorin.restype = D
         _lib = L
     return _lib
 
@@ -258,6 +264,37 @@ def logdet(op: Op, a: float, b: float, n: int, m: int, seed: int,
     mu = moments(op, a, b, n, seed, range(probe_begin, probe_begin + m), workers)
     gamma, gp, se = gamma_from_moments(c, mu)
     return {"gamma": gamma, "gamma_p": gp, "stderr": se, "mu": mu, "c": c}
+
+
+def affine_power_moments(op: Op, alpha: float, beta: float, n: int, seed: int,
+                         probes: Sequence[int]) -> np.ndarray:
+    """mu[p][j] = v_p^T (alpha M - beta I)^j v_p for Rademacher probes (block power iteration)."""
+    out = []
+    st = op._struct()
+    for p in probes:
+        mu = np.empty(n + 1)
+        rc = lib().orc_affine_power_moments_probe(ctypes.byref(st), alpha, beta, n, seed, int(p), _ptr(mu))
+        if rc != 0:
+            raise RuntimeError(f"orc_affine_power_moments_probe rc={rc}")
+        out.append(mu)
+    return np.array(out)
+
+
+def affine_power_moments_vec(op: Op, alpha: float, beta: float, n: int, v: np.ndarray) -> np.ndarray:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    mu = np.empty(n + 1)
+    st = op._struct()
+    if lib().orc_affine_power_moments_vec(ctypes.byref(st), alpha, beta, n, _ptr(v), _ptr(mu)) != 0:
+        raise RuntimeError("orc_affine_power_moments_vec")
+    return mu
+
+
+def gershgorin(A) -> float:
+    rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.col_idx, dtype=np.int32)
+    va = np.ascontiguousarray(A.val, dtype=np.float64)
+    cs = _CSR(A.n_rows, A.n_cols, _ptr(rp), _ptr(ci), _ptr(va))
+    return float(lib().orc_gershgorin(ctypes.byref(cs)))
 
 
 def taylor_logdet(op: Op, s: float, n: int, m: int, seed: int, workers: Optional[int] = None):

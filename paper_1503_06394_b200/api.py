@@ -164,6 +164,44 @@ def power_moments(op: Operator, s: float, degree: int, probe_begin: int, probe_e
     return mu_out
 
 
+def affine_power_moments(op: Operator, alpha: float, beta: float, degree: int, probe_begin: int,
+                         probe_end: int, seed: int, k: int, workspace: Optional[torch.Tensor] = None,
+                         stream=None) -> torch.Tensor:
+    """mu[(p - probe_begin), j] = v_p^T (alpha M - beta I)^j v_p on the device."""
+    dev = op.A.val.device
+    mu_out = torch.empty((probe_end - probe_begin, degree + 1), dtype=torch.float64, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(op, k)
+    st = op.struct()
+    check(_lib.load().cheb_affine_power_moments(ctypes.byref(st), float(alpha), float(beta), int(degree),
+                                                int(probe_begin), int(probe_end), int(seed) & (2 ** 64 - 1),
+                                                int(k), workspace.data_ptr(), workspace.numel(),
+                                                mu_out.data_ptr(), _stream_ptr(stream)))
+    return mu_out
+
+
+def norm_bound(op: Operator, stream=None) -> float:
+    """Device upper bound s >= lambda_max(M) (Gershgorin / ||B||_1 ||B||_inf)."""
+    s = ctypes.c_double()
+    st = op.struct()
+    check(_lib.load().cheb_norm_bound(ctypes.byref(st), ctypes.byref(s), _stream_ptr(stream)))
+    return s.value
+
+
+def spectrum_estimate(op: Operator, iters: int = 60, probes: int = 8, seed: int = 12345, k: int = 8):
+    """Block power iteration on the fused kernels: with s = norm_bound,
+    lambda_max ~ s * R(M/s) and lambda_min ~ s * (1 - R(I - M/s)), where R is the ratio of
+    the probe-summed last two power moments.  These are INNER estimates (lambda_max from
+    below, lambda_min from above); widen them before using them as [a, b]."""
+    s = norm_bound(op)
+    hi = affine_power_moments(op, 1.0 / s, 0.0, iters, 0, probes, seed, k).sum(dim=0).cpu().numpy()
+    lo = affine_power_moments(op, -1.0 / s, -1.0, iters, 0, probes, seed, k).sum(dim=0).cpu().numpy()
+    lam_max = s * hi[-1] / hi[-2]
+    lam_min = s * (1.0 - lo[-1] / lo[-2])
+    return {"lambda_min": float(lam_min), "lambda_max": float(lam_max), "norm_bound": s,
+            "iters": iters, "probes": probes}
+
+
 def taylor_coeffs(s: float, degree: int) -> np.ndarray:
     c = np.empty(degree + 1)
     check(_lib.load().cheb_taylor_coeffs(float(s), int(degree), c.ctypes.data))

@@ -1185,6 +1185,30 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Gershgorin-type upper bound on lambda_max of a CSR operator: out[0] <- max_i sum_j |a_ij|,
+// out[1] <- max_i |u_i| (rank-1 u, if given).  Ordered-key atomics (order-independent).
+__global__ void __launch_bounds__(kThreads)
+gershgorin_kernel(int64_t d, const int64_t* __restrict__ rp, const double* __restrict__ va,
+                  const double* __restrict__ u, unsigned long long* out) {
+    double rmax = 0.0, umax = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double r = 0.0;
+        for (int64_t e = rp[i]; e < rp[i + 1]; e++) r += fabs(va[e]);
+        rmax = fmax(rmax, r);
+        if (u) umax = fmax(umax, fabs(u[i]));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
+        umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out + 0, order_key(rmax));
+        atomicMax(out + 1, order_key(umax));
+    }
+}
+
 __global__ void __launch_bounds__(kThreads)
 bounds_btb_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                   const double* __restrict__ va, const int64_t* __restrict__ trp,

@@ -88,6 +88,11 @@ int sm_count() {
 }
 
 constexpr int kMaxCtasPerSm = 8;  // partial buffers are sized for this
+
+struct DevBuf {  // owning device allocation (freed on scope exit)
+    void* p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+};
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64 || k == 128; }
@@ -533,6 +538,74 @@ int cheb_power_moments(const cl_operator* op, double s, int32_t degree, int64_t 
                         workspace, ws_bytes, mu_out, stream);
 }
 
+int cheb_affine_power_moments(const cl_operator* op, double alpha, double beta, int32_t degree,
+                              int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                              void* workspace, size_t ws_bytes, double* mu_out, void* stream) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if (!std::isfinite(alpha) || !std::isfinite(beta)) return fail(CL_EINVAL, "alpha/beta not finite");
+    if (degree < 0) return fail(CL_EINVAL, "degree < 0");
+    return moments_impl(op, alpha, beta, true, degree, probe_begin, probe_end, seed, probe_block, workspace,
+                        ws_bytes, mu_out, stream);
+}
+
+namespace {
+double unkey(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double x;
+    memcpy(&x, &b, sizeof(x));
+    return x;
+}
+}  // namespace
+
+int cheb_norm_bound(const cl_operator* op, double* s_out, void* stream) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if (!s_out) return fail(CL_EINVAL, "s_out is NULL");
+    if (op->kind == CL_OP_BTB) {
+        double ab[2];
+        // ||B||_1 ||B||_inf bounds sigma_max(B)^2; Johnson's bound is not needed here
+        cudaStream_t st = (cudaStream_t)stream;
+        DevBuf buf;
+        CL_CUDA(cudaMalloc(&buf.p, 3 * sizeof(unsigned long long)));
+        unsigned long long init[3] = {~0ull, 0ull, 0ull};
+        CL_CUDA(cudaMemcpyAsync(buf.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        const int64_t d = op->A.n_rows;
+        int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+        bounds_btb_kernel<<<grid, kThreads, 0, st>>>(d, op->A.row_ptr, op->A.col_idx, op->A.val,
+                                                      op->At.row_ptr, op->At.col_idx, op->At.val,
+                                                      (unsigned long long*)buf.p);
+        g_launches++;
+        CL_CUDA(cudaGetLastError());
+        unsigned long long h[3];
+        CL_CUDA(cudaMemcpyAsync(h, buf.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CL_CUDA(cudaStreamSynchronize(st));
+        ab[1] = unkey(h[1]) * unkey(h[2]);
+        *s_out = ab[1];
+        return CL_OK;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf buf;
+    CL_CUDA(cudaMalloc(&buf.p, 2 * sizeof(unsigned long long)));
+    CL_CUDA(cudaMemsetAsync(buf.p, 0, 2 * sizeof(unsigned long long), st));
+    const int64_t d = op->A.n_rows;
+    int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    const double* u = op->kind == CL_OP_CSR_RANK1 ? op->r1_u : nullptr;
+    gershgorin_kernel<<<grid, kThreads, 0, st>>>(d, op->A.row_ptr, op->A.val, u, (unsigned long long*)buf.p);
+    g_launches++;
+    CL_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    CL_CUDA(cudaMemcpyAsync(h, buf.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    double s = unkey(h[0]);
+    if (op->kind == CL_OP_CSR_RANK1) {
+        const double umax = op->r1_u ? unkey(h[1]) : 1.0;
+        s += std::fabs(op->r1_c) * umax * umax * (double)d;  // |c| |u_i| sum_j |u_j| <= |c| umax^2 d
+    }
+    *s_out = s;
+    return CL_OK;
+}
+
 int cheb_taylor_coeffs(double s, int32_t degree, double* c_out) {
     if (!std::isfinite(s) || !(s > 0.0)) return fail(CL_EINVAL, "need finite s > 0");
     if (degree < 0 || !c_out) return fail(CL_EINVAL, "bad degree or NULL c_out");
@@ -628,10 +701,6 @@ int cheb_finalize(const double* mu, const double* c, int64_t m, int32_t degree,
 
 namespace {
 
-struct DevBuf {
-    void* p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
-};
 
 int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
                   uint64_t seed, int32_t probe_block, cl_result* out, cudaStream_t st) {

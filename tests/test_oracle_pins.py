@@ -439,3 +439,31 @@ def test_chebyshev_beats_taylor_exact_traces(orc):
     x = 1 - cf.grid_eigs(N, theta) / (a + b)
     taylor = (N * N) * math.log(a + b) + sum(-(x ** k).sum() / k for k in range(1, n + 1))
     assert abs(cheb - exact) < 0.01 * abs(taylor - exact)
+
+
+# ---------------------------------------------------------------- power iteration
+def test_affine_power_moments_diagonal_closed_form(orc):
+    """M = diag(lam): v^T (alpha M - beta I)^j v = sum_i (alpha lam_i - beta)^j exactly (v_i^2 = 1)."""
+    lam = np.linspace(0.3, 2.9, 41)
+    d = lam.size
+    M = W.csr.from_coo(d, d, np.arange(d), np.arange(d), lam)
+    alpha, beta, n = 0.31, -0.2, 12
+    v = orc.rademacher(4, 1, d)
+    mu = orc.affine_power_moments_vec(orc.Op("csr", M), alpha, beta, n, v)
+    want = np.array([((alpha * lam - beta) ** j).sum() for j in range(n + 1)])
+    assert np.allclose(mu, want, rtol=1e-13)
+
+
+def test_power_iteration_grid_extremes_and_gershgorin(orc):
+    """Block power iteration recovers the closed-form extreme eigenvalues of the grid
+    precision, and the Gershgorin bound equals 1 + 4 theta (interior rows)."""
+    N, theta = 14, 0.21
+    A = W.grid_gmrf(N, theta)
+    s = orc.gershgorin(A)
+    assert abs(s - (1 + 4 * theta)) < 1e-15
+    op = orc.Op("csr", A)
+    hi = orc.affine_power_moments(op, 1 / s, 0.0, 400, 7, range(6)).sum(axis=0)
+    lo = orc.affine_power_moments(op, -1 / s, -1.0, 400, 7, range(6)).sum(axis=0)
+    lam = cf.grid_eigs(N, theta)
+    assert abs(s * hi[-1] / hi[-2] - lam.max()) < 2e-3
+    assert abs(s * (1 - lo[-1] / lo[-2]) - lam.min()) < 2e-3

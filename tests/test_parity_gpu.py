@@ -345,3 +345,36 @@ def test_chebyshev_beats_taylor_config2():
     exact = cf.grid_logdet(1000, 0.24)
     assert abs(r.logdet - exact) <= 4 * r.stderr
     assert abs(r.logdet - exact) < abs(gt - exact)
+
+
+# ------------------------------------------------------------------ spectral bounds
+@pytest.mark.parametrize("name", ["gmrf_s", "torus_s", "btb_s"])
+def test_affine_power_moments_parity(orc, name):
+    wl = W.get_workload(name)
+    A, At = _mats(wl)
+    op = _dev_op(wl.mode, A, At, wl.r1_c)
+    s = P.norm_bound(op)
+    for alpha, beta in ((1.0 / s, 0.0), (-1.0 / s, -1.0)):
+        mu = P.affine_power_moments(op, alpha, beta, 30, 0, 9, 5, 16).cpu().numpy()
+        want = orc.affine_power_moments(orc.Op(wl.mode, A, wl.r1_c), alpha, beta, 30, 5, range(9))
+        assert np.all(np.abs(mu - want) <= 1e-11 * np.maximum(np.abs(want), wl.d))
+
+
+def test_norm_bounds_match_oracle(orc):
+    G = W.grid_gmrf(40, 0.23)
+    assert P.norm_bound(_dev_op("csr", G)) == orc.gershgorin(G)
+    B = W.random_nonsingular(3000, 4)
+    ob = orc.bounds_btb(B)[1]
+    assert abs(P.norm_bound(_dev_op("btb", B, W.transpose(B))) - ob) <= 1e-13 * ob
+
+
+def test_spectrum_estimate_grid_closed_form():
+    """Device power iteration recovers the grid's closed-form extreme eigenvalues."""
+    from oracle import closed_forms as cf
+    N, theta = 20, 0.2
+    op = _dev_op("csr", W.grid_gmrf(N, theta))
+    est = P.spectrum_estimate(op, iters=500, probes=8)
+    lam = cf.grid_eigs(N, theta)
+    assert lam.max() - 2e-3 < est["lambda_max"] <= lam.max() + 1e-9
+    assert lam.min() - 1e-9 <= est["lambda_min"] < lam.min() + 2e-3
+    assert est["norm_bound"] >= lam.max()
