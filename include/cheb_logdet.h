@@ -126,6 +126,17 @@ int cheb_affine_power_moments(const cl_operator *op, double alpha, double beta, 
                               void *workspace, size_t ws_bytes, double *mu_out, void *stream);
 int cheb_norm_bound(const cl_operator *op, double *s_out, void *stream);
 
+/* x^T A x for a DEVICE CSR A (square) and DEVICE vector x[d]; result to the HOST double
+ * *out; deterministic (fixed reduction order); synchronous on `stream`.  The GMRF
+ * log-likelihood scan (§5.2) is
+ *   log p(x | rho) = 1/2 log det J(rho) - 1/2 x^T J(rho) x - d/2 log(2 pi). */
+int cheb_quadform(const cl_csr *A, const double *x, double *out, void *stream);
+
+/* Gershgorin interval of a DEVICE CSR: lo_hi[0] = min_i (a_ii - sum_{j!=i} |a_ij|),
+ * lo_hi[1] = max_i sum_j |a_ij| (HOST array[2]); for a symmetric A it encloses spec(A)
+ * (the GMRF configs' [1-4theta, 1+4theta]).  Synchronous on `stream`. */
+int cheb_gershgorin(const cl_csr *A, double *lo_hi, void *stream);
+
 /* ASYNCHRONOUS device accumulation (reading G7):
  *   gamma_p[p] = sum_{j=0..n} c[j] mu[p*(n+1)+j] (ascending j),
  *   stats[0] = Gamma = (sum_p gamma_p, ascending p)/m,

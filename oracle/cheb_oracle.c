@@ -437,3 +437,15 @@ double orc_gershgorin(const orc_csr *A)
     }
     return best;
 }
+
+/* x^T A x (compensated), for the GMRF log-likelihood scan:
+ *   log p(x | rho) = 1/2 log det J(rho) - 1/2 x^T J(rho) x - d/2 log(2 pi)  (reading G16). */
+double orc_quadform(const orc_csr *A, const double *x)
+{
+    double *ax = (double *)malloc(sizeof(double) * (size_t)A->n_rows);
+    if (!ax) return NAN;
+    csr_mv(A, x, ax);
+    double r = dot(x, ax, A->n_rows);
+    free(ax);
+    return r;
+}

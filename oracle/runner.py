@@ -84,6 +84,8 @@ def lib():
         L.orc_affine_power_moments_probe.restype = I32
         L.orc_gershgorin.argtypes = [ctypes.POINTER(_CSR)]
         L.orc_gershgorin.restype = D
+        L.orc_quadform.argtypes = [ctypes.POINTER(_CSR), P]
+        L.orc_quadform.restype = D
         _lib = L
     return _lib
 
@@ -295,6 +297,16 @@ def gershgorin(A) -> float:
     va = np.ascontiguousarray(A.val, dtype=np.float64)
     cs = _CSR(A.n_rows, A.n_cols, _ptr(rp), _ptr(ci), _ptr(va))
     return float(lib().orc_gershgorin(ctypes.byref(cs)))
+
+
+def quadform(A, x: np.ndarray) -> float:
+    """x^T A x (compensated)."""
+    rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.col_idx, dtype=np.int32)
+    va = np.ascontiguousarray(A.val, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    cs = _CSR(A.n_rows, A.n_cols, _ptr(rp), _ptr(ci), _ptr(va))
+    return float(lib().orc_quadform(ctypes.byref(cs), _ptr(x)))
 
 
 def taylor_logdet(op: Op, s: float, n: int, m: int, seed: int, workers: Optional[int] = None):

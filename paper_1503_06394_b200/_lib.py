@@ -67,6 +67,8 @@ def load():
         "cheb_taylor_coeffs": (I, [D, I32, P]),
         "cheb_affine_power_moments": (I, [OPP, D, D, I32, I64, I64, U64, I32, P, SZ, P, P]),
         "cheb_norm_bound": (I, [OPP, P, P]),
+        "cheb_quadform": (I, [ctypes.POINTER(CLCsr), P, P, P]),
+        "cheb_gershgorin": (I, [ctypes.POINTER(CLCsr), P, P]),
         "cheb_logdet": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_logdet_host": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_bounds_btb": (I, [OPP, P, P]),

@@ -1185,27 +1185,67 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// Gershgorin-type upper bound on lambda_max of a CSR operator: out[0] <- max_i sum_j |a_ij|,
-// out[1] <- max_i |u_i| (rank-1 u, if given).  Ordered-key atomics (order-independent).
+// Quadratic form x^T A x for the GMRF likelihood scan: per-CTA partials
+// (grid-stride rows, warp xor-butterfly, warps in order) then quadform_final_kernel sums
+// the partials in CTA order -- deterministic.
 __global__ void __launch_bounds__(kThreads)
-gershgorin_kernel(int64_t d, const int64_t* __restrict__ rp, const double* __restrict__ va,
-                  const double* __restrict__ u, unsigned long long* out) {
-    double rmax = 0.0, umax = 0.0;
+quadform_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                const double* __restrict__ va, const double* __restrict__ x, double* __restrict__ part) {
+    __shared__ double wsum[kThreads / 32];
+    double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
          i += (int64_t)gridDim.x * blockDim.x) {
         double r = 0.0;
-        for (int64_t e = rp[i]; e < rp[i + 1]; e++) r += fabs(va[e]);
+        for (int64_t e = rp[i]; e < rp[i + 1]; e++) r = fma(va[e], x[ci[e]], r);
+        acc = fma(x[i], r, acc);
+    }
+    acc = warp_sum_xor(acc);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kThreads / 32; w++) t += wsum[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void quadform_final_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int c = 0; c < n; c++) t += part[c];
+        *out = t;
+    }
+}
+
+// Gershgorin-type upper bound on lambda_max of a CSR operator: out[0] <- max_i sum_j |a_ij|,
+// out[1] <- max_i |u_i| (rank-1 u, if given).  Ordered-key atomics (order-independent).
+// out[2] <- min_i (a_ii - sum_{j != i} |a_ij|) (Gershgorin lower end; ordered-key min).
+__global__ void __launch_bounds__(kThreads)
+gershgorin_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                  const double* __restrict__ va, const double* __restrict__ u, unsigned long long* out) {
+    double rmax = 0.0, umax = 0.0, lmin = INFINITY;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double r = 0.0, off = 0.0, dg = 0.0;
+        for (int64_t e = rp[i]; e < rp[i + 1]; e++) {
+            const double x = fabs(va[e]);
+            r += x;
+            if (ci[e] == i) dg = va[e]; else off += x;
+        }
         rmax = fmax(rmax, r);
+        lmin = fmin(lmin, dg - off);
         if (u) umax = fmax(umax, fabs(u[i]));
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
         umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+        lmin = fmin(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
     }
     if ((threadIdx.x & 31) == 0) {
         atomicMax(out + 0, order_key(rmax));
         atomicMax(out + 1, order_key(umax));
+        atomicMin(out + 2, order_key(lmin));
     }
 }
 

@@ -586,15 +586,17 @@ int cheb_norm_bound(const cl_operator* op, double* s_out, void* stream) {
     }
     cudaStream_t st = (cudaStream_t)stream;
     DevBuf buf;
-    CL_CUDA(cudaMalloc(&buf.p, 2 * sizeof(unsigned long long)));
-    CL_CUDA(cudaMemsetAsync(buf.p, 0, 2 * sizeof(unsigned long long), st));
+    CL_CUDA(cudaMalloc(&buf.p, 3 * sizeof(unsigned long long)));
+    unsigned long long init[3] = {0ull, 0ull, ~0ull};
+    CL_CUDA(cudaMemcpyAsync(buf.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
     const int64_t d = op->A.n_rows;
     int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
     const double* u = op->kind == CL_OP_CSR_RANK1 ? op->r1_u : nullptr;
-    gershgorin_kernel<<<grid, kThreads, 0, st>>>(d, op->A.row_ptr, op->A.val, u, (unsigned long long*)buf.p);
+    gershgorin_kernel<<<grid, kThreads, 0, st>>>(d, op->A.row_ptr, op->A.col_idx, op->A.val, u,
+                                                  (unsigned long long*)buf.p);
     g_launches++;
     CL_CUDA(cudaGetLastError());
-    unsigned long long h[2];
+    unsigned long long h[3];
     CL_CUDA(cudaMemcpyAsync(h, buf.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     CL_CUDA(cudaStreamSynchronize(st));
     double s = unkey(h[0]);
@@ -603,6 +605,50 @@ int cheb_norm_bound(const cl_operator* op, double* s_out, void* stream) {
         s += std::fabs(op->r1_c) * umax * umax * (double)d;  // |c| |u_i| sum_j |u_j| <= |c| umax^2 d
     }
     *s_out = s;
+    return CL_OK;
+}
+
+int cheb_gershgorin(const cl_csr* A, double* lo_hi, void* stream) {
+    int rc;
+    if (!A || !lo_hi) return fail(CL_EINVAL, "NULL pointer");
+    if ((rc = check_csr(*A, "A"))) return rc;
+    if (A->n_rows != A->n_cols || A->n_rows < 1) return fail(CL_EDIM, "A must be square and non-empty");
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf buf;
+    CL_CUDA(cudaMalloc(&buf.p, 3 * sizeof(unsigned long long)));
+    unsigned long long init[3] = {0ull, 0ull, ~0ull};
+    CL_CUDA(cudaMemcpyAsync(buf.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const int64_t d = A->n_rows;
+    int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    gershgorin_kernel<<<grid, kThreads, 0, st>>>(d, A->row_ptr, A->col_idx, A->val, nullptr,
+                                                  (unsigned long long*)buf.p);
+    g_launches++;
+    CL_CUDA(cudaGetLastError());
+    unsigned long long h[3];
+    CL_CUDA(cudaMemcpyAsync(h, buf.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    lo_hi[0] = unkey(h[2]);
+    lo_hi[1] = unkey(h[0]);
+    return CL_OK;
+}
+
+int cheb_quadform(const cl_csr* A, const double* x, double* out, void* stream) {
+    int rc;
+    if (!A || !x || !out) return fail(CL_EINVAL, "NULL pointer");
+    if ((rc = check_csr(*A, "A"))) return rc;
+    if (A->n_rows != A->n_cols || A->n_rows < 1) return fail(CL_EDIM, "A must be square and non-empty");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t d = A->n_rows;
+    const int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    DevBuf buf;
+    CL_CUDA(cudaMalloc(&buf.p, sizeof(double) * (grid + 1)));
+    double* part = (double*)buf.p;
+    quadform_kernel<<<grid, kThreads, 0, st>>>(d, A->row_ptr, A->col_idx, A->val, x, part);
+    quadform_final_kernel<<<1, 32, 0, st>>>(part, grid, part + grid);
+    g_launches += 2;
+    CL_CUDA(cudaGetLastError());
+    CL_CUDA(cudaMemcpyAsync(out, part + grid, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
     return CL_OK;
 }
 

@@ -467,3 +467,11 @@ def test_power_iteration_grid_extremes_and_gershgorin(orc):
     lam = cf.grid_eigs(N, theta)
     assert abs(s * hi[-1] / hi[-2] - lam.max()) < 2e-3
     assert abs(s * (1 - lo[-1] / lo[-2]) - lam.min()) < 2e-3
+
+
+# ---------------------------------------------------------------- GMRF likelihood
+def test_quadform_matches_dense(orc):
+    A = W.grid_gmrf(9, 0.2, 7)
+    x = np.random.default_rng(5).standard_normal(63)
+    D = W.to_dense(A)
+    assert abs(orc.quadform(A, x) - x @ D @ x) < 1e-12 * abs(x @ D @ x)

@@ -378,3 +378,53 @@ def test_spectrum_estimate_grid_closed_form():
     assert lam.max() - 2e-3 < est["lambda_max"] <= lam.max() + 1e-9
     assert lam.min() - 1e-9 <= est["lambda_min"] < lam.min() + 2e-3
     assert est["norm_bound"] >= lam.max()
+
+
+# ------------------------------------------------------------------ GMRF likelihood scan
+def _grid_family(N):
+    import paper_1503_06394_b200.gmrf as G
+    base = W.grid_gmrf(N, 1.0)  # I - Adj: D = I, O = -Adj
+    return G, G.PrecisionFamily(P.DeviceCSR.from_host(base)), base
+
+
+def test_quadform_and_gershgorin_parity(orc):
+    G, fam, base = _grid_family(37)
+    J = fam.at(-0.22)
+    Jh = W.grid_gmrf(37, -0.22)
+    x = np.random.default_rng(3).standard_normal(J.n_rows)
+    q = G.quadform(J, torch.from_numpy(x).cuda())
+    oq = orc.quadform(Jh, x)
+    assert abs(q - oq) <= 1e-13 * abs(oq)
+    lo, hi = G.gershgorin(J)
+    assert abs(lo - (1 - 4 * 0.22)) < 1e-15 and abs(hi - (1 + 4 * 0.22)) < 1e-15
+
+
+def test_likelihood_scan_parity(orc):
+    """Scan values vs the oracle's (same probes, same formula, P:670 with reading G16)."""
+    import math
+    G, fam, base = _grid_family(30)
+    rng = np.random.default_rng(8)
+    xs = [rng.standard_normal(900) for _ in range(2)]
+    thetas = [-0.24, -0.2, 0.1]
+    res = G.likelihood_scan(fam, thetas, [torch.from_numpy(x).cuda() for x in xs], 40, 16, seed=4)
+    for th, ll in zip(thetas, res.loglik):
+        A = W.grid_gmrf(30, th)
+        a, b = 1 - 4 * abs(th), 1 + 4 * abs(th)
+        og = orc.logdet(orc.Op("csr", A), a, b, 40, 16, 4, workers=4)["gamma"]
+        oq = sum(orc.quadform(A, x) for x in xs)
+        oll = 0.5 * 2 * og - 0.5 * oq - 0.5 * 2 * 900 * math.log(2 * math.pi)
+        assert abs(ll - oll) <= 1e-10 * abs(oll)
+
+
+def test_likelihood_scan_recovers_rho():
+    """§5.2 at desk scale: exact samples x ~ N(0, J(rho*)^-1) (dense Cholesky)
+    of a 64x64 grid GMRF with rho* = -0.22; the scan's argmax lands next to rho*."""
+    G, fam, base = _grid_family(64)
+    rho = -0.22
+    Jd = W.to_dense(W.grid_gmrf(64, rho))
+    L = np.linalg.cholesky(Jd)
+    rng = np.random.default_rng(11)
+    xs = [np.linalg.solve(L.T, rng.standard_normal(Jd.shape[0])) for _ in range(8)]
+    thetas = np.round(np.arange(-0.245, -0.1949, 0.005), 4)
+    res = G.likelihood_scan(fam, thetas, [torch.from_numpy(x).cuda() for x in xs], 80, 64, seed=2)
+    assert abs(res.argmax - rho) <= 0.0151, (res.argmax, res.loglik)
