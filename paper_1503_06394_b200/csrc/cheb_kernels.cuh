@@ -45,6 +45,13 @@ constexpr int kThreads = 256;
 #ifndef CHEB_MIN_CTAS
 #define CHEB_MIN_CTAS 4  // resident CTAs per SM the step kernel is register-budgeted for
 #endif
+#ifndef CHEB_RPG
+#define CHEB_RPG 2  // rows per lane group per tile (tile = 256*RPG*4/K rows)
+#endif
+#ifndef CHEB_STAGES
+#define CHEB_STAGES 2  // shared-memory pipeline depth of cheb_step_kernel
+#endif
+constexpr int kStepStages = CHEB_STAGES;
 #ifndef CHEB_NNZ_UNROLL
 #define CHEB_NNZ_UNROLL 5  // nnz of a row whose gathers are in flight together (5-point stencil: 1 chunk)
 #endif
@@ -61,7 +68,7 @@ struct Geo {
     static constexpr int PPL = 4;
     static constexpr int L = K / PPL;               // lanes per row: 2..32
     static constexpr int GROUPS = kThreads / L;     // rows in flight per CTA
-    static constexpr int RPG = 2;                   // rows per group per tile
+    static constexpr int RPG = CHEB_RPG;            // rows per group per tile
     static constexpr int TILE = GROUPS * RPG;       // rows per tile: 256 .. 16
     static constexpr int WORDS = words_for(K);
     static constexpr int CAP = TILE * 8;            // staged nnz capacity (avg 8 per row)
@@ -604,10 +611,11 @@ cheb_step_kernel(StepArgs a) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
+    constexpr int NS = kStepStages;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int64_t s_base_c[2], s_base_v[2];
-    __shared__ int s_fit[2];
+    __shared__ __align__(8) uint64_t bar[NS];
+    __shared__ int64_t s_base_c[NS], s_base_v[NS];
+    __shared__ int s_fit[NS];
 
     const int tid = threadIdx.x;
     const int pa = 2 * (tid % G::L), pb = K / 2 + pa;
@@ -658,10 +666,10 @@ cheb_step_kernel(StepArgs a) {
 
     int64_t ne0 = 0, ne1 = 0;
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int i = 0; i < NS; i++) mbar_init(&bar[i], 1);
         fence_mbar_init();
-        for (int64_t i = 0; i < 2 && i < nmine; i++) {
+        for (int64_t i = 0; i < NS && i < nmine; i++) {
             int64_t e0, e1;
             bounds(tile_of(i), e0, e1);
             issue(tile_of(i), (int)i, e0, e1);
@@ -670,10 +678,10 @@ cheb_step_kernel(StepArgs a) {
     __syncthreads();
 
     for (int64_t it = 0; it < nmine; it++) {
-        const int b = (int)(it & 1);
-        const uint32_t phase = (uint32_t)((it >> 1) & 1);
+        const int b = (int)(it % NS);
+        const uint32_t phase = (uint32_t)((it / NS) & 1);
         const int64_t t = tile_of(it);
-        if (tid == 0 && it + 2 < nmine) bounds(tile_of(it + 2), ne0, ne1);  // consumed below
+        if (tid == 0 && it + NS < nmine) bounds(tile_of(it + NS), ne0, ne1);  // consumed below
         mbar_wait(&bar[b], phase);
         const unsigned char* st = smem + b * SL::BYTES;
         const int64_t r0 = t * G::TILE;
@@ -684,7 +692,7 @@ cheb_step_kernel(StepArgs a) {
         else
             step_tile<K, MODE, FIRST, false>(a, st, r0, rows, 0, 0, r1a, r1b, mu, s, a.xg, a.wcur, a.wnext);
         __syncthreads();  // every warp is done with stage b
-        if (tid == 0 && it + 2 < nmine) issue(tile_of(it + 2), b, ne0, ne1);
+        if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);
     }
     grid_reduce_finish<K, 4, HAS_S, true>(mu, s, a);
 }

@@ -53,8 +53,13 @@ struct Profiler {
     int64_t n[3] = {0, 0, 0};
 } g_prof;
 
-std::atomic<int> g_fusion{1};     // temporal fusion mode: 1 off (default), 2 auto, 3 forced
-std::atomic<int> g_persistent{1};  // persistent multi-step kernel: 0 off, 1 auto (default), 2 forced
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+// schedule controls (process-wide; CHEB_FUSION / CHEB_PERSISTENT env vars set the initial value)
+std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};          // 1 off (default), 2 auto, 3 forced
+std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
 
 struct ProfScope {
     cudaStream_t s;
@@ -267,9 +272,10 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     if (n < 1) return CL_OK;
 
     a.ntiles = (d + G::TILE - 1) / G::TILE;
-    const size_t smem = SL::SMEM;
-    const int grid_first = grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem);
-    const int grid_step = grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem);
+    const size_t smem = SL::SMEM;                          // 2-stage kernels (persistent, fused)
+    const size_t smem_step = (size_t)kStepStages * SL::BYTES;  // cheb_step_kernel
+    const int grid_first = grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem_step);
+    const int grid_step = grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem_step);
     int grid_spmm = 1;
     if (MODE == MODE_BTB) {
         const int64_t ng = (op->A.n_rows + G::GROUPS - 1) / G::GROUPS;
@@ -333,9 +339,9 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.mu_col = j;
         ProfScope ps(st);
         if (j == 1 || fp.power)  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
-            cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem, st>>>(a);
+            cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem_step, st>>>(a);
         else
-            cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem, st>>>(a);
+            cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem_step, st>>>(a);
         g_launches++;
     }
     return CL_OK;
@@ -382,11 +388,11 @@ int fused_occupancy(int k) {
 
 int step_grid_csr(int k, int64_t ntiles, int sms) {
     switch (k) {
-        case 8: return grid_for(cheb_step_kernel<8, MODE_CSR, false>, ntiles, sms, StageLayout<8, MODE_CSR>::SMEM);
-        case 16: return grid_for(cheb_step_kernel<16, MODE_CSR, false>, ntiles, sms, StageLayout<16, MODE_CSR>::SMEM);
-        case 32: return grid_for(cheb_step_kernel<32, MODE_CSR, false>, ntiles, sms, StageLayout<32, MODE_CSR>::SMEM);
-        case 64: return grid_for(cheb_step_kernel<64, MODE_CSR, false>, ntiles, sms, StageLayout<64, MODE_CSR>::SMEM);
-        default: return grid_for(cheb_step_kernel<128, MODE_CSR, false>, ntiles, sms, StageLayout<128, MODE_CSR>::SMEM);
+        case 8: return grid_for(cheb_step_kernel<8, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<8, MODE_CSR>::BYTES);
+        case 16: return grid_for(cheb_step_kernel<16, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<16, MODE_CSR>::BYTES);
+        case 32: return grid_for(cheb_step_kernel<32, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<32, MODE_CSR>::BYTES);
+        case 64: return grid_for(cheb_step_kernel<64, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<64, MODE_CSR>::BYTES);
+        default: return grid_for(cheb_step_kernel<128, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<128, MODE_CSR>::BYTES);
     }
 }
 

@@ -7,6 +7,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1503_06394_b200 import _build  # noqa: E402
 
 VARIANTS = {
+    "s3": ["CHEB_STAGES=3"],
+    "s3c3": ["CHEB_STAGES=3", "CHEB_MIN_CTAS=3"],
+    "r1": ["CHEB_RPG=1"],
+    "r1s3": ["CHEB_RPG=1", "CHEB_STAGES=3"],
+    "r4": ["CHEB_RPG=4"],
+    "r4c3": ["CHEB_RPG=4", "CHEB_MIN_CTAS=3"],
     "checked": ["CHEB_CHECKS=1"],
     "f_s1": ["CHEB_FUSED_SLACK=1"],
     "f_s2": ["CHEB_FUSED_SLACK=2"],
