@@ -54,16 +54,17 @@ def _traffic_per_launch(workload, k):
     return float(e["dram_bytes_per_launch"]) if e else None
 
 
-def step_bytes(d, nnz, k, first=False, mode="csr"):
+def step_bytes(d, nnz, k, first=False, mode="csr", doubling=False):
     """Algorithmic HBM bytes of one cheb_step_kernel launch over a block of k probes
     (SURVEY §8(d)): gather matrix (val 8 + col 4 per nnz, row_ptr 8 per
     row) once per block; per row and probe 8 B each for the gather source read, W_prev
     read and W_next write (no W_prev on the first step) -- plus, for B^T B, the W_cur
-    read of the -beta*w term; sign bits (4 B per row per 32 probes, >= 4)."""
+    read of the -beta*w term; sign bits (4 B per row per 32 probes, >= 4; the
+    moment-doubling schedule reads none: its dots are w_j.w_j and w_j.w_{j-1})."""
     vec = (16 if first else 24) * d * k
     if mode == "btb":
         vec += 8 * d * k
-    return 12 * nnz + 8 * (d + 1) + vec + d * max(4, k // 8)
+    return 12 * nnz + 8 * (d + 1) + vec + (0 if doubling else d * max(4, k // 8))
 
 
 def fused_bytes(d, nnz, k):
@@ -219,6 +220,8 @@ def run_ours(args):
     a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
     group = None
     sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, group=group, basis=args.basis)
+    if args.doubling:
+        P.set_doubling(True)
 
     def barrier():
         if world > 1:
@@ -257,6 +260,11 @@ def run_ours(args):
     t_ms = float(elapsed.item())
     st = stats.cpu().numpy()
 
+    # ---- the other schedule on the same operator (Algorithm 1 <-> moment doubling)
+    alt = None
+    if not args.no_alt and args.basis == "chebyshev":
+        alt = run_alt_schedule(args, sh, P, torch, dist, world, dev, float(st[0]))
+
     # ---- end-to-end through the public C ABI with HOST buffers (pinned)
     e2e = None
     if not args.no_e2e:
@@ -266,7 +274,7 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return 0
-    units = m_total * wl.degree * args.steps
+    units = m_total * wl.degree * args.steps  # degree-n Chebyshev moments delivered per probe
     value = units / (t_ms / 1e3)
     hbm, peak_kind = _peaks()
     d, nnz = wl.d, (A.nnz + (At.nnz if At is not None else 0))
@@ -289,8 +297,9 @@ def run_ours(args):
         if args.basis == "taylor":  # power recurrence: every launch reads w_{j-1}, writes w_j
             tot = s_n * step_bytes(d, gnnz, k, True, wl.mode)
         else:
-            tot = blocks * args.steps * (step_bytes(d, gnnz, k, True, wl.mode)
-                                         + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode))
+            dbl = bool(args.doubling)
+            tot = blocks * args.steps * (step_bytes(d, gnnz, k, True, wl.mode, dbl)
+                                         + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode, dbl))
         bytes_per_launch = tot / max(s_n, 1)
         avg_launch_ms, dom_ms = s_ms / max(s_n, 1), s_ms
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
@@ -313,17 +322,54 @@ def run_ours(args):
            "config": {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": d,
                       "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total,
                       "probes_per_gpu": m_per_gpu, "probe_block": k, "a": a, "b": b,
-                      "basis": args.basis, "parallelism": f"probe-dp{world}", "l2": "inputs larger than L2 (W blocks "
+                      "basis": args.basis,
+                      "schedule": ("moment doubling: ceil(n/2) applications of A~ per probe, value counts "
+                                   "the n Chebyshev steps delivered" if args.doubling else
+                                   "Algorithm 1: n applications of A~ per probe"),
+                      "applications_per_probe": (wl.degree + 1) // 2 if args.doubling else wl.degree,
+                      "parallelism": f"probe-dp{world}", "l2": "inputs larger than L2 (W blocks "
                       f"{2 * d * k * 8 / 1e9:.1f} GB/GPU), no flush needed",
                       "logdet_wall_s": t_ms / args.steps / 1e3, "gamma": float(st[0]),
                       "stderr": float(st[1])},
            "roofline": roof, "gpu_launches": int(launches),
            "gpu_launches_per_step": launches / args.steps, "clocks": clk, "cpu_baseline": cpu,
-           "e2e": e2e}
+           "e2e": e2e, "alt_schedule": alt}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_alt_schedule(args, sh, P, torch, dist, world, dev, gamma_main):
+    """Time the other moment schedule on the same sharded estimator (device events, max
+    over ranks): with the default Algorithm 1 run this measures moment doubling, and vice
+    versa.  Reported beside the headline, never instead of it."""
+    other = not args.doubling
+    P.set_doubling(other)
+    try:
+        sh.run()
+        torch.cuda.synchronize()
+        reps = max(1, min(args.steps, 3))
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        ev0.record()
+        for _ in range(reps):
+            gp, stats = sh.run()
+        ev1.record()
+        torch.cuda.synchronize()
+        el = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        g = float(stats.cpu().numpy()[0])
+    finally:
+        P.set_doubling(args.doubling)
+    wall = float(el.item()) / reps / 1e3
+    n = sh.est.degree
+    return {"schedule": "moment doubling" if other else "Algorithm 1 recurrence",
+            "applications_per_probe": (n + 1) // 2 if other else n, "logdet_wall_s": wall,
+            "chebyshev_steps_per_s": sh.est.m * n / wall, "gamma": g,
+            "rel_diff_gamma_vs_headline": abs(g - gamma_main) / abs(gamma_main), "reps": reps}
 
 
 def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, torch, dist):
@@ -405,6 +451,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--doubling", action="store_true",
+                    help="moment-doubling schedule (ceil(n/2) applications of A~) for the timed region")
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the other moment schedule")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

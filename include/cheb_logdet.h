@@ -210,6 +210,19 @@ int cheb_set_persistent(int32_t mode);
  * bandwidth).  CL_EINVAL for other values. */
 int cheb_set_fusion(int32_t steps);
 
+/* Moment-doubling schedule for cheb_moments / cheb_logdet / cheb_logdet_host (process-wide;
+ * default 0; env CHEB_DOUBLING sets the initial value).  DESIGN.md reading G25:
+ *   0 = Algorithm 1 as written: n applications of Ã per probe, mu_j = v^T w_j;
+ *   1 = ceil(n/2) applications: for a SYMMETRIC Ã the Chebyshev identities
+ *       T_{2j} = 2 T_j^2 - I and T_{2j+1} = 2 T_{j+1} T_j - T_1 give
+ *         mu_{2j}   = 2 w_j^T w_j     - mu_0,
+ *         mu_{2j-1} = 2 w_j^T w_{j-1} - mu_1   (mu_1 = w_1^T w_0 = v^T Ã v),
+ *       i.e. the same moments mu_0..mu_n (equal in exact arithmetic, rounding differs) from half
+ *       the matrix passes.  Requires M symmetric (A symmetric; B^T B always is).  Not applied
+ *       to the power-basis entry points.  CL_EINVAL for other values. */
+int cheb_set_doubling(int32_t on);
+int cheb_get_doubling(void);
+
 /* Thread-local message for the last failing call on this thread. */
 const char *cheb_last_error(void);
 

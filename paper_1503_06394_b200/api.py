@@ -318,6 +318,17 @@ def set_persistent(mode: int):
     check(_lib.load().cheb_set_persistent(int(mode)))
 
 
+def set_doubling(on: bool):
+    """Moment-doubling schedule (cheb_set_doubling; reading G25): ceil(n/2)
+    applications of Ã per probe give mu_0..mu_n via T_{2j} = 2T_j^2 - I and
+    T_{2j+1} = 2T_{j+1}T_j - T_1 (symmetric operators only).  Process-wide; default off."""
+    check(_lib.load().cheb_set_doubling(1 if on else 0))
+
+
+def get_doubling() -> bool:
+    return bool(_lib.load().cheb_get_doubling())
+
+
 def set_fusion(steps: int):
     """Temporal fusion for CSR operators: 1 (off), 2 (auto, default), 3 (always fuse pairs)."""
     check(_lib.load().cheb_set_fusion(int(steps)))

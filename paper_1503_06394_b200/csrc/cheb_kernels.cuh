@@ -45,6 +45,9 @@ constexpr int kThreads = 256;
 #ifndef CHEB_MIN_CTAS
 #define CHEB_MIN_CTAS 4  // resident CTAs per SM the step kernel is register-budgeted for
 #endif
+#ifndef CHEB_MIN_CTAS_DBL
+#define CHEB_MIN_CTAS_DBL 3  // moment doubling carries two more accumulator channels
+#endif
 #ifndef CHEB_RPG
 #define CHEB_RPG 2  // rows per lane group per tile (tile = 256*RPG*4/K rows)
 #endif
@@ -82,12 +85,15 @@ struct Geo {
     static constexpr int UBYTES = ((TILE * 8 + 15) / 16) * 16;
 };
 
-template <int K, int MODE>
+// WC: the tile's own W_cur rows are staged too (always for BTB; the per-step moment-doubling
+// kernel needs w_{j-1}[i] for its w_j^T w_{j-1} dot).
+template <int K, int MODE, bool WC = false>
 struct StageLayout {
     using G = Geo<K>;
+    static constexpr bool HAS_WC = (MODE == MODE_BTB) || WC;
     static constexpr int OFF_WPREV = 0;
-    static constexpr int OFF_WCUR = OFF_WPREV + G::WBYTES;                       // BTB only
-    static constexpr int OFF_VAL = OFF_WCUR + (MODE == MODE_BTB ? G::WBYTES : 0);
+    static constexpr int OFF_WCUR = OFF_WPREV + G::WBYTES;                       // HAS_WC only
+    static constexpr int OFF_VAL = OFF_WCUR + (HAS_WC ? G::WBYTES : 0);
     static constexpr int OFF_RP = OFF_VAL + G::VALBYTES;
     static constexpr int OFF_COL = OFF_RP + G::RPBYTES;
     static constexpr int OFF_SGN = OFF_COL + G::COLBYTES;
@@ -176,6 +182,11 @@ __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t t) {
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
 
+// x with its sign bit xor'ed by bit 31 of m (exactly -x or x)
+__device__ __forceinline__ double signflip(double x, uint32_t m) {
+    return __hiloint2double(__double2hiint(x) ^ (int)(m & 0x80000000u), __double2loint(x));
+}
+
 __device__ __forceinline__ double2 ldg2(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
 }
@@ -196,8 +207,7 @@ struct StepArgs {
     const double* r1u;    // padded u copy (nullptr = ones)
     const double* s_cur;  // [K] u^T w_{j-1}
     double* s_next;       // [K] u^T w_j
-    double* part_mu;      // [gridDim.x][K]
-    double* part_s;       // [gridDim.x][K]
+    double* part;         // per-CTA partials [NCH][gridDim.x][K] (persistent: [2][NCH][G][K])
     unsigned int* ticket;
     double* mu_out;       // mu_out[p*mu_stride + mu_col]
     int64_t mu_stride;
@@ -223,45 +233,41 @@ __device__ __forceinline__ double warp_sum_xor(double v) {
     return v;
 }
 
-// All K probes by one CTA (last-CTA-done epilogue).  out_mu/out_s: shared arrays [K].
-template <int K, bool HAS_S>
-__device__ __forceinline__ void reduce_partials_all(const double* part, const double* part_s, int G,
-                                                    double* out_mu, double* out_s) {
-    __shared__ double wsum[2][kThreads / 32][8];
+// All K probes of NCH channels by one CTA (last-CTA-done epilogue).  part: [NCH][G][K];
+// out: shared [NCH][K].  Each channel is summed in the canonical order independently.
+template <int K, int NCH>
+__device__ __forceinline__ void reduce_partials_all(const double* part, int G, double (*out)[K],
+                                                    double (*wsum)[kThreads / 32][8]) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int p0 = 0; p0 < K; p0 += 8) {
-        double m[8], t[8];
+        double m[NCH][8];
 #pragma unroll
-        for (int q = 0; q < 8; q++) m[q] = t[q] = 0.0;
+        for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+            for (int q = 0; q < 8; q++) m[ch][q] = 0.0;
         for (int c = tid; c < G; c += kThreads) {
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                m[q] += __ldcg(part + (size_t)c * K + p0 + q);
-                if (HAS_S) t[q] += __ldcg(part_s + (size_t)c * K + p0 + q);
-            }
+            for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+                for (int q = 0; q < 8; q++) m[ch][q] += __ldcg(part + ((size_t)ch * G + c) * K + p0 + q);
         }
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-            m[q] = warp_sum_xor(m[q]);
-            if (HAS_S) t[q] = warp_sum_xor(t[q]);
-        }
+        for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+            for (int q = 0; q < 8; q++) m[ch][q] = warp_sum_xor(m[ch][q]);
         if (lane == 0) {
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                wsum[0][warp][q] = m[q];
-                if (HAS_S) wsum[1][warp][q] = t[q];
-            }
+            for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+                for (int q = 0; q < 8; q++) wsum[ch][warp][q] = m[ch][q];
         }
         __syncthreads();
-        if (tid < 8) {
-            double mm = 0.0, tt = 0.0;
+        if (tid < 8 * NCH) {
+            const int ch = tid >> 3, q = tid & 7;
+            double mm = 0.0;
 #pragma unroll
-            for (int w = 0; w < kThreads / 32; w++) {
-                mm += wsum[0][w][tid];
-                if (HAS_S) tt += wsum[1][w][tid];
-            }
-            out_mu[p0 + tid] = mm;
-            if (HAS_S) out_s[p0 + tid] = tt;
+            for (int w = 0; w < kThreads / 32; w++) mm += wsum[ch][w][q];
+            out[ch][p0 + q] = mm;
         }
         __syncthreads();
     }
@@ -292,42 +298,66 @@ __device__ __forceinline__ int probe_of(int lg, int q) {
     return SPLIT ? 2 * lg + (q & 1) + (q >> 1) * (K / 2) : PPL * lg + q;
 }
 
-template <int K, int PPL, bool HAS_S, bool SPLIT = false, bool S_IS_MU = false>
-__device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s)[PPL], const StepArgs& a) {
+// Epilogues of the last CTA:
+//   EPI_STEP  ch0 -> mu[p][col]                        (+ rank-1: ch1 -> s_next)
+//   EPI_PAIR  ch0 -> mu[p][col], ch1 -> mu[p][col+1]   (temporally fused pair)
+//   EPI_DBL   moment doubling, step j = col: ch0 = w_j^T w_j, ch1 = w_j^T w_{j-1}
+//             mu[p][2j] = 2 ch0 - mu[p][0],  mu[p][2j-1] = 2 ch1 - mu[p][1]  (j = 1: mu[p][1] = ch1)
+//             (indices > n = mu_stride - 1 are not written)   (+ rank-1: ch2 -> s_next)
+enum { EPI_STEP = 0, EPI_PAIR = 1, EPI_DBL = 2 };
+
+// Moment-doubling epilogue for one probe row (T_{2j} = 2 T_j^2 - I, T_{2j+1} = 2 T_{j+1} T_j - T_1
+// for the symmetric Ã; reading G25).
+__device__ __forceinline__ void dbl_write(double* row, int j, int64_t n, double q, double r) {
+    if (j == 1) {
+        if (n >= 1) row[1] = r;
+    } else if (2 * (int64_t)j - 1 <= n) {
+        row[2 * j - 1] = 2.0 * r - row[1];
+    }
+    if (2 * (int64_t)j <= n) row[2 * j] = 2.0 * q - row[0];
+}
+
+// Shared-memory scratch of grid_reduce_finish (aliases the callers' dynamic shared memory,
+// which is idle once every tile is consumed): red[NCH][8][K], fin[NCH][K], wsum[NCH][8][8].
+template <int K, int NCH>
+__host__ __device__ constexpr int red_scratch_bytes() {
+    return 8 * (NCH * (kThreads / 32) * K + NCH * K + NCH * (kThreads / 32) * 8);
+}
+
+template <int K, int PPL, int NCH, int EPI, bool HAS_S, bool SPLIT = false>
+__device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], const StepArgs& a,
+                                                   unsigned char* scratch) {
     constexpr int LG = K / PPL;
-    __shared__ double red_mu[kThreads / 32][K];
-    __shared__ double red_s[HAS_S ? kThreads / 32 : 1][K];
-    __shared__ double fin_mu[K];
-    __shared__ double fin_s[HAS_S ? K : 1];
+    auto red = reinterpret_cast<double(*)[kThreads / 32][K]>(scratch);
+    auto fin = reinterpret_cast<double(*)[K]>(scratch + 8 * NCH * (kThreads / 32) * K);
+    auto wsum = reinterpret_cast<double(*)[kThreads / 32][8]>(scratch + 8 * (NCH * (kThreads / 32) * K + NCH * K));
     __shared__ bool is_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = lane % LG;
 #pragma unroll
     for (int off = LG; off < 32; off <<= 1) {
 #pragma unroll
-        for (int q = 0; q < PPL; q++) {
-            mu[q] += __shfl_xor_sync(0xffffffffu, mu[q], off);
-            if (HAS_S) s[q] += __shfl_xor_sync(0xffffffffu, s[q], off);
-        }
+        for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+            for (int q = 0; q < PPL; q++) acc[ch][q] += __shfl_xor_sync(0xffffffffu, acc[ch][q], off);
     }
     if (lane < LG) {
 #pragma unroll
         for (int q = 0; q < PPL; q++) {
             const int p = probe_of<K, PPL, SPLIT>(lg, q);
-            red_mu[warp][p] = mu[q];
-            if (HAS_S) red_s[warp][p] = s[q];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch++) red[ch][warp][p] = acc[ch][q];
         }
     }
     __syncthreads();
     if (tid < K) {
-        double m = 0.0, t = 0.0;
 #pragma unroll
-        for (int w = 0; w < kThreads / 32; w++) {
-            m += red_mu[w][tid];
-            if (HAS_S) t += red_s[w][tid];
+        for (int ch = 0; ch < NCH; ch++) {
+            double m = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; w++) m += red[ch][w][tid];
+            a.part[((size_t)ch * gridDim.x + blockIdx.x) * K + tid] = m;
         }
-        a.part_mu[(size_t)blockIdx.x * K + tid] = m;
-        if (HAS_S) a.part_s[(size_t)blockIdx.x * K + tid] = t;
     }
     __threadfence();
     __syncthreads();
@@ -338,11 +368,18 @@ __device__ __forceinline__ void grid_reduce_finish(double (&mu)[PPL], double (&s
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    reduce_partials_all<K, HAS_S>(a.part_mu, a.part_s, (int)gridDim.x, fin_mu, fin_s);
+    reduce_partials_all<K, NCH>(a.part, (int)gridDim.x, fin, wsum);
     if (tid < K) {
-        if (tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col] = fin_mu[tid];
-        if (HAS_S && S_IS_MU && tid < a.kvalid) a.mu_out[(size_t)tid * a.mu_stride + a.mu_col + 1] = fin_s[tid];
-        if (HAS_S && !S_IS_MU) a.s_next[tid] = fin_s[tid];
+        double* row = a.mu_out + (size_t)tid * a.mu_stride;
+        if (tid < a.kvalid) {
+            if (EPI == EPI_STEP) row[a.mu_col] = fin[0][tid];
+            if (EPI == EPI_PAIR) {
+                row[a.mu_col] = fin[0][tid];
+                row[a.mu_col + 1] = fin[1][tid];
+            }
+            if (EPI == EPI_DBL) dbl_write(row, a.mu_col, a.mu_stride - 1, fin[0][tid], fin[1][tid]);
+        }
+        if (HAS_S) a.s_next[tid] = fin[NCH - 1][tid];
     }
     if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch (stream-ordered)
 }
@@ -417,9 +454,12 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
     const int group = threadIdx.x / LG;
     const int pl = PPL * lg;
     const uint64_t d = (uint64_t)a.d;
-    double mu[PPL], s[PPL];
+    constexpr int NCH = HAS_S ? 2 : 1;
+    double acc[NCH][PPL];
 #pragma unroll
-    for (int q = 0; q < PPL; q++) mu[q] = s[q] = 0.0;
+    for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+        for (int q = 0; q < PPL; q++) acc[ch][q] = 0.0;
     const int64_t niter = (a.d + GROUPS - 1) / GROUPS;
     for (int64_t t = blockIdx.x; t < niter; t += gridDim.x) {
         const int64_t i = t * GROUPS + group;
@@ -433,7 +473,7 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
                 const uint32_t bq = (uint32_t)(z >> 63);
                 v[q] = bq ? -1.0 : 1.0;
                 bits |= bq << ((pl + q) & 31);
-                mu[q] += v[q] * v[q];
+                acc[0][q] += v[q] * v[q];
             }
 #pragma unroll
             for (int q = 0; q < PPL; q += 2)
@@ -441,7 +481,7 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
             if (HAS_S) {
                 const double u = a.r1u ? a.r1u[i] : 1.0;
 #pragma unroll
-                for (int q = 0; q < PPL; q++) s[q] += u * v[q];
+                for (int q = 0; q < PPL; q++) acc[NCH - 1][q] += u * v[q];
             }
         }
         // OR the bits of the lanes that share one 32-bit word
@@ -450,7 +490,8 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
         for (int off = 1; off < LW; off <<= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, off);
         if (ok && (lg % LW) == 0) sbits[(size_t)i * WORDS + (pl >> 5)] = bits;
     }
-    grid_reduce_finish<K, PPL, HAS_S>(mu, s, a);
+    extern __shared__ __align__(128) unsigned char smem[];
+    grid_reduce_finish<K, PPL, NCH, EPI_STEP, HAS_S>(acc, a, smem);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -472,14 +513,24 @@ __device__ __forceinline__ double2 ldcg2(const double* p) {
 // One staged tile of the fused step.  xg: gather source; wcur: W_cur (for rows without a
 // stored diagonal); wout: output rows (in place over W_prev).  CG: gather through L2 only
 // (data produced earlier in the same launch by other CTAs -- temporally fused kernel).
-template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false>
+// Accumulator channels (acc[ch][q], probe q of the lane):
+//   !DBL: ch0 = v^T w_j (sign bits)                        [+ rank-1 ch1 = u^T w_j]
+//    DBL: ch0 = w_j^T w_j, ch1 = w_{j-1}^T w_j (own rows)   [+ rank-1 ch2 = u^T w_j]
+template <int MODE, bool DBL>
+__host__ __device__ constexpr int n_channels() { return (DBL ? 2 : 1) + (MODE == MODE_RANK1 ? 1 : 0); }
+
+template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false, bool DBL = false,
+          bool WCS = false>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, double2 r1a, double2 r1b,
-                                          double (&mu)[4], double (&s)[4], const double* xg,
+                                          double (&acc)[n_channels<MODE, DBL>()][4], const double* xg,
                                           const double* wcur, double* wout) {
     using G = Geo<K>;
-    using SL = StageLayout<K, MODE>;
+    using SL = StageLayout<K, MODE, WCS>;
+    constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
+    constexpr bool CAPTURE = DBL && !OWN_SMEM;     // else: taken from the diagonal's gather
     constexpr bool HAS_S = (MODE == MODE_RANK1);
+    constexpr int SCH = n_channels<MODE, DBL>() - 1;  // rank-1 channel
     const int lg = threadIdx.x % G::L;
     const int grp = threadIdx.x / G::L;
     const int pa = 2 * lg, pb = K / 2 + 2 * lg;  // probe pairs (first / second half of the row)
@@ -497,36 +548,41 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         const int64_t i = r0 + lr;
         const int64_t e_lo = rp_s[lr], e_hi = rp_s[lr + 1];
         CHEB_ASSERT(rows <= G::TILE && i < a.d && e_lo <= e_hi);
+        // "no stored diagonal" flag word, loaded before the gathers so its latency overlaps them
+        const uint32_t ndw = (MODE == MODE_BTB) ? 0u : __ldg(a.nodiag + (i >> 5));
+        // 32-bit row-local offsets (a row's nnz and its staged slice fit in int32)
+        const int nr = (int)(e_hi - e_lo);
+        const int oc = STAGED ? (int)(e_lo - base_c) : 0;
+        const int ov = STAGED ? (int)(e_lo - base_v) : 0;
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-        // all nnz of a chunk issue their gathers before any is consumed (predicated tail)
-        for (int64_t e0 = e_lo; e0 < e_hi; e0 += CHEB_NNZ_UNROLL) {
+        double2 own0 = make_double2(0.0, 0.0), own1 = make_double2(0.0, 0.0);  // w_{j-1}[i]
+        // all nnz of a chunk issue their gathers before any is consumed; entries past the row
+        // end gather the row's first column again (a valid, cache-hot address) with value 0
+        for (int t0 = 0; t0 < nr; t0 += CHEB_NNZ_UNROLL) {
             int32_t c[CHEB_NNZ_UNROLL];
             double v[CHEB_NNZ_UNROLL];
 #pragma unroll
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                const bool in = e0 + q < e_hi;
-                const int64_t e = in ? e0 + q : e_lo;
-                CHEB_ASSERT(!STAGED || (e - base_c >= 0 && e - base_c < G::CAP + 8));
-                CHEB_ASSERT(!STAGED || (e - base_v >= 0 && e - base_v < G::CAP + 4));
-                c[q] = STAGED ? col_s[e - base_c] : __ldg(a.ci + e);
-                CHEB_ASSERT(!in || (c[q] >= 0 && (int64_t)c[q] < a.d));
-                v[q] = in ? (STAGED ? val_s[e - base_v] : __ldg(a.va + e)) : 0.0;
+                const bool in = t0 + q < nr;
+                const int t = in ? t0 + q : 0;
+                CHEB_ASSERT(!STAGED || (oc + t >= 0 && oc + t < G::CAP + 8));
+                CHEB_ASSERT(!STAGED || (ov + t >= 0 && ov + t < G::CAP + 4));
+                c[q] = STAGED ? col_s[oc + t] : __ldg(a.ci + e_lo + t);
+                CHEB_ASSERT(c[q] >= 0 && (int64_t)c[q] < a.d);
+                const double vv = STAGED ? val_s[ov + t] : __ldg(a.va + e_lo + t);
+                v[q] = in ? vv : 0.0;
             }
             double2 x0[CHEB_NNZ_UNROLL], x1[CHEB_NNZ_UNROLL];
 #pragma unroll
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                if (e0 + q < e_hi) {
-                    const double* p = xg + (size_t)(uint32_t)c[q] * K;
-                    if (KEEP && CHEB_FUSED_HINTS) {
-                        const uint64_t pol = policy_evict_last();
-                        x0[q] = ldnc2_hint(p + pa, pol);
-                        x1[q] = ldnc2_hint(p + pb, pol);
-                    } else {
-                        x0[q] = CG ? ldcg2(p + pa) : ldg2(p + pa);
-                        x1[q] = CG ? ldcg2(p + pb) : ldg2(p + pb);
-                    }
+                const double* p = xg + (size_t)(uint32_t)c[q] * K;
+                if (KEEP && CHEB_FUSED_HINTS) {
+                    const uint64_t pol = policy_evict_last();
+                    x0[q] = ldnc2_hint(p + pa, pol);
+                    x1[q] = ldnc2_hint(p + pb, pol);
                 } else {
-                    x0[q] = x1[q] = make_double2(0.0, 0.0);
+                    x0[q] = CG ? ldcg2(p + pa) : ldg2(p + pa);
+                    x1[q] = CG ? ldcg2(p + pb) : ldg2(p + pb);
                 }
             }
 #pragma unroll
@@ -535,23 +591,31 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                 acc0.y = fma(v[q], x0[q].y, acc0.y);
                 acc1.x = fma(v[q], x1[q].x, acc1.x);
                 acc1.y = fma(v[q], x1[q].y, acc1.y);
+                if (CAPTURE && (int64_t)c[q] == i) {  // padded entries repeat column 0: same value
+                    own0 = x0[q];
+                    own1 = x1[q];
+                }
             }
         }
         // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
+        if (OWN_SMEM) {
+            own0 = *reinterpret_cast<const double2*>(wc_s + lr * K + pa);
+            own1 = *reinterpret_cast<const double2*>(wc_s + lr * K + pb);
+        }
         if (MODE == MODE_BTB) {
-            const double2 w0 = *reinterpret_cast<const double2*>(wc_s + lr * K + pa);
-            const double2 w1 = *reinterpret_cast<const double2*>(wc_s + lr * K + pb);
-            acc0.x = fma(-a.beta, w0.x, acc0.x);
-            acc0.y = fma(-a.beta, w0.y, acc0.y);
-            acc1.x = fma(-a.beta, w1.x, acc1.x);
-            acc1.y = fma(-a.beta, w1.y, acc1.y);
-        } else if ((__ldg(a.nodiag + (i >> 5)) >> (i & 31)) & 1u) {
-            const double2 w0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
-            const double2 w1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
-            acc0.x = fma(-a.beta, w0.x, acc0.x);
-            acc0.y = fma(-a.beta, w0.y, acc0.y);
-            acc1.x = fma(-a.beta, w1.x, acc1.x);
-            acc1.y = fma(-a.beta, w1.y, acc1.y);
+            acc0.x = fma(-a.beta, own0.x, acc0.x);
+            acc0.y = fma(-a.beta, own0.y, acc0.y);
+            acc1.x = fma(-a.beta, own1.x, acc1.x);
+            acc1.y = fma(-a.beta, own1.y, acc1.y);
+        } else if ((ndw >> (i & 31)) & 1u) {
+            if (!OWN_SMEM) {
+                own0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
+                own1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
+            }
+            acc0.x = fma(-a.beta, own0.x, acc0.x);
+            acc0.y = fma(-a.beta, own0.y, acc0.y);
+            acc1.x = fma(-a.beta, own1.x, acc1.x);
+            acc1.y = fma(-a.beta, own1.y, acc1.y);
         }
         double ui = 1.0;
         if (HAS_S) {
@@ -585,33 +649,49 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             __stcs(reinterpret_cast<double2*>(out + pa), n0);
             __stcs(reinterpret_cast<double2*>(out + pb), n1);
         }
-        const uint32_t ba = sg_s[lr * G::WORDS + (pa >> 5)] >> (pa & 31);
-        const uint32_t bb = sg_s[lr * G::WORDS + (pb >> 5)] >> (pb & 31);
-        mu[0] += (ba & 1u) ? -n0.x : n0.x;
-        mu[1] += (ba & 2u) ? -n0.y : n0.y;
-        mu[2] += (bb & 1u) ? -n1.x : n1.x;
-        mu[3] += (bb & 2u) ? -n1.y : n1.y;
+        if (DBL) {
+            // w_j^T w_j and w_{j-1}^T w_j over this CTA's rows (w_{j-1} row i: staged, or
+            // captured from the diagonal's gather / loaded for rows without one)
+            const double2 c0 = own0, c1 = own1;
+            acc[0][0] = fma(n0.x, n0.x, acc[0][0]);
+            acc[0][1] = fma(n0.y, n0.y, acc[0][1]);
+            acc[0][2] = fma(n1.x, n1.x, acc[0][2]);
+            acc[0][3] = fma(n1.y, n1.y, acc[0][3]);
+            acc[1][0] = fma(c0.x, n0.x, acc[1][0]);
+            acc[1][1] = fma(c0.y, n0.y, acc[1][1]);
+            acc[1][2] = fma(c1.x, n1.x, acc[1][2]);
+            acc[1][3] = fma(c1.y, n1.y, acc[1][3]);
+        } else {
+            // v_p[i] w_j[i][p]: flip the sign bit of w where the probe bit is set
+            const uint32_t ba = sg_s[lr * G::WORDS + (pa >> 5)] >> (pa & 31);
+            const uint32_t bb = sg_s[lr * G::WORDS + (pb >> 5)] >> (pb & 31);
+            acc[0][0] += signflip(n0.x, ba << 31);
+            acc[0][1] += signflip(n0.y, ba << 30);
+            acc[0][2] += signflip(n1.x, bb << 31);
+            acc[0][3] += signflip(n1.y, bb << 30);
+        }
         if (HAS_S) {
-            s[0] = fma(ui, n0.x, s[0]);
-            s[1] = fma(ui, n0.y, s[1]);
-            s[2] = fma(ui, n1.x, s[2]);
-            s[3] = fma(ui, n1.y, s[3]);
+            acc[SCH][0] = fma(ui, n0.x, acc[SCH][0]);
+            acc[SCH][1] = fma(ui, n0.y, acc[SCH][1]);
+            acc[SCH][2] = fma(ui, n1.x, acc[SCH][2]);
+            acc[SCH][3] = fma(ui, n1.y, acc[SCH][3]);
         }
     }
 }
 
 // resident CTAs per SM each mode is register-budgeted for (BTB is smem-limited to 2)
-__host__ __device__ constexpr int min_ctas(int mode) {
-    return mode == MODE_CSR ? CHEB_MIN_CTAS : (mode == MODE_RANK1 ? 3 : 2);
+__host__ __device__ constexpr int min_ctas(int mode, bool dbl = false) {
+    return mode == MODE_CSR ? (dbl ? CHEB_MIN_CTAS_DBL : CHEB_MIN_CTAS) : (mode == MODE_RANK1 && !dbl ? 3 : 2);
 }
 
-template <int K, int MODE, bool FIRST>
-__global__ void __launch_bounds__(kThreads, min_ctas(MODE))
+template <int K, int MODE, bool FIRST, bool DBL = false>
+__global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_step_kernel(StepArgs a) {
     using G = Geo<K>;
-    using SL = StageLayout<K, MODE>;
+    using SL = StageLayout<K, MODE, DBL>;  // DBL: own W_cur rows staged (w_{j-1}^T w_j)
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int NS = kStepStages;
+    constexpr int NCH = n_channels<MODE, DBL>();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[NS];
     __shared__ int64_t s_base_c[NS], s_base_v[NS];
@@ -619,7 +699,11 @@ cheb_step_kernel(StepArgs a) {
 
     const int tid = threadIdx.x;
     const int pa = 2 * (tid % G::L), pb = K / 2 + pa;
-    double mu[4] = {0.0, 0.0, 0.0, 0.0}, s[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[NCH][4];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[ch][q] = 0.0;
     double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
     if (HAS_S) {
         r1a = make_double2(a.r1c_alpha * a.s_cur[pa], a.r1c_alpha * a.s_cur[pa + 1]);
@@ -639,18 +723,18 @@ cheb_step_kernel(StepArgs a) {
         s_base_c[b] = c0;
         s_base_v[b] = v0;
         const uint32_t wbytes = (uint32_t)rows * K * 8;
-        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+        const uint32_t sgbytes = DBL ? 0u : ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;  // DBL: no signs
         uint32_t bytes = G::RPBYTES + sgbytes;
         if (!FIRST) bytes += wbytes;
-        if (MODE == MODE_BTB) bytes += wbytes;
+        if (SL::HAS_WC) bytes += wbytes;
         if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
         const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
         if (HAS_S && a.r1u) bytes += ubytes;
         mbar_expect_tx(&bar[b], bytes);
         bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
-        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        if (!DBL) bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
         if (!FIRST) bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
-        if (MODE == MODE_BTB) bulk_g2s(st + SL::OFF_WCUR, a.wcur + (size_t)r0 * K, wbytes, &bar[b]);
+        if (SL::HAS_WC) bulk_g2s(st + SL::OFF_WCUR, a.wcur + (size_t)r0 * K, wbytes, &bar[b]);
         if (fit) {
             bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
             bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
@@ -687,14 +771,15 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu, s,
-                                            a.xg, a.wcur, a.wnext);
+            step_tile<K, MODE, FIRST, true, false, false, DBL, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b,
+                                                               acc, a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false>(a, st, r0, rows, 0, 0, r1a, r1b, mu, s, a.xg, a.wcur, a.wnext);
+            step_tile<K, MODE, FIRST, false, false, false, DBL, DBL>(a, st, r0, rows, 0, 0, r1a, r1b, acc, a.xg, a.wcur,
+                                                                a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);
     }
-    grid_reduce_finish<K, 4, HAS_S, true>(mu, s, a);
+    grid_reduce_finish<K, 4, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, true>(acc, a, smem);
 }
 
 
@@ -751,7 +836,9 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
     const int tid = threadIdx.x;
     const int64_t Gd = gridDim.x;
     const unsigned int nctas = gridDim.x;
-    double mu1[4] = {0.0, 0.0, 0.0, 0.0}, mu2[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};  // stage 1 / stage 2 moments
+    double (&mu1)[1][4] = *reinterpret_cast<double(*)[1][4]>(&acc[0]);
+    double (&mu2)[1][4] = *reinterpret_cast<double(*)[1][4]>(&acc[1]);
     const double2 z2 = make_double2(0.0, 0.0);
     const int64_t npos = a.ntiles + f.D;  // positions 0 .. ntiles + D - 1
     const int64_t M = blockIdx.x < npos ? 2 * ((npos - 1 - blockIdx.x) / Gd + 1) : 0;
@@ -859,16 +946,16 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
         if (stg == 0) {
             if (s_fit[b])
                 step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
-                                                                 mu1, mu1, f.B, f.B, f.A);
+                                                                 mu1, f.B, f.B, f.A);
             else
-                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, z2, mu1, mu1, f.B,
+                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, z2, mu1, f.B,
                                                                   f.B, f.A);
         } else {
             if (s_fit[b])
                 step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
-                                                                 mu2, mu2, f.A, f.A, f.B);
+                                                                 mu2, f.A, f.A, f.B);
             else
-                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, z2, mu2, mu2, f.A,
+                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, z2, mu2, f.A,
                                                                   f.A, f.B);
         }
         __syncthreads();  // every warp is done with stage b (and, for stage 1, with its stores)
@@ -886,7 +973,7 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
         const int64_t iters = (npos + Gd - 1) / Gd;
         for (int64_t k = (M >> 1); k < iters; k++) red_release_add(f.wave + k, 1u);
     }
-    grid_reduce_finish<K, 4, true, true, true>(mu1, mu2, a);
+    grid_reduce_finish<K, 4, 2, EPI_PAIR, false, true>(acc, a, smem);
 }
 
 
@@ -907,8 +994,7 @@ struct PersistArgs {
     double* w0;               // holds v (from probe_init) at entry
     double* w1;
     int32_t n;                // degree
-    double* part;             // [2][gridDim.x][K] mu partials (double-buffered by step parity)
-    double* part_s;           // [2][gridDim.x][K] rank-1 partials
+    double* part;             // [2][NCH][gridDim.x][K] partials (double-buffered by step parity)
     double* s_buf;            // [2][K] s_j by step parity (s_0 from probe_init in s_buf[0])
     unsigned int* bar_count;  // grid barrier arrivals (zeroed; monotone)
     unsigned int* s_count;    // rank-1: probes whose s_j is published (zeroed; monotone)
@@ -927,18 +1013,18 @@ __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned i
     }
 }
 
-template <int K, int MODE>
-__global__ void __launch_bounds__(kThreads, min_ctas(MODE))
+template <int K, int MODE, bool DBL = false>
+__global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
+    constexpr int NCH = n_channels<MODE, DBL>();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ int64_t s_base_c[2], s_base_v[2];
     __shared__ int s_fit[2];
-    __shared__ double red_mu[kThreads / 32][K];
-    __shared__ double red_s[HAS_S ? kThreads / 32 : 1][K];
+    __shared__ double red[NCH][kThreads / 32][K];
     __shared__ double wbuf[kThreads / 32];
     __shared__ double s_sh[HAS_S ? K : 1];
 
@@ -963,7 +1049,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         s_base_c[b] = c0;
         s_base_v[b] = v0;
         const uint32_t wbytes = (uint32_t)rows * K * 8;
-        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+        const uint32_t sgbytes = DBL ? 0u : ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;  // DBL: no signs
         const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
         uint32_t bytes = G::RPBYTES + sgbytes;
         if (!first) bytes += wbytes;
@@ -971,7 +1057,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         if (HAS_S && a.r1u) bytes += ubytes;
         mbar_expect_tx(&bar[b], bytes);
         bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
-        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        if (!DBL) bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
         if (!first) bulk_g2s(st + SL::OFF_WPREV, wprev + (size_t)r0 * K, wbytes, &bar[b]);
         if (fit) {
             bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
@@ -998,7 +1084,11 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             r1a = make_double2(a.r1c_alpha * s_sh[pa], a.r1c_alpha * s_sh[pa + 1]);
             r1b = make_double2(a.r1c_alpha * s_sh[pb], a.r1c_alpha * s_sh[pb + 1]);
         }
-        double mu[4] = {0.0, 0.0, 0.0, 0.0}, sacc[4] = {0.0, 0.0, 0.0, 0.0};
+        double acc[NCH][4];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[ch][q] = 0.0;
         for (int64_t it = 0; it < nmine; it++) {
             const int b = (int)(it & 1);
             mbar_wait(&bar[b], uses[b] & 1u);
@@ -1009,16 +1099,18 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
             if (first) {
                 if (s_fit[b])
-                    step_tile<K, MODE, true, true, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu,
-                                                         sacc, cur, cur, nxt);
+                    step_tile<K, MODE, true, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a,
+                                                                     r1b, acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, true, false, true>(a, st, r0, rows, 0, 0, r1a, r1b, mu, sacc, cur, cur, nxt);
+                    step_tile<K, MODE, true, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1a, r1b, acc, cur, cur,
+                                                                      nxt);
             } else {
                 if (s_fit[b])
-                    step_tile<K, MODE, false, true, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b, mu,
-                                                          sacc, cur, cur, nxt);
+                    step_tile<K, MODE, false, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a,
+                                                                      r1b, acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, false, false, true>(a, st, r0, rows, 0, 0, r1a, r1b, mu, sacc, cur, cur, nxt);
+                    step_tile<K, MODE, false, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1a, r1b, acc, cur, cur,
+                                                                       nxt);
             }
             __syncthreads();
             if (tid == 0 && it + 2 < nmine) issue(j, (int64_t)blockIdx.x + (it + 2) * gridDim.x, b);
@@ -1027,31 +1119,28 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
 #pragma unroll
         for (int off = G::L; off < 32; off <<= 1) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                mu[q] += __shfl_xor_sync(0xffffffffu, mu[q], off);
-                if (HAS_S) sacc[q] += __shfl_xor_sync(0xffffffffu, sacc[q], off);
-            }
+            for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+                for (int q = 0; q < 4; q++) acc[ch][q] += __shfl_xor_sync(0xffffffffu, acc[ch][q], off);
         }
         if (lane < G::L) {
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int p = probe_of<K, 4, true>(lg, q);
-                red_mu[warp][p] = mu[q];
-                if (HAS_S) red_s[warp][p] = sacc[q];
+#pragma unroll
+                for (int ch = 0; ch < NCH; ch++) red[ch][warp][p] = acc[ch][q];
             }
         }
         __syncthreads();
-        double* part = pa_.part + (size_t)(j & 1) * gridDim.x * K;
-        double* part_s = pa_.part_s + (size_t)(j & 1) * gridDim.x * K;
+        double* part = pa_.part + (size_t)(j & 1) * NCH * gridDim.x * K;  // [NCH][G][K] of step j
         if (tid < K) {
-            double m = 0.0, t2 = 0.0;
 #pragma unroll
-            for (int w = 0; w < kThreads / 32; w++) {
-                m += red_mu[w][tid];
-                if (HAS_S) t2 += red_s[w][tid];
+            for (int ch = 0; ch < NCH; ch++) {
+                double m = 0.0;
+#pragma unroll
+                for (int w = 0; w < kThreads / 32; w++) m += red[ch][w][tid];
+                part[((size_t)ch * gridDim.x + blockIdx.x) * K + tid] = m;
             }
-            part[(size_t)blockIdx.x * K + tid] = m;
-            if (HAS_S) part_s[(size_t)blockIdx.x * K + tid] = t2;
         }
         // ---- grid barrier, split: arrive, stage step j+1, wait
         __syncthreads();
@@ -1072,12 +1161,16 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         __syncthreads();
         // ---- canonical reductions of step j's partials: CTA c owns probes c, c+G, ...
         for (int p = blockIdx.x; p < K; p += gridDim.x) {
-            const double m = reduce_partials_one(part, K, (int)gridDim.x, p, wbuf);
-            if (tid == 0 && p < a.kvalid) a.mu_out[(size_t)p * a.mu_stride + j] = m;
-            if (HAS_S) {
-                const double t2 = reduce_partials_one(part_s, K, (int)gridDim.x, p, wbuf);
-                if (tid == 0) pa_.s_buf[(j & 1) * K + p] = t2;
+            double v[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch++)
+                v[ch] = reduce_partials_one(part + (size_t)ch * gridDim.x * K, K, (int)gridDim.x, p, wbuf);
+            if (tid == 0 && p < a.kvalid) {
+                double* row = a.mu_out + (size_t)p * a.mu_stride;
+                if (DBL) dbl_write(row, j, a.mu_stride - 1, v[0], v[1]);
+                else row[j] = v[0];
             }
+            if (HAS_S && tid == 0) pa_.s_buf[(j & 1) * K + p] = v[NCH - 1];
         }
         if (HAS_S) {
             if (tid == 0) {

@@ -1,6 +1,7 @@
 // cheb_logdet.cu -- host side of the C ABI (include/cheb_logdet.h): validation,
 // fp64 coefficient routine, workspace planning, stream-ordered launch sequence,
 // kernel accounting.  Device kernels live in cheb_kernels.cuh.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -60,6 +61,7 @@ int env_int(const char* name, int dflt) {
 // schedule controls (process-wide; CHEB_FUSION / CHEB_PERSISTENT env vars set the initial value)
 std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};          // 1 off (default), 2 auto, 3 forced
 std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
+std::atomic<int> g_doubling{env_int("CHEB_DOUBLING", 0)};      // 0 off (default), 1 moment doubling
 
 struct ProfScope {
     cudaStream_t s;
@@ -105,7 +107,7 @@ bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64 || k == 128
 int tile_rows(int k) { return 2 * kThreads * 4 / k; }  // Geo<K>::TILE
 
 struct Layout {
-    size_t w0, w1, y, sbits, part_mu, part_s, sbuf, ticket;
+    size_t w0, w1, y, sbits, part, sbuf, ticket;
     size_t rp2, ci2, va2, nodiag, u2, cnt, misc, total;
     int64_t rp2_len;
 };
@@ -122,8 +124,8 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.w1 = off; off += wbytes;
     L.y = off; if (kind == CL_OP_BTB) off += wbytes;
     L.sbits = off; off += align256((size_t)d * words * sizeof(uint32_t) + 16);
-    L.part_mu = off; off += align256(2 * maxgrid * k * sizeof(double));  // x2: persistent kernel
-    L.part_s = off; off += align256(2 * maxgrid * k * sizeof(double));
+    // per-CTA partials: up to 3 channels (doubling + rank-1) x 2 step parities (persistent kernel)
+    L.part = off; off += align256(6 * maxgrid * k * sizeof(double));
     L.sbuf = off; off += align256(2 * (size_t)k * sizeof(double));
     L.ticket = off; off += 256;
     L.rp2_len = ntiles * tile_rows(k) + 2;
@@ -188,11 +190,21 @@ int min_tiles_per_cta() {
     return v;
 }
 
+// Cap on resident CTAs per SM for the staged step kernels (CHEB_STEP_OCC; 0 = occupancy limit).
+int step_occ_cap() {
+    static int v = [] {
+        const char* e = getenv("CHEB_STEP_OCC");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <typename Kern>
 int grid_for(Kern kern, int64_t ntiles, int sms, size_t dyn_smem = 0) {
     int occ = 0;
     if (dyn_smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, dyn_smem);
+    if (dyn_smem > 0 && step_occ_cap() > 0 && occ > step_occ_cap()) occ = step_occ_cap();
     if (occ < 1) occ = 1;
     if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
     int64_t g = (int64_t)sms * occ;
@@ -227,6 +239,7 @@ struct FusionPlan {
     int64_t H = 0, D = 0;
     int G = 0;                // fused grid (= the single-step grid, for bit-identical moments)
     bool power = false;       // power basis (Taylor baseline): w_j = Ã w_{j-1}, every step "FIRST"
+    bool doubling = false;    // moment doubling: ceil(n/2) applications of Ã give mu_0..mu_n
 };
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
@@ -252,8 +265,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.beta = beta;
     a.r1c_alpha = alpha * op->r1_c;
     a.r1u = (MODE == MODE_RANK1 && op->r1_u) ? (const double*)(ws + L.u2) : nullptr;
-    a.part_mu = (double*)(ws + L.part_mu);
-    a.part_s = (double*)(ws + L.part_s);
+    a.part = (double*)(ws + L.part);
     a.ticket = (unsigned int*)(ws + L.ticket);
     a.mu_out = mu_rows;
     a.mu_stride = mu_stride;
@@ -263,32 +275,43 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     {
         constexpr int groups = kThreads / (K <= 64 ? K / 2 : K / 4);
         const int64_t niter = (d + groups - 1) / groups;
+        constexpr size_t init_smem = red_scratch_bytes<K, MODE == MODE_RANK1 ? 2 : 1>();
+        cudaFuncSetAttribute(probe_init_kernel<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)init_smem);
         const int grid = grid_for(probe_init_kernel<K, MODE>, niter, sms);
         a.mu_col = 0;
         a.s_next = sbuf;
-        probe_init_kernel<K, MODE><<<grid, kThreads, 0, st>>>(a, seed, (uint64_t)p0, w[0], sbits);
+        probe_init_kernel<K, MODE><<<grid, kThreads, init_smem, st>>>(a, seed, (uint64_t)p0, w[0], sbits);
         g_launches++;
     }
     if (n < 1) return CL_OK;
 
     a.ntiles = (d + G::TILE - 1) / G::TILE;
-    const size_t smem = SL::SMEM;                          // 2-stage kernels (persistent, fused)
-    const size_t smem_step = (size_t)kStepStages * SL::BYTES;  // cheb_step_kernel
-    const int grid_first = grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem_step);
-    const int grid_step = grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem_step);
+    // dynamic shared memory: the staged tiles, reused as the reduction scratch at the end
+    const size_t smem = std::max<size_t>(SL::SMEM, red_scratch_bytes<K, 2>());  // persistent, fused
+    const size_t smem_step = std::max<size_t>(
+        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, true>::BYTES : SL::BYTES),
+        red_scratch_bytes<K, 3>());  // cheb_step_kernel
+    const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true>, a.ntiles, sms, smem_step)
+                                       : grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem_step);
+    const int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true>, a.ntiles, sms, smem_step)
+                                      : grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem_step);
     int grid_spmm = 1;
     if (MODE == MODE_BTB) {
         const int64_t ng = (op->A.n_rows + G::GROUPS - 1) / G::GROUPS;
         grid_spmm = grid_for(spmm_kernel<K>, ng, sms);
     }
+    // moment doubling (reading G25): steps j = 1..ceil(n/2); the epilogue of step j writes
+    // mu_{2j-1} and mu_{2j} (indices <= n) from w_j^T w_{j-1} and w_j^T w_j
+    const int32_t nsteps = fp.doubling ? (n + 1) / 2 : n;
     if (MODE != MODE_BTB && fp.persistent) {
-        const int grid_p = grid_for(cheb_persist_kernel<K, MODE>, a.ntiles, sms, smem);
+        auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true> : cheb_persist_kernel<K, MODE, false>;
+        const int grid_p = grid_for(pkern, a.ntiles, sms, smem);
         PersistArgs pp{};
         pp.w0 = w[0];
         pp.w1 = w[1];
-        pp.n = n;
-        pp.part = (double*)(ws + L.part_mu);
-        pp.part_s = (double*)(ws + L.part_s);
+        pp.n = nsteps;
+        pp.part = (double*)(ws + L.part);
         pp.s_buf = sbuf;
         pp.bar_count = (unsigned int*)(ws + L.misc + 16);
         pp.s_count = (unsigned int*)(ws + L.misc + 20);
@@ -297,17 +320,16 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
         void* args[] = {&a, &pp};
         ProfScope ps(st, 2);
-        CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_persist_kernel<K, MODE>, dim3(grid_p), dim3(kThreads),
-                                            args, smem, st));
+        CL_CUDA(cudaLaunchCooperativeKernel((const void*)pkern, dim3(grid_p), dim3(kThreads), args, smem, st));
         g_launches++;
         return CL_OK;
     }
     int grid_fused = 0;
     if (MODE == MODE_CSR && fp.on) grid_fused = fp.G;
-    for (int32_t j = 1; j <= n; j++) {
+    for (int32_t j = 1; j <= nsteps; j++) {
         const double* cur = w[(j - 1) & 1];
         double* nxt = w[j & 1];
-        if (MODE == MODE_CSR && fp.on && j >= 2 && j + 1 <= n) {
+        if (MODE == MODE_CSR && fp.on && !fp.doubling && j >= 2 && j + 1 <= n) {
             // steps j and j+1 in one launch: A = w_{j-2} -> w_j, B = w_{j-1} -> w_{j+1}
             FusedArgs f{};
             f.A = nxt;
@@ -338,10 +360,16 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.s_next = sbuf + (j & 1) * K;
         a.mu_col = j;
         ProfScope ps(st);
-        if (j == 1 || fp.power)  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
+        if (fp.doubling) {
+            if (j == 1)
+                cheb_step_kernel<K, MODE, true, true><<<grid_first, kThreads, smem_step, st>>>(a);
+            else
+                cheb_step_kernel<K, MODE, false, true><<<grid_step, kThreads, smem_step, st>>>(a);
+        } else if (j == 1 || fp.power) {  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
             cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem_step, st>>>(a);
-        else
+        } else {
             cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem_step, st>>>(a);
+        }
         g_launches++;
     }
     return CL_OK;
@@ -378,21 +406,21 @@ int fused_occupancy(int k) {
         return occ < 1 ? 1 : (occ > kMaxCtasPerSm ? kMaxCtasPerSm : occ);
     };
     switch (k) {
-        case 8: return occ_of(cheb_step2_kernel<8>, StageLayout<8, MODE_CSR>::SMEM);
-        case 16: return occ_of(cheb_step2_kernel<16>, StageLayout<16, MODE_CSR>::SMEM);
-        case 32: return occ_of(cheb_step2_kernel<32>, StageLayout<32, MODE_CSR>::SMEM);
-        case 64: return occ_of(cheb_step2_kernel<64>, StageLayout<64, MODE_CSR>::SMEM);
-        default: return occ_of(cheb_step2_kernel<128>, StageLayout<128, MODE_CSR>::SMEM);
+        case 8: return occ_of(cheb_step2_kernel<8>, std::max<size_t>(StageLayout<8, MODE_CSR>::SMEM, red_scratch_bytes<8, 2>()));
+        case 16: return occ_of(cheb_step2_kernel<16>, std::max<size_t>(StageLayout<16, MODE_CSR>::SMEM, red_scratch_bytes<16, 2>()));
+        case 32: return occ_of(cheb_step2_kernel<32>, std::max<size_t>(StageLayout<32, MODE_CSR>::SMEM, red_scratch_bytes<32, 2>()));
+        case 64: return occ_of(cheb_step2_kernel<64>, std::max<size_t>(StageLayout<64, MODE_CSR>::SMEM, red_scratch_bytes<64, 2>()));
+        default: return occ_of(cheb_step2_kernel<128>, std::max<size_t>(StageLayout<128, MODE_CSR>::SMEM, red_scratch_bytes<128, 2>()));
     }
 }
 
 int step_grid_csr(int k, int64_t ntiles, int sms) {
     switch (k) {
-        case 8: return grid_for(cheb_step_kernel<8, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<8, MODE_CSR>::BYTES);
-        case 16: return grid_for(cheb_step_kernel<16, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<16, MODE_CSR>::BYTES);
-        case 32: return grid_for(cheb_step_kernel<32, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<32, MODE_CSR>::BYTES);
-        case 64: return grid_for(cheb_step_kernel<64, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<64, MODE_CSR>::BYTES);
-        default: return grid_for(cheb_step_kernel<128, MODE_CSR, false>, ntiles, sms, kStepStages * StageLayout<128, MODE_CSR>::BYTES);
+        case 8: return grid_for(cheb_step_kernel<8, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<8, MODE_CSR>::BYTES, red_scratch_bytes<8, 3>()));
+        case 16: return grid_for(cheb_step_kernel<16, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<16, MODE_CSR>::BYTES, red_scratch_bytes<16, 3>()));
+        case 32: return grid_for(cheb_step_kernel<32, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<32, MODE_CSR>::BYTES, red_scratch_bytes<32, 3>()));
+        case 64: return grid_for(cheb_step_kernel<64, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<64, MODE_CSR>::BYTES, red_scratch_bytes<64, 3>()));
+        default: return grid_for(cheb_step_kernel<128, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<128, MODE_CSR>::BYTES, red_scratch_bytes<128, 3>()));
     }
 }
 
@@ -469,6 +497,14 @@ int cheb_set_persistent(int32_t mode) {
     g_persistent = mode;
     return CL_OK;
 }
+
+int cheb_set_doubling(int32_t on) {
+    if (on < 0 || on > 1) return fail(CL_EINVAL, "doubling mode must be 0 or 1");
+    g_doubling = on;
+    return CL_OK;
+}
+
+int cheb_get_doubling(void) { return g_doubling.load(); }
 
 int cheb_set_fusion(int32_t steps) {
     if (steps < 1 || steps > 3) return fail(CL_EINVAL, "fusion mode must be 1, 2 or 3");
@@ -689,6 +725,7 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     prep_mode(op, alpha, beta, ws, L, st, sms);
     FusionPlan fp;
     fp.power = power;
+    fp.doubling = !power && g_doubling.load() == 1;
     if (op->kind != CL_OP_BTB && g_persistent.load() > 0 && degree >= 1) {
         // L2-resident working set (two probe-block buffers + matrix): the per-step launch and
         // drain gaps dominate, so run all steps in one launch
@@ -699,7 +736,7 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
-    if (!fp.persistent && !power && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
+    if (!fp.persistent && !power && !fp.doubling && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
         // needs the operator bandwidth computed by the prep kernel: one small D2H per call
         unsigned long long bw = 0;
         CL_CUDA(cudaMemcpyAsync(&bw, ws + L.misc, sizeof(bw), cudaMemcpyDeviceToHost, st));
@@ -721,9 +758,9 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         fp.on = g_fusion.load() == 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
     }
     if (getenv("CHEB_DEBUG"))
-        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d H=%lld D=%lld\n",
+        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d doubling=%d H=%lld D=%lld\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
-                (int)fp.on, (long long)fp.H, (long long)fp.D);
+                (int)fp.on, (int)fp.doubling, (long long)fp.H, (long long)fp.D);
     for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
         const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
