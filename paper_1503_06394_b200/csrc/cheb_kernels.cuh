@@ -48,6 +48,9 @@ constexpr int kThreads = 256;
 #ifndef CHEB_MIN_CTAS_DBL
 #define CHEB_MIN_CTAS_DBL 3  // moment doubling carries two more accumulator channels
 #endif
+#ifndef CHEB_DBL_STAGE_WC
+#define CHEB_DBL_STAGE_WC 0
+#endif
 #ifndef CHEB_RPG
 #define CHEB_RPG 2  // rows per lane group per tile (tile = 256*RPG*4/K rows)
 #endif
@@ -528,7 +531,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     using G = Geo<K>;
     using SL = StageLayout<K, MODE, WCS>;
     constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
-    constexpr bool CAPTURE = DBL && !OWN_SMEM;     // else: taken from the diagonal's gather
+    constexpr bool OWN_EARLY = DBL && !OWN_SMEM;   // else: loaded at the row start (L1/L2-hot)
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int SCH = n_channels<MODE, DBL>() - 1;  // rank-1 channel
     const int lg = threadIdx.x % G::L;
@@ -556,6 +559,10 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         const int ov = STAGED ? (int)(e_lo - base_v) : 0;
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
         double2 own0 = make_double2(0.0, 0.0), own1 = make_double2(0.0, 0.0);  // w_{j-1}[i]
+        if (OWN_EARLY) {  // issued before the gathers so its latency overlaps them
+            own0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
+            own1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
+        }
         // all nnz of a chunk issue their gathers before any is consumed; entries past the row
         // end gather the row's first column again (a valid, cache-hot address) with value 0
         for (int t0 = 0; t0 < nr; t0 += CHEB_NNZ_UNROLL) {
@@ -591,10 +598,6 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                 acc0.y = fma(v[q], x0[q].y, acc0.y);
                 acc1.x = fma(v[q], x1[q].x, acc1.x);
                 acc1.y = fma(v[q], x1[q].y, acc1.y);
-                if (CAPTURE && (int64_t)c[q] == i) {  // padded entries repeat column 0: same value
-                    own0 = x0[q];
-                    own1 = x1[q];
-                }
             }
         }
         // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
@@ -608,7 +611,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             acc1.x = fma(-a.beta, own1.x, acc1.x);
             acc1.y = fma(-a.beta, own1.y, acc1.y);
         } else if ((ndw >> (i & 31)) & 1u) {
-            if (!OWN_SMEM) {
+            if (!OWN_SMEM && !OWN_EARLY) {
                 own0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
                 own1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
             }
@@ -688,7 +691,10 @@ template <int K, int MODE, bool FIRST, bool DBL = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_step_kernel(StepArgs a) {
     using G = Geo<K>;
-    using SL = StageLayout<K, MODE, DBL>;  // DBL: own W_cur rows staged (w_{j-1}^T w_j)
+    // DBL: w_{j-1}[i] (for w_{j-1}^T w_j) from an early L1/L2 load; CHEB_DBL_STAGE_WC=1 stages
+    // the own W_cur rows by TMA instead (measured slower: the extra shared memory shrinks L1)
+    constexpr bool WCS = DBL && CHEB_DBL_STAGE_WC;
+    using SL = StageLayout<K, MODE, WCS>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int NS = kStepStages;
     constexpr int NCH = n_channels<MODE, DBL>();
@@ -771,10 +777,10 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true, false, false, DBL, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b,
+            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b,
                                                                acc, a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false, false, false, DBL, DBL>(a, st, r0, rows, 0, 0, r1a, r1b, acc, a.xg, a.wcur,
+            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS>(a, st, r0, rows, 0, 0, r1a, r1b, acc, a.xg, a.wcur,
                                                                 a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);

@@ -290,7 +290,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     // dynamic shared memory: the staged tiles, reused as the reduction scratch at the end
     const size_t smem = std::max<size_t>(SL::SMEM, red_scratch_bytes<K, 2>());  // persistent, fused
     const size_t smem_step = std::max<size_t>(
-        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, true>::BYTES : SL::BYTES),
+        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
     const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true>, a.ntiles, sms, smem_step)
                                        : grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem_step);

@@ -23,6 +23,9 @@ VARIANTS = {
     "u8c2": ["CHEB_NNZ_UNROLL=8", "CHEB_MIN_CTAS=2"],
     "u6c3": ["CHEB_NNZ_UNROLL=6", "CHEB_MIN_CTAS=3"],
     "u5c4": ["CHEB_NNZ_UNROLL=5", "CHEB_MIN_CTAS=4"],
+    "dbl4": ["CHEB_MIN_CTAS_DBL=4"],
+    "dblwc": ["CHEB_DBL_STAGE_WC=1"],
+    "dbl4u4": ["CHEB_MIN_CTAS_DBL=4", "CHEB_NNZ_UNROLL=4"],
 }
 
 if __name__ == "__main__":
