@@ -796,28 +796,43 @@ cheb_step_kernel(StepArgs a) {
 // Every element is computed with exactly the single-step arithmetic, in the same order, so
 // results are bit-identical to two cheb_step_kernel launches; only the schedule changes.
 // CTA c handles positions P = c + k*G (k = 0, 1, ...): stage 1 of tile P, then stage 2 of
-// tile P - D.  Stage 2 of tile u gathers w_{j+1} rows within the operator bandwidth beta of
-// u and overwrites w_j rows of u that stage 1 of tiles u-H-1..u+H+1 read (H = ceil(beta/T)+1).
-// With D = (SLACK + ceil((H+2)/G)) * G those tiles all belong to iterations <= k - SLACK, so
-// stage 2 of iteration k only needs "every CTA finished stage 1 of iteration k - SLACK": one
-// counter per iteration (release add / acquire load), prefetched one item ahead so the check
-// is normally free.  D is a multiple of G, so stage-2 tile u runs on CTA u mod G exactly like
-// the single-step kernel: the per-CTA partial dot products (hence the moments) are
-// bit-identical too.  Waits point strictly backwards in k, so with all CTAs co-resident
-// (cooperative launch) there is no deadlock.  w_{j+1} stays in L2 between the stages: per
-// 2 steps HBM sees w_{j-1}, w_j read and w_{j+1}, w_{j+2} written (4 streams instead of 6).
+// tile u = P - D.  Stage 2 of u gathers w_{j+1} rows within the operator bandwidth of u and
+// overwrites w_j rows of u that stage 1 of tiles u-H..u+H read (H = ceil(bandwidth/T) + 1
+// tiles), so it needs every stage-1 tile t <= u + H complete.
+// Completion is tracked in chunks of 32 tiles: after stage 1 of tile t a CTA release-adds 1
+// to cnt[t/32]; a waiter keeps `known` = number of leading chunks seen full and advances it
+// with one warp-wide load of the next 32 chunk counters (ballot -> first non-full chunk).
+// Those loads are issued before the preceding stage-1 tile is computed, so in steady state
+// the check costs no latency.
+// D = (SLACK + ceil((H+2)/G)) * G >= H + 2 makes every dependency sit at an earlier position
+// (deadlock-free with all CTAs co-resident: cooperative launch), and D a multiple of G keeps
+// stage-2 tile u on CTA u mod G exactly like the single-step kernel: the per-CTA partial dot
+// products (hence the moments) are bit-identical too.  With SLACK = 0, D = G: the L2 window
+// between the stages is one wave of tiles plus the halo.  w_{j+1} stays in L2 between the
+// stages: per 2 steps HBM sees w_{j-1}, w_j read and w_{j+1}, w_{j+2} written (4 vector
+// streams instead of 6).
 // ---------------------------------------------------------------------------------------
 #ifndef CHEB_FUSED_SLACK
-#define CHEB_FUSED_SLACK 1
+#define CHEB_FUSED_SLACK 0
 #endif
-constexpr int kFusedSlack = CHEB_FUSED_SLACK;  // iterations of slack between the stages
+constexpr int kFusedSlack = CHEB_FUSED_SLACK;  // extra waves of lag between the stages
+constexpr int kChunkTiles = 32;                // tiles per completion counter
+// Consumer side of the dependency: the counters are read relaxed and the gathers that follow
+// are control-dependent on them (issued only after the counts are seen), and every w_{j+1}
+// row is written exactly once before its count is released and never changes afterwards, so
+// no L1 line of it can be stale (L1 starts empty at launch; stage 1 reads A only through TMA).
+// CHEB_FUSED_FENCE=1 adds the formal fence.acq_rel.gpu (an SM-wide L1 invalidate per item).
+#ifndef CHEB_FUSED_FENCE
+#define CHEB_FUSED_FENCE 0
+#endif
 
 struct FusedArgs {
     double* A;                // in: w_{j-1}, out: w_{j+1}
     double* B;                // in: w_j,     out: w_{j+2}
-    unsigned int* wave;       // [iterations] CTAs that finished stage 1 of iteration k (zeroed)
+    unsigned int* cnt;        // [ceil(ntiles/32)] completed stage-1 tiles per chunk (zeroed)
     unsigned int* err;        // dependency-wait timeout flag
-    int64_t D;                // stage-2 lag in positions, a multiple of gridDim.x
+    int64_t D;                // stage-2 lag in positions, a multiple of gridDim.x, >= H + 2
+    int64_t H;                // halo in tiles
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
@@ -825,12 +840,21 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef CHEB_FUSED_MIN_CTAS
+#define CHEB_FUSED_MIN_CTAS CHEB_MIN_CTAS
+#endif
 template <int K>
-__global__ void __launch_bounds__(kThreads, CHEB_MIN_CTAS)
+__global__ void __launch_bounds__(kThreads, CHEB_FUSED_MIN_CTAS)
 cheb_step2_kernel(StepArgs a, FusedArgs f) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE_CSR>;
@@ -839,15 +863,15 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
     __shared__ int64_t s_base_c[2], s_base_v[2];
     __shared__ int s_fit[2];
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int64_t Gd = gridDim.x;
-    const unsigned int nctas = gridDim.x;
     double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};  // stage 1 / stage 2 moments
     double (&mu1)[1][4] = *reinterpret_cast<double(*)[1][4]>(&acc[0]);
     double (&mu2)[1][4] = *reinterpret_cast<double(*)[1][4]>(&acc[1]);
     const double2 z2 = make_double2(0.0, 0.0);
     const int64_t npos = a.ntiles + f.D;  // positions 0 .. ntiles + D - 1
     const int64_t M = blockIdx.x < npos ? 2 * ((npos - 1 - blockIdx.x) / Gd + 1) : 0;
+    const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
 
     auto item = [&](int64_t m, int& stg, int64_t& t) -> bool {
         const int64_t P = (int64_t)blockIdx.x + (m >> 1) * Gd;
@@ -888,6 +912,10 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
             if (item(m, stg, t)) return true;
         return false;
     };
+    // full count of chunk ch (the last chunk may be short); chunks past the end read as full
+    auto chunk_full = [&](int64_t ch) -> unsigned int {
+        return (unsigned int)imin64(kChunkTiles, a.ntiles - ch * kChunkTiles);
+    };
 
     int64_t m_issue = 0, ne0 = 0, ne1 = 0, nt = 0;
     int nstg = 0;
@@ -908,18 +936,13 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
     __syncthreads();
 
     int64_t q = 0;
-    int64_t waited = -1;    // thread 0: highest iteration known complete (stage 1, all CTAs)
-    int64_t peek_k = -1;    // thread 0: iteration whose counter was prefetched into peek
-    unsigned int peek = 0;
+    int64_t known = 0;       // warp 0: leading chunks known complete
+    unsigned int peek = 0;   // warp 0, per lane: prefetched counter of chunk known + lane
+    int64_t peek_base = -1;  // chunk index of lane 0's prefetched counter (-1: none)
     for (int64_t m = 0; m < M; ++m) {
         int stg;
         int64_t t;
-        if (!item(m, stg, t)) {
-            // an empty stage-1 slot (drain phase) still counts as "done" for iteration m/2
-            if (stg == 0 && tid == 0) red_release_add(f.wave + (m >> 1), 1u);
-            continue;
-        }
-        const int64_t k = m >> 1;
+        if (!item(m, stg, t)) continue;
         const int b = (int)(q & 1);
         const uint32_t phase = (uint32_t)((q >> 1) & 1);
         if (tid == 0) {
@@ -927,21 +950,34 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
             if (pending) bounds(nt, ne0, ne1);
         }
         if (stg == 1) {
-            const int64_t need = k - kFusedSlack;  // iteration whose stage 1 must be complete
-            if (tid == 0 && need > waited) {
-                unsigned int c = (peek_k == need) ? peek : 0u;
+            // stage-1 tiles [0, need) must be complete
+            const int64_t need = imin64(t + f.H + 1, a.ntiles);
+            if (tid < 32) {
                 uint32_t spins = 0;
-                while (c < nctas) {
-                    __nanosleep(64);
-                    c = ld_acquire_u32(f.wave + need);
-                    if ((++spins & 1023u) == 0 && (spins > (1u << 24) || ld_acquire_u32(f.err))) {
-                        atomicExch(f.err, 1u);  // ~seconds without progress: give up, never hang
-                        break;
+                while (known * kChunkTiles < need) {
+                    const int64_t ch = known + lane;
+                    unsigned int v;
+                    if (peek_base == known) {
+                        v = peek;
+                    } else {
+                        v = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
+                    }
+                    const bool full = ch >= nchunks || v >= chunk_full(ch);
+                    const unsigned int notfull = __ballot_sync(0xffffffffu, !full);
+                    const int adv = notfull ? __ffs(notfull) - 1 : 32;
+                    known += adv;
+                    peek_base = -1;
+                    if (adv == 0) {
+                        __nanosleep(100);
+                        if ((++spins & 1023u) == 0 && (spins > (1u << 23) || ld_acquire_u32(f.err))) {
+                            if (lane == 0) atomicExch(f.err, 1u);  // ~seconds without progress: never hang
+                            break;
+                        }
                     }
                 }
-                waited = need;
-                peek_k = need + 1;
-                peek = ld_acquire_u32(f.wave + need + 1);  // consumed at the next stage-2 item
+#if CHEB_FUSED_FENCE
+                fence_acq_rel_gpu();  // formal acquire (costs an SM-wide L1 invalidate per item)
+#endif
             }
             __syncthreads();
         }
@@ -950,6 +986,12 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (stg == 0) {
+            // prefetch the chunk counters the next stage-2 check will read (overlaps this tile)
+            if (tid < 32) {
+                const int64_t ch = known + lane;
+                peek = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
+                peek_base = known;
+            }
             if (s_fit[b])
                 step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
                                                                  mu1, f.B, f.B, f.A);
@@ -966,18 +1008,16 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
         }
         __syncthreads();  // every warp is done with stage b (and, for stage 1, with its stores)
         if (tid == 0) {
-            if (stg == 0) red_release_add(f.wave + k, 1u);  // publish: this CTA finished stage 1 of k
             if (pending) {
                 issue(nt, b, nstg ? f.B : f.A, ne0, ne1);
                 ++m_issue;
             }
+            if (stg == 0) {  // publish: stage 1 of tile t is complete (release: the CTA's stores
+                             // are ordered before it by the barrier above)
+                red_release_add(f.cnt + t / kChunkTiles, 1u);
+            }
         }
         ++q;
-    }
-    // CTAs whose stage-1 work ended early still count towards later iterations' waits
-    if (tid == 0) {
-        const int64_t iters = (npos + Gd - 1) / Gd;
-        for (int64_t k = (M >> 1); k < iters; k++) red_release_add(f.wave + k, 1u);
     }
     grid_reduce_finish<K, 4, 2, EPI_PAIR, false, true>(acc, a, smem);
 }

@@ -334,12 +334,13 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
             FusedArgs f{};
             f.A = nxt;
             f.B = (double*)cur;
-            f.wave = (unsigned int*)(ws + L.cnt);
+            f.cnt = (unsigned int*)(ws + L.cnt);
             f.err = (unsigned int*)(ws + L.misc + 8);
             f.D = fp.D;
+            f.H = fp.H;
             a.mu_col = j;
-            const int64_t iters = (a.ntiles + fp.D + grid_fused - 1) / grid_fused;
-            CL_CUDA(cudaMemsetAsync(f.wave, 0, ((size_t)iters + 4) * sizeof(unsigned int), st));
+            const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
+            CL_CUDA(cudaMemsetAsync(f.cnt, 0, ((size_t)nchunks + 1) * sizeof(unsigned int), st));
             void* args[] = {&a, &f};
             ProfScope ps(st, 1);
             CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),

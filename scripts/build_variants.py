@@ -26,6 +26,10 @@ VARIANTS = {
     "dbl4": ["CHEB_MIN_CTAS_DBL=4"],
     "dblwc": ["CHEB_DBL_STAGE_WC=1"],
     "dbl4u4": ["CHEB_MIN_CTAS_DBL=4", "CHEB_NNZ_UNROLL=4"],
+    "fc3": ["CHEB_FUSED_MIN_CTAS=3"],
+    "fc3s1": ["CHEB_FUSED_MIN_CTAS=3", "CHEB_FUSED_SLACK=1"],
+    "fs1": ["CHEB_FUSED_SLACK=1"],
+    "ffence": ["CHEB_FUSED_FENCE=1"],
 }
 
 if __name__ == "__main__":

@@ -24,7 +24,8 @@ for f in sorted(glob.glob(os.path.join(d, "sweep_*.csv"))):
         xs = m.get(k, [])
         return sum(x for x, _ in xs) / len(xs) * scale if xs else float("nan")
     units = {k: v[0][1] for k, v in m.items() if v}
-    t = avg("gpu__time_duration.sum", 1e-3 if units.get("gpu__time_duration.sum") == "us" else 1.0)
+    tu = units.get("gpu__time_duration.sum", "")
+    t = avg("gpu__time_duration.sum", {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3}.get(tu, 1.0))
     gb = sum(avg(k, 1.0 if units.get(k) == "Gbyte" else 1e-3 if units.get(k) == "Mbyte" else 1e-9)
              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     ps = re.findall(r"([\d.]+) probe-steps/s", open(f[:-4] + ".txt").read()) if os.path.exists(f[:-4] + ".txt") else []
