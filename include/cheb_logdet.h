@@ -198,16 +198,17 @@ int cheb_profile_persistent(double *ms, int64_t *launches);
  * Moments are bit-identical to per-step launches when both use the same grid size. */
 int cheb_set_persistent(int32_t mode);
 
-/* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 1 -- the fused
- * kernel is correct and bit-identical but not yet faster on B200):
+/* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 1, see DESIGN.md §7
+ * for the measured status):
  *   1 = one launch per Chebyshev step;
  *   2 = auto: pairs of steps (w_{j+1}, w_{j+2}) in one cooperative launch when the
  *       operator's bandwidth max|i - col| is small enough for the two-step wavefront to
- *       stay in L2 and the matrix has enough row tiles to fill the pipeline;
- *   3 = always fuse pairs (testing; correct for any bandwidth, slow when it is large).
- * Results are bit-identical across modes; only the schedule changes.  With modes 2/3,
- * cheb_moments synchronises its stream once after the operator prep (to read the
- * bandwidth).  CL_EINVAL for other values. */
+ *       stay in L2 and the matrix has enough row tiles to fill the pipeline; tiles are
+ *       handed out by dynamic tickets (moments deterministic only up to rounding order);
+ *   3 = always fuse pairs, dynamic tickets (testing; correct for any bandwidth);
+ *   4 = always fuse pairs, static tile->CTA map: moments bit-identical to mode 1.
+ * With modes 2-4, cheb_moments synchronises its stream once after the operator prep (to
+ * read the bandwidth).  CL_EINVAL for other values. */
 int cheb_set_fusion(int32_t steps);
 
 /* Moment-doubling schedule for cheb_moments / cheb_logdet / cheb_logdet_host (process-wide;

@@ -330,7 +330,8 @@ def get_doubling() -> bool:
 
 
 def set_fusion(steps: int):
-    """Temporal fusion for CSR operators: 1 (off), 2 (auto, default), 3 (always fuse pairs)."""
+    """Temporal fusion for CSR operators: 1 (off, default), 2 (auto), 3 (always fuse pairs,
+    dynamic tile tickets), 4 (always fuse pairs, static tile map: bit-identical to 1)."""
     check(_lib.load().cheb_set_fusion(int(steps)))
 
 

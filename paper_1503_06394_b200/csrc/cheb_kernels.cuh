@@ -66,15 +66,28 @@ enum { MODE_CSR = 0, MODE_RANK1 = 1, MODE_BTB = 2 };
 
 __host__ __device__ constexpr int words_for(int K) { return K >= 32 ? K / 32 : 1; }
 
-// Geometry of the step / spmm kernels: each lane owns PPL = 4 consecutive probes
-// (two 16-byte double2), L = K/4 lanes own a row; RPG rows per group per tile.
+// Probes per lane of the step kernels: PPL/2 16-byte slots per gathered row (4: two slots, the
+// probes {2l, 2l+1, K/2+2l, K/2+2l+1}; 8: four slots at stride K/4).  More probes per lane
+// amortise the per-nonzero index work (column/value reads, address math) over more DFMAs.
+#ifndef CHEB_PPL
+#define CHEB_PPL 4
+#endif
+constexpr int kPPL = CHEB_PPL;
+static_assert(kPPL == 4 || kPPL == 8, "CHEB_PPL must be 4 or 8");
+
+// Geometry of the step / spmm kernels: each lane owns PPL probes in PPL/2 slots of two
+// consecutive probes, L = K/PPL lanes own a row; RPG rows per group per tile.  The tile
+// (rows) does not depend on PPL.
 template <int K>
 struct Geo {
     static_assert(K == 8 || K == 16 || K == 32 || K == 64 || K == 128, "K in {8,...,128}");
-    static constexpr int PPL = 4;
-    static constexpr int L = K / PPL;               // lanes per row: 2..32
+    static constexpr int PPL = kPPL;
+    static constexpr int NSL = PPL / 2;             // 16-byte slots per lane and row
+    static constexpr int SS = K / NSL;              // probe stride between a lane's slots
+    static constexpr int L = K / PPL;               // lanes per row: 1..32
     static constexpr int GROUPS = kThreads / L;     // rows in flight per CTA
-    static constexpr int RPG = CHEB_RPG;            // rows per group per tile
+    static constexpr int RPG = CHEB_RPG * 4 / PPL;  // rows per group per tile
+    static_assert(RPG >= 1, "CHEB_RPG too small for CHEB_PPL");
     static constexpr int TILE = GROUPS * RPG;       // rows per tile: 256 .. 16
     static constexpr int WORDS = words_for(K);
     static constexpr int CAP = TILE * 8;            // staged nnz capacity (avg 8 per row)
@@ -90,6 +103,13 @@ struct Geo {
 
 // WC: the tile's own W_cur rows are staged too (always for BTB; the per-step moment-doubling
 // kernel needs w_{j-1}[i] for its w_j^T w_{j-1} dot).
+// spmm_kernel: 4 probes per lane in two slots {2l, 2l+1, K/2+2l, K/2+2l+1}, K/4 lanes per row
+template <int K>
+struct SpmmGeo {
+    static constexpr int L = K / 4;
+    static constexpr int GROUPS = kThreads / L;
+};
+
 template <int K, int MODE, bool WC = false>
 struct StageLayout {
     using G = Geo<K>;
@@ -294,11 +314,11 @@ __device__ __forceinline__ double reduce_partials_one(const double* part, int K,
 }
 
 // Lane lg of a row group owns probes probe_of<K,PPL,SPLIT>(lg, q), q < PPL: contiguous
-// (pl = PPL*lg + q) or, with SPLIT (PPL = 4), two pairs from the two halves of the row
-// {2lg, 2lg+1, K/2+2lg, K/2+2lg+1} so that every 16-byte access of a warp is contiguous.
+// (pl = PPL*lg + q) or, with SPLIT, PPL/2 pairs at stride K/(PPL/2): {2lg, 2lg+1} + s*K/(PPL/2)
+// (PPL = 4: {2lg, 2lg+1, K/2+2lg, K/2+2lg+1}) so that every 16-byte access of a warp is contiguous.
 template <int K, int PPL, bool SPLIT>
 __device__ __forceinline__ int probe_of(int lg, int q) {
-    return SPLIT ? 2 * lg + (q & 1) + (q >> 1) * (K / 2) : PPL * lg + q;
+    return SPLIT ? 2 * lg + (q & 1) + (q >> 1) * (K / (PPL / 2)) : PPL * lg + q;
 }
 
 // Epilogues of the last CTA:
@@ -525,18 +545,21 @@ __host__ __device__ constexpr int n_channels() { return (DBL ? 2 : 1) + (MODE ==
 template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false, bool DBL = false,
           bool WCS = false>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
-                                          int64_t base_c, int64_t base_v, double2 r1a, double2 r1b,
-                                          double (&acc)[n_channels<MODE, DBL>()][4], const double* xg,
+                                          int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
+                                          double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
                                           const double* wcur, double* wout) {
     using G = Geo<K>;
     using SL = StageLayout<K, MODE, WCS>;
+    constexpr int NSL = G::NSL;
     constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
     constexpr bool OWN_EARLY = DBL && !OWN_SMEM;   // else: loaded at the row start (L1/L2-hot)
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int SCH = n_channels<MODE, DBL>() - 1;  // rank-1 channel
     const int lg = threadIdx.x % G::L;
     const int grp = threadIdx.x / G::L;
-    const int pa = 2 * lg, pb = K / 2 + 2 * lg;  // probe pairs (first / second half of the row)
+    int pp[NSL];  // first probe of each slot: {2lg, 2lg+1} + s*SS
+#pragma unroll
+    for (int sl = 0; sl < NSL; sl++) pp[sl] = 2 * lg + sl * G::SS;
     const int64_t* rp_s = reinterpret_cast<const int64_t*>(st + SL::OFF_RP);
     const int32_t* col_s = reinterpret_cast<const int32_t*>(st + SL::OFF_COL);
     const double* val_s = reinterpret_cast<const double*>(st + SL::OFF_VAL);
@@ -557,11 +580,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         const int nr = (int)(e_hi - e_lo);
         const int oc = STAGED ? (int)(e_lo - base_c) : 0;
         const int ov = STAGED ? (int)(e_lo - base_v) : 0;
-        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-        double2 own0 = make_double2(0.0, 0.0), own1 = make_double2(0.0, 0.0);  // w_{j-1}[i]
-        if (OWN_EARLY) {  // issued before the gathers so its latency overlaps them
-            own0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
-            own1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
+        const double* wrow = wcur + (size_t)i * K;
+        double2 g[NSL], own[NSL];  // gathered sum (Ã w_{j-1} row i), w_{j-1}[i]
+#pragma unroll
+        for (int sl = 0; sl < NSL; sl++) {
+            g[sl] = make_double2(0.0, 0.0);
+            own[sl] = make_double2(0.0, 0.0);
+            if (OWN_EARLY)  // issued before the gathers so its latency overlaps them
+                own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
         }
         // all nnz of a chunk issue their gathers before any is consumed; entries past the row
         // end gather the row's first column again (a valid, cache-hot address) with value 0
@@ -579,105 +605,89 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                 const double vv = STAGED ? val_s[ov + t] : __ldg(a.va + e_lo + t);
                 v[q] = in ? vv : 0.0;
             }
-            double2 x0[CHEB_NNZ_UNROLL], x1[CHEB_NNZ_UNROLL];
+            double2 x[CHEB_NNZ_UNROLL][NSL];
 #pragma unroll
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
                 const double* p = xg + (size_t)(uint32_t)c[q] * K;
-                if (KEEP && CHEB_FUSED_HINTS) {
-                    const uint64_t pol = policy_evict_last();
-                    x0[q] = ldnc2_hint(p + pa, pol);
-                    x1[q] = ldnc2_hint(p + pb, pol);
-                } else {
-                    x0[q] = CG ? ldcg2(p + pa) : ldg2(p + pa);
-                    x1[q] = CG ? ldcg2(p + pb) : ldg2(p + pb);
+#pragma unroll
+                for (int sl = 0; sl < NSL; sl++) {
+                    if (KEEP && CHEB_FUSED_HINTS)
+                        x[q][sl] = ldnc2_hint(p + pp[sl], policy_evict_last());
+                    else
+                        x[q][sl] = CG ? ldcg2(p + pp[sl]) : ldg2(p + pp[sl]);
                 }
             }
 #pragma unroll
-            for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                acc0.x = fma(v[q], x0[q].x, acc0.x);
-                acc0.y = fma(v[q], x0[q].y, acc0.y);
-                acc1.x = fma(v[q], x1[q].x, acc1.x);
-                acc1.y = fma(v[q], x1[q].y, acc1.y);
-            }
+            for (int q = 0; q < CHEB_NNZ_UNROLL; q++)
+#pragma unroll
+                for (int sl = 0; sl < NSL; sl++) {
+                    g[sl].x = fma(v[q], x[q][sl].x, g[sl].x);
+                    g[sl].y = fma(v[q], x[q][sl].y, g[sl].y);
+                }
         }
         // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
         if (OWN_SMEM) {
-            own0 = *reinterpret_cast<const double2*>(wc_s + lr * K + pa);
-            own1 = *reinterpret_cast<const double2*>(wc_s + lr * K + pb);
+#pragma unroll
+            for (int sl = 0; sl < NSL; sl++) own[sl] = *reinterpret_cast<const double2*>(wc_s + lr * K + pp[sl]);
         }
-        if (MODE == MODE_BTB) {
-            acc0.x = fma(-a.beta, own0.x, acc0.x);
-            acc0.y = fma(-a.beta, own0.y, acc0.y);
-            acc1.x = fma(-a.beta, own1.x, acc1.x);
-            acc1.y = fma(-a.beta, own1.y, acc1.y);
-        } else if ((ndw >> (i & 31)) & 1u) {
-            if (!OWN_SMEM && !OWN_EARLY) {
-                own0 = CG ? ldcg2(wcur + (size_t)i * K + pa) : ldg2(wcur + (size_t)i * K + pa);
-                own1 = CG ? ldcg2(wcur + (size_t)i * K + pb) : ldg2(wcur + (size_t)i * K + pb);
+        if (MODE == MODE_BTB || ((ndw >> (i & 31)) & 1u)) {
+#pragma unroll
+            for (int sl = 0; sl < NSL; sl++) {
+                if (MODE != MODE_BTB && !OWN_SMEM && !OWN_EARLY)
+                    own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
+                g[sl].x = fma(-a.beta, own[sl].x, g[sl].x);
+                g[sl].y = fma(-a.beta, own[sl].y, g[sl].y);
             }
-            acc0.x = fma(-a.beta, own0.x, acc0.x);
-            acc0.y = fma(-a.beta, own0.y, acc0.y);
-            acc1.x = fma(-a.beta, own1.x, acc1.x);
-            acc1.y = fma(-a.beta, own1.y, acc1.y);
         }
         double ui = 1.0;
         if (HAS_S) {
             ui = a.r1u ? u_s[lr] : 1.0;
-            acc0.x = fma(ui, r1a.x, acc0.x);
-            acc0.y = fma(ui, r1a.y, acc0.y);
-            acc1.x = fma(ui, r1b.x, acc1.x);
-            acc1.y = fma(ui, r1b.y, acc1.y);
+#pragma unroll
+            for (int sl = 0; sl < NSL; sl++) {
+                g[sl].x = fma(ui, r1[sl].x, g[sl].x);
+                g[sl].y = fma(ui, r1[sl].y, g[sl].y);
+            }
         }
-        double2 n0, n1;
-        if (FIRST) {
-            n0 = acc0;
-            n1 = acc1;
-        } else {
-            const double2 p0 = *reinterpret_cast<const double2*>(wp_s + lr * K + pa);
-            const double2 p1 = *reinterpret_cast<const double2*>(wp_s + lr * K + pb);
-            n0 = make_double2(2.0 * acc0.x - p0.x, 2.0 * acc0.y - p0.y);
-            n1 = make_double2(2.0 * acc1.x - p1.x, 2.0 * acc1.y - p1.y);
+        double2 nw[NSL];  // w_j row i
+#pragma unroll
+        for (int sl = 0; sl < NSL; sl++) {
+            if (FIRST) {
+                nw[sl] = g[sl];
+            } else {
+                const double2 pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
+                nw[sl] = make_double2(2.0 * g[sl].x - pv.x, 2.0 * g[sl].y - pv.y);
+            }
         }
         double* out = wout + (size_t)i * K;
-        if (KEEP) {  // re-read from L2 later in the same launch (fused kernel, stage 1)
-            if (CHEB_FUSED_HINTS) {
-                const uint64_t pol = policy_evict_last();
-                st2_hint(out + pa, n0, pol);
-                st2_hint(out + pb, n1, pol);
-            } else {
-                *reinterpret_cast<double2*>(out + pa) = n0;
-                *reinterpret_cast<double2*>(out + pb) = n1;
+#pragma unroll
+        for (int sl = 0; sl < NSL; sl++) {
+            if (KEEP) {  // re-read from L2 later in the same launch (fused kernel, stage 1)
+                if (CHEB_FUSED_HINTS)
+                    st2_hint(out + pp[sl], nw[sl], policy_evict_last());
+                else
+                    *reinterpret_cast<double2*>(out + pp[sl]) = nw[sl];
+            } else {     // streamed: next read is by a later launch
+                __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw[sl]);
             }
-        } else {     // streamed: next read is by a later launch
-            __stcs(reinterpret_cast<double2*>(out + pa), n0);
-            __stcs(reinterpret_cast<double2*>(out + pb), n1);
         }
-        if (DBL) {
-            // w_j^T w_j and w_{j-1}^T w_j over this CTA's rows (w_{j-1} row i: staged, or
-            // captured from the diagonal's gather / loaded for rows without one)
-            const double2 c0 = own0, c1 = own1;
-            acc[0][0] = fma(n0.x, n0.x, acc[0][0]);
-            acc[0][1] = fma(n0.y, n0.y, acc[0][1]);
-            acc[0][2] = fma(n1.x, n1.x, acc[0][2]);
-            acc[0][3] = fma(n1.y, n1.y, acc[0][3]);
-            acc[1][0] = fma(c0.x, n0.x, acc[1][0]);
-            acc[1][1] = fma(c0.y, n0.y, acc[1][1]);
-            acc[1][2] = fma(c1.x, n1.x, acc[1][2]);
-            acc[1][3] = fma(c1.y, n1.y, acc[1][3]);
-        } else {
-            // v_p[i] w_j[i][p]: flip the sign bit of w where the probe bit is set
-            const uint32_t ba = sg_s[lr * G::WORDS + (pa >> 5)] >> (pa & 31);
-            const uint32_t bb = sg_s[lr * G::WORDS + (pb >> 5)] >> (pb & 31);
-            acc[0][0] += signflip(n0.x, ba << 31);
-            acc[0][1] += signflip(n0.y, ba << 30);
-            acc[0][2] += signflip(n1.x, bb << 31);
-            acc[0][3] += signflip(n1.y, bb << 30);
-        }
-        if (HAS_S) {
-            acc[SCH][0] = fma(ui, n0.x, acc[SCH][0]);
-            acc[SCH][1] = fma(ui, n0.y, acc[SCH][1]);
-            acc[SCH][2] = fma(ui, n1.x, acc[SCH][2]);
-            acc[SCH][3] = fma(ui, n1.y, acc[SCH][3]);
+#pragma unroll
+        for (int sl = 0; sl < NSL; sl++) {
+            if (DBL) {
+                // w_j^T w_j and w_{j-1}^T w_j over this CTA's rows
+                acc[0][2 * sl] = fma(nw[sl].x, nw[sl].x, acc[0][2 * sl]);
+                acc[0][2 * sl + 1] = fma(nw[sl].y, nw[sl].y, acc[0][2 * sl + 1]);
+                acc[1][2 * sl] = fma(own[sl].x, nw[sl].x, acc[1][2 * sl]);
+                acc[1][2 * sl + 1] = fma(own[sl].y, nw[sl].y, acc[1][2 * sl + 1]);
+            } else {
+                // v_p[i] w_j[i][p]: flip the sign bit of w where the probe bit is set
+                const uint32_t bits = sg_s[lr * G::WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
+                acc[0][2 * sl] += signflip(nw[sl].x, bits << 31);
+                acc[0][2 * sl + 1] += signflip(nw[sl].y, bits << 30);
+            }
+            if (HAS_S) {
+                acc[SCH][2 * sl] = fma(ui, nw[sl].x, acc[SCH][2 * sl]);
+                acc[SCH][2 * sl + 1] = fma(ui, nw[sl].y, acc[SCH][2 * sl + 1]);
+            }
         }
     }
 }
@@ -704,16 +714,16 @@ cheb_step_kernel(StepArgs a) {
     __shared__ int s_fit[NS];
 
     const int tid = threadIdx.x;
-    const int pa = 2 * (tid % G::L), pb = K / 2 + pa;
-    double acc[NCH][4];
+    double acc[NCH][kPPL];
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc[ch][q] = 0.0;
-    double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
-    if (HAS_S) {
-        r1a = make_double2(a.r1c_alpha * a.s_cur[pa], a.r1c_alpha * a.s_cur[pa + 1]);
-        r1b = make_double2(a.r1c_alpha * a.s_cur[pb], a.r1c_alpha * a.s_cur[pb + 1]);
+        for (int q = 0; q < kPPL; q++) acc[ch][q] = 0.0;
+    double2 r1[G::NSL];  // alpha c s_{j-1}[p] of the lane's probes (rank-1)
+#pragma unroll
+    for (int sl = 0; sl < G::NSL; sl++) {
+        const int p = 2 * (tid % G::L) + sl * G::SS;
+        r1[sl] = HAS_S ? make_double2(a.r1c_alpha * a.s_cur[p], a.r1c_alpha * a.s_cur[p + 1]) : make_double2(0.0, 0.0);
     }
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -777,15 +787,15 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a, r1b,
+            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                acc, a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS>(a, st, r0, rows, 0, 0, r1a, r1b, acc, a.xg, a.wcur,
+            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
                                                                 a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);
     }
-    grid_reduce_finish<K, 4, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, true>(acc, a, smem);
+    grid_reduce_finish<K, kPPL, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, true>(acc, a, smem);
 }
 
 
@@ -865,10 +875,14 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t Gd = gridDim.x;
-    double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};  // stage 1 / stage 2 moments
-    double (&mu1)[1][4] = *reinterpret_cast<double(*)[1][4]>(&acc[0]);
-    double (&mu2)[1][4] = *reinterpret_cast<double(*)[1][4]>(&acc[1]);
-    const double2 z2 = make_double2(0.0, 0.0);
+    double acc[2][kPPL];  // stage 1 / stage 2 moments
+#pragma unroll
+    for (int q = 0; q < kPPL; q++) acc[0][q] = acc[1][q] = 0.0;
+    double (&mu1)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[0]);
+    double (&mu2)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[1]);
+    double2 z2[G::NSL];
+#pragma unroll
+    for (int sl = 0; sl < G::NSL; sl++) z2[sl] = make_double2(0.0, 0.0);
     const int64_t npos = a.ntiles + f.D;  // positions 0 .. ntiles + D - 1
     const int64_t M = blockIdx.x < npos ? 2 * ((npos - 1 - blockIdx.x) / Gd + 1) : 0;
     const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
@@ -993,17 +1007,17 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
                 peek_base = known;
             }
             if (s_fit[b])
-                step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
+                step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
                                                                  mu1, f.B, f.B, f.A);
             else
-                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, z2, mu1, f.B,
+                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, mu1, f.B,
                                                                   f.B, f.A);
         } else {
             if (s_fit[b])
-                step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2, z2,
+                step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
                                                                  mu2, f.A, f.A, f.B);
             else
-                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, z2, mu2, f.A,
+                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, mu2, f.A,
                                                                   f.A, f.B);
         }
         __syncthreads();  // every warp is done with stage b (and, for stage 1, with its stores)
@@ -1019,9 +1033,192 @@ cheb_step2_kernel(StepArgs a, FusedArgs f) {
         }
         ++q;
     }
-    grid_reduce_finish<K, 4, 2, EPI_PAIR, false, true>(acc, a, smem);
+    grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
 }
 
+
+// ---------------------------------------------------------------------------------------
+// K2x2d: temporally fused pair with DYNAMIC tile tickets.  Same two stages as cheb_step2_kernel,
+// but tiles are handed out by two global counters instead of a static tile -> CTA map, so a slow
+// CTA delays only the one tile it holds (no accumulated skew):
+//   * a CTA takes a stage-1 ticket t1 = c1++; if t1 >= D it then takes one stage-2 ticket
+//     u = c2++ (alternating); once c1 is exhausted it drains stage-2 tickets;
+//   * every stage-2 ticket u taken this way satisfies u + D < c1, so the stage-1 tiles it needs
+//     (<= u + H < u + D) have all been handed out, and stage-1 work never waits;
+//   * a CTA's own pending stage-1 ticket is always > its current stage-2 need, and a wait chain
+//     X -> Y implies u_X > u_Y: no cycle, deadlock-free with all CTAs co-resident.
+// Tickets are taken when the TMA staging of the item is issued (two items ahead).
+// Moments: per-CTA partial sums as in the other kernels, but which tiles a CTA sums now depends
+// on the run, so the rounding of mu is run-dependent (still within the parity tolerances).
+// ---------------------------------------------------------------------------------------
+struct FusedDynArgs {
+    unsigned int* c1;         // stage-1 ticket counter (zeroed)
+    unsigned int* c2;         // stage-2 ticket counter (zeroed)
+};
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, CHEB_FUSED_MIN_CTAS)
+cheb_step2d_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
+    using G = Geo<K>;
+    using SL = StageLayout<K, MODE_CSR>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int64_t s_base_c[2], s_base_v[2];
+    __shared__ int s_fit[2];
+    __shared__ int64_t s_t[2];   // tile of the item staged in buffer b (-1: no more items)
+    __shared__ int s_stg[2];     // its stage
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    double acc[2][kPPL];  // stage 1 / stage 2 moments
+#pragma unroll
+    for (int q = 0; q < kPPL; q++) acc[0][q] = acc[1][q] = 0.0;
+    double (&mu1)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[0]);
+    double (&mu2)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[1]);
+    double2 z2[G::NSL];
+#pragma unroll
+    for (int sl = 0; sl < G::NSL; sl++) z2[sl] = make_double2(0.0, 0.0);
+    const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
+    const unsigned int ntl = (unsigned int)a.ntiles;
+
+    auto issue = [&](int64_t t, int b, const double* wsrc, int64_t e0, int64_t e1) {
+        unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
+        const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+        const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
+        s_fit[b] = fit;
+        s_base_c[b] = c0;
+        s_base_v[b] = v0;
+        const uint32_t wbytes = (uint32_t)rows * K * 8;
+        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+        uint32_t bytes = G::RPBYTES + sgbytes + wbytes;
+        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+        mbar_expect_tx(&bar[b], bytes);
+        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
+        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        bulk_g2s_hint(st + SL::OFF_WPREV, wsrc + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
+        if (fit) {
+            bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
+            bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
+        }
+    };
+    // thread 0: ticket policy (see above)
+    bool want2 = false, done1 = false, done2 = false;
+    auto take = [&](int& stg, int64_t& t) -> bool {
+        if (want2 || done1) {
+            want2 = false;
+            if (!done2) {
+                const unsigned int u = atomicAdd(dy.c2, 1u);
+                if (u < ntl) {
+                    stg = 1;
+                    t = u;
+                    return true;
+                }
+                done2 = true;
+            }
+        }
+        if (!done1) {
+            const unsigned int t1 = atomicAdd(dy.c1, 1u);
+            if (t1 < ntl) {
+                stg = 0;
+                t = t1;
+                want2 = (int64_t)t1 >= f.D;
+                return true;
+            }
+            done1 = true;
+        }
+        if (!done2) {
+            const unsigned int u = atomicAdd(dy.c2, 1u);
+            if (u < ntl) {
+                stg = 1;
+                t = u;
+                return true;
+            }
+            done2 = true;
+        }
+        return false;
+    };
+    auto stage_next = [&](int b) {  // thread 0: take the next item and stage it into buffer b
+        int stg;
+        int64_t t;
+        if (take(stg, t)) {
+            s_t[b] = t;
+            s_stg[b] = stg;
+            const int64_t r0 = t * G::TILE;
+            issue(t, b, stg ? f.B : f.A, __ldg(a.rp + r0), __ldg(a.rp + imin64(r0 + G::TILE, a.d)));
+        } else {
+            s_t[b] = -1;
+        }
+    };
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        stage_next(0);
+        stage_next(1);
+    }
+    __syncthreads();
+
+    int64_t known = 0;       // warp 0: leading chunks known complete
+    for (int64_t q = 0;; ++q) {
+        const int b = (int)(q & 1);
+        const uint32_t phase = (uint32_t)((q >> 1) & 1);
+        const int64_t t = s_t[b];
+        if (t < 0) break;
+        const int stg = s_stg[b];
+        if (stg == 1) {
+            const int64_t need = imin64(t + f.H + 1, a.ntiles);  // stage-1 tiles [0, need) complete
+            if (tid < 32) {
+                uint32_t spins = 0;
+                while (known * kChunkTiles < need) {
+                    const int64_t ch = known + lane;
+                    const unsigned int v = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
+                    const bool full = ch >= nchunks || v >= (unsigned int)imin64(kChunkTiles, a.ntiles - ch * kChunkTiles);
+                    const unsigned int notfull = __ballot_sync(0xffffffffu, !full);
+                    const int adv = notfull ? __ffs(notfull) - 1 : 32;
+                    known += adv;
+                    if (adv == 0) {
+                        __nanosleep(64);
+                        if ((++spins & 1023u) == 0 && (spins > (1u << 23) || ld_acquire_u32(f.err))) {
+                            if (lane == 0) atomicExch(f.err, 1u);  // ~seconds without progress: never hang
+                            break;
+                        }
+                    }
+                }
+#if CHEB_FUSED_FENCE
+                fence_acq_rel_gpu();
+#endif
+            }
+            __syncthreads();
+        }
+        mbar_wait(&bar[b], phase);
+        const unsigned char* st = smem + b * SL::BYTES;
+        const int64_t r0 = t * G::TILE;
+        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+        if (stg == 0) {
+            if (s_fit[b])
+                step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
+                                                                 mu1, f.B, f.B, f.A);
+            else
+                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, mu1, f.B, f.B, f.A);
+        } else {
+            if (s_fit[b])
+                step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
+                                                                 mu2, f.A, f.A, f.B);
+            else
+                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, mu2, f.A, f.A, f.B);
+        }
+        __syncthreads();  // every warp is done with buffer b (and, for stage 1, with its stores)
+        if (tid == 0) {
+            if (stg == 0) red_release_add(f.cnt + t / kChunkTiles, 1u);  // publish stage 1 of t
+            stage_next(b);
+        }
+        __syncthreads();  // s_t[b] / s_stg[b] of the next use of b are visible
+    }
+    grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
+}
 
 // ---------------------------------------------------------------------------------------
 // K2p: persistent multi-step kernel for small / L2-resident operators (csr, rank-1).
@@ -1076,7 +1273,6 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = tid % G::L;
-    const int pa = 2 * lg, pb = K / 2 + pa;
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     uint32_t uses[2] = {0u, 0u};
 
@@ -1125,16 +1321,17 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         const bool first = (j == 1) || pa_.power;
         const double* cur = (j & 1) ? pa_.w0 : pa_.w1;  // w_{j-1}
         double* nxt = (j & 1) ? pa_.w1 : pa_.w0;        // w_{j-2} -> w_j
-        double2 r1a = make_double2(0.0, 0.0), r1b = make_double2(0.0, 0.0);
-        if (HAS_S) {
-            r1a = make_double2(a.r1c_alpha * s_sh[pa], a.r1c_alpha * s_sh[pa + 1]);
-            r1b = make_double2(a.r1c_alpha * s_sh[pb], a.r1c_alpha * s_sh[pb + 1]);
+        double2 r1[G::NSL];
+#pragma unroll
+        for (int sl = 0; sl < G::NSL; sl++) {
+            const int p = 2 * lg + sl * G::SS;
+            r1[sl] = HAS_S ? make_double2(a.r1c_alpha * s_sh[p], a.r1c_alpha * s_sh[p + 1]) : make_double2(0.0, 0.0);
         }
-        double acc[NCH][4];
+        double acc[NCH][kPPL];
 #pragma unroll
         for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
-            for (int q = 0; q < 4; q++) acc[ch][q] = 0.0;
+            for (int q = 0; q < kPPL; q++) acc[ch][q] = 0.0;
         for (int64_t it = 0; it < nmine; it++) {
             const int b = (int)(it & 1);
             mbar_wait(&bar[b], uses[b] & 1u);
@@ -1145,17 +1342,17 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
             if (first) {
                 if (s_fit[b])
-                    step_tile<K, MODE, true, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a,
-                                                                     r1b, acc, cur, cur, nxt);
+                    step_tile<K, MODE, true, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+                                                                     acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, true, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1a, r1b, acc, cur, cur,
+                    step_tile<K, MODE, true, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
                                                                       nxt);
             } else {
                 if (s_fit[b])
-                    step_tile<K, MODE, false, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1a,
-                                                                      r1b, acc, cur, cur, nxt);
+                    step_tile<K, MODE, false, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+                                                                      acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, false, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1a, r1b, acc, cur, cur,
+                    step_tile<K, MODE, false, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
                                                                        nxt);
             }
             __syncthreads();
@@ -1167,12 +1364,12 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
 #pragma unroll
             for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
-                for (int q = 0; q < 4; q++) acc[ch][q] += __shfl_xor_sync(0xffffffffu, acc[ch][q], off);
+                for (int q = 0; q < kPPL; q++) acc[ch][q] += __shfl_xor_sync(0xffffffffu, acc[ch][q], off);
         }
         if (lane < G::L) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const int p = probe_of<K, 4, true>(lg, q);
+            for (int q = 0; q < kPPL; q++) {
+                const int p = probe_of<K, kPPL, true>(lg, q);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ch++) red[ch][warp][p] = acc[ch][q];
             }
@@ -1242,7 +1439,7 @@ template <int K>
 __global__ void __launch_bounds__(kThreads, CHEB_MIN_CTAS)
 spmm_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ va, const double* __restrict__ x, double* __restrict__ y) {
-    using G = Geo<K>;
+    using G = SpmmGeo<K>;
     const int lg = threadIdx.x % G::L;
     const int grp = threadIdx.x / G::L;
     const int pa = 2 * lg, pb = K / 2 + 2 * lg;

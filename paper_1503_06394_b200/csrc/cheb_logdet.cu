@@ -59,7 +59,7 @@ int env_int(const char* name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 // schedule controls (process-wide; CHEB_FUSION / CHEB_PERSISTENT env vars set the initial value)
-std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};          // 1 off (default), 2 auto, 3 forced
+std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};  // 1 off (default), 2 auto, 3 forced, 4 forced static
 std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
 std::atomic<int> g_doubling{env_int("CHEB_DOUBLING", 0)};      // 0 off (default), 1 moment doubling
 
@@ -232,6 +232,20 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
     g_launches++;
 }
 
+// Fused pairs with dynamic tile tickets (cheb_step2d_kernel) instead of the static map
+// (CHEB_FUSED_DYN, default 1).
+bool fused_dynamic() { return g_fusion.load() != 4; }
+// Dynamic lag beyond the halo, in units of the grid size (CHEB_FUSED_LAG, default 1.0): the
+// stage-1 tiles a stage-2 ticket needs were handed out D - H tiles earlier; up to G of them can
+// still be in flight.
+double fused_lag_waves() {
+    static double v = [] {
+        const char* e = getenv("CHEB_FUSED_LAG");
+        return e ? atof(e) : 1.0;
+    }();
+    return v;
+}
+
 // Temporal fusion plan (CSR mode): stage-2 halo H (tiles) and lag D (positions).
 struct FusionPlan {
     bool on = false;          // temporally fused pairs
@@ -298,7 +312,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
                                       : grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem_step);
     int grid_spmm = 1;
     if (MODE == MODE_BTB) {
-        const int64_t ng = (op->A.n_rows + G::GROUPS - 1) / G::GROUPS;
+        const int64_t ng = (op->A.n_rows + SpmmGeo<K>::GROUPS - 1) / SpmmGeo<K>::GROUPS;
         grid_spmm = grid_for(spmm_kernel<K>, ng, sms);
     }
     // moment doubling (reading G25): steps j = 1..ceil(n/2); the epilogue of step j writes
@@ -341,10 +355,20 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
             a.mu_col = j;
             const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
             CL_CUDA(cudaMemsetAsync(f.cnt, 0, ((size_t)nchunks + 1) * sizeof(unsigned int), st));
-            void* args[] = {&a, &f};
             ProfScope ps(st, 1);
-            CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),
-                                                dim3(kThreads), args, smem, st));
+            if (fused_dynamic()) {
+                FusedDynArgs dy{};
+                dy.c1 = (unsigned int*)(ws + L.misc + 32);
+                dy.c2 = (unsigned int*)(ws + L.misc + 36);
+                CL_CUDA(cudaMemsetAsync(ws + L.misc + 32, 0, 8, st));
+                void* args[] = {&a, &f, &dy};
+                CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2d_kernel<K>, dim3(grid_fused),
+                                                    dim3(kThreads), args, smem, st));
+            } else {
+                void* args[] = {&a, &f};
+                CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),
+                                                    dim3(kThreads), args, smem, st));
+            }
             g_launches++;
             j++;  // consumed two steps
             continue;
@@ -400,18 +424,21 @@ void prep_mode(const cl_operator* op, double alpha, double beta, char* ws, const
 }
 
 int fused_occupancy(int k) {
+    // both fused kernels (static map / dynamic tickets) run with the same shared memory; a
+    // cooperative grid must fit the smaller occupancy
     auto occ_of = [](auto kern, size_t smem) {
         int occ = 0;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
         return occ < 1 ? 1 : (occ > kMaxCtasPerSm ? kMaxCtasPerSm : occ);
     };
+    auto both = [&](auto ks, auto kd, size_t smem) { return std::min(occ_of(ks, smem), occ_of(kd, smem)); };
     switch (k) {
-        case 8: return occ_of(cheb_step2_kernel<8>, std::max<size_t>(StageLayout<8, MODE_CSR>::SMEM, red_scratch_bytes<8, 2>()));
-        case 16: return occ_of(cheb_step2_kernel<16>, std::max<size_t>(StageLayout<16, MODE_CSR>::SMEM, red_scratch_bytes<16, 2>()));
-        case 32: return occ_of(cheb_step2_kernel<32>, std::max<size_t>(StageLayout<32, MODE_CSR>::SMEM, red_scratch_bytes<32, 2>()));
-        case 64: return occ_of(cheb_step2_kernel<64>, std::max<size_t>(StageLayout<64, MODE_CSR>::SMEM, red_scratch_bytes<64, 2>()));
-        default: return occ_of(cheb_step2_kernel<128>, std::max<size_t>(StageLayout<128, MODE_CSR>::SMEM, red_scratch_bytes<128, 2>()));
+        case 8: return both(cheb_step2_kernel<8>, cheb_step2d_kernel<8>, std::max<size_t>(StageLayout<8, MODE_CSR>::SMEM, red_scratch_bytes<8, 2>()));
+        case 16: return both(cheb_step2_kernel<16>, cheb_step2d_kernel<16>, std::max<size_t>(StageLayout<16, MODE_CSR>::SMEM, red_scratch_bytes<16, 2>()));
+        case 32: return both(cheb_step2_kernel<32>, cheb_step2d_kernel<32>, std::max<size_t>(StageLayout<32, MODE_CSR>::SMEM, red_scratch_bytes<32, 2>()));
+        case 64: return both(cheb_step2_kernel<64>, cheb_step2d_kernel<64>, std::max<size_t>(StageLayout<64, MODE_CSR>::SMEM, red_scratch_bytes<64, 2>()));
+        default: return both(cheb_step2_kernel<128>, cheb_step2d_kernel<128>, std::max<size_t>(StageLayout<128, MODE_CSR>::SMEM, red_scratch_bytes<128, 2>()));
     }
 }
 
@@ -508,7 +535,7 @@ int cheb_set_doubling(int32_t on) {
 int cheb_get_doubling(void) { return g_doubling.load(); }
 
 int cheb_set_fusion(int32_t steps) {
-    if (steps < 1 || steps > 3) return fail(CL_EINVAL, "fusion mode must be 1, 2 or 3");
+    if (steps < 1 || steps > 4) return fail(CL_EINVAL, "fusion mode must be 1, 2, 3 or 4");
     g_fusion = steps;
     return CL_OK;
 }
@@ -752,11 +779,13 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         fp.G = (int)G;
         fp.H = (int64_t)((bw + T - 1) / T) + 1;
         fp.D = (kFusedSlack + (fp.H + 2 + G - 1) / G) * G;
+        if (fused_dynamic()) fp.D = fp.H + 2 + (int64_t)(G * fused_lag_waves());  // tickets: any D > H
+        if (getenv("CHEB_FUSED_NOWAIT")) fp.H = -1;  // TIMING DIAGNOSTIC ONLY: wrong results
         const double window = (double)(fp.D + fp.H + 2) * T * probe_block * 8.0 * 2.0;
         int l2 = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        fp.on = g_fusion.load() == 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
+        fp.on = g_fusion.load() >= 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
     }
     if (getenv("CHEB_DEBUG"))
         fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d doubling=%d H=%lld D=%lld\n",

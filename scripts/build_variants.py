@@ -30,6 +30,10 @@ VARIANTS = {
     "fc3s1": ["CHEB_FUSED_MIN_CTAS=3", "CHEB_FUSED_SLACK=1"],
     "fs1": ["CHEB_FUSED_SLACK=1"],
     "ffence": ["CHEB_FUSED_FENCE=1"],
+    "p8c2": ["CHEB_PPL=8", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
+    "p8u3c3": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
+    "p8u3c2": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
+    "p8u5c3": ["CHEB_PPL=8", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
 }
 
 if __name__ == "__main__":

@@ -28,6 +28,10 @@ for f in sorted(glob.glob(os.path.join(d, "sweep_*.csv"))):
     t = avg("gpu__time_duration.sum", {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3}.get(tu, 1.0))
     gb = sum(avg(k, 1.0 if units.get(k) == "Gbyte" else 1e-3 if units.get(k) == "Mbyte" else 1e-9)
              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-    ps = re.findall(r"([\d.]+) probe-steps/s", open(f[:-4] + ".txt").read()) if os.path.exists(f[:-4] + ".txt") else []
-    print(f"{tag:10s} launch {t:7.3f} ms  dram {gb:6.2f} GB  grid {avg('launch__grid_size'):5.0f}  "
+    txt = f.replace("sweep_", "var_")[:-4] + ".txt"
+    if not os.path.exists(txt):
+        txt = f[:-4] + ".txt"
+    ps = re.findall(r"([\d.]+) probe-steps/s", open(txt).read()) if os.path.exists(txt) else []
+    inst = avg("smsp__inst_executed.sum") / 1e9
+    print(f"{tag:10s} launch {t:7.3f} ms  dram {gb:6.2f} GB  grid {avg('launch__grid_size'):5.0f}  inst {inst:5.2f}e9  "
           f"timed probe-steps/s {ps[-1] if ps else '-'}")
