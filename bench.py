@@ -283,8 +283,10 @@ def run_ours(args):
     (s_ms, s_n), (f_ms, f_n), (p_ms, p_n) = prof["single"], prof["fused"], prof["persistent"]
     if p_ms > max(s_ms, f_ms):  # persistent multi-step kernel: one launch = all steps of a block
         kern = f"cheb_persist_kernel<{k},{wl.mode}>"
-        bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode)
-                            + (wl.degree - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode))
+        apps = (wl.degree + 1) // 2 if args.doubling else wl.degree  # applications of A~ per launch
+        dbl = bool(args.doubling)
+        bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode, dbl)
+                            + (apps - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode, dbl))
         avg_launch_ms, dom_ms = p_ms / max(p_n, 1), p_ms
     elif f_ms > s_ms:  # temporally fused pairs dominate
         kern = f"cheb_step2_kernel<{k}>"
