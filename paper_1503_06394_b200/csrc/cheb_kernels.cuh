@@ -411,6 +411,19 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
 // Operator prep (once per estimate): padded copies for 16-byte bulk copies and the Ã map
 // folded into the values:  val'_e = alpha*a_e (- beta if e is row i's diagonal, csr/rank1).
 // ---------------------------------------------------------------------------------------
+// Padded row lengths: every row of the prepped gather matrix is padded to a multiple of the
+// gather chunk U = CHEB_NNZ_UNROLL with entries (column i, value 0), so the step kernels' chunk
+// loop needs no bounds checks.  cnt[i] = ceil(nnz_i / U) * U, cnt[d] = 0 (exclusive-scanned into
+// the prepped row pointer).
+__global__ void __launch_bounds__(kThreads)
+prep_count_kernel(int64_t d, const int64_t* __restrict__ rp, int64_t* __restrict__ cnt) {
+    constexpr int U = CHEB_NNZ_UNROLL;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= d; i += (int64_t)gridDim.x * blockDim.x)
+        cnt[i] = i < d ? (rp[i + 1] - rp[i] + U - 1) / U * U : 0;
+}
+
+// rp2: prepped row pointer (exclusive scan of the padded lengths, entries [0, d]); this kernel
+// writes the scaled entries of row i at rp2[i].. and pads the row with (i, 0.0).
 template <int MODE>
 __global__ void __launch_bounds__(kThreads)
 prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -418,7 +431,7 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
             int64_t rp2_len, int32_t* __restrict__ ci2, double* __restrict__ va2,
             uint32_t* __restrict__ nodiag, const double* __restrict__ u, double* __restrict__ u2,
             unsigned long long* __restrict__ bw) {
-    const int64_t nnz = rp[d];
+    const int64_t total = rp2[d];  // padded nnz
     int64_t bwmax = 0;  // operator bandwidth max |i - col| (temporal fusion planning)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of 32
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < d; i0 += stride) {
@@ -426,7 +439,7 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
         bool has = true;
         if (i < d) {
             const int64_t e0 = rp[i], e1 = rp[i + 1];
-            rp2[i] = e0;
+            const int64_t o0 = rp2[i], o1 = rp2[i + 1];
             has = (MODE == MODE_BTB);
             for (int64_t e = e0; e < e1; e++) {
                 const int32_t c = ci[e];
@@ -435,10 +448,14 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
                     v = fma(alpha, va[e], -beta);
                     has = true;
                 }
-                ci2[e] = c;
-                va2[e] = v;
+                ci2[o0 + (e - e0)] = c;
+                va2[o0 + (e - e0)] = v;
                 const int64_t dist = c > i ? c - i : i - c;
                 bwmax = dist > bwmax ? dist : bwmax;
+            }
+            for (int64_t o = o0 + (e1 - e0); o < o1; o++) {  // padding: (i, 0.0)
+                ci2[o] = (int32_t)i;
+                va2[o] = 0.0;
             }
             if (u2) u2[i] = u ? u[i] : 1.0;
         }
@@ -454,9 +471,9 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
         if ((threadIdx.x & 31) == 0) atomicMax(bw, (unsigned long long)bwmax);
     }
     if (blockIdx.x == 0) {
-        for (int64_t k = d + threadIdx.x; k < rp2_len; k += blockDim.x) rp2[k] = nnz;
-        if (threadIdx.x < 8) ci2[nnz + threadIdx.x] = 0;
-        if (threadIdx.x < 4) va2[nnz + threadIdx.x] = 0.0;
+        for (int64_t k = d + 1 + threadIdx.x; k < rp2_len; k += blockDim.x) rp2[k] = total;
+        if (threadIdx.x < 8) ci2[total + threadIdx.x] = 0;
+        if (threadIdx.x < 4) va2[total + threadIdx.x] = 0.0;
         if (u2 && threadIdx.x < 2) u2[d + threadIdx.x] = 0.0;
     }
 }
@@ -589,21 +606,21 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             if (OWN_EARLY)  // issued before the gathers so its latency overlaps them
                 own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
         }
-        // all nnz of a chunk issue their gathers before any is consumed; entries past the row
-        // end gather the row's first column again (a valid, cache-hot address) with value 0
+        // all nnz of a chunk issue their gathers before any is consumed; rows are padded to a
+        // multiple of the chunk with (i, 0.0) entries by the prep pass (no bounds checks here)
+        CHEB_ASSERT(nr % CHEB_NNZ_UNROLL == 0);
+        const int32_t* crow = STAGED ? col_s + oc : a.ci + e_lo;
+        const double* vrow = STAGED ? val_s + ov : a.va + e_lo;
         for (int t0 = 0; t0 < nr; t0 += CHEB_NNZ_UNROLL) {
             int32_t c[CHEB_NNZ_UNROLL];
             double v[CHEB_NNZ_UNROLL];
 #pragma unroll
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                const bool in = t0 + q < nr;
-                const int t = in ? t0 + q : 0;
-                CHEB_ASSERT(!STAGED || (oc + t >= 0 && oc + t < G::CAP + 8));
-                CHEB_ASSERT(!STAGED || (ov + t >= 0 && ov + t < G::CAP + 4));
-                c[q] = STAGED ? col_s[oc + t] : __ldg(a.ci + e_lo + t);
+                CHEB_ASSERT(!STAGED || (oc + t0 + q >= 0 && oc + t0 + q < G::CAP + 8));
+                CHEB_ASSERT(!STAGED || (ov + t0 + q >= 0 && ov + t0 + q < G::CAP + 4));
+                c[q] = STAGED ? crow[t0 + q] : __ldg(crow + t0 + q);
                 CHEB_ASSERT(c[q] >= 0 && (int64_t)c[q] < a.d);
-                const double vv = STAGED ? val_s[ov + t] : __ldg(a.va + e_lo + t);
-                v[q] = in ? vv : 0.0;
+                v[q] = STAGED ? vrow[t0 + q] : __ldg(vrow + t0 + q);
             }
             double2 x[CHEB_NNZ_UNROLL][NSL];
 #pragma unroll

@@ -78,7 +78,7 @@ def test_doubling_degrees_odd_even(orc, doubling, n, persist):
     steps = (n + 1) // 2
     blocks = 2
     if persist == 0:
-        assert nl == 1 + blocks * (1 + steps) + 1  # prep, (init + ceil(n/2) steps) per block, finalize
+        assert nl == 2 + blocks * (1 + steps) + 1  # prep (count + scatter), (init + ceil(n/2) steps) per block, finalize
     mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, 2, range(9))
     _check(r.moments, mu, wl.d)
 
@@ -127,11 +127,11 @@ def test_doubling_off_restores_algorithm1(orc):
     try:
         n0 = P.launch_count()
         P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-        assert P.launch_count() - n0 == 1 + 1 + 10 + 1
+        assert P.launch_count() - n0 == 2 + 1 + 10 + 1
         P.set_doubling(True)
         n0 = P.launch_count()
         P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-        assert P.launch_count() - n0 == 1 + 1 + 5 + 1
+        assert P.launch_count() - n0 == 2 + 1 + 5 + 1
     finally:
         P.set_doubling(False)
         P.set_persistent(1)

@@ -115,7 +115,7 @@ def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, persistent_mode,
         fused = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
         nl = P.launch_count() - n0
         blocks = -(-m // k)
-        assert nl == 1 + blocks * (1 + 1 + (degree - 1) // 2 + (degree - 1) % 2)  # prep; init, first, pairs, tail
+        assert nl == 2 + blocks * (1 + 1 + (degree - 1) // 2 + (degree - 1) % 2)  # prep (2); init, first, pairs, tail
         if mode == 4:
             assert np.array_equal(single, fused)
         else:
@@ -240,11 +240,11 @@ def test_launch_count_increases(persistent_mode):
     persistent_mode(0)
     n0 = P.launch_count()
     P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-    assert P.launch_count() - n0 == 1 + 1 + 10 + 1  # prep + init + 10 steps + finalize
+    assert P.launch_count() - n0 == 2 + 1 + 10 + 1  # prep (count + scatter) + init + 10 steps + finalize
     persistent_mode(2)
     n0 = P.launch_count()
     P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-    assert P.launch_count() - n0 == 1 + 1 + 1 + 1  # prep + init + persistent + finalize
+    assert P.launch_count() - n0 == 2 + 1 + 1 + 1  # prep (2) + init + persistent + finalize
 
 
 @pytest.mark.parametrize("name", ["gmrf32", "torus_s", "gmrf_s"])
