@@ -288,8 +288,8 @@ def run_ours(args):
         bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode, dbl)
                             + (apps - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode, dbl))
         avg_launch_ms, dom_ms = p_ms / max(p_n, 1), p_ms
-    elif f_ms > s_ms:  # temporally fused pairs dominate
-        kern = f"cheb_step2_kernel<{k}>"
+    elif f_ms > s_ms:  # temporally fused pairs dominate (static / dynamic / warp-specialised)
+        kern = f"cheb_step2[w|d]_kernel<{k}> (fusion mode {os.environ.get('CHEB_FUSION', '1')})"
         bytes_per_launch = fused_bytes(d, gnnz, k)
         avg_launch_ms, dom_ms = f_ms / max(f_n, 1), f_ms
     else:

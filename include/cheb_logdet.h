@@ -205,8 +205,10 @@ int cheb_set_persistent(int32_t mode);
  *       operator's bandwidth max|i - col| is small enough for the two-step wavefront to
  *       stay in L2 and the matrix has enough row tiles to fill the pipeline; tiles are
  *       handed out by dynamic tickets (moments deterministic only up to rounding order);
- *   3 = always fuse pairs, dynamic tickets (testing; correct for any bandwidth);
- *   4 = always fuse pairs, static tile->CTA map: moments bit-identical to mode 1.
+ *   3 = always fuse pairs, dynamic tickets, warp-specialised producer (testing; correct
+ *       for any bandwidth);
+ *   4 = always fuse pairs, static tile->CTA map: moments bit-identical to mode 1;
+ *   5 = always fuse pairs, dynamic tickets, thread-0 producer (comparison).
  * With modes 2-4, cheb_moments synchronises its stream once after the operator prep (to
  * read the bandwidth).  CL_EINVAL for other values. */
 int cheb_set_fusion(int32_t steps);

@@ -137,6 +137,24 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrival
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {  // non-blocking
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // release.cta
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
@@ -268,7 +286,7 @@ __device__ __forceinline__ void reduce_partials_all(const double* part, int G, d
         for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
             for (int q = 0; q < 8; q++) m[ch][q] = 0.0;
-        for (int c = tid; c < G; c += kThreads) {
+        for (int c = tid; c < G && tid < kThreads; c += kThreads) {  // extra (producer) warps: none
 #pragma unroll
             for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
@@ -278,7 +296,7 @@ __device__ __forceinline__ void reduce_partials_all(const double* part, int G, d
         for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
             for (int q = 0; q < 8; q++) m[ch][q] = warp_sum_xor(m[ch][q]);
-        if (lane == 0) {
+        if (lane == 0 && warp < kThreads / 32) {
 #pragma unroll
             for (int ch = 0; ch < NCH; ch++)
 #pragma unroll
@@ -364,7 +382,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
 #pragma unroll
             for (int q = 0; q < PPL; q++) acc[ch][q] += __shfl_xor_sync(0xffffffffu, acc[ch][q], off);
     }
-    if (lane < LG) {
+    if (lane < LG && warp < kThreads / 32) {  // extra (producer) warps contribute nothing
 #pragma unroll
         for (int q = 0; q < PPL; q++) {
             const int p = probe_of<K, PPL, SPLIT>(lg, q);
@@ -1234,6 +1252,224 @@ cheb_step2d_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
         }
         __syncthreads();  // s_t[b] / s_stg[b] of the next use of b are visible
     }
+    grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
+}
+
+// ---------------------------------------------------------------------------------------
+// K2x2w: dynamic-ticket fused pair, warp-specialised.  Warps 0..7 only compute tiles; a ninth
+// (producer) warp takes the tickets (same policy as cheb_step2d_kernel), stages each item by TMA,
+// waits for a stage-2 item's dependencies and then arrives on the item's "full" mbarrier
+// (expect_tx first, so the phase completes when both the bytes and the arrival are in); the
+// compute warps arrive on the buffer's "empty" mbarrier when done, after which the producer
+// publishes a finished stage-1 tile (consumer stores -> arrive.release.cta -> producer
+// wait.acquire.cta -> red.release.gpu: cumulative).  No ticket atomic, bound load, fence or
+// dependency wait sits between two tiles of the compute warps.
+// ---------------------------------------------------------------------------------------
+#ifndef CHEB_FUSEDW_MIN_CTAS
+#define CHEB_FUSEDW_MIN_CTAS 3
+#endif
+constexpr int kFusedWThreads = kThreads + 32;
+#ifndef CHEB_FUSEDW_STAGES
+#define CHEB_FUSEDW_STAGES 3
+#endif
+constexpr int kWStages = CHEB_FUSEDW_STAGES;  // staged items in flight per CTA
+
+template <int K>
+__global__ void __launch_bounds__(kFusedWThreads, CHEB_FUSEDW_MIN_CTAS)
+cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
+    using G = Geo<K>;
+    using SL = StageLayout<K, MODE_CSR>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int NS = kWStages;
+    __shared__ __align__(8) uint64_t full[NS], empty[NS];
+    __shared__ int64_t s_base_c[NS], s_base_v[NS], s_t[NS];
+    __shared__ int s_fit[NS], s_stg[NS];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc[2][kPPL];  // stage 1 / stage 2 moments (compute warps)
+#pragma unroll
+    for (int q = 0; q < kPPL; q++) acc[0][q] = acc[1][q] = 0.0;
+    if (tid == 0) {
+        for (int x = 0; x < NS; x++) {
+            mbar_init(&full[x], 1);
+            mbar_init(&empty[x], kThreads / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kThreads / 32) {
+        // ------------------------------------------------------------------ producer warp
+        const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
+        const unsigned int ntl = (unsigned int)a.ntiles;
+        bool want2 = false, done1 = false, done2 = false;  // lane 0
+        auto take = [&](int& stg, int64_t& t) -> bool {
+            if (want2 || done1) {
+                want2 = false;
+                if (!done2) {
+                    const unsigned int u = atomicAdd(dy.c2, 1u);
+                    if (u < ntl) {
+                        stg = 1;
+                        t = u;
+                        return true;
+                    }
+                    done2 = true;
+                }
+            }
+            if (!done1) {
+                const unsigned int t1 = atomicAdd(dy.c1, 1u);
+                if (t1 < ntl) {
+                    stg = 0;
+                    t = t1;
+                    want2 = (int64_t)t1 >= f.D;
+                    return true;
+                }
+                done1 = true;
+            }
+            if (!done2) {
+                const unsigned int u = atomicAdd(dy.c2, 1u);
+                if (u < ntl) {
+                    stg = 1;
+                    t = u;
+                    return true;
+                }
+                done2 = true;
+            }
+            return false;
+        };
+        int64_t known = 0;
+        int64_t prev_t[NS], pend[NS];  // pend: item in buffer x whose completion is not yet observed
+        int prev_stg[NS];
+        for (int x = 0; x < NS; x++) {
+            prev_t[x] = -1;
+            pend[x] = -1;
+            prev_stg[x] = 1;
+        }
+        // Publish finished stage-1 tiles as soon as the compute warps release them -- also while
+        // this warp spins on a dependency, so a wait never holds back this CTA's own finished
+        // tiles (else two CTAs could wait on each other's unpublished tiles).
+        auto retire = [&](int x, bool block) {
+            if (pend[x] < 0) return;
+            const uint32_t ph = (uint32_t)((pend[x] / NS) & 1);
+            if (block) mbar_wait(&empty[x], ph);
+            else if (!mbar_test(&empty[x], ph)) return;
+            if (lane == 0 && prev_stg[x] == 0) red_release_add(f.cnt + prev_t[x] / kChunkTiles, 1u);
+            pend[x] = -1;
+        };
+        int64_t q = 0;
+        for (;; ++q) {
+            const int b = (int)(q % NS);
+            for (int x = 0; x < NS; x++)
+                if (x != b) retire(x, false);
+            retire(b, true);  // buffer b is free once the compute warps are done with item q-NS
+            int stg = 0;
+            int64_t t = -1;
+            bool ok = false;
+            if (lane == 0) ok = take(stg, t);
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) {
+                if (lane == 0) {
+                    s_t[b] = -1;
+                    mbar_arrive(&full[b]);
+                }
+                break;
+            }
+            stg = __shfl_sync(0xffffffffu, stg, 0);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (lane == 0) {
+                unsigned char* st = smem + b * SL::BYTES;
+                const int64_t r0 = t * G::TILE;
+                const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+                const int64_t e0 = __ldg(a.rp + r0), e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+                const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
+                const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+                const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
+                s_fit[b] = fit;
+                s_base_c[b] = c0;
+                s_base_v[b] = v0;
+                s_t[b] = t;
+                s_stg[b] = stg;
+                const double* wsrc = stg ? f.B : f.A;
+                const uint32_t wbytes = (uint32_t)rows * K * 8;
+                const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
+                uint32_t bytes = G::RPBYTES + sgbytes + wbytes;
+                if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+                mbar_expect_tx_only(&full[b], bytes);
+                bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &full[b]);
+                bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &full[b]);
+                bulk_g2s_hint(st + SL::OFF_WPREV, wsrc + (size_t)r0 * K, wbytes, &full[b], policy_evict_first());
+                if (fit) {
+                    bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &full[b]);
+                    bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &full[b]);
+                }
+            }
+            if (stg == 1) {  // stage-1 tiles [0, need) must be complete before the gathers
+                const int64_t need = imin64(t + f.H + 1, a.ntiles);
+                uint32_t spins = 0;
+                while (known * kChunkTiles < need) {
+                    const int64_t ch = known + lane;
+                    const unsigned int v = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
+                    const bool fullc = ch >= nchunks || v >= (unsigned int)imin64(kChunkTiles, a.ntiles - ch * kChunkTiles);
+                    const unsigned int notfull = __ballot_sync(0xffffffffu, !fullc);
+                    const int adv = notfull ? __ffs(notfull) - 1 : 32;
+                    known += adv;
+                    if (adv == 0) {
+                        for (int x = 0; x < NS; x++)
+                            if (x != b) retire(x, false);  // keep publishing while waiting
+                        __nanosleep(64);
+                        if ((++spins & 1023u) == 0 && (spins > (1u << 23) || ld_acquire_u32(f.err))) {
+                            if (lane == 0) atomicExch(f.err, 1u);  // ~seconds without progress: never hang
+                            break;
+                        }
+                    }
+                }
+#if CHEB_FUSED_FENCE
+                fence_acq_rel_gpu();
+#endif
+            }
+            __syncwarp();
+            prev_t[b] = t;
+            prev_stg[b] = stg;
+            pend[b] = q;
+            if (lane == 0) mbar_arrive(&full[b]);  // release.cta: the smem metadata above
+        }
+        for (int x = 0; x < NS; x++) retire(x, true);  // the last items may still be computing
+    } else {
+        // ------------------------------------------------------------------ compute warps
+        double2 z2[G::NSL];
+#pragma unroll
+        for (int sl = 0; sl < G::NSL; sl++) z2[sl] = make_double2(0.0, 0.0);
+        double (&mu1)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[0]);
+        double (&mu2)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[1]);
+        for (int64_t q = 0;; ++q) {
+            const int b = (int)(q % NS);
+            mbar_wait(&full[b], (uint32_t)((q / NS) & 1));
+            const int64_t t = s_t[b];
+            if (t < 0) break;
+            const int stg = s_stg[b];
+            const unsigned char* st = smem + b * SL::BYTES;
+            const int64_t r0 = t * G::TILE;
+            const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
+            if (stg == 0) {
+                if (s_fit[b])
+                    step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
+                                                                     mu1, f.B, f.B, f.A);
+                else
+                    step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, mu1, f.B, f.B,
+                                                                      f.A);
+            } else {
+                if (s_fit[b])
+                    step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
+                                                                     mu2, f.A, f.A, f.B);
+                else
+                    step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, mu2, f.A, f.A,
+                                                                      f.B);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);  // release.cta: this warp's stores and smem reads
+        }
+    }
+    __syncthreads();  // all warps out of the loops; the stage buffers become the reduction scratch
     grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
 }
 

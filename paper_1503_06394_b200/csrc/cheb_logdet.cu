@@ -248,7 +248,10 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
 
 // Fused pairs with dynamic tile tickets (cheb_step2d_kernel) instead of the static map
 // (CHEB_FUSED_DYN, default 1).
+// fusion modes: 2 auto / 3 forced -> warp-specialised dynamic kernel; 4 static map; 5 dynamic,
+// thread-0 producer
 bool fused_dynamic() { return g_fusion.load() != 4; }
+bool fused_ws() { return g_fusion.load() == 2 || g_fusion.load() == 3; }
 // Dynamic lag beyond the halo, in units of the grid size (CHEB_FUSED_LAG, default 1.0): the
 // stage-1 tiles a stage-2 ticket needs were handed out D - H tiles earlier; up to G of them can
 // still be in flight.
@@ -376,8 +379,15 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
                 dy.c2 = (unsigned int*)(ws + L.misc + 36);
                 CL_CUDA(cudaMemsetAsync(ws + L.misc + 32, 0, 8, st));
                 void* args[] = {&a, &f, &dy};
-                CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2d_kernel<K>, dim3(grid_fused),
-                                                    dim3(kThreads), args, smem, st));
+                if (fused_ws()) {
+                    const size_t smem_w = std::max<size_t>((size_t)kWStages * SL::BYTES, red_scratch_bytes<K, 2>());
+                    cudaFuncSetAttribute(cheb_step2w_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w);
+                    CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2w_kernel<K>, dim3(grid_fused),
+                                                        dim3(kFusedWThreads), args, smem_w, st));
+                } else {
+                    CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2d_kernel<K>, dim3(grid_fused),
+                                                        dim3(kThreads), args, smem, st));
+                }
             } else {
                 void* args[] = {&a, &f};
                 CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),
@@ -434,6 +444,22 @@ void prep_mode(const cl_operator* op, double alpha, double beta, char* ws, const
         case CL_OP_CSR: run_prep<MODE_CSR>(op, alpha, beta, ws, L, st, sms); break;
         case CL_OP_CSR_RANK1: run_prep<MODE_RANK1>(op, alpha, beta, ws, L, st, sms); break;
         default: run_prep<MODE_BTB>(op, alpha, beta, ws, L, st, sms); break;
+    }
+}
+
+int fused_ws_occupancy(int k) {  // cheb_step2w_kernel: 288 threads per CTA
+    auto occ_of = [](auto kern, size_t smem) {
+        int occ = 0;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFusedWThreads, smem);
+        return occ < 1 ? 1 : (occ > kMaxCtasPerSm ? kMaxCtasPerSm : occ);
+    };
+    switch (k) {
+        case 8: return occ_of(cheb_step2w_kernel<8>, std::max<size_t>((size_t)kWStages * StageLayout<8, MODE_CSR>::BYTES, red_scratch_bytes<8, 2>()));
+        case 16: return occ_of(cheb_step2w_kernel<16>, std::max<size_t>((size_t)kWStages * StageLayout<16, MODE_CSR>::BYTES, red_scratch_bytes<16, 2>()));
+        case 32: return occ_of(cheb_step2w_kernel<32>, std::max<size_t>((size_t)kWStages * StageLayout<32, MODE_CSR>::BYTES, red_scratch_bytes<32, 2>()));
+        case 64: return occ_of(cheb_step2w_kernel<64>, std::max<size_t>((size_t)kWStages * StageLayout<64, MODE_CSR>::BYTES, red_scratch_bytes<64, 2>()));
+        default: return occ_of(cheb_step2w_kernel<128>, std::max<size_t>((size_t)kWStages * StageLayout<128, MODE_CSR>::BYTES, red_scratch_bytes<128, 2>()));
     }
 }
 
@@ -549,7 +575,7 @@ int cheb_set_doubling(int32_t on) {
 int cheb_get_doubling(void) { return g_doubling.load(); }
 
 int cheb_set_fusion(int32_t steps) {
-    if (steps < 1 || steps > 4) return fail(CL_EINVAL, "fusion mode must be 1, 2, 3 or 4");
+    if (steps < 1 || steps > 5) return fail(CL_EINVAL, "fusion mode must be 1..5");
     g_fusion = steps;
     return CL_OK;
 }
@@ -788,7 +814,7 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         // same grid as the single-step kernel (bit-identical per-CTA partial sums), limited to
         // what the fused kernel can keep co-resident
         int64_t G = step_grid_csr(probe_block, ntiles, sms);
-        const int64_t Gmax = (int64_t)sms * fused_occupancy(probe_block);
+        const int64_t Gmax = (int64_t)sms * (fused_ws() ? fused_ws_occupancy(probe_block) : fused_occupancy(probe_block));
         if (G > Gmax) G = Gmax;
         fp.G = (int)G;
         fp.H = (int64_t)((bw + T - 1) / T) + 1;

@@ -30,6 +30,8 @@ VARIANTS = {
     "fc3s1": ["CHEB_FUSED_MIN_CTAS=3", "CHEB_FUSED_SLACK=1"],
     "fs1": ["CHEB_FUSED_SLACK=1"],
     "ffence": ["CHEB_FUSED_FENCE=1"],
+    "w2": ["CHEB_FUSEDW_STAGES=2"],
+    "w4": ["CHEB_FUSEDW_STAGES=4", "CHEB_FUSEDW_MIN_CTAS=2"],
     "p8c2": ["CHEB_PPL=8", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
     "p8u3c3": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
     "p8u3c2": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],

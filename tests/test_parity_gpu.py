@@ -109,7 +109,7 @@ def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, persistent_mode,
     fusion_mode(1)
     single = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
     mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, degree, wl.seed, range(m), workers=4)
-    for mode in (4, 3):
+    for mode in (4, 3, 5):
         fusion_mode(mode)
         n0 = P.launch_count()
         fused = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
@@ -134,9 +134,10 @@ def test_fused_wide_band_forced(orc, fusion_mode, persistent_mode):
     single = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
     fusion_mode(4)
     assert np.array_equal(single, P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy())
-    fusion_mode(3)
-    fused = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
-    assert np.allclose(single, fused, rtol=1e-12, atol=1e-12 * S.n_rows)
+    for mode in (3, 5):
+        fusion_mode(mode)
+        fused = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
+        assert np.allclose(single, fused, rtol=1e-12, atol=1e-12 * S.n_rows)
 
 
 def test_rank1_explicit_u(orc):
