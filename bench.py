@@ -436,7 +436,10 @@ def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, tor
             "d2h_bytes_per_step": int(d2h), "steps": steps,
             "api": "cheb_logdet_host (C ABI, pinned host CSR)" if world == 1 else
                    "ShardedEstimator after pinned H2D of the CSR",
-            "includes": "H2D CSR copy, workspace alloc, all steps, D2H result"}
+            "includes": ("H2D copy of the CSR from pinned host memory, operator prep, all steps, D2H "
+                         "of the result; device workspace from the library's per-thread arena "
+                         "(allocated by the warm-up call)" if world == 1 else
+                         "H2D CSR copy, estimator workspace alloc, all steps, all-reduce, D2H result")}
 
 
 def main():

@@ -25,8 +25,9 @@
  *   - All validation runs before any device work; outputs are written only on
  *     success (device outputs of the asynchronous calls: on successful launch).
  *   - The caller owns every buffer passed in; the library never frees or keeps
- *     a pointer past the call.  Only cheb_logdet / cheb_logdet_host /
- *     cheb_probes / cheb_bounds_btb allocate (and free) device memory.
+ *     a pointer past the call.  Only cheb_logdet / cheb_logdet_host (per-thread
+ *     arenas, see cheb_release_cache) and cheb_probes / cheb_bounds_btb /
+ *     cheb_norm_bound / cheb_gershgorin / cheb_quadform allocate device memory.
  *   - Matrices are canonical CSR: row_ptr int64[n_rows+1] (row_ptr[0] = 0),
  *     col_idx int32[nnz] sorted & unique within a row, val fp64[nnz].
  *   - Probe-block layout on the device: W[d][k] fp64 row-major, the k probes of a
@@ -225,6 +226,12 @@ int cheb_set_fusion(int32_t steps);
  *       to the power-basis entry points.  CL_EINVAL for other values. */
 int cheb_set_doubling(int32_t on);
 int cheb_get_doubling(void);
+
+/* cheb_logdet / cheb_logdet_host keep their device workspace (and cheb_logdet_host the device
+ * copy of the operator) in grow-only per-thread arenas, so repeated estimates do not pay a
+ * multi-GB cudaMalloc/cudaFree per call.  cheb_release_cache() frees the calling thread's
+ * arenas (they are also freed when the thread exits). */
+int cheb_release_cache(void);
 
 /* Thread-local message for the last failing call on this thread. */
 const char *cheb_last_error(void);

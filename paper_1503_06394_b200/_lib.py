@@ -82,6 +82,7 @@ def load():
         "cheb_set_persistent": (I, [I32]),
         "cheb_set_doubling": (I, [I32]),
         "cheb_get_doubling": (I, []),
+        "cheb_release_cache": (I, []),
         "cheb_last_error": (ctypes.c_char_p, []),
         "cheb_version": (I, []),
     }

@@ -325,6 +325,11 @@ def set_doubling(on: bool):
     check(_lib.load().cheb_set_doubling(1 if on else 0))
 
 
+def release_cache():
+    """Free this thread's device arenas of cheb_logdet / cheb_logdet_host."""
+    check(_lib.load().cheb_release_cache())
+
+
 def get_doubling() -> bool:
     return bool(_lib.load().cheb_get_doubling())
 

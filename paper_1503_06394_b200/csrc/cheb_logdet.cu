@@ -101,6 +101,46 @@ struct DevBuf {  // owning device allocation (freed on scope exit)
     void* p = nullptr;
     ~DevBuf() { if (p) cudaFree(p); }
 };
+
+// Grow-only device arenas reused across the synchronous entry points (cheb_logdet,
+// cheb_logdet_host) of a host thread: repeated estimates do not pay cudaMalloc/cudaFree of a
+// multi-GB workspace every call.  [0]: workspace + result buffers, [1]: the host operator's
+// device copy.  cheb_release_cache() frees them.
+struct Arena {
+    int dev = -1;
+    void* p = nullptr;
+    size_t cap = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        dev = -1;
+    }
+    ~Arena() { release(); }
+};
+thread_local Arena g_arena[2];
+
+int arena_get(int slot, size_t bytes, void** out) {
+    Arena& A = g_arena[slot];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (A.p && (A.cap < bytes || A.dev != dev)) A.release();
+    if (!A.p) {
+        cudaError_t e = cudaMalloc(&A.p, bytes);
+        if (e != cudaSuccess) {
+            A.p = nullptr;
+            return fail(CL_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        }
+        A.cap = bytes;
+        A.dev = dev;
+    }
+    *out = A.p;
+    return CL_OK;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64 || k == 128; }
@@ -508,6 +548,11 @@ extern "C" {
 
 int cheb_version(void) { return 100; }
 
+int cheb_release_cache(void) {
+    for (auto& A : g_arena) A.release();
+    return CL_OK;
+}
+
 const char* cheb_last_error(void) { return g_err.c_str(); }
 
 int64_t cheb_launch_count(void) { return g_launches.load(); }
@@ -867,10 +912,11 @@ int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int
     if (!valid_k(k)) return fail(CL_EINVAL, "probe_block must be 0, 8, 16, 32, 64 or 128");
     const size_t ws_bytes = plan(op->A.n_cols, gather_nnz(op), k, op->kind, sm_count()).total;
     const size_t mu_n = (size_t)num_probes * (degree + 1);
-    DevBuf ws, aux;
-    CL_CUDA(cudaMalloc(&ws.p, ws_bytes));
     const size_t aux_bytes = sizeof(double) * (mu_n + (degree + 1) + num_probes + 4);
-    CL_CUDA(cudaMalloc(&aux.p, aux_bytes));
+    struct { void* p; } ws, aux;
+    int rc0 = arena_get(0, align256(ws_bytes) + aux_bytes, &ws.p);
+    if (rc0) return rc0;
+    aux.p = (char*)ws.p + align256(ws_bytes);
     double* mu = (double*)aux.p;
     double* c = mu + mu_n;
     double* gp = c + degree + 1;
@@ -933,13 +979,27 @@ int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, 
     cudaStream_t st;
     CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     cl_operator dop = *op;
-    DevBuf bufs[8];
-    int nb = 0;
+    // one arena block holds the device copy of every operator array
+    auto csr_bytes = [](const cl_csr& A) {
+        return align256(sizeof(int64_t) * (A.n_rows + 1)) + align256(sizeof(int32_t) * A.nnz) +
+               align256(sizeof(double) * A.nnz);
+    };
+    size_t need = csr_bytes(op->A);
+    if (op->kind == CL_OP_BTB) need += csr_bytes(op->At);
+    if (op->kind == CL_OP_CSR_RANK1 && op->r1_u) need += align256(sizeof(double) * op->A.n_cols);
+    void* blk = nullptr;
+    const double t_alloc = now_s();
+    if ((rc = arena_get(1, need, &blk))) {
+        cudaStreamDestroy(st);
+        return rc;
+    }
+    size_t used = 0;
     auto up = [&](const void* h, size_t bytes, const void** dptr) -> int {
         if (!h || bytes == 0) return CL_OK;
-        CL_CUDA(cudaMalloc(&bufs[nb].p, bytes));
-        CL_CUDA(cudaMemcpyAsync(bufs[nb].p, h, bytes, cudaMemcpyHostToDevice, st));
-        *dptr = bufs[nb++].p;
+        char* d = (char*)blk + used;
+        used += align256(bytes);
+        CL_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+        *dptr = d;
         return CL_OK;
     };
     auto up_csr = [&](cl_csr& A) -> int {
@@ -952,9 +1012,17 @@ int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, 
     if (!rc && dop.kind == CL_OP_BTB) rc = up_csr(dop.At);
     if (!rc && dop.kind == CL_OP_CSR_RANK1 && dop.r1_u)
         rc = up(dop.r1_u, sizeof(double) * dop.A.n_cols, (const void**)&dop.r1_u);
+    const double t_h2d = now_s();
+    if (getenv("CHEB_DEBUG")) {
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[chebld] host call: arena %.1f ms, H2D %.1f ms (%zu B)\n", (t_h2d - t_alloc) * 1e3,
+                (now_s() - t_h2d) * 1e3, used);
+    }
+    const double t_est = now_s();
     if (!rc) rc = logdet_device(&dop, a, b, degree, num_probes, seed, probe_block, out, st);
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
+    if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] host call: estimate %.1f ms\n", (now_s() - t_est) * 1e3);
     out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return rc;
 }
