@@ -124,8 +124,21 @@ class ClockSampler:
 
 def build_workload(name):
     wl = W.get_workload(name)
+    t0 = time.perf_counter()
     A, At = wl.matrices()
+    build_workload.gen_s = time.perf_counter() - t0  # host generation time of the operator
     return wl, A, At
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------------- oracle (CPU) arm
@@ -179,7 +192,7 @@ def run_reference(args):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": wl.name, "d": wl.d, "degree": wl.degree,
                                             "num_probes_per_step": workers, "steps_per_probe": steps},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle", "cpu_model": cpu_model(),
                             "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -208,16 +221,20 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers, steps = _oracle_plan(wl, budget_s=args.ref_budget)
         v, dt = oracle_sample(wl, A, steps, workers, workers)
-        cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle",
+        cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{workers} probes x {steps} Chebyshev steps of {wl.name} (d={wl.d}), "
                          f"one single-threaded oracle process per probe, {dt:.1f} s"}
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    torch.cuda.synchronize()
+    t_up = time.perf_counter()
     dA = P.DeviceCSR.from_host(A, dev)
     dAt = P.DeviceCSR.from_host(At, dev) if At is not None else None
     op = P.Operator(wl.mode, dA, dAt, wl.r1_c)
     a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+    torch.cuda.synchronize()
+    upload_s = time.perf_counter() - t_up
     group = None
     sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, group=group, basis=args.basis)
     if args.doubling:
@@ -331,7 +348,9 @@ def run_ours(args):
                       "applications_per_probe": (wl.degree + 1) // 2 if args.doubling else wl.degree,
                       "parallelism": f"probe-dp{world}", "l2": "inputs larger than L2 (W blocks "
                       f"{2 * d * k * 8 / 1e9:.1f} GB/GPU), no flush needed",
-                      "logdet_wall_s": t_ms / args.steps / 1e3, "gamma": float(st[0]),
+                      "logdet_wall_s": t_ms / args.steps / 1e3,
+                      "logdet_wall_incl_generation_upload_s": build_workload.gen_s + upload_s + t_ms / args.steps / 1e3,
+                      "generation_s": build_workload.gen_s, "upload_s": upload_s, "gamma": float(st[0]),
                       "stderr": float(st[1])},
            "roofline": roof, "gpu_launches": int(launches),
            "gpu_launches_per_step": launches / args.steps, "clocks": clk, "cpu_baseline": cpu,
