@@ -362,35 +362,43 @@ def run_ours(args):
 
 
 def run_alt_schedule(args, sh, P, torch, dist, world, dev, gamma_main):
-    """Time the other moment schedule on the same sharded estimator (device events, max
-    over ranks): with the default Algorithm 1 run this measures moment doubling, and vice
-    versa.  Reported beside the headline, never instead of it."""
-    other = not args.doubling
-    P.set_doubling(other)
-    try:
-        sh.run()
-        torch.cuda.synchronize()
-        reps = max(1, min(args.steps, 3))
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
-        ev0.record()
-        for _ in range(reps):
-            gp, stats = sh.run()
-        ev1.record()
-        torch.cuda.synchronize()
-        el = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        g = float(stats.cpu().numpy()[0])
-    finally:
-        P.set_doubling(args.doubling)
-    wall = float(el.item()) / reps / 1e3
+    """Time the other schedules on the same sharded estimator (device events, max over ranks),
+    reported beside the headline, never instead of it: moment doubling (G25) and temporally
+    fused step pairs (warp-specialised, fusion mode 2) when the headline is Algorithm 1."""
     n = sh.est.degree
-    return {"schedule": "moment doubling" if other else "Algorithm 1 recurrence",
-            "applications_per_probe": (n + 1) // 2 if other else n, "logdet_wall_s": wall,
-            "chebyshev_steps_per_s": sh.est.m * n / wall, "gamma": g,
-            "rel_diff_gamma_vs_headline": abs(g - gamma_main) / abs(gamma_main), "reps": reps}
+    alts = []
+    if not args.doubling:
+        alts.append(("moment doubling", (n + 1) // 2, lambda on: P.set_doubling(on)))
+    else:
+        alts.append(("Algorithm 1 recurrence", n, lambda on: P.set_doubling(not on)))
+    if not args.doubling and sh.est.op.kind == "csr":
+        alts.append(("fused step pairs (fusion mode 2)", n, lambda on: P.set_fusion(2 if on else 1)))
+    out = []
+    for name, apps, switch in alts:
+        switch(True)
+        try:
+            sh.run()
+            torch.cuda.synchronize()
+            reps = max(1, min(args.steps, 3))
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            ev0.record()
+            for _ in range(reps):
+                gp, stats = sh.run()
+            ev1.record()
+            torch.cuda.synchronize()
+            el = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(el, op=dist.ReduceOp.MAX)
+            g = float(stats.cpu().numpy()[0])
+        finally:
+            switch(False)
+        wall = float(el.item()) / reps / 1e3
+        out.append({"schedule": name, "applications_per_probe": apps, "logdet_wall_s": wall,
+                    "chebyshev_steps_per_s": sh.est.m * n / wall, "gamma": g,
+                    "rel_diff_gamma_vs_headline": abs(g - gamma_main) / abs(gamma_main), "reps": reps})
+    return out
 
 
 def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, torch, dist):

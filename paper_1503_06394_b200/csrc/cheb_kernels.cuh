@@ -1302,40 +1302,34 @@ cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
         // ------------------------------------------------------------------ producer warp
         const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
         const unsigned int ntl = (unsigned int)a.ntiles;
-        bool want2 = false, done1 = false, done2 = false;  // lane 0
-        auto take = [&](int& stg, int64_t& t) -> bool {
-            if (want2 || done1) {
+        // Ticket policy of cheb_step2d_kernel, split so the atomic for item q+1 is issued one item
+        // ahead and only examined in the next iteration (it overlaps this item's bound loads, TMA
+        // issue and dependency wait).  lane 0 state:
+        bool want2 = false, done1 = false, done2 = false;
+        auto choose = [&]() -> int {  // counter of the next ticket: 1, 2, or 0 (none left)
+            if ((want2 || done1) && !done2) {
                 want2 = false;
-                if (!done2) {
-                    const unsigned int u = atomicAdd(dy.c2, 1u);
-                    if (u < ntl) {
-                        stg = 1;
-                        t = u;
-                        return true;
-                    }
-                    done2 = true;
-                }
+                return 2;
             }
-            if (!done1) {
-                const unsigned int t1 = atomicAdd(dy.c1, 1u);
-                if (t1 < ntl) {
-                    stg = 0;
-                    t = t1;
-                    want2 = (int64_t)t1 >= f.D;
+            if (!done1) return 1;
+            return done2 ? 0 : 2;
+        };
+        auto draw = [&](int ctr) -> unsigned int { return ctr == 1 ? atomicAdd(dy.c1, 1u) : ctr == 2 ? atomicAdd(dy.c2, 1u) : 0u; };
+        // classify a drawn ticket (falling back to the other counter when one is exhausted)
+        auto resolve = [&](int ctr, unsigned int raw, int& stg, int64_t& t) -> bool {
+            for (;;) {
+                if (ctr == 0) return false;
+                if (raw < ntl) {
+                    stg = ctr == 2 ? 1 : 0;
+                    t = raw;
+                    if (ctr == 1) want2 = (int64_t)raw >= f.D;
                     return true;
                 }
-                done1 = true;
+                if (ctr == 1) done1 = true;
+                else done2 = true;
+                ctr = choose();
+                raw = draw(ctr);
             }
-            if (!done2) {
-                const unsigned int u = atomicAdd(dy.c2, 1u);
-                if (u < ntl) {
-                    stg = 1;
-                    t = u;
-                    return true;
-                }
-                done2 = true;
-            }
-            return false;
         };
         int64_t known = 0;
         int64_t prev_t[NS], pend[NS];  // pend: item in buffer x whose completion is not yet observed
@@ -1356,16 +1350,31 @@ cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
             if (lane == 0 && prev_stg[x] == 0) red_release_add(f.cnt + prev_t[x] / kChunkTiles, 1u);
             pend[x] = -1;
         };
+        int ctr_n = 0;          // lane 0: counter and raw value of the ticket drawn for the next item
+        unsigned int raw_n = 0;
+        if (lane == 0) {
+            ctr_n = choose();
+            raw_n = draw(ctr_n);
+        }
         int64_t q = 0;
         for (;; ++q) {
             const int b = (int)(q % NS);
+            int stg = 0;
+            int64_t t = -1, e0 = 0, e1 = 0;
+            bool ok = false;
+            if (lane == 0) {
+                ok = resolve(ctr_n, raw_n, stg, t);
+                if (ok) {  // bound loads of this item, then the next ticket: both in flight below
+                    const int64_t r0 = t * G::TILE;
+                    e0 = __ldg(a.rp + r0);
+                    e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+                    ctr_n = choose();
+                    raw_n = draw(ctr_n);
+                }
+            }
             for (int x = 0; x < NS; x++)
                 if (x != b) retire(x, false);
             retire(b, true);  // buffer b is free once the compute warps are done with item q-NS
-            int stg = 0;
-            int64_t t = -1;
-            bool ok = false;
-            if (lane == 0) ok = take(stg, t);
             ok = __shfl_sync(0xffffffffu, ok, 0);
             if (!ok) {
                 if (lane == 0) {
@@ -1380,7 +1389,6 @@ cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
                 unsigned char* st = smem + b * SL::BYTES;
                 const int64_t r0 = t * G::TILE;
                 const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-                const int64_t e0 = __ldg(a.rp + r0), e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
                 const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
                 const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
                 const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;

@@ -292,15 +292,13 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
 // thread-0 producer
 bool fused_dynamic() { return g_fusion.load() != 4; }
 bool fused_ws() { return g_fusion.load() == 2 || g_fusion.load() == 3; }
-// Dynamic lag beyond the halo, in units of the grid size (CHEB_FUSED_LAG, default 1.0): the
-// stage-1 tiles a stage-2 ticket needs were handed out D - H tiles earlier; up to G of them can
-// still be in flight.
+// Dynamic lag beyond the halo, in units of the grid size (CHEB_FUSED_LAG; default 1.5 for the
+// warp-specialised kernel, whose producer holds up to kWStages + 1 tickets, 1.0 otherwise): the
+// stage-1 tiles a stage-2 ticket needs were handed out D - H tiles earlier and may still be in
+// flight; measured optimum on configs[3] (profiles/r01_fusion_study.md).
 double fused_lag_waves() {
-    static double v = [] {
-        const char* e = getenv("CHEB_FUSED_LAG");
-        return e ? atof(e) : 1.0;
-    }();
-    return v;
+    const char* e = getenv("CHEB_FUSED_LAG");
+    return e ? atof(e) : (fused_ws() ? 1.5 : 1.0);
 }
 
 // Temporal fusion plan (CSR mode): stage-2 halo H (tiles) and lag D (positions).
