@@ -1506,15 +1506,18 @@ struct PersistArgs {
     int32_t power;            // power basis (Taylor baseline): every step is w_j = Ã w_{j-1}
 };
 
+// Relaxed polling (an acquire load compiles to an SM-wide L1 invalidate per iteration, which
+// would flush the L1 of every CTA on the SM while one spins), then one acquire fence.
 __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned int want, unsigned int* err) {
     uint32_t spins = 0;
-    while (ld_acquire_u32(p) < want) {
+    while (ld_relaxed_u32(p) < want) {
         __nanosleep(20);
-        if ((++spins & 1023u) == 0 && (spins > (1u << 25) || ld_acquire_u32(err))) {
+        if ((++spins & 1023u) == 0 && (spins > (1u << 25) || ld_relaxed_u32(err))) {
             atomicExch(err, 1u);  // ~seconds without progress: give up, never hang
             break;
         }
     }
+    fence_acq_rel_gpu();
 }
 
 template <int K, int MODE, bool DBL = false>
@@ -1649,8 +1652,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         // ---- grid barrier, split: arrive, stage step j+1, wait
         __syncthreads();
         if (tid == 0) {
-            __threadfence();
-            atomicAdd(pa_.bar_count, 1u);
+            red_release_add(pa_.bar_count, 1u);  // release: the CTA's stores of step j (barrier above)
             if (j < pa_.n) {
                 // w_{j-1} (W_prev of step j+1) and the matrix are final: stage ahead.  The
                 // proxy fence orders other CTAs' generic stores of w_{j-1} (step j-1, already
@@ -1659,8 +1661,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
                 for (int64_t i = 0; i < 2 && i < nmine; i++)
                     issue(j + 1, (int64_t)blockIdx.x + i * gridDim.x, (int)i);  // stages are all consumed
             }
-            spin_until_geq(pa_.bar_count, (unsigned int)j * gridDim.x, pa_.err);
-            __threadfence();
+            spin_until_geq(pa_.bar_count, (unsigned int)j * gridDim.x, pa_.err);  // + acquire (L1 invalidated)
         }
         __syncthreads();
         // ---- canonical reductions of step j's partials: CTA c owns probes c, c+G, ...
@@ -1679,12 +1680,8 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         if (HAS_S) {
             if (tid == 0) {
                 const unsigned int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-                if (mine) {
-                    __threadfence();
-                    atomicAdd(pa_.s_count, mine);
-                }
+                if (mine) red_release_add(pa_.s_count, mine);
                 spin_until_geq(pa_.s_count, (unsigned int)j * K, pa_.err);  // every s_j published
-                __threadfence();
             }
             __syncthreads();
             if (tid < K) s_sh[tid] = __ldcg(pa_.s_buf + (j & 1) * K + tid);

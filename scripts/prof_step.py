@@ -28,7 +28,8 @@ def main():
                     wl.r1_c)
     a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
     m = args.probes or wl.num_probes
-    est = P.Estimator(op, a, b, args.degree or wl.degree, m, args.k, seed=wl.seed)
+    k = args.k or next((kk for kk in (8, 16, 32, 64) if kk >= m), 64)  # 0: the bench's choice
+    est = P.Estimator(op, a, b, args.degree or wl.degree, m, k, seed=wl.seed)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for r in range(args.reps):
         ev0.record()

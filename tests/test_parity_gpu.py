@@ -461,3 +461,23 @@ def test_sharded_estimators_sum_to_single_run(world):
     _, st_full = P.finalize(full.mu, full.c)
     _, st_sum = P.finalize(total, full.c)
     assert torch.equal(st_full, st_sum)
+
+
+def test_fusion_auto_at_config2_size(orc, fusion_mode, persistent_mode):
+    """Fusion mode 2 (auto) engages the warp-specialised fused kernel at configs[2] size
+    (d = 1e6, banded); moments agree with per-step launches to rounding and with the oracle on
+    sampled probes."""
+    wl = W.get_workload("gmrf1000")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    n, m = 21, 64
+    fusion_mode(1)
+    single = P.moments(op, wl.a, wl.b, n, 0, m, wl.seed, 64).cpu().numpy()
+    fusion_mode(2)
+    P.profile_begin()
+    fused = P.moments(op, wl.a, wl.b, n, 0, m, wl.seed, 64).cpu().numpy()
+    prof = P.profile_end()
+    assert prof["fused"][1] == (n - 1) // 2  # pairs (2,3), (4,5), ... launched as fused kernels
+    assert np.allclose(single, fused, rtol=1e-13, atol=1e-13 * wl.d)
+    mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, wl.seed, [0, 63], workers=2)
+    _check_moments(fused[[0, 63]], mu, wl.d)
