@@ -31,8 +31,17 @@ def main():
             P.taylor_logdet(op_g, 2.0, 5, 9, 1, k)
     P.set_persistent(1)
     P.logdet(op_b, a, b, 5, 9, seed=1, k=16)
-    P.set_fusion(3)
-    P.moments(op_g, 0.2, 1.8, 6, 0, 9, 1, 16)
+    P.set_doubling(True)  # moment-doubling kernels, per step and persistent
+    for persist in (0, 2):
+        P.set_persistent(persist)
+        P.logdet(op_g, 0.2, 1.8, 7, 11, seed=1, k=16)
+        P.logdet(op_t, 0.01, 8.5, 7, 11, seed=1, k=16)
+    P.set_persistent(1)
+    P.logdet(op_b, a, b, 5, 9, seed=1, k=16)
+    P.set_doubling(False)
+    for mode in (3, 4, 5):  # fused pairs: warp-specialised, static, dynamic
+        P.set_fusion(mode)
+        P.moments(op_g, 0.2, 1.8, 6, 0, 9, 1, 16)
     P.set_fusion(1)
     torch.cuda.synchronize()
     print("sanitize smoke ok")
