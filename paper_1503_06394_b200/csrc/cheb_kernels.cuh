@@ -232,12 +232,26 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
 }
 
+// L2 prefetch of each staged tile's first-touch gather rows (CHEB_L2_PREFETCH, default 0): with
+// rows processed in ascending order, the rows a banded operator's tile touches for the first time
+// are [r0 + bw, r0 + bw + T) (bw = max |i - col|); the staging thread can prefetch them into L2.
+// Measured harmful on configs[3] (6.20 -> 9.36 ms per launch, DRAM 40.3 -> 60.8 GB): tiles are
+// staged two items per CTA ahead, i.e. ~2G tiles ahead of the chip-wide front, and the prefetched
+// rows are evicted by the ~60 MB of traffic before their use.  Kept as a build option.
+#ifndef CHEB_L2_PREFETCH
+#define CHEB_L2_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 struct StepArgs {
     int64_t d;            // rows of the gather matrix (= dimension of M)
     int64_t ntiles;
     const int64_t* rp;    // prepped gather matrix: padded row_ptr copy
     const int32_t* ci;    //   padded col copy
     const double* va;     //   padded scaled values (alpha*a, diagonal alpha*a_ii - beta)
+    const unsigned long long* bw;  // operator bandwidth max|i - col| (device), nullptr: no prefetch
     const uint32_t* nodiag;  // bit i: row i has no stored diagonal (csr/rank1)
     const double* xg;     // gather source: W_cur (csr/rank1) or Y = B W_cur (btb)
     const double* wcur;   // W_cur
@@ -762,6 +776,12 @@ cheb_step_kernel(StepArgs a) {
     }
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
+    // thread 0: bandwidth for the L2 prefetch (only for banded operators, bw < d/4)
+    int64_t pf_bw = -1;
+    if (CHEB_L2_PREFETCH && MODE != MODE_BTB && tid == 0 && a.bw) {
+        const int64_t bwv = (int64_t)*a.bw;
+        pf_bw = (4 * bwv < a.d) ? bwv : -1;
+    }
     // ---- producer (thread 0): issue the bulk copies of tile t into stage b
     auto issue = [&](int64_t t, int b, int64_t e0, int64_t e1) {
         unsigned char* st = smem + b * SL::BYTES;
@@ -791,6 +811,10 @@ cheb_step_kernel(StepArgs a) {
             bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
         }
         if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
+        if (CHEB_L2_PREFETCH && MODE != MODE_BTB && pf_bw >= 0) {  // first-touch gather rows -> L2
+            const int64_t p0 = r0 + pf_bw, p1 = imin64(p0 + rows, a.d);
+            if (p1 > p0) prefetch_l2(a.xg + (size_t)p0 * K, (uint32_t)(p1 - p0) * K * 8);
+        }
     };
     auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
     auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
@@ -1331,6 +1355,11 @@ cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
                 raw = draw(ctr);
             }
         };
+        int64_t pf_bw = -1;  // lane 0: bandwidth for the L2 prefetch (banded operators only)
+        if (CHEB_L2_PREFETCH && lane == 0 && a.bw) {
+            const int64_t bwv = (int64_t)*a.bw;
+            pf_bw = (4 * bwv < a.d) ? bwv : -1;
+        }
         int64_t known = 0;
         int64_t prev_t[NS], pend[NS];  // pend: item in buffer x whose completion is not yet observed
         int prev_stg[NS];
@@ -1409,6 +1438,10 @@ cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
                 if (fit) {
                     bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &full[b]);
                     bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &full[b]);
+                }
+                if (CHEB_L2_PREFETCH && stg == 0 && pf_bw >= 0) {  // stage-1 first-touch rows of w_j
+                    const int64_t p0 = r0 + pf_bw, p1 = imin64(p0 + rows, a.d);
+                    if (p1 > p0) prefetch_l2(f.B + (size_t)p0 * K, (uint32_t)(p1 - p0) * K * 8);
                 }
             }
             if (stg == 1) {  // stage-1 tiles [0, need) must be complete before the gathers

@@ -282,7 +282,7 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
         d, G2.row_ptr, G2.col_idx, G2.val, alpha, beta, (int64_t*)(ws + L.rp2), L.rp2_len,
         (int32_t*)(ws + L.ci2), (double*)(ws + L.va2), (uint32_t*)(ws + L.nodiag),
         MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr,
-        MODE == MODE_CSR ? (unsigned long long*)(ws + L.misc) : nullptr);
+        MODE != MODE_BTB ? (unsigned long long*)(ws + L.misc) : nullptr);
     g_launches++;
 }
 
@@ -330,6 +330,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.ci = (const int32_t*)(ws + L.ci2);
     a.va = (const double*)(ws + L.va2);
     a.nodiag = (const uint32_t*)(ws + L.nodiag);
+    a.bw = (MODE != MODE_BTB && op->A.nnz > 0) ? (const unsigned long long*)(ws + L.misc) : nullptr;
     a.sbits = sbits;
     a.beta = beta;
     a.r1c_alpha = alpha * op->r1_c;

@@ -31,6 +31,7 @@ VARIANTS = {
     "fs1": ["CHEB_FUSED_SLACK=1"],
     "ffence": ["CHEB_FUSED_FENCE=1"],
     "w2": ["CHEB_FUSEDW_STAGES=2"],
+    "pf1": ["CHEB_L2_PREFETCH=1"],
     "w4": ["CHEB_FUSEDW_STAGES=4", "CHEB_FUSEDW_MIN_CTAS=2"],
     "p8c2": ["CHEB_PPL=8", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
     "p8u3c3": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
