@@ -49,7 +49,10 @@ constexpr int kThreads = 256;
 #define CHEB_MIN_CTAS_DBL 3  // moment doubling carries two more accumulator channels
 #endif
 #ifndef CHEB_DBL_STAGE_WC
-#define CHEB_DBL_STAGE_WC 0
+#define CHEB_DBL_STAGE_WC 1  // moment doubling stages the tile's own W_cur rows (w_{j-1}^T w_j)
+#endif
+#ifndef CHEB_RPG_DBL
+#define CHEB_RPG_DBL 1  // rows per lane group of the moment-doubling kernels (16-row tiles at k=64)
 #endif
 #ifndef CHEB_RPG
 #define CHEB_RPG 2  // rows per lane group per tile (tile = 256*RPG*4/K rows)
@@ -78,7 +81,8 @@ static_assert(kPPL == 4 || kPPL == 8, "CHEB_PPL must be 4 or 8");
 // Geometry of the step / spmm kernels: each lane owns PPL probes in PPL/2 slots of two
 // consecutive probes, L = K/PPL lanes own a row; RPG rows per group per tile.  The tile
 // (rows) does not depend on PPL.
-template <int K>
+// R4: rows per lane group at PPL = 4 (CHEB_RPG; the moment-doubling kernels use CHEB_RPG_DBL).
+template <int K, int R4 = CHEB_RPG>
 struct Geo {
     static_assert(K == 8 || K == 16 || K == 32 || K == 64 || K == 128, "K in {8,...,128}");
     static constexpr int PPL = kPPL;
@@ -86,7 +90,7 @@ struct Geo {
     static constexpr int SS = K / NSL;              // probe stride between a lane's slots
     static constexpr int L = K / PPL;               // lanes per row: 1..32
     static constexpr int GROUPS = kThreads / L;     // rows in flight per CTA
-    static constexpr int RPG = CHEB_RPG * 4 / PPL;  // rows per group per tile
+    static constexpr int RPG = R4 * 4 / PPL;        // rows per group per tile
     static_assert(RPG >= 1, "CHEB_RPG too small for CHEB_PPL");
     static constexpr int TILE = GROUPS * RPG;       // rows per tile: 256 .. 16
     static constexpr int WORDS = words_for(K);
@@ -110,9 +114,9 @@ struct SpmmGeo {
     static constexpr int GROUPS = kThreads / L;
 };
 
-template <int K, int MODE, bool WC = false>
+template <int K, int MODE, bool WC = false, int R4 = CHEB_RPG>
 struct StageLayout {
-    using G = Geo<K>;
+    using G = Geo<K, R4>;
     static constexpr bool HAS_WC = (MODE == MODE_BTB) || WC;
     static constexpr int OFF_WPREV = 0;
     static constexpr int OFF_WCUR = OFF_WPREV + G::WBYTES;                       // HAS_WC only
@@ -592,13 +596,13 @@ template <int MODE, bool DBL>
 __host__ __device__ constexpr int n_channels() { return (DBL ? 2 : 1) + (MODE == MODE_RANK1 ? 1 : 0); }
 
 template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false, bool DBL = false,
-          bool WCS = false>
+          bool WCS = false, int R4 = CHEB_RPG>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
                                           double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
                                           const double* wcur, double* wout) {
-    using G = Geo<K>;
-    using SL = StageLayout<K, MODE, WCS>;
+    using G = Geo<K, R4>;
+    using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr int NSL = G::NSL;
     constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
     constexpr bool OWN_EARLY = DBL && !OWN_SMEM;   // else: loaded at the row start (L1/L2-hot)
@@ -749,11 +753,13 @@ __host__ __device__ constexpr int min_ctas(int mode, bool dbl = false) {
 template <int K, int MODE, bool FIRST, bool DBL = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_step_kernel(StepArgs a) {
-    using G = Geo<K>;
-    // DBL: w_{j-1}[i] (for w_{j-1}^T w_j) from an early L1/L2 load; CHEB_DBL_STAGE_WC=1 stages
-    // the own W_cur rows by TMA instead (measured slower: the extra shared memory shrinks L1)
+    // DBL: 16-row tiles (CHEB_RPG_DBL) with the own W_cur rows staged by TMA for w_{j-1}^T w_j
+    // (measured best: 6.50 ms per configs[3] launch vs 6.82 ms with 32-row tiles and an early
+    // L1/L2 load of the own row; staging with 32-row tiles shrinks L1 too much)
+    constexpr int R4 = DBL ? CHEB_RPG_DBL : CHEB_RPG;
+    using G = Geo<K, R4>;
     constexpr bool WCS = DBL && CHEB_DBL_STAGE_WC;
-    using SL = StageLayout<K, MODE, WCS>;
+    using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int NS = kStepStages;
     constexpr int NCH = n_channels<MODE, DBL>();
@@ -846,10 +852,10 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                acc, a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
+            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS, R4>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
                                                                 a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);
@@ -1556,8 +1562,9 @@ __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned i
 template <int K, int MODE, bool DBL = false>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
-    using G = Geo<K>;
-    using SL = StageLayout<K, MODE>;
+    constexpr int R4 = DBL ? CHEB_RPG_DBL : CHEB_RPG;  // same tile geometry as cheb_step_kernel
+    using G = Geo<K, R4>;
+    using SL = StageLayout<K, MODE, false, R4>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int NCH = n_channels<MODE, DBL>();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1639,17 +1646,17 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
             if (first) {
                 if (s_fit[b])
-                    step_tile<K, MODE, true, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+                    step_tile<K, MODE, true, true, true, false, DBL, false, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                      acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, true, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
+                    step_tile<K, MODE, true, false, true, false, DBL, false, R4>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
                                                                       nxt);
             } else {
                 if (s_fit[b])
-                    step_tile<K, MODE, false, true, true, false, DBL>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+                    step_tile<K, MODE, false, true, true, false, DBL, false, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                       acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, false, false, true, false, DBL>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
+                    step_tile<K, MODE, false, false, true, false, DBL, false, R4>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
                                                                        nxt);
             }
             __syncthreads();

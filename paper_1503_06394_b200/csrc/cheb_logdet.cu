@@ -145,7 +145,9 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool valid_k(int k) { return k == 8 || k == 16 || k == 32 || k == 64 || k == 128; }
 
-int tile_rows(int k) { return 2 * kThreads * 4 / k; }  // Geo<K>::TILE
+// rows per tile: Geo<K, R4>::TILE; the workspace is planned for the larger of the two geometries
+int tile_rows(int k, int r4 = CHEB_RPG) { return r4 * kThreads * 4 / k; }
+int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL)); }
 
 struct Layout {
     size_t w0, w1, y, sbits, part, sbuf, ticket;
@@ -161,7 +163,7 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     const size_t wbytes = align256((size_t)d * k * sizeof(double));
     const int words = k >= 32 ? k / 32 : 1;
     const size_t maxgrid = (size_t)sms * kMaxCtasPerSm;
-    const int64_t ntiles = (d + tile_rows(k) - 1) / tile_rows(k);
+    const int64_t ntiles = (d + tile_rows_max(k) - 1) / tile_rows_max(k);
     L.w0 = off; off += wbytes;
     L.w1 = off; off += wbytes;
     L.y = off; if (kind == CL_OP_BTB) off += wbytes;
@@ -170,7 +172,7 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.part = off; off += align256(6 * maxgrid * k * sizeof(double));
     L.sbuf = off; off += align256(2 * (size_t)k * sizeof(double));
     L.ticket = off; off += 256;
-    L.rp2_len = ntiles * tile_rows(k) + 2;
+    L.rp2_len = ntiles * tile_rows_max(k) + 2;
     L.rp2 = off; off += align256((size_t)L.rp2_len * sizeof(int64_t));
     // rows padded to a multiple of the gather chunk: at most (U - 1) extra entries per row
     const size_t pnnz = (size_t)nnz + (size_t)(CHEB_NNZ_UNROLL - 1) * (size_t)d;
@@ -316,8 +318,10 @@ template <int K, int MODE>
 int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
               int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
-    using G = Geo<K>;
+    using G = Geo<K>;  // per-step / fused geometry; the doubling kernels use Geo<K, CHEB_RPG_DBL>
+    using GD = Geo<K, CHEB_RPG_DBL>;
     using SL = StageLayout<K, MODE>;
+    using SLD = StageLayout<K, MODE, false, CHEB_RPG_DBL>;
     const int64_t d = op->A.n_cols;
     double* w[2] = {(double*)(ws + L.w0), (double*)(ws + L.w1)};
     double* y = (double*)(ws + L.y);
@@ -356,11 +360,12 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     }
     if (n < 1) return CL_OK;
 
-    a.ntiles = (d + G::TILE - 1) / G::TILE;
+    const int tile = fp.doubling ? GD::TILE : G::TILE;
+    a.ntiles = (d + tile - 1) / tile;
     // dynamic shared memory: the staged tiles, reused as the reduction scratch at the end
-    const size_t smem = std::max<size_t>(SL::SMEM, red_scratch_bytes<K, 2>());  // persistent, fused
+    const size_t smem = std::max<size_t>(fp.doubling ? SLD::SMEM : SL::SMEM, red_scratch_bytes<K, 2>());  // persistent, fused
     const size_t smem_step = std::max<size_t>(
-        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC>::BYTES : SL::BYTES),
+        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, CHEB_RPG_DBL>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
     const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true>, a.ntiles, sms, smem_step)
                                        : grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem_step);

@@ -32,6 +32,11 @@ VARIANTS = {
     "ffence": ["CHEB_FUSED_FENCE=1"],
     "w2": ["CHEB_FUSEDW_STAGES=2"],
     "pf1": ["CHEB_L2_PREFETCH=1"],
+    "wc4": ["CHEB_FUSEDW_MIN_CTAS=4"],
+    "dr1wc4": ["CHEB_RPG=1", "CHEB_DBL_STAGE_WC=1", "CHEB_MIN_CTAS_DBL=4"],
+    "dr1wc3": ["CHEB_RPG=1", "CHEB_DBL_STAGE_WC=1", "CHEB_MIN_CTAS_DBL=3"],
+    "dr1c4": ["CHEB_RPG=1", "CHEB_MIN_CTAS_DBL=4"],
+    "wc4s2": ["CHEB_FUSEDW_MIN_CTAS=4", "CHEB_FUSEDW_STAGES=2"],
     "w4": ["CHEB_FUSEDW_STAGES=4", "CHEB_FUSEDW_MIN_CTAS=2"],
     "p8c2": ["CHEB_PPL=8", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
     "p8u3c3": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
