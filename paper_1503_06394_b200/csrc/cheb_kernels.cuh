@@ -227,6 +227,11 @@ __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t t) {
 
 __device__ __forceinline__ int64_t imin64(int64_t x, int64_t y) { return x < y ? x : y; }
 
+// +-1.0 from bit `b` of `w` (set -> -1.0, the probe convention)
+__device__ __forceinline__ double pm1(uint32_t w, int b) {
+    return __hiloint2double((int)(0x3FF00000u | (((w >> b) & 1u) << 31)), 0);
+}
+
 // x with its sign bit xor'ed by bit 31 of m (exactly -x or x)
 __device__ __forceinline__ double signflip(double x, uint32_t m) {
     return __hiloint2double(__double2hiint(x) ^ (int)(m & 0x80000000u), __double2loint(x));
@@ -552,8 +557,9 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
                 acc[0][q] += v[q] * v[q];
             }
 #pragma unroll
-            for (int q = 0; q < PPL; q += 2)
-                *reinterpret_cast<double2*>(w0 + (size_t)i * K + pl + q) = make_double2(v[q], v[q + 1]);
+            if (w0)  // nullptr: the per-step path reads v from the sign bits only
+                for (int q = 0; q < PPL; q += 2)
+                    *reinterpret_cast<double2*>(w0 + (size_t)i * K + pl + q) = make_double2(v[q], v[q + 1]);
             if (HAS_S) {
                 const double u = a.r1u ? a.r1u[i] : 1.0;
 #pragma unroll
@@ -595,8 +601,11 @@ __device__ __forceinline__ double2 ldcg2(const double* p) {
 template <int MODE, bool DBL>
 __host__ __device__ constexpr int n_channels() { return (DBL ? 2 : 1) + (MODE == MODE_RANK1 ? 1 : 0); }
 
+// VB: the probe vector v = w_0 is never materialised in HBM on the per-step path, its sign bits
+// stand in for it: VB = 1 (step 1) gathers v from the bits, VB = 2 (step 2) takes w_{j-2} = v
+// from the staged bits.  x * (+-1) is exact, so results are bit-identical to reading v.
 template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false, bool DBL = false,
-          bool WCS = false, int R4 = CHEB_RPG>
+          bool WCS = false, int R4 = CHEB_RPG, int VB = 0>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
                                           double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
@@ -606,6 +615,8 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     constexpr int NSL = G::NSL;
     constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
     constexpr bool OWN_EARLY = DBL && !OWN_SMEM;   // else: loaded at the row start (L1/L2-hot)
+    static_assert(VB == 0 || (MODE != MODE_BTB && !CG && !KEEP && (VB != 1 || !OWN_SMEM)),
+                  "sign-bit probes: per-step csr/rank-1");
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int SCH = n_channels<MODE, DBL>() - 1;  // rank-1 channel
     const int lg = threadIdx.x % G::L;
@@ -639,8 +650,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         for (int sl = 0; sl < NSL; sl++) {
             g[sl] = make_double2(0.0, 0.0);
             own[sl] = make_double2(0.0, 0.0);
-            if (OWN_EARLY)  // issued before the gathers so its latency overlaps them
-                own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
+            if (OWN_EARLY) {  // issued before the gathers so its latency overlaps them
+                if (VB == 1) {  // w_{j-1} = v: from the staged sign bits
+                    const uint32_t wv = sg_s[lr * G::WORDS + (pp[sl] >> 5)];
+                    own[sl] = make_double2(pm1(wv, pp[sl] & 31), pm1(wv, (pp[sl] & 31) + 1));
+                } else {
+                    own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
+                }
+            }
         }
         // all nnz of a chunk issue their gathers before any is consumed; rows are padded to a
         // multiple of the chunk with (i, 0.0) entries by the prep pass (no bounds checks here)
@@ -659,15 +676,29 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                 v[q] = STAGED ? vrow[t0 + q] : __ldg(vrow + t0 + q);
             }
             double2 x[CHEB_NNZ_UNROLL][NSL];
+            if (VB == 1) {  // gather v = +-1 from the sign bits (4-8 B per row instead of 8K)
+                uint32_t wd[CHEB_NNZ_UNROLL][NSL];
 #pragma unroll
-            for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                const double* p = xg + (size_t)(uint32_t)c[q] * K;
+                for (int q = 0; q < CHEB_NNZ_UNROLL; q++)
 #pragma unroll
-                for (int sl = 0; sl < NSL; sl++) {
-                    if (KEEP && CHEB_FUSED_HINTS)
-                        x[q][sl] = ldnc2_hint(p + pp[sl], policy_evict_last());
-                    else
-                        x[q][sl] = CG ? ldcg2(p + pp[sl]) : ldg2(p + pp[sl]);
+                    for (int sl = 0; sl < NSL; sl++)
+                        wd[q][sl] = __ldg(a.sbits + (size_t)(uint32_t)c[q] * G::WORDS + (pp[sl] >> 5));
+#pragma unroll
+                for (int q = 0; q < CHEB_NNZ_UNROLL; q++)
+#pragma unroll
+                    for (int sl = 0; sl < NSL; sl++)
+                        x[q][sl] = make_double2(pm1(wd[q][sl], pp[sl] & 31), pm1(wd[q][sl], (pp[sl] & 31) + 1));
+            } else {
+#pragma unroll
+                for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
+                    const double* p = xg + (size_t)(uint32_t)c[q] * K;
+#pragma unroll
+                    for (int sl = 0; sl < NSL; sl++) {
+                        if (KEEP && CHEB_FUSED_HINTS)
+                            x[q][sl] = ldnc2_hint(p + pp[sl], policy_evict_last());
+                        else
+                            x[q][sl] = CG ? ldcg2(p + pp[sl]) : ldg2(p + pp[sl]);
+                    }
                 }
             }
 #pragma unroll
@@ -686,8 +717,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         if (MODE == MODE_BTB || ((ndw >> (i & 31)) & 1u)) {
 #pragma unroll
             for (int sl = 0; sl < NSL; sl++) {
-                if (MODE != MODE_BTB && !OWN_SMEM && !OWN_EARLY)
-                    own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
+                if (MODE != MODE_BTB && !OWN_SMEM && !OWN_EARLY) {
+                    if (VB == 1) {
+                        const uint32_t wv = sg_s[lr * G::WORDS + (pp[sl] >> 5)];
+                        own[sl] = make_double2(pm1(wv, pp[sl] & 31), pm1(wv, (pp[sl] & 31) + 1));
+                    } else {
+                        own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
+                    }
+                }
                 g[sl].x = fma(-a.beta, own[sl].x, g[sl].x);
                 g[sl].y = fma(-a.beta, own[sl].y, g[sl].y);
             }
@@ -707,7 +744,13 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             if (FIRST) {
                 nw[sl] = g[sl];
             } else {
-                const double2 pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
+                double2 pv;
+                if (VB == 2) {  // w_{j-2} = v: from the staged sign bits
+                    const uint32_t wv = sg_s[lr * G::WORDS + (pp[sl] >> 5)];
+                    pv = make_double2(pm1(wv, pp[sl] & 31), pm1(wv, (pp[sl] & 31) + 1));
+                } else {
+                    pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
+                }
                 nw[sl] = make_double2(2.0 * g[sl].x - pv.x, 2.0 * g[sl].y - pv.y);
             }
         }
@@ -750,7 +793,7 @@ __host__ __device__ constexpr int min_ctas(int mode, bool dbl = false) {
     return mode == MODE_CSR ? (dbl ? CHEB_MIN_CTAS_DBL : CHEB_MIN_CTAS) : (mode == MODE_RANK1 && !dbl ? 3 : 2);
 }
 
-template <int K, int MODE, bool FIRST, bool DBL = false>
+template <int K, int MODE, bool FIRST, bool DBL = false, int VB = 0>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_step_kernel(StepArgs a) {
     // DBL: 16-row tiles (CHEB_RPG_DBL) with the own W_cur rows staged by TMA for w_{j-1}^T w_j
@@ -758,7 +801,7 @@ cheb_step_kernel(StepArgs a) {
     // L1/L2 load of the own row; staging with 32-row tiles shrinks L1 too much)
     constexpr int R4 = DBL ? CHEB_RPG_DBL : CHEB_RPG;
     using G = Geo<K, R4>;
-    constexpr bool WCS = DBL && CHEB_DBL_STAGE_WC;
+    constexpr bool WCS = DBL && CHEB_DBL_STAGE_WC && VB != 1;  // step 1 on sign bits: v from the bits
     using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int NS = kStepStages;
@@ -800,17 +843,19 @@ cheb_step_kernel(StepArgs a) {
         s_base_c[b] = c0;
         s_base_v[b] = v0;
         const uint32_t wbytes = (uint32_t)rows * K * 8;
-        const uint32_t sgbytes = DBL ? 0u : ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;  // DBL: no signs
+        constexpr bool SIGNS = !DBL || VB != 0;  // DBL reads no sign bits, except for v itself
+        const uint32_t sgbytes = SIGNS ? ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u : 0u;
         uint32_t bytes = G::RPBYTES + sgbytes;
-        if (!FIRST) bytes += wbytes;
+        if (!FIRST && VB != 2) bytes += wbytes;
         if (SL::HAS_WC) bytes += wbytes;
         if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
         const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
         if (HAS_S && a.r1u) bytes += ubytes;
         mbar_expect_tx(&bar[b], bytes);
         bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
-        if (!DBL) bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
-        if (!FIRST) bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
+        if (SIGNS) bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
+        if (!FIRST && VB != 2)
+            bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
         if (SL::HAS_WC) bulk_g2s(st + SL::OFF_WCUR, a.wcur + (size_t)r0 * K, wbytes, &bar[b]);
         if (fit) {
             bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
@@ -852,10 +897,10 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                acc, a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS, R4>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
+            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
                                                                 a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);

@@ -311,7 +311,24 @@ struct FusionPlan {
     int G = 0;                // fused grid (= the single-step grid, for bit-identical moments)
     bool power = false;       // power basis (Taylor baseline): w_j = Ã w_{j-1}, every step "FIRST"
     bool doubling = false;    // moment doubling: ceil(n/2) applications of Ã give mu_0..mu_n
+    bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
 };
+
+// launch of a sign-bit step variant (own attribute for its dynamic shared memory)
+template <int K, int MODE, bool FIRST, bool DBL, int VB>
+void launch_step(int grid, size_t smem, cudaStream_t st, const StepArgs& a) {
+    if (VB == 0) {
+        cheb_step_kernel<K, MODE, FIRST, DBL><<<grid, kThreads, smem, st>>>(a);
+        return;
+    }
+    static bool attr = false;  // benign race: the attribute value is the same for every caller
+    if (!attr) {
+        cudaFuncSetAttribute(cheb_step_kernel<K, MODE, FIRST, DBL, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(200 * 1024));
+        attr = true;
+    }
+    cheb_step_kernel<K, MODE, FIRST, DBL, VB><<<grid, kThreads, smem, st>>>(a);
+}
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
 template <int K, int MODE>
@@ -355,7 +372,8 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         const int grid = grid_for(probe_init_kernel<K, MODE>, niter, sms);
         a.mu_col = 0;
         a.s_next = sbuf;
-        probe_init_kernel<K, MODE><<<grid, kThreads, init_smem, st>>>(a, seed, (uint64_t)p0, w[0], sbits);
+        probe_init_kernel<K, MODE><<<grid, kThreads, init_smem, st>>>(a, seed, (uint64_t)p0,
+                                                                    fp.vbits ? nullptr : w[0], sbits);
         g_launches++;
     }
     if (n < 1) return CL_OK;
@@ -453,15 +471,24 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.s_next = sbuf + (j & 1) * K;
         a.mu_col = j;
         ProfScope ps(st);
+        // steps 1 and 2 read v = w_0 from the sign bits when it was not materialised (fp.vbits);
+        // same grids as the plain kernels, so the moments are bit-identical either way
+        constexpr int V1 = MODE != MODE_BTB ? 1 : 0, V2 = MODE != MODE_BTB ? 2 : 0;
+        const bool vb1 = fp.vbits && j == 1, vb2 = fp.vbits && j == 2 && !fp.power;
         if (fp.doubling) {
-            if (j == 1)
-                cheb_step_kernel<K, MODE, true, true><<<grid_first, kThreads, smem_step, st>>>(a);
-            else
-                cheb_step_kernel<K, MODE, false, true><<<grid_step, kThreads, smem_step, st>>>(a);
+            if (j == 1) {
+                if (vb1) launch_step<K, MODE, true, true, V1>(grid_first, smem_step, st, a);
+                else cheb_step_kernel<K, MODE, true, true><<<grid_first, kThreads, smem_step, st>>>(a);
+            } else {
+                if (vb2) launch_step<K, MODE, false, true, V2>(grid_step, smem_step, st, a);
+                else cheb_step_kernel<K, MODE, false, true><<<grid_step, kThreads, smem_step, st>>>(a);
+            }
         } else if (j == 1 || fp.power) {  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
-            cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem_step, st>>>(a);
+            if (vb1) launch_step<K, MODE, true, false, V1>(grid_first, smem_step, st, a);
+            else cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem_step, st>>>(a);
         } else {
-            cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem_step, st>>>(a);
+            if (vb2) launch_step<K, MODE, false, false, V2>(grid_step, smem_step, st, a);
+            else cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem_step, st>>>(a);
         }
         g_launches++;
     }
@@ -876,6 +903,8 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         fp.on = g_fusion.load() >= 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
     }
+    // per-step csr/rank-1 without fused pairs: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
+    fp.vbits = !fp.persistent && !fp.on && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
     if (getenv("CHEB_DEBUG"))
         fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d doubling=%d H=%lld D=%lld\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
