@@ -381,6 +381,29 @@ class Estimator:
         self.enqueue_moments(stream)
         return self.enqueue_finalize(stream)
 
+    def capture(self):
+        """Capture one whole estimate (operator prep, probe init, every step launch, finalize) into
+        a CUDA graph; returns (replay, gamma_p, stats): replay() re-runs it with one launch call on
+        the capture stream's successors and refreshes gamma_p / stats in place.  Useful when many
+        small estimates are served (launch gaps dominate below ~1 ms per estimate); the schedule
+        switches (persistent / fusion / doubling) in effect at capture time are baked in (fusion
+        mode 2 is not capturable: it synchronises to read the operator bandwidth)."""
+        s = torch.cuda.Stream(device=self.mu.device)
+        s.wait_stream(torch.cuda.current_stream(self.mu.device))
+        with torch.cuda.stream(s):
+            self.run(s)  # warm-up outside the capture: kernel attributes, lazy module loading
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gp, stats = self.run(s)
+
+        def replay():
+            g.replay()
+            return gp, stats
+
+        self._graph = g  # keep the graph (and its memory pool) alive with the estimator
+        return replay, gp, stats
+
 
 def log_abs_det_from_btb(gamma: float) -> float:
     """Alg. 2: log|det B| = 1/2 log det B^T B ([a,b] form: the

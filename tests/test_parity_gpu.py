@@ -481,3 +481,23 @@ def test_fusion_auto_at_config2_size(orc, fusion_mode, persistent_mode):
     assert np.allclose(single, fused, rtol=1e-13, atol=1e-13 * wl.d)
     mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, wl.seed, [0, 63], workers=2)
     _check_moments(fused[[0, 63]], mu, wl.d)
+
+
+@pytest.mark.parametrize("name", ["gmrf32", "torus_s", "btb_s", "gmrf_s"])
+def test_cuda_graph_replay_identical(name):
+    """A captured estimate replays to the bit-identical result of an eager run."""
+    wl = W.get_workload(name)
+    A, At = _mats(wl)
+    op = _dev_op(wl.mode, A, At, wl.r1_c)
+    a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+    m = wl.num_probes
+    k = next(kk for kk in (8, 16, 32, 64, 128) if kk >= min(m, 64))
+    est = P.Estimator(op, a, b, wl.degree, m, k, seed=wl.seed)
+    gp0, st0 = est.run()
+    torch.cuda.synchronize()
+    gp0, st0 = gp0.clone(), st0.clone()
+    replay, gp, st = est.capture()
+    for _ in range(3):
+        replay()
+    torch.cuda.synchronize()
+    assert torch.equal(st, st0) and torch.equal(gp, gp0)
