@@ -1750,24 +1750,32 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         }
         __syncthreads();
         // ---- canonical reductions of step j's partials: CTA c owns probes c, c+G, ...
+        // rank-1: s_j = u^T w_j gates the next step, so it is reduced and published first; the
+        // moments follow off the critical path (the parity-double-buffered partials of step j are
+        // next overwritten in step j+2, which starts after this CTA publishes s_{j+1})
+        if (HAS_S) {
+            for (int p = blockIdx.x; p < K; p += gridDim.x) {
+                const double sv = reduce_partials_one(part + (size_t)(NCH - 1) * gridDim.x * K, K, (int)gridDim.x, p, wbuf);
+                if (tid == 0) pa_.s_buf[(j & 1) * K + p] = sv;
+            }
+            if (tid == 0) {
+                const unsigned int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+                if (mine) red_release_add(pa_.s_count, mine);
+            }
+        }
         for (int p = blockIdx.x; p < K; p += gridDim.x) {
             double v[NCH];
 #pragma unroll
-            for (int ch = 0; ch < NCH; ch++)
+            for (int ch = 0; ch < (HAS_S ? NCH - 1 : NCH); ch++)
                 v[ch] = reduce_partials_one(part + (size_t)ch * gridDim.x * K, K, (int)gridDim.x, p, wbuf);
             if (tid == 0 && p < a.kvalid) {
                 double* row = a.mu_out + (size_t)p * a.mu_stride;
                 if (DBL) dbl_write(row, j, a.mu_stride - 1, v[0], v[1]);
                 else row[j] = v[0];
             }
-            if (HAS_S && tid == 0) pa_.s_buf[(j & 1) * K + p] = v[NCH - 1];
         }
         if (HAS_S) {
-            if (tid == 0) {
-                const unsigned int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-                if (mine) red_release_add(pa_.s_count, mine);
-                spin_until_geq(pa_.s_count, (unsigned int)j * K, pa_.err);  // every s_j published
-            }
+            if (tid == 0) spin_until_geq(pa_.s_count, (unsigned int)j * K, pa_.err);  // every s_j published
             __syncthreads();
             if (tid < K) s_sh[tid] = __ldcg(pa_.s_buf + (j & 1) * K + tid);
             __syncthreads();
