@@ -95,7 +95,8 @@ size_t cheb_workspace_bytes(const cl_operator *op, int32_t probe_block);
  * = v_p^T T_j(Ã) v_p, j = 0..degree (DEVICE array).  All CSR / u pointers are
  * DEVICE pointers.  Probes are addressed by global index, so sharding never
  * changes a probe.  `stream` is a cudaStream_t (NULL = legacy default).
- * Allocates nothing; `workspace` must hold cheb_workspace_bytes(op, k) bytes.
+ * Allocates nothing; `workspace` must hold cheb_workspace_bytes(op, k) bytes and may be used
+ * by one call at a time (calls on different streams need separate workspaces).
  * Non-finite moments are NOT detected here (see cheb_finalize / cheb_logdet). */
 int cheb_moments(const cl_operator *op, double a, double b, int32_t degree,
                  int64_t probe_begin, int64_t probe_end, uint64_t seed,
