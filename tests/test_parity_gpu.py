@@ -501,3 +501,18 @@ def test_cuda_graph_replay_identical(name):
         replay()
     torch.cuda.synchronize()
     assert torch.equal(st, st0) and torch.equal(gp, gp0)
+
+
+def test_rank1_ones_general_path_when_rows_do_not_sum_to_zero(orc, persistent_mode):
+    """u = 1 on an operator whose rows do not sum to zero (a GMRF: S 1 != 0) must take the
+    general u^T w reduction path (the eigenvector shortcut only applies when S 1 = 0 exactly)."""
+    wl = W.get_workload("gmrf_s")
+    A, _ = _mats(wl)
+    c = 1e-4
+    op = _dev_op("rank1", A, None, c)
+    a, b = wl.a, wl.b + c * A.n_rows
+    for persist in (0, 2):
+        persistent_mode(persist)
+        r = P.logdet(op, a, b, 30, 12, seed=6, k=16, want_moments=True)
+        mu = orc.moments(orc.Op("rank1", A, c), a, b, 30, 6, range(12), workers=4)
+        _check_moments(r.moments, mu, A.n_rows)
