@@ -118,8 +118,15 @@ class ClockSampler:
                           if r[5 + i].lower() == "active"})
         if not sm:
             return None
+        pw = []
+        for r in rows:
+            try:
+                pw.append(float(r[3]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": reasons}
+                "power_w_median": float(np.median(pw)) if pw else None, "samples": len(sm),
+                "reasons": reasons}
 
 
 def build_workload(name):

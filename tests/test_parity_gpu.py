@@ -516,3 +516,19 @@ def test_rank1_ones_general_path_when_rows_do_not_sum_to_zero(orc, persistent_mo
         r = P.logdet(op, a, b, 30, 12, seed=6, k=16, want_moments=True)
         mu = orc.moments(orc.Op("rank1", A, c), a, b, 30, 6, range(12), workers=4)
         _check_moments(r.moments, mu, A.n_rows)
+
+
+def test_host_entry_arena_reuse_across_operators(orc):
+    """cheb_logdet_host reuses (and grows) its per-thread device arenas across calls with
+    operators of different sizes and modes; every result equals the device-operator call."""
+    P.release_cache()
+    cases = [("gmrf32", 8), ("btb_s", 8), ("gmrf32", 16), ("torus_s", 8)]
+    for name, k in cases:
+        wl = W.get_workload(name)
+        A, At = _mats(wl)
+        op = _dev_op(wl.mode, A, At, wl.r1_c)
+        a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
+        rd = P.logdet(op, a, b, 12, 9, seed=3, k=k, want_moments=True)
+        rh = P.logdet_host(wl.mode, A, a, b, 12, 9, seed=3, k=k, At=At, c=wl.r1_c, want_moments=True)
+        assert np.array_equal(rd.moments, rh.moments) and rd.logdet == rh.logdet, name
+    P.release_cache()
