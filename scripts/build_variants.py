@@ -38,10 +38,13 @@ VARIANTS = {
     "dr1c4": ["CHEB_RPG=1", "CHEB_MIN_CTAS_DBL=4"],
     "wc4s2": ["CHEB_FUSEDW_MIN_CTAS=4", "CHEB_FUSEDW_STAGES=2"],
     "w4": ["CHEB_FUSEDW_STAGES=4", "CHEB_FUSEDW_MIN_CTAS=2"],
-    "p8c2": ["CHEB_PPL=8", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
-    "p8u3c3": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
-    "p8u3c2": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2"],
-    "p8u5c3": ["CHEB_PPL=8", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3"],
+    # 8 probes per lane needs >= 2 rows per lane group at PPL 4, also for the doubling kernels
+    "p8c2": ["CHEB_PPL=8", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2", "CHEB_RPG_DBL=2", "CHEB_DBL_STAGE_WC=0"],
+    "p8u3c3": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3", "CHEB_RPG_DBL=2",
+               "CHEB_DBL_STAGE_WC=0"],
+    "p8u3c2": ["CHEB_PPL=8", "CHEB_NNZ_UNROLL=3", "CHEB_MIN_CTAS=2", "CHEB_MIN_CTAS_DBL=2", "CHEB_RPG_DBL=2",
+               "CHEB_DBL_STAGE_WC=0"],
+    "p8u5c3": ["CHEB_PPL=8", "CHEB_MIN_CTAS=3", "CHEB_MIN_CTAS_DBL=3", "CHEB_RPG_DBL=2", "CHEB_DBL_STAGE_WC=0"],
 }
 
 if __name__ == "__main__":
