@@ -228,6 +228,18 @@ int cheb_set_fusion(int32_t steps);
 int cheb_set_doubling(int32_t on);
 int cheb_get_doubling(void);
 
+/* Gather-staged step kernels for CL_OP_CSR with probe blocks k >= 16 (process-wide; default 0;
+ * env CHEB_GATHER).  A pass after the operator prep lists, per tile of 1024/k rows, the unique
+ * rows of W_cur its nonzeros reference (at most 4096/k) and gives every nonzero a 16-bit slot
+ * in that list; each step then fetches the listed rows into shared memory with TMA tile::gather4
+ * (a tensor map over W_cur) and the compute warps read their neighbours from shared memory.
+ * Applies to the per-step Algorithm-1 schedule only (not persistent / fused / doubling / power);
+ * operators whose tiles exceed the capacity keep the regular kernels.  cheb_moments then
+ * synchronises its stream once after the list pass.  Moments are deterministic (static tile map)
+ * but round differently from the regular kernels.  CL_EINVAL for other values. */
+int cheb_set_gather(int32_t on);
+int cheb_get_gather(void);
+
 /* cheb_logdet / cheb_logdet_host keep their device workspace (and cheb_logdet_host the device
  * copy of the operator) in grow-only per-thread arenas, so repeated estimates do not pay a
  * multi-GB cudaMalloc/cudaFree per call.  cheb_release_cache() frees the calling thread's

@@ -83,6 +83,8 @@ def load():
         "cheb_set_doubling": (I, [I32]),
         "cheb_get_doubling": (I, []),
         "cheb_release_cache": (I, []),
+        "cheb_set_gather": (I, [I32]),
+        "cheb_get_gather": (I, []),
         "cheb_last_error": (ctypes.c_char_p, []),
         "cheb_version": (I, []),
     }

@@ -325,6 +325,15 @@ def set_doubling(on: bool):
     check(_lib.load().cheb_set_doubling(1 if on else 0))
 
 
+def set_gather(on: bool):
+    """Gather-staged step kernels (csr, k >= 16; TMA tile::gather4 of each tile's rows)."""
+    check(_lib.load().cheb_set_gather(1 if on else 0))
+
+
+def get_gather() -> bool:
+    return bool(_lib.load().cheb_get_gather())
+
+
 def release_cache():
     """Free this thread's device arenas of cheb_logdet / cheb_logdet_host."""
     check(_lib.load().cheb_release_cache())

@@ -25,6 +25,7 @@
 #pragma once
 #include <cassert>
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 // CHEB_CHECKS=1 builds (scripts/build_variants.py "checked") turn on device-side bounds
@@ -175,6 +176,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
             : "=r"(done)
             : "r"(addr), "r"(phase)
             : "memory");
+    } while (!done);
+}
+// mbar_wait with a bounded spin: sets *err and gives up instead of hanging the GPU (new kernels)
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t phase, unsigned int* err) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0, spins = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(phase)
+            : "memory");
+        if (!done && ++spins > (1u << 22)) {
+            atomicExch(err, 1u);
+            return;
+        }
     } while (!done);
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -1781,6 +1800,299 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             __syncthreads();
         }
     }
+}
+
+// ---------------------------------------------------------------------------------------
+// Gather-staged step (opt-in, CSR): per tile of T = 1024/K rows, the sorted unique rows of W_cur the
+// tile's nonzeros reference ("gather list", at most S = 4096/K rows) are fetched into shared memory
+// by TMA tile::gather4 (4 rows per instruction); every nonzero carries a 16-bit slot into that
+// list instead of its column, so the compute warps read their neighbours from shared memory.
+// ---------------------------------------------------------------------------------------
+__host__ __device__ constexpr int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+template <int K>
+struct GsGeo {
+    static_assert(K >= 16, "gather-staged kernels: K >= 16");
+    static constexpr int T = 1024 / K;        // rows per tile (one row per lane group of 256 threads)
+    static constexpr int S = 4096 / K;        // gather-list capacity (32 KB of W_cur rows)
+    static constexpr int CAPV = T * 8;        // staged nonzeros per tile (padded CSR)
+    static constexpr int WORDS = words_for(K);
+    static constexpr int OFF_GATH = 0;
+    static constexpr int OFF_WPREV = OFF_GATH + S * K * 8;
+    static constexpr int OFF_VAL = OFF_WPREV + T * K * 8;
+    static constexpr int OFF_SL = OFF_VAL + (CAPV + 4) * 8;
+    static constexpr int OFF_RP = OFF_SL + ((CAPV + 16) * 2 + 15) / 16 * 16;
+    static constexpr int OFF_SGN = OFF_RP + (T + 2) * 8;
+    static constexpr int BYTES = (OFF_SGN + ((T * WORDS * 4 + 15) / 16) * 16 + 1023) / 1024 * 1024;  // TMA dst alignment
+};
+
+// One warp per tile: sort the tile's (padded) columns in shared memory (bitonic), compact the
+// unique ones into gl[t*S ..], pad the list to a multiple of 4 with its last row, and write each
+// nonzero's slot (lower_bound in the list).  Tiles with more than CAPV nonzeros or S unique rows
+// set *ovf (the host then keeps the regular kernels for this operator).
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+gather_list_kernel(int64_t d, int64_t ntiles, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                   int32_t* __restrict__ gl, int32_t* __restrict__ gl_len, uint16_t* __restrict__ sl,
+                   unsigned int* __restrict__ ovf) {
+    using GG = GsGeo<K>;
+    constexpr int C2 = next_pow2(GG::CAPV);
+    __shared__ int32_t buf[kThreads / 32][C2];
+    __shared__ int32_t uq[kThreads / 32][GG::S + 4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t t = (int64_t)blockIdx.x * (kThreads / 32) + warp; t < ntiles; t += (int64_t)gridDim.x * (kThreads / 32)) {
+        const int64_t r0 = t * GG::T;
+        const int64_t r1 = imin64(r0 + GG::T, d);
+        const int64_t e0 = rp[r0], e1 = rp[r1];
+        const int n = (int)(e1 - e0);
+        if (n > GG::CAPV) {
+            if (lane == 0) {
+                gl_len[t] = -1;
+                atomicOr(ovf, 1u);
+            }
+            continue;
+        }
+        int32_t* b = buf[warp];
+        for (int x = lane; x < C2; x += 32) b[x] = x < n ? ci[e0 + x] : 0x7fffffff;
+        __syncwarp();
+        int np = 1;
+        while (np < n) np <<= 1;
+        for (int k2 = 2; k2 <= np; k2 <<= 1)
+            for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+                for (int x = lane; x < np; x += 32) {
+                    const int y = x ^ j2;
+                    if (y > x) {
+                        const bool up = (x & k2) == 0;
+                        const int32_t bx = b[x], by = b[y];
+                        if ((bx > by) == up) {
+                            b[x] = by;
+                            b[y] = bx;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        // compact the unique values (warp ballot prefix per 32-chunk)
+        int u = 0;
+        for (int base = 0; base < np; base += 32) {
+            const int x = base + lane;
+            const bool keep = x < n && (x == 0 || b[x] != b[x - 1]);
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            const int pos = u + __popc(m & ((1u << lane) - 1u));
+            if (keep && pos < GG::S) uq[warp][pos] = b[x];
+            u += __popc(m);
+        }
+        __syncwarp();
+        if (u > GG::S) {
+            if (lane == 0) {
+                gl_len[t] = -1;
+                atomicOr(ovf, 1u);
+            }
+            continue;
+        }
+        const int u4 = n == 0 ? 0 : (u + 3) & ~3;
+        for (int x = lane; x < u4; x += 32) gl[t * GG::S + x] = uq[warp][x < u ? x : u - 1];
+        if (lane == 0) gl_len[t] = u4;
+        for (int x = lane; x < n; x += 32) {  // slot of each nonzero: lower_bound in uq
+            const int32_t c = ci[e0 + x];
+            int lo = 0, hi = u;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (uq[warp][mid] < c) lo = mid + 1;
+                else hi = mid;
+            }
+            sl[e0 + x] = (uint16_t)lo;
+        }
+        __syncwarp();
+    }
+}
+
+struct GsArgs {
+    const int32_t* gl;      // [ntiles][S] gather rows of each tile (multiple of 4 used)
+    const int32_t* gl_len;  // [ntiles] used entries of gl (multiple of 4)
+    const uint16_t* sl;     // [padded nnz] slot of each nonzero in its tile's gather list
+    int64_t ntiles;         // tiles of GsGeo<K>::T rows
+    unsigned int* err;      // wait-timeout flag (never hang)
+};
+
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tmap, int32_t col, int4 rows,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Gather-staged fused Chebyshev step (CSR, Algorithm 1).  Warps 0..7 compute (one row per lane
+// group, T rows per tile), warp 8 stages tiles: gather list + row bounds (one warp-wide load),
+// expect_tx, then every lane issues its own gather4 of 4 list rows, lane 0 the bulk copies of
+// W_prev, the tile's values / slots, row pointers and sign words; NS-deep pipeline with
+// full/empty mbarriers.  Static tile -> CTA map (t = c + i*G) and per-CTA partial sums: moments are
+// deterministic.  The gather source W_cur is described by a 2D tensor map [d][K] fp64, box {K, 1}.
+#ifndef CHEB_GS_STAGES
+#define CHEB_GS_STAGES 2
+#endif
+template <int K, bool FIRST>
+__global__ void __launch_bounds__(kThreads + 32, 2)
+cheb_step_gs_kernel(StepArgs a, GsArgs g, const __grid_constant__ CUtensorMap tmap) {
+    using GG = GsGeo<K>;
+    using G = Geo<K>;
+    constexpr int NS = CHEB_GS_STAGES;
+    static_assert(G::GROUPS == GG::T, "one row per lane group");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[NS], empty[NS];
+    __shared__ int64_t s_v0[NS], s_s0[NS], s_e0[NS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nmine = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    double acc[1][kPPL];
+#pragma unroll
+    for (int q = 0; q < kPPL; q++) acc[0][q] = 0.0;
+    if (tid == 0) {
+        for (int x = 0; x < NS; x++) {
+            mbar_init(&full[x], 1);
+            mbar_init(&empty[x], kThreads / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kThreads / 32) {
+        // ------------------------------------------------------------------ producer warp
+        // metadata of a tile (list length, the list, row bounds): all loads issued together and
+        // one tile ahead, so their latency overlaps the current tile's staging
+        constexpr int LPL = (GG::S / 4 + 31) / 32;  // int4 list chunks per lane
+        struct Meta {
+            int len;
+            int4 gr[LPL];
+            int64_t e0, e1;
+        };
+        auto load_meta = [&](int64_t t, Meta& m) {
+            const int64_t r0 = t * GG::T;
+            const int rows = (int)imin64((int64_t)GG::T, a.d - r0);
+            m.len = __ldg(g.gl_len + t);
+#pragma unroll
+            for (int c = 0; c < LPL; c++) {
+                const int x = lane + 32 * c;
+                m.gr[c] = x < GG::S / 4 ? __ldg(reinterpret_cast<const int4*>(g.gl + t * GG::S) + x) : make_int4(0, 0, 0, 0);
+            }
+            m.e0 = __ldg(a.rp + r0);
+            m.e1 = __ldg(a.rp + r0 + rows);
+        };
+        Meta cur, nxt;
+        if (nmine > 0) load_meta(blockIdx.x, nxt);
+        for (int64_t it = 0; it < nmine; it++) {
+            const int b = (int)(it % NS);
+            cur = nxt;
+            if (it + 1 < nmine) load_meta((int64_t)blockIdx.x + (it + 1) * gridDim.x, nxt);
+            if (it >= NS) mbar_wait_bounded(&empty[b], (uint32_t)(((it / NS) - 1) & 1), g.err);
+            const int64_t t = (int64_t)blockIdx.x + it * gridDim.x;
+            const int64_t r0 = t * GG::T;
+            const int rows = (int)imin64((int64_t)GG::T, a.d - r0);
+            const int len = cur.len;  // multiple of 4, <= S
+            unsigned char* st = smem + b * GG::BYTES;
+            if (lane == 0) {
+                const int64_t e0 = cur.e0, e1 = cur.e1;
+                const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
+                const int64_t s0 = e0 & ~int64_t(7), s1 = (e1 + 7) & ~int64_t(7);
+                s_v0[b] = v0;
+                s_s0[b] = s0;
+                s_e0[b] = e0;
+                const uint32_t wbytes = (uint32_t)rows * K * 8;
+                const uint32_t sgbytes = ((uint32_t)rows * GG::WORDS * 4 + 15) & ~15u;
+                uint32_t bytes = (uint32_t)len * K * 8 + (uint32_t)(GG::T + 2) * 8 + sgbytes +
+                                 (uint32_t)(v1 - v0) * 8 + (uint32_t)(s1 - s0) * 2;
+                if (!FIRST) bytes += wbytes;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[b])),
+                             "r"(bytes)
+                             : "memory");
+                bulk_g2s(st + GG::OFF_RP, a.rp + r0, (GG::T + 2) * 8, &full[b]);
+                bulk_g2s(st + GG::OFF_SGN, a.sbits + (size_t)r0 * GG::WORDS, sgbytes, &full[b]);
+                if (!FIRST)
+                    bulk_g2s_hint(st + GG::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &full[b], policy_evict_first());
+                bulk_g2s(st + GG::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &full[b]);
+                bulk_g2s(st + GG::OFF_SL, g.sl + s0, (uint32_t)(s1 - s0) * 2, &full[b]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < LPL; c++) {  // every 4-row chunk of the list: one gather4
+                const int x = lane + 32 * c;
+                if (4 * x < len) tma_gather4(st + GG::OFF_GATH + (size_t)x * 4 * K * 8, &tmap, 0, cur.gr[c], &full[b]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ compute warps
+        const int lg = tid % G::L, grp = tid / G::L;
+        int pp[G::NSL];
+#pragma unroll
+        for (int sl = 0; sl < G::NSL; sl++) pp[sl] = 2 * lg + sl * G::SS;
+        for (int64_t it = 0; it < nmine; it++) {
+            const int b = (int)(it % NS);
+            mbar_wait_bounded(&full[b], (uint32_t)((it / NS) & 1), g.err);
+            const unsigned char* st = smem + b * GG::BYTES;
+            const int64_t t = (int64_t)blockIdx.x + it * gridDim.x;
+            const int64_t r0 = t * GG::T;
+            const int rows = (int)imin64((int64_t)GG::T, a.d - r0);
+            const int lr = grp;
+            if (lr < rows) {
+                const int64_t i = r0 + lr;
+                const int64_t* rp_s = reinterpret_cast<const int64_t*>(st + GG::OFF_RP);
+                const double* val_s = reinterpret_cast<const double*>(st + GG::OFF_VAL);
+                const uint16_t* sl_s = reinterpret_cast<const uint16_t*>(st + GG::OFF_SL);
+                const double* gath = reinterpret_cast<const double*>(st + GG::OFF_GATH);
+                const double* wp_s = reinterpret_cast<const double*>(st + GG::OFF_WPREV);
+                const uint32_t* sg_s = reinterpret_cast<const uint32_t*>(st + GG::OFF_SGN);
+                const uint32_t ndw = __ldg(a.nodiag + (i >> 5));
+                const int ov = (int)(rp_s[lr] - s_v0[b]), os = (int)(rp_s[lr] - s_s0[b]);
+                const int nr = (int)(rp_s[lr + 1] - rp_s[lr]);
+                double2 g2[G::NSL];
+#pragma unroll
+                for (int sl = 0; sl < G::NSL; sl++) g2[sl] = make_double2(0.0, 0.0);
+                for (int t0 = 0; t0 < nr; t0 += CHEB_NNZ_UNROLL) {
+#pragma unroll
+                    for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
+                        const double v = val_s[ov + t0 + q];
+                        const double* xr = gath + (int)sl_s[os + t0 + q] * K;
+#pragma unroll
+                        for (int sl = 0; sl < G::NSL; sl++) {
+                            const double2 x = *reinterpret_cast<const double2*>(xr + pp[sl]);
+                            g2[sl].x = fma(v, x.x, g2[sl].x);
+                            g2[sl].y = fma(v, x.y, g2[sl].y);
+                        }
+                    }
+                }
+                if ((ndw >> (i & 31)) & 1u) {  // no stored diagonal: -beta w_{j-1}[i]
+#pragma unroll
+                    for (int sl = 0; sl < G::NSL; sl++) {
+                        const double2 o = ldg2(a.wcur + (size_t)i * K + pp[sl]);
+                        g2[sl].x = fma(-a.beta, o.x, g2[sl].x);
+                        g2[sl].y = fma(-a.beta, o.y, g2[sl].y);
+                    }
+                }
+                double* out = a.wnext + (size_t)i * K;
+#pragma unroll
+                for (int sl = 0; sl < G::NSL; sl++) {
+                    double2 nw = g2[sl];
+                    if (!FIRST) {
+                        const double2 pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
+                        nw = make_double2(2.0 * g2[sl].x - pv.x, 2.0 * g2[sl].y - pv.y);
+                    }
+                    __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw);
+                    const uint32_t bits = sg_s[lr * GG::WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
+                    acc[0][2 * sl] += signflip(nw.x, bits << 31);
+                    acc[0][2 * sl + 1] += signflip(nw.y, bits << 30);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);
+        }
+    }
+    __syncthreads();  // stage buffers become the reduction scratch
+    grid_reduce_finish<K, kPPL, 1, EPI_STEP, false, true>(acc, a, smem);
 }
 
 // ---------------------------------------------------------------------------------------

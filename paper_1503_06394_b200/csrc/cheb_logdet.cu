@@ -63,6 +63,7 @@ int env_int(const char* name, int dflt) {
 std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};  // 1 off (default), 2 auto, 3 forced, 4 forced static
 std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
 std::atomic<int> g_doubling{env_int("CHEB_DOUBLING", 0)};      // 0 off (default), 1 moment doubling
+std::atomic<int> g_gather{env_int("CHEB_GATHER", 0)};          // 0 off (default), 1 gather-staged steps
 
 struct ProfScope {
     cudaStream_t s;
@@ -151,7 +152,8 @@ int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL))
 
 struct Layout {
     size_t w0, w1, y, sbits, part, sbuf, ticket;
-    size_t rp2, ci2, va2, nodiag, u2, cnt, misc, cnt64, scan, total;
+    size_t rp2, ci2, va2, nodiag, u2, cnt, misc, cnt64, scan, gl, gl_len, sl, total;
+    int64_t gs_ntiles;
     size_t scan_bytes;
     int64_t rp2_len;
 };
@@ -185,6 +187,16 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.nodiag = off; off += align256(((size_t)d / 32 + 1) * sizeof(uint32_t));
     L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
     L.cnt = off; off += align256(((size_t)ntiles + 64) * sizeof(unsigned int));  // fused wave counters
+    // gather-staged kernels (csr, k >= 16): per-tile gather lists and per-nonzero slots
+    L.gs_ntiles = 0;
+    L.gl = L.gl_len = L.sl = off;
+    if (kind == CL_OP_CSR && k >= 16) {
+        const int T = 1024 / k, S = 4096 / k;
+        L.gs_ntiles = (d + T - 1) / T;
+        L.gl = off; off += align256((size_t)L.gs_ntiles * S * sizeof(int32_t));
+        L.gl_len = off; off += align256((size_t)L.gs_ntiles * sizeof(int32_t));
+        L.sl = off; off += align256((pnnz + 16) * sizeof(uint16_t));
+    }
     L.misc = off; off += 256;  // [0] u64 bandwidth, [8] u32 wait-timeout flag, [16] barrier count,
                                // [20] barrier generation, [24] rank-1 s_ready
     L.total = off;
@@ -312,7 +324,34 @@ struct FusionPlan {
     bool power = false;       // power basis (Taylor baseline): w_j = Ã w_{j-1}, every step "FIRST"
     bool doubling = false;    // moment doubling: ceil(n/2) applications of Ã give mu_0..mu_n
     bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
+    bool gather = false;      // gather-staged step kernels (csr): TMA gather4 of each tile's rows
+    CUtensorMap tmap[2];      // W buffers 0/1 as [d][k] fp64 tensors (gather mode)
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda
+// dependency, so the library still loads on machines without a driver).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int encode_rows_map(CUtensorMap* m, void* base, int64_t d, int k) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return fail(CL_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        fn = (EncodeTiledFn)p;
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)k, (cuuint64_t)d};
+    cuuint64_t gstride[1] = {(cuuint64_t)k * 8};
+    cuuint32_t box[2] = {(cuuint32_t)k, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CL_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return CL_OK;
+}
 
 // launch of a sign-bit step variant (own attribute for its dynamic shared memory)
 template <int K, int MODE, bool FIRST, bool DBL, int VB>
@@ -471,6 +510,28 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.s_next = sbuf + (j & 1) * K;
         a.mu_col = j;
         ProfScope ps(st);
+        if (MODE == MODE_CSR && fp.gather) {  // gather-staged steps (Algorithm 1, csr)
+            if constexpr (K >= 16) {
+                using GG = GsGeo<K>;
+                GsArgs gs{};
+                gs.gl = (const int32_t*)(ws + L.gl);
+                gs.gl_len = (const int32_t*)(ws + L.gl_len);
+                gs.sl = (const uint16_t*)(ws + L.sl);
+                gs.ntiles = L.gs_ntiles;
+                gs.err = (unsigned int*)(ws + L.misc + 8);
+                const size_t smem_gs = std::max<size_t>((size_t)CHEB_GS_STAGES * GG::BYTES, red_scratch_bytes<K, 1>());
+                const int grid_gs = (int)std::min<int64_t>((int64_t)sms * 2, L.gs_ntiles);
+                if (j == 1) {
+                    cudaFuncSetAttribute(cheb_step_gs_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gs);
+                    cheb_step_gs_kernel<K, true><<<grid_gs, kThreads + 32, smem_gs, st>>>(a, gs, fp.tmap[(j - 1) & 1]);
+                } else {
+                    cudaFuncSetAttribute(cheb_step_gs_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gs);
+                    cheb_step_gs_kernel<K, false><<<grid_gs, kThreads + 32, smem_gs, st>>>(a, gs, fp.tmap[(j - 1) & 1]);
+                }
+                g_launches++;
+                continue;
+            }
+        }
         // steps 1 and 2 read v = w_0 from the sign bits when it was not materialised (fp.vbits);
         // same grids as the plain kernels, so the moments are bit-identical either way
         constexpr int V1 = MODE != MODE_BTB ? 1 : 0, V2 = MODE != MODE_BTB ? 2 : 0;
@@ -649,6 +710,14 @@ int cheb_set_doubling(int32_t on) {
 }
 
 int cheb_get_doubling(void) { return g_doubling.load(); }
+
+int cheb_set_gather(int32_t on) {
+    if (on < 0 || on > 1) return fail(CL_EINVAL, "gather mode must be 0 or 1");
+    g_gather = on;
+    return CL_OK;
+}
+
+int cheb_get_gather(void) { return g_gather.load(); }
 
 int cheb_set_fusion(int32_t steps) {
     if (steps < 1 || steps > 5) return fail(CL_EINVAL, "fusion mode must be 1..5");
@@ -903,12 +972,34 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         fp.on = g_fusion.load() >= 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
     }
+    // gather-staged steps (opt-in): csr, Algorithm 1, per-step schedule, k >= 16; needs every tile's
+    // nonzeros / unique rows within capacity (checked by the list-building pass: one sync)
+    if (g_gather.load() == 1 && op->kind == CL_OP_CSR && probe_block >= 16 && !fp.persistent && !fp.on && !power &&
+        !fp.doubling && L.gs_ntiles > 0) {
+        unsigned int* ovf = (unsigned int*)(ws + L.misc + 44);
+        const int grid = (int)std::min<int64_t>((L.gs_ntiles + 7) / 8, (int64_t)sms * 16);
+        switch (probe_block) {
+            case 16: gather_list_kernel<16><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
+            case 32: gather_list_kernel<32><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
+            case 64: gather_list_kernel<64><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
+            default: gather_list_kernel<128><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
+        }
+        g_launches++;
+        unsigned int hovf = 1;
+        CL_CUDA(cudaMemcpyAsync(&hovf, ovf, sizeof(hovf), cudaMemcpyDeviceToHost, st));
+        CL_CUDA(cudaStreamSynchronize(st));
+        fp.gather = (hovf == 0);
+        if (fp.gather) {
+            if ((rc = encode_rows_map(&fp.tmap[0], ws + L.w0, op->A.n_cols, probe_block))) return rc;
+            if ((rc = encode_rows_map(&fp.tmap[1], ws + L.w1, op->A.n_cols, probe_block))) return rc;
+        }
+    }
     // per-step csr/rank-1 without fused pairs: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
-    fp.vbits = !fp.persistent && !fp.on && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
+    fp.vbits = !fp.persistent && !fp.on && !fp.gather && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
     if (getenv("CHEB_DEBUG"))
-        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d doubling=%d H=%lld D=%lld\n",
+        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d doubling=%d gather=%d H=%lld D=%lld\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
-                (int)fp.on, (int)fp.doubling, (long long)fp.H, (long long)fp.D);
+                (int)fp.on, (int)fp.doubling, (int)fp.gather, (long long)fp.H, (long long)fp.D);
     for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
         const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;

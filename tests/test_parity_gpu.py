@@ -532,3 +532,41 @@ def test_host_entry_arena_reuse_across_operators(orc):
         rh = P.logdet_host(wl.mode, A, a, b, 12, 9, seed=3, k=k, At=At, c=wl.r1_c, want_moments=True)
         assert np.array_equal(rd.moments, rh.moments) and rd.logdet == rh.logdet, name
     P.release_cache()
+
+
+@pytest.fixture
+def gather_mode():
+    yield P.set_gather
+    P.set_gather(False)
+
+
+@pytest.mark.parametrize("name", ["gmrf_s", "gmrf32", "spd"])
+@pytest.mark.parametrize("k", [16, 32, 64, 128])
+def test_gather_staged_parity(orc, gather_mode, persistent_mode, name, k):
+    """Gather-staged steps (TMA gather4 of each tile's unique rows) against the oracle, and
+    deterministic run to run; 'spd' is the paper's 5.1 random SPD matrix as a CSR operator
+    (random columns: long gather lists, ragged rows) with its Gershgorin interval."""
+    persistent_mode(0)
+    gather_mode(True)
+    if name == "spd":
+        A = W.random_spd(3001, 4)
+        op = _dev_op("csr", A)
+        a, b, n, m, seed, d = 1e-3, P.norm_bound(op), 20, 20, 3, A.n_rows
+    else:
+        wl = W.get_workload(name)
+        A, _ = _mats(wl)
+        op = _dev_op("csr", A)
+        a, b, n, m, seed, d = wl.a, wl.b, wl.degree, wl.num_probes, wl.seed, wl.d
+    r = P.logdet(op, a, b, n, m, seed=seed, k=k, want_moments=True)
+    mu = orc.moments(orc.Op("csr", A), a, b, n, seed, range(m), workers=4)
+    _check_moments(r.moments, mu, d)
+    g, _, _ = orc.gamma_from_moments(orc.coeffs_log(a, b, n), mu)
+    assert abs(r.logdet - g) <= GAMMA_RTOL * abs(g)
+    r2 = P.logdet(op, a, b, n, m, seed=seed, k=k, want_moments=True)
+    assert np.array_equal(r.moments, r2.moments)
+
+
+def test_gather_staged_full_config2(orc, gather_mode, persistent_mode):
+    persistent_mode(0)
+    gather_mode(True)
+    _full_size(orc, "gmrf1000", 64, [0, 63])
