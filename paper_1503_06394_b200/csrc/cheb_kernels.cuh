@@ -1808,6 +1808,9 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
 // by TMA tile::gather4 (4 rows per instruction); every nonzero carries a 16-bit slot into that
 // list instead of its column, so the compute warps read their neighbours from shared memory.
 // ---------------------------------------------------------------------------------------
+#ifndef CHEB_GS_LIST
+#define CHEB_GS_LIST 3328  // gather-list capacity x k: 52 rows at k = 64 (5-point stencil tiles need 50)
+#endif
 __host__ __device__ constexpr int next_pow2(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -1818,7 +1821,7 @@ template <int K>
 struct GsGeo {
     static_assert(K >= 16, "gather-staged kernels: K >= 16");
     static constexpr int T = 1024 / K;        // rows per tile (one row per lane group of 256 threads)
-    static constexpr int S = 4096 / K;        // gather-list capacity (32 KB of W_cur rows)
+    static constexpr int S = (CHEB_GS_LIST / K) & ~3;  // gather-list capacity (rows, multiple of 4)
     static constexpr int CAPV = T * 8;        // staged nonzeros per tile (padded CSR)
     static constexpr int WORDS = words_for(K);
     static constexpr int OFF_GATH = 0;
@@ -1936,7 +1939,7 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tmap, 
 // full/empty mbarriers.  Static tile -> CTA map (t = c + i*G) and per-CTA partial sums: moments are
 // deterministic.  The gather source W_cur is described by a 2D tensor map [d][K] fp64, box {K, 1}.
 #ifndef CHEB_GS_STAGES
-#define CHEB_GS_STAGES 2
+#define CHEB_GS_STAGES 3
 #endif
 template <int K, bool FIRST>
 __global__ void __launch_bounds__(kThreads + 32, 2)

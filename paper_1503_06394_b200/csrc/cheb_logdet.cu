@@ -191,7 +191,7 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.gs_ntiles = 0;
     L.gl = L.gl_len = L.sl = off;
     if (kind == CL_OP_CSR && k >= 16) {
-        const int T = 1024 / k, S = 4096 / k;
+        const int T = 1024 / k, S = (CHEB_GS_LIST / k) & ~3;
         L.gs_ntiles = (d + T - 1) / T;
         L.gl = off; off += align256((size_t)L.gs_ntiles * S * sizeof(int32_t));
         L.gl_len = off; off += align256((size_t)L.gs_ntiles * sizeof(int32_t));

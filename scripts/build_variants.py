@@ -32,6 +32,8 @@ VARIANTS = {
     "ffence": ["CHEB_FUSED_FENCE=1"],
     "w2": ["CHEB_FUSEDW_STAGES=2"],
     "pf1": ["CHEB_L2_PREFETCH=1"],
+    "gs2w": ["CHEB_GS_STAGES=2", "CHEB_GS_LIST=4096"],
+    "gs4s": ["CHEB_GS_STAGES=4", "CHEB_GS_LIST=2048"],
     "wc4": ["CHEB_FUSEDW_MIN_CTAS=4"],
     "dr1wc4": ["CHEB_RPG=1", "CHEB_DBL_STAGE_WC=1", "CHEB_MIN_CTAS_DBL=4"],
     "dr1wc3": ["CHEB_RPG=1", "CHEB_DBL_STAGE_WC=1", "CHEB_MIN_CTAS_DBL=3"],
