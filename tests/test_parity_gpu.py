@@ -570,3 +570,12 @@ def test_gather_staged_full_config2(orc, gather_mode, persistent_mode):
     persistent_mode(0)
     gather_mode(True)
     _full_size(orc, "gmrf1000", 64, [0, 63])
+
+
+@pytest.mark.slow
+def test_fused_pairs_full_config3(orc, fusion_mode, persistent_mode):
+    """Fused step pairs (fusion mode 2: warp-specialised, dynamic tickets) at the headline size
+    in the bench launch configuration (k = 64, two blocks), sampled probes vs the oracle."""
+    persistent_mode(0)
+    fusion_mode(2)
+    _full_size(orc, "gmrf5000", 64, [0, 127])
