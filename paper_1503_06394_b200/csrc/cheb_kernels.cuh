@@ -650,6 +650,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     const double* wc_s = reinterpret_cast<const double*>(st + SL::OFF_WCUR);
     const uint32_t* sg_s = reinterpret_cast<const uint32_t*>(st + SL::OFF_SGN);
     const double* u_s = reinterpret_cast<const double*>(st + SL::OFF_U);
+    const double* xl = xg + pp[0];
 #pragma unroll
     for (int rr = 0; rr < G::RPG; rr++) {
         const int lr = grp + rr * G::GROUPS;
@@ -710,13 +711,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             } else {
 #pragma unroll
                 for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                    const double* p = xg + (size_t)(uint32_t)c[q] * K;
+                    // lane offset folded into the base: one IMAD.WIDE per gathered row
+                    const double* p = xl + (size_t)(uint32_t)c[q] * K;
 #pragma unroll
                     for (int sl = 0; sl < NSL; sl++) {
                         if (KEEP && CHEB_FUSED_HINTS)
-                            x[q][sl] = ldnc2_hint(p + pp[sl], policy_evict_last());
+                            x[q][sl] = ldnc2_hint(p + sl * G::SS, policy_evict_last());
                         else
-                            x[q][sl] = CG ? ldcg2(p + pp[sl]) : ldg2(p + pp[sl]);
+                            x[q][sl] = CG ? ldcg2(p + sl * G::SS) : ldg2(p + sl * G::SS);
                     }
                 }
             }
