@@ -772,7 +772,8 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                 } else {
                     pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
                 }
-                nw[sl] = make_double2(2.0 * g[sl].x - pv.x, 2.0 * g[sl].y - pv.y);
+                // 2g - p in one DFMA: 2g is exact, so this rounds exactly like (g + g) - p
+                nw[sl] = make_double2(fma(2.0, g[sl].x, -pv.x), fma(2.0, g[sl].y, -pv.y));
             }
         }
         double* out = wout + (size_t)i * K;
@@ -2084,7 +2085,7 @@ cheb_step_gs_kernel(StepArgs a, GsArgs g, const __grid_constant__ CUtensorMap tm
                     double2 nw = g2[sl];
                     if (!FIRST) {
                         const double2 pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
-                        nw = make_double2(2.0 * g2[sl].x - pv.x, 2.0 * g2[sl].y - pv.y);
+                        nw = make_double2(fma(2.0, g2[sl].x, -pv.x), fma(2.0, g2[sl].y, -pv.y));
                     }
                     __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw);
                     const uint32_t bits = sg_s[lr * GG::WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
