@@ -252,6 +252,13 @@ __device__ __forceinline__ double pm1(uint32_t w, int b) {
 }
 
 // x with its sign bit xor'ed by bit 31 of m (exactly -x or x)
+// 8-byte global -> shared async copy (LDGSTS): the data never occupies a register
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ double signflip(double x, uint32_t m) {
     return __hiloint2double(__double2hiint(x) ^ (int)(m & 0x80000000u), __double2loint(x));
 }
@@ -280,7 +287,6 @@ struct StepArgs {
     const int32_t* ci;    //   padded col copy
     const double* va;     //   padded scaled values (alpha*a, diagonal alpha*a_ii - beta)
     const unsigned long long* bw;  // operator bandwidth max|i - col| (device), nullptr: no prefetch
-    const uint32_t* nodiag;  // bit i: row i has no stored diagonal (csr/rank1)
     const double* xg;     // gather source: W_cur (csr/rank1) or Y = B W_cur (btb)
     const double* wcur;   // W_cur
     double* wnext;        // in: W_prev (unless FIRST); out: W_next (in place)
@@ -476,20 +482,36 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
 // loop needs no bounds checks.  cnt[i] = ceil(nnz_i / U) * U, cnt[d] = 0 (exclusive-scanned into
 // the prepped row pointer).
 __global__ void __launch_bounds__(kThreads)
-prep_count_kernel(int64_t d, const int64_t* __restrict__ rp, int64_t* __restrict__ cnt) {
+prep_count_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int with_diag,
+                  int64_t* __restrict__ cnt) {
     constexpr int U = CHEB_NNZ_UNROLL;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= d; i += (int64_t)gridDim.x * blockDim.x)
-        cnt[i] = i < d ? (rp[i + 1] - rp[i] + U - 1) / U * U : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= d; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == d) {
+            cnt[i] = 0;
+            continue;
+        }
+        int64_t len = rp[i + 1] - rp[i];
+        if (with_diag) {  // csr / rank-1: one extra slot for the -beta entry of a row with no stored diagonal
+            bool has = false;
+            for (int64_t e = rp[i]; e < rp[i + 1]; e++) has |= (ci[e] == i);
+            len += has ? 0 : 1;
+        }
+        cnt[i] = (len + U - 1) / U * U;
+    }
 }
 
 // rp2: prepped row pointer (exclusive scan of the padded lengths, entries [0, d]); this kernel
-// writes the scaled entries of row i at rp2[i].. and pads the row with (i, 0.0).
+// writes the scaled entries of row i at rp2[i].. and pads the row with (i, 0.0).  A csr / rank-1
+// row with no stored diagonal gets (i, -beta) as its first padding entry (prep_count_kernel reserved
+// the slot), so every row of Ã = alpha M - beta I is a plain sparse row: the step kernels have no
+// diagonal special case, and the order of operations is the same as adding -beta w_{j-1}[i] after
+// the row's stored entries (the remaining padding adds exact zeros).
 template <int MODE>
 __global__ void __launch_bounds__(kThreads)
 prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ va, double alpha, double beta, int64_t* __restrict__ rp2,
             int64_t rp2_len, int32_t* __restrict__ ci2, double* __restrict__ va2,
-            uint32_t* __restrict__ nodiag, const double* __restrict__ u, double* __restrict__ u2,
+            const double* __restrict__ u, double* __restrict__ u2,
             unsigned long long* __restrict__ bw) {
     const int64_t total = rp2[d];  // padded nnz
     int64_t bwmax = 0;  // operator bandwidth max |i - col| (temporal fusion planning)
@@ -513,14 +535,12 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
                 const int64_t dist = c > i ? c - i : i - c;
                 bwmax = dist > bwmax ? dist : bwmax;
             }
-            for (int64_t o = o0 + (e1 - e0); o < o1; o++) {  // padding: (i, 0.0)
+            for (int64_t o = o0 + (e1 - e0); o < o1; o++) {  // padding: (i, 0.0); first: (i, -beta) if no diagonal
                 ci2[o] = (int32_t)i;
-                va2[o] = 0.0;
+                va2[o] = (!has && o == o0 + (e1 - e0)) ? -beta : 0.0;
             }
             if (u2) u2[i] = u ? u[i] : 1.0;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, !has);
-        if ((threadIdx.x & 31) == 0 && i < d) nodiag[i >> 5] = m;
     }
     if (bw) {
 #pragma unroll
@@ -658,8 +678,6 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         const int64_t i = r0 + lr;
         const int64_t e_lo = rp_s[lr], e_hi = rp_s[lr + 1];
         CHEB_ASSERT(rows <= G::TILE && i < a.d && e_lo <= e_hi);
-        // "no stored diagonal" flag word, loaded before the gathers so its latency overlaps them
-        const uint32_t ndw = (MODE == MODE_BTB) ? 0u : __ldg(a.nodiag + (i >> 5));
         // 32-bit row-local offsets (a row's nnz and its staged slice fit in int32)
         const int nr = (int)(e_hi - e_lo);
         const int oc = STAGED ? (int)(e_lo - base_c) : 0;
@@ -730,22 +748,15 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                     g[sl].y = fma(v[q], x[q][sl].y, g[sl].y);
                 }
         }
-        // -beta * w_{j-1}[i] where it is not folded into a stored diagonal
         if (OWN_SMEM) {
 #pragma unroll
             for (int sl = 0; sl < NSL; sl++) own[sl] = *reinterpret_cast<const double2*>(wc_s + lr * K + pp[sl]);
         }
-        if (MODE == MODE_BTB || ((ndw >> (i & 31)) & 1u)) {
+        // -beta w_{j-1}[i]: csr / rank-1 carry it in the prepped matrix (the folded diagonal, or an
+        // (i, -beta) entry the prep added to a row with none); B^T B has no matrix diagonal to fold into
+        if (MODE == MODE_BTB) {
 #pragma unroll
             for (int sl = 0; sl < NSL; sl++) {
-                if (MODE != MODE_BTB && !OWN_SMEM && !OWN_EARLY) {
-                    if (VB == 1) {
-                        const uint32_t wv = sg_s[lr * G::WORDS + (pp[sl] >> 5)];
-                        own[sl] = make_double2(pm1(wv, pp[sl] & 31), pm1(wv, (pp[sl] & 31) + 1));
-                    } else {
-                        own[sl] = CG ? ldcg2(wrow + pp[sl]) : ldg2(wrow + pp[sl]);
-                    }
-                }
                 g[sl].x = fma(-a.beta, own[sl].x, g[sl].x);
                 g[sl].y = fma(-a.beta, own[sl].y, g[sl].y);
             }
@@ -832,6 +843,7 @@ cheb_step_kernel(StepArgs a) {
     __shared__ __align__(8) uint64_t bar[NS];
     __shared__ int64_t s_base_c[NS], s_base_v[NS];
     __shared__ int s_fit[NS];
+    __shared__ __align__(16) int64_t s_ne[2];  // row bounds of the next tile to stage (cp.async)
 
     const int tid = threadIdx.x;
     double acc[NCH][kPPL];
@@ -896,7 +908,14 @@ cheb_step_kernel(StepArgs a) {
         e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
     };
 
-    int64_t ne0 = 0, ne1 = 0;
+    // thread 0 fetches the next tile's row bounds into shared memory with cp.async (no register
+    // live across the tile, no stall), and reads them after the tile, just before staging it
+    auto bounds_async = [&](int64_t t) {
+        const int64_t r0 = t * G::TILE;
+        cp_async8(&s_ne[0], a.rp + r0);
+        cp_async8(&s_ne[1], a.rp + imin64(r0 + G::TILE, a.d));
+        cp_async_commit();
+    };
     if (tid == 0) {
 #pragma unroll
         for (int i = 0; i < NS; i++) mbar_init(&bar[i], 1);
@@ -913,7 +932,7 @@ cheb_step_kernel(StepArgs a) {
         const int b = (int)(it % NS);
         const uint32_t phase = (uint32_t)((it / NS) & 1);
         const int64_t t = tile_of(it);
-        if (tid == 0 && it + NS < nmine) bounds(tile_of(it + NS), ne0, ne1);  // consumed below
+        if (tid == 0 && it + NS < nmine) bounds_async(tile_of(it + NS));  // consumed below
         mbar_wait(&bar[b], phase);
         const unsigned char* st = smem + b * SL::BYTES;
         const int64_t r0 = t * G::TILE;
@@ -925,7 +944,10 @@ cheb_step_kernel(StepArgs a) {
             step_tile<K, MODE, FIRST, false, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
                                                                 a.wnext);
         __syncthreads();  // every warp is done with stage b
-        if (tid == 0 && it + NS < nmine) issue(tile_of(it + NS), b, ne0, ne1);
+        if (tid == 0 && it + NS < nmine) {
+            cp_async_wait_all();
+            issue(tile_of(it + NS), b, s_ne[0], s_ne[1]);
+        }
     }
     grid_reduce_finish<K, kPPL, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, true>(acc, a, smem);
 }
@@ -2052,7 +2074,6 @@ cheb_step_gs_kernel(StepArgs a, GsArgs g, const __grid_constant__ CUtensorMap tm
                 const double* gath = reinterpret_cast<const double*>(st + GG::OFF_GATH);
                 const double* wp_s = reinterpret_cast<const double*>(st + GG::OFF_WPREV);
                 const uint32_t* sg_s = reinterpret_cast<const uint32_t*>(st + GG::OFF_SGN);
-                const uint32_t ndw = __ldg(a.nodiag + (i >> 5));
                 const int ov = (int)(rp_s[lr] - s_v0[b]), os = (int)(rp_s[lr] - s_s0[b]);
                 const int nr = (int)(rp_s[lr + 1] - rp_s[lr]);
                 double2 g2[G::NSL];
@@ -2069,14 +2090,6 @@ cheb_step_gs_kernel(StepArgs a, GsArgs g, const __grid_constant__ CUtensorMap tm
                             g2[sl].x = fma(v, x.x, g2[sl].x);
                             g2[sl].y = fma(v, x.y, g2[sl].y);
                         }
-                    }
-                }
-                if ((ndw >> (i & 31)) & 1u) {  // no stored diagonal: -beta w_{j-1}[i]
-#pragma unroll
-                    for (int sl = 0; sl < G::NSL; sl++) {
-                        const double2 o = ldg2(a.wcur + (size_t)i * K + pp[sl]);
-                        g2[sl].x = fma(-a.beta, o.x, g2[sl].x);
-                        g2[sl].y = fma(-a.beta, o.y, g2[sl].y);
                     }
                 }
                 double* out = a.wnext + (size_t)i * K;

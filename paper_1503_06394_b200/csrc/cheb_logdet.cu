@@ -152,7 +152,7 @@ int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL))
 
 struct Layout {
     size_t w0, w1, y, sbits, part, sbuf, ticket;
-    size_t rp2, ci2, va2, nodiag, u2, cnt, misc, cnt64, scan, gl, gl_len, sl, total;
+    size_t rp2, ci2, va2, u2, cnt, misc, cnt64, scan, gl, gl_len, sl, total;
     int64_t gs_ntiles;
     size_t scan_bytes;
     int64_t rp2_len;
@@ -177,14 +177,14 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.rp2_len = ntiles * tile_rows_max(k) + 2;
     L.rp2 = off; off += align256((size_t)L.rp2_len * sizeof(int64_t));
     // rows padded to a multiple of the gather chunk: at most (U - 1) extra entries per row
-    const size_t pnnz = (size_t)nnz + (size_t)(CHEB_NNZ_UNROLL - 1) * (size_t)d;
+    // (a row with no stored diagonal gets one extra (i, -beta) entry: at most U more per row)
+    const size_t pnnz = (size_t)nnz + (size_t)CHEB_NNZ_UNROLL * (size_t)d;
     L.ci2 = off; off += align256((pnnz + 8) * sizeof(int32_t));
     L.va2 = off; off += align256((pnnz + 4) * sizeof(double));
     L.cnt64 = off; off += align256(((size_t)d + 1) * sizeof(int64_t));  // padded row lengths
     L.scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, L.scan_bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(d + 1));
     L.scan = off; off += align256(L.scan_bytes);
-    L.nodiag = off; off += align256(((size_t)d / 32 + 1) * sizeof(uint32_t));
     L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
     L.cnt = off; off += align256(((size_t)ntiles + 64) * sizeof(unsigned int));  // fused wave counters
     // gather-staged kernels (csr, k >= 16): per-tile gather lists and per-nonzero slots
@@ -287,14 +287,15 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
     int grid = (int)std::min<int64_t>((d + kThreads) / kThreads, (int64_t)sms * 8);
     if (grid < 1) grid = 1;
     // padded row pointer: lengths rounded up to the gather chunk, exclusive scan (CUB)
-    prep_count_kernel<<<grid, kThreads, 0, st>>>(d, G2.row_ptr, (int64_t*)(ws + L.cnt64));
+    prep_count_kernel<<<grid, kThreads, 0, st>>>(d, G2.row_ptr, G2.col_idx, MODE != MODE_BTB ? 1 : 0,
+                                                 (int64_t*)(ws + L.cnt64));
     size_t sb = L.scan_bytes;
     cub::DeviceScan::ExclusiveSum(ws + L.scan, sb, (const int64_t*)(ws + L.cnt64), (int64_t*)(ws + L.rp2),
                                   (int)(d + 1), st);
     g_launches += 1;  // prep_count_kernel (the CUB scan kernels are library code, not counted)
     prep_kernel<MODE><<<grid, kThreads, 0, st>>>(
         d, G2.row_ptr, G2.col_idx, G2.val, alpha, beta, (int64_t*)(ws + L.rp2), L.rp2_len,
-        (int32_t*)(ws + L.ci2), (double*)(ws + L.va2), (uint32_t*)(ws + L.nodiag),
+        (int32_t*)(ws + L.ci2), (double*)(ws + L.va2),
         MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr,
         MODE != MODE_BTB ? (unsigned long long*)(ws + L.misc) : nullptr);
     g_launches++;
@@ -389,7 +390,6 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.rp = (const int64_t*)(ws + L.rp2);
     a.ci = (const int32_t*)(ws + L.ci2);
     a.va = (const double*)(ws + L.va2);
-    a.nodiag = (const uint32_t*)(ws + L.nodiag);
     a.bw = (MODE != MODE_BTB && op->A.nnz > 0) ? (const unsigned long long*)(ws + L.misc) : nullptr;
     a.sbits = sbits;
     a.beta = beta;
