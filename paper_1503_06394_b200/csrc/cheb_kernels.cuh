@@ -1663,20 +1663,35 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     __shared__ double red[NCH][kThreads / 32][K];
     __shared__ double wbuf[kThreads / 32];
     __shared__ double s_sh[HAS_S ? K : 1];
+    // row bounds of this CTA's tiles, loaded once (they are the same every step): staging a tile
+    // then needs no global load on thread 0 (a per-tile ~1 us stall of warp 0, which the end-of-tile
+    // barrier passes on to the whole CTA); CTAs with more tiles load them at issue time
+    constexpr int kBoundsCache = 32;
+    __shared__ int64_t s_eb[2 * kBoundsCache];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = tid % G::L;
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     uint32_t uses[2] = {0u, 0u};
 
-    // staging of tile t of step j into stage b (thread 0)
-    auto issue = [&](int32_t j, int64_t t, int b) {
+    const bool cached = nmine <= kBoundsCache;
+    if (cached) {
+        for (int x = tid; x < 2 * nmine; x += kThreads) {
+            const int64_t r0 = ((int64_t)blockIdx.x + (x >> 1) * (int64_t)gridDim.x) * G::TILE;
+            s_eb[x] = __ldg(a.rp + ((x & 1) ? imin64(r0 + G::TILE, a.d) : r0));
+        }
+        __syncthreads();
+    }
+    // staging of the CTA's it-th tile of step j into stage b (thread 0)
+    auto issue = [&](int32_t j, int64_t it, int b) {
         const bool first = (j == 1) || pa_.power;
         const double* wprev = (j & 1) ? pa_.w1 : pa_.w0;  // w_{j-2}
         unsigned char* st = smem + b * SL::BYTES;
+        const int64_t t = (int64_t)blockIdx.x + it * gridDim.x;
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-        const int64_t e0 = __ldg(a.rp + r0), e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
+        const int64_t e0 = cached ? s_eb[2 * it] : __ldg(a.rp + r0);
+        const int64_t e1 = cached ? s_eb[2 * it + 1] : __ldg(a.rp + imin64(r0 + G::TILE, a.d));
         const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
         const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
         const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
@@ -1705,7 +1720,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_mbar_init();
-        for (int64_t i = 0; i < 2 && i < nmine; i++) issue(1, (int64_t)blockIdx.x + i * gridDim.x, (int)i);
+        for (int64_t i = 0; i < 2 && i < nmine; i++) issue(1, i, (int)i);
     }
     if (HAS_S && tid < K) s_sh[tid] = __ldcg(pa_.s_buf + tid);  // s_0
     __syncthreads();
@@ -1749,7 +1764,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
                                                                        nxt);
             }
             __syncthreads();
-            if (tid == 0 && it + 2 < nmine) issue(j, (int64_t)blockIdx.x + (it + 2) * gridDim.x, b);
+            if (tid == 0 && it + 2 < nmine) issue(j, it + 2, b);
         }
         // ---- per-CTA partials (same tree as grid_reduce_finish)
 #pragma unroll
@@ -1787,8 +1802,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
                 // proxy fence orders other CTAs' generic stores of w_{j-1} (step j-1, already
                 // behind the previous barrier) before these async-proxy reads.
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                for (int64_t i = 0; i < 2 && i < nmine; i++)
-                    issue(j + 1, (int64_t)blockIdx.x + i * gridDim.x, (int)i);  // stages are all consumed
+                for (int64_t i = 0; i < 2 && i < nmine; i++) issue(j + 1, i, (int)i);  // stages are all consumed
             }
             spin_until_geq(pa_.bar_count, (unsigned int)j * gridDim.x, pa_.err);  // + acquire (L1 invalidated)
         }
