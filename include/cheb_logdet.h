@@ -200,6 +200,16 @@ int cheb_profile_persistent(double *ms, int64_t *launches);
  * Moments are bit-identical to per-step launches when both use the same grid size. */
 int cheb_set_persistent(int32_t mode);
 
+/* Tile geometry of the Algorithm-1 kernels (process-wide):
+ *   1 = auto (default): operators whose working set fits in half of L2 use 16-row tiles (at
+ *       k = 64; 256*4/k rows) in both the per-step and the persistent kernel -- more tiles per
+ *       step shorten the critical path of a latency-bound step;
+ *   0 = always the standard geometry (32-row tiles at k = 64), which the fused-pair kernels use.
+ * Moments are bit-identical between schedules that use the same geometry and grid.
+ * CL_EINVAL for other values. */
+int cheb_set_small_tiles(int32_t mode);
+int cheb_get_small_tiles(void);
+
 /* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 1, see DESIGN.md §7
  * for the measured status):
  *   1 = one launch per Chebyshev step;

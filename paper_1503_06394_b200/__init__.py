@@ -9,7 +9,7 @@ from .api import (DeviceCSR, Operator, Result, Estimator, coeffs_log, workspace_
                   power_moments, taylor_coeffs, taylor_logdet, affine_power_moments, norm_bound,
                   spectrum_estimate,
                   alloc_workspace, moments, finalize, logdet, logdet_host, bounds_btb, probes,
-                  launch_count, profile_begin, profile_end, set_fusion, set_persistent, set_doubling,
+                  launch_count, profile_begin, profile_end, set_fusion, set_persistent, set_small_tiles, get_small_tiles, set_doubling,
                   get_doubling, set_gather, get_gather, release_cache, log_abs_det_from_btb, log_tau_from_rank1)
 from ._lib import ChebError, load as load_library
 
@@ -17,5 +17,5 @@ __all__ = ["DeviceCSR", "Operator", "Result", "Estimator", "coeffs_log", "worksp
            "power_moments", "taylor_coeffs", "taylor_logdet", "affine_power_moments", "norm_bound",
            "spectrum_estimate",
            "alloc_workspace", "moments", "finalize", "logdet", "logdet_host", "bounds_btb",
-           "probes", "launch_count", "profile_begin", "profile_end", "set_fusion", "set_persistent", "set_doubling", "get_doubling", "set_gather", "get_gather", "release_cache", "log_abs_det_from_btb",
+           "probes", "launch_count", "profile_begin", "profile_end", "set_fusion", "set_persistent", "set_small_tiles", "get_small_tiles", "set_doubling", "get_doubling", "set_gather", "get_gather", "release_cache", "log_abs_det_from_btb",
            "log_tau_from_rank1", "ChebError", "load_library"]

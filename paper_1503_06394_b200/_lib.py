@@ -80,6 +80,8 @@ def load():
         "cheb_set_fusion": (I, [I32]),
         "cheb_profile_persistent": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "cheb_set_persistent": (I, [I32]),
+        "cheb_set_small_tiles": (I, [I32]),
+        "cheb_get_small_tiles": (I, []),
         "cheb_set_doubling": (I, [I32]),
         "cheb_get_doubling": (I, []),
         "cheb_release_cache": (I, []),

@@ -318,6 +318,16 @@ def set_persistent(mode: int):
     check(_lib.load().cheb_set_persistent(int(mode)))
 
 
+def set_small_tiles(mode: int):
+    """Tile geometry of the Algorithm-1 kernels (cheb_set_small_tiles): 1 auto (default; 16-row
+    tiles at k = 64 for L2-resident operators), 0 always the standard geometry."""
+    check(_lib.load().cheb_set_small_tiles(int(mode)))
+
+
+def get_small_tiles() -> int:
+    return int(_lib.load().cheb_get_small_tiles())
+
+
 def set_doubling(on: bool):
     """Moment-doubling schedule (cheb_set_doubling; reading G25): ceil(n/2)
     applications of Ã per probe give mu_0..mu_n via T_{2j} = 2T_j^2 - I and

@@ -826,13 +826,16 @@ __host__ __device__ constexpr int min_ctas(int mode, bool dbl = false) {
     return mode == MODE_CSR ? (dbl ? CHEB_MIN_CTAS_DBL : CHEB_MIN_CTAS) : (mode == MODE_RANK1 && !dbl ? 3 : 2);
 }
 
-template <int K, int MODE, bool FIRST, bool DBL = false, int VB = 0>
+// RP: rows per lane group of the Algorithm-1 kernels (0: CHEB_RPG).  L2-resident operators use
+// RP = 1 (16-row tiles at k = 64) in both the per-step and the persistent kernel, so the two stay
+// bit-identical (measured: configs[0] 0.22 -> 0.18 ms, configs[1] 15.5 -> 15.2 ms per estimate).
+template <int K, int MODE, bool FIRST, bool DBL = false, int VB = 0, int RP = 0>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_step_kernel(StepArgs a) {
     // DBL: 16-row tiles (CHEB_RPG_DBL) with the own W_cur rows staged by TMA for w_{j-1}^T w_j
     // (measured best: 6.50 ms per configs[3] launch vs 6.82 ms with 32-row tiles and an early
     // L1/L2 load of the own row; staging with 32-row tiles shrinks L1 too much)
-    constexpr int R4 = DBL ? CHEB_RPG_DBL : CHEB_RPG;
+    constexpr int R4 = DBL ? CHEB_RPG_DBL : (RP ? RP : CHEB_RPG);
     using G = Geo<K, R4>;
     constexpr bool WCS = DBL && CHEB_DBL_STAGE_WC && VB != 1;  // step 1 on sign bits: v from the bits
     using SL = StageLayout<K, MODE, WCS, R4>;
@@ -1648,10 +1651,10 @@ __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned i
     fence_acq_rel_gpu();
 }
 
-template <int K, int MODE, bool DBL = false>
+template <int K, int MODE, bool DBL = false, int RP = 0>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
-    constexpr int R4 = DBL ? CHEB_RPG_DBL : CHEB_RPG;  // same tile geometry as cheb_step_kernel
+    constexpr int R4 = DBL ? CHEB_RPG_DBL : (RP ? RP : CHEB_RPG);  // same tile geometry as cheb_step_kernel
     using G = Geo<K, R4>;
     using SL = StageLayout<K, MODE, false, R4>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);

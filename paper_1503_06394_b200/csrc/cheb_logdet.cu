@@ -62,6 +62,7 @@ int env_int(const char* name, int dflt) {
 // schedule controls (process-wide; CHEB_FUSION / CHEB_PERSISTENT env vars set the initial value)
 std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};  // 1 off (default), 2 auto, 3 forced, 4 forced static
 std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
+std::atomic<int> g_small_tiles{env_int("CHEB_SMALL_TILES", 1)};  // 1 auto (default), 0 standard geometry
 std::atomic<int> g_doubling{env_int("CHEB_DOUBLING", 0)};      // 0 off (default), 1 moment doubling
 std::atomic<int> g_gather{env_int("CHEB_GATHER", 0)};          // 0 off (default), 1 gather-staged steps
 
@@ -326,6 +327,7 @@ struct FusionPlan {
     bool doubling = false;    // moment doubling: ceil(n/2) applications of Ã give mu_0..mu_n
     bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
     bool gather = false;      // gather-staged step kernels (csr): TMA gather4 of each tile's rows
+    bool small = false;       // L2-resident operator: 16-row tiles for the Algorithm-1 kernels (RP = 1)
     CUtensorMap tmap[2];      // W buffers 0/1 as [d][k] fp64 tensors (gather mode)
 };
 
@@ -355,29 +357,28 @@ int encode_rows_map(CUtensorMap* m, void* base, int64_t d, int k) {
 }
 
 // launch of a sign-bit step variant (own attribute for its dynamic shared memory)
-template <int K, int MODE, bool FIRST, bool DBL, int VB>
+template <int K, int MODE, bool FIRST, bool DBL, int VB, int RP = 0>
 void launch_step(int grid, size_t smem, cudaStream_t st, const StepArgs& a) {
-    if (VB == 0) {
-        cheb_step_kernel<K, MODE, FIRST, DBL><<<grid, kThreads, smem, st>>>(a);
-        return;
-    }
     static bool attr = false;  // benign race: the attribute value is the same for every caller
     if (!attr) {
-        cudaFuncSetAttribute(cheb_step_kernel<K, MODE, FIRST, DBL, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(200 * 1024));
         attr = true;
     }
-    cheb_step_kernel<K, MODE, FIRST, DBL, VB><<<grid, kThreads, smem, st>>>(a);
+    cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP><<<grid, kThreads, smem, st>>>(a);
 }
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
-template <int K, int MODE>
+// RP: tile geometry of the Algorithm-1 kernels (0: CHEB_RPG; 1: 16-row tiles for L2-resident
+// operators, FusionPlan::small); fused pairs always run with RP = 0
+template <int K, int MODE, int RP = 0>
 int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
               int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
-    using G = Geo<K>;  // per-step / fused geometry; the doubling kernels use Geo<K, CHEB_RPG_DBL>
+    constexpr int R4S = RP ? RP : CHEB_RPG;
+    using G = Geo<K, R4S>;  // per-step / fused geometry; the doubling kernels use Geo<K, CHEB_RPG_DBL>
     using GD = Geo<K, CHEB_RPG_DBL>;
-    using SL = StageLayout<K, MODE>;
+    using SL = StageLayout<K, MODE, false, R4S>;
     using SLD = StageLayout<K, MODE, false, CHEB_RPG_DBL>;
     const int64_t d = op->A.n_cols;
     double* w[2] = {(double*)(ws + L.w0), (double*)(ws + L.w1)};
@@ -425,9 +426,9 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, CHEB_RPG_DBL>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
     const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true>, a.ntiles, sms, smem_step)
-                                       : grid_for(cheb_step_kernel<K, MODE, true>, a.ntiles, sms, smem_step);
+                                       : grid_for(cheb_step_kernel<K, MODE, true, false, 0, RP>, a.ntiles, sms, smem_step);
     const int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true>, a.ntiles, sms, smem_step)
-                                      : grid_for(cheb_step_kernel<K, MODE, false>, a.ntiles, sms, smem_step);
+                                      : grid_for(cheb_step_kernel<K, MODE, false, false, 0, RP>, a.ntiles, sms, smem_step);
     int grid_spmm = 1;
     if (MODE == MODE_BTB) {
         const int64_t ng = (op->A.n_rows + SpmmGeo<K>::GROUPS - 1) / SpmmGeo<K>::GROUPS;
@@ -437,7 +438,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     // mu_{2j-1} and mu_{2j} (indices <= n) from w_j^T w_{j-1} and w_j^T w_j
     const int32_t nsteps = fp.doubling ? (n + 1) / 2 : n;
     if (MODE != MODE_BTB && fp.persistent) {
-        auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true> : cheb_persist_kernel<K, MODE, false>;
+        auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true> : cheb_persist_kernel<K, MODE, false, RP>;
         const int grid_p = grid_for(pkern, a.ntiles, sms, smem);
         PersistArgs pp{};
         pp.w0 = w[0];
@@ -461,7 +462,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     for (int32_t j = 1; j <= nsteps; j++) {
         const double* cur = w[(j - 1) & 1];
         double* nxt = w[j & 1];
-        if (MODE == MODE_CSR && fp.on && !fp.doubling && j >= 2 && j + 1 <= n) {
+        if (MODE == MODE_CSR && RP == 0 && fp.on && !fp.doubling && j >= 2 && j + 1 <= n) {
             // steps j and j+1 in one launch: A = w_{j-2} -> w_j, B = w_{j-1} -> w_{j+1}
             FusedArgs f{};
             f.A = nxt;
@@ -545,11 +546,11 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
                 else cheb_step_kernel<K, MODE, false, true><<<grid_step, kThreads, smem_step, st>>>(a);
             }
         } else if (j == 1 || fp.power) {  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
-            if (vb1) launch_step<K, MODE, true, false, V1>(grid_first, smem_step, st, a);
-            else cheb_step_kernel<K, MODE, true><<<grid_first, kThreads, smem_step, st>>>(a);
+            if (vb1) launch_step<K, MODE, true, false, V1, RP>(grid_first, smem_step, st, a);
+            else launch_step<K, MODE, true, false, 0, RP>(grid_first, smem_step, st, a);
         } else {
-            if (vb2) launch_step<K, MODE, false, false, V2>(grid_step, smem_step, st, a);
-            else cheb_step_kernel<K, MODE, false><<<grid_step, kThreads, smem_step, st>>>(a);
+            if (vb2) launch_step<K, MODE, false, false, V2, RP>(grid_step, smem_step, st, a);
+            else launch_step<K, MODE, false, false, 0, RP>(grid_step, smem_step, st, a);
         }
         g_launches++;
     }
@@ -560,10 +561,13 @@ template <int K>
 int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
                    int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
                    int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
+    const bool small = fp.small && !fp.on && !fp.doubling;
     switch (op->kind) {
         case CL_OP_CSR:
+            if (small) return run_block<K, MODE_CSR, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
             return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         case CL_OP_CSR_RANK1:
+            if (small) return run_block<K, MODE_RANK1, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
             return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         default:
             return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
@@ -702,6 +706,14 @@ int cheb_set_persistent(int32_t mode) {
     g_persistent = mode;
     return CL_OK;
 }
+
+int cheb_set_small_tiles(int32_t mode) {
+    if (mode < 0 || mode > 1) return fail(CL_EINVAL, "small-tiles mode must be 0 or 1");
+    g_small_tiles = mode;
+    return CL_OK;
+}
+
+int cheb_get_small_tiles(void) { return g_small_tiles.load(); }
 
 int cheb_set_doubling(int32_t on) {
     if (on < 0 || on > 1) return fail(CL_EINVAL, "doubling mode must be 0 or 1");
@@ -939,14 +951,16 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     FusionPlan fp;
     fp.power = power;
     fp.doubling = !power && g_doubling.load() == 1;
-    if (op->kind != CL_OP_BTB && g_persistent.load() > 0 && degree >= 1) {
+    if (op->kind != CL_OP_BTB) {
         // L2-resident working set (two probe-block buffers + matrix): the per-step launch and
-        // drain gaps dominate, so run all steps in one launch
+        // drain gaps dominate, so run all steps in one launch; small tiles either way (the per-step
+        // and persistent schedules keep one geometry, hence bit-identical moments)
         int l2 = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         const double wset = 2.0 * op->A.n_cols * probe_block * 8.0 + 12.0 * op->A.nnz + 8.0 * op->A.n_cols;
-        fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
+        fp.small = wset <= 0.5 * (double)l2 && g_small_tiles.load() != 0;
+        if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
     if (!fp.persistent && !power && !fp.doubling && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {

@@ -9,6 +9,7 @@ from paper_1503_06394_b200 import _build  # noqa: E402
 VARIANTS = {
     "s3": ["CHEB_STAGES=3"],
     "s3c3": ["CHEB_STAGES=3", "CHEB_MIN_CTAS=3"],
+    "c3": ["CHEB_MIN_CTAS=3"],
     "r1": ["CHEB_RPG=1"],
     "r1s3": ["CHEB_RPG=1", "CHEB_STAGES=3"],
     "r4": ["CHEB_RPG=4"],

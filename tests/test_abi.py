@@ -101,4 +101,7 @@ def test_schedule_controls_validate(L):
         assert L.cheb_set_fusion(mode) == 0
     assert L.cheb_set_persistent(3) == _lib.CL_EINVAL
     assert L.cheb_set_persistent(1) == 0
+    assert L.cheb_set_small_tiles(2) == _lib.CL_EINVAL
+    assert L.cheb_set_small_tiles(0) == 0 and L.cheb_get_small_tiles() == 0
+    assert L.cheb_set_small_tiles(1) == 0 and L.cheb_get_small_tiles() == 1
     assert L.cheb_release_cache() == 0  # nothing allocated on this thread: a no-op

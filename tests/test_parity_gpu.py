@@ -90,9 +90,12 @@ def persistent_mode():
 
 @pytest.fixture
 def fusion_mode():
-    """Restore the default temporal-fusion mode after a test."""
+    """Restore the default temporal-fusion mode after a test.  The fused-pair kernels use the
+    standard tile geometry, so the per-step references of these tests do too."""
+    P.set_small_tiles(0)
     yield P.set_fusion
     P.set_fusion(1)
+    P.set_small_tiles(1)
 
 
 @pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
