@@ -352,7 +352,7 @@ def run_ours(args):
         gather_aware = {"bytes_per_launch": ga, "achieved": ga / (avg_launch_ms / 1e3) / 1e9,
                         "frac": ga / (avg_launch_ms / 1e3) / 1e9 / hbm}
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "peak_kind": peak_kind, "kernel": kern, "bytes_per_launch": bytes_per_launch,
+            "peak_kind": peak_kind, "frac_vs_nominal_8000": achieved / 8000.0, "kernel": kern, "bytes_per_launch": bytes_per_launch,
             "avg_launch_ms": avg_launch_ms, "step_kernel_share": dom_ms / t_ms,
             "traffic": _traffic_per_launch(wl.name, k), "gather_aware": gather_aware}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
