@@ -50,10 +50,10 @@ constexpr int kThreads = 256;
 #define CHEB_MIN_CTAS_DBL 3  // moment doubling carries two more accumulator channels
 #endif
 #ifndef CHEB_DBL_STAGE_WC
-#define CHEB_DBL_STAGE_WC 1  // moment doubling stages the tile's own W_cur rows (w_{j-1}^T w_j)
+#define CHEB_DBL_STAGE_WC 0  // 1: moment doubling stages the tile's own W_cur rows (else: first gather)
 #endif
 #ifndef CHEB_RPG_DBL
-#define CHEB_RPG_DBL 1  // rows per lane group of the moment-doubling kernels (16-row tiles at k=64)
+#define CHEB_RPG_DBL 2  // rows per lane group of the moment-doubling kernels (32-row tiles at k=64)
 #endif
 #ifndef CHEB_RPG
 #define CHEB_RPG 2  // rows per lane group per tile (tile = 256*RPG*4/K rows)
@@ -502,10 +502,9 @@ prep_count_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __re
 
 // rp2: prepped row pointer (exclusive scan of the padded lengths, entries [0, d]); this kernel
 // writes the scaled entries of row i at rp2[i].. and pads the row with (i, 0.0).  A csr / rank-1
-// row with no stored diagonal gets (i, -beta) as its first padding entry (prep_count_kernel reserved
-// the slot), so every row of Ã = alpha M - beta I is a plain sparse row: the step kernels have no
-// diagonal special case, and the order of operations is the same as adding -beta w_{j-1}[i] after
-// the row's stored entries (the remaining padding adds exact zeros).
+// row's first entry is its diagonal (alpha a_ii - beta, or (i, -beta) in the slot prep_count_kernel
+// reserved when none is stored), so every row of Ã = alpha M - beta I is a plain sparse row and the
+// step kernels have no diagonal special case; padding (i, 0.0) adds exact zeros.
 template <int MODE>
 __global__ void __launch_bounds__(kThreads)
 prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -523,21 +522,40 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
             const int64_t e0 = rp[i], e1 = rp[i + 1];
             const int64_t o0 = rp2[i], o1 = rp2[i + 1];
             has = (MODE == MODE_BTB);
-            for (int64_t e = e0; e < e1; e++) {
-                const int32_t c = ci[e];
-                double v = alpha * va[e];
-                if (MODE != MODE_BTB && c == i) {
-                    v = fma(alpha, va[e], -beta);
-                    has = true;
+            int64_t o = o0;
+            if (MODE != MODE_BTB) {
+                // csr / rank-1: the diagonal entry first (alpha a_ii - beta, or -beta when none is
+                // stored), then the off-diagonal entries in CSR order: the doubling kernels take
+                // w_{j-1}[i] from the row's first gather
+                double dv = -beta;
+                o = o0 + 1;
+                for (int64_t e = e0; e < e1; e++) {
+                    const int32_t c = ci[e];
+                    if (c == i) {
+                        dv = fma(alpha, va[e], -beta);
+                        has = true;
+                    } else {
+                        ci2[o] = c;
+                        va2[o] = alpha * va[e];
+                        o++;
+                    }
+                    const int64_t dist = c > i ? c - i : i - c;
+                    bwmax = dist > bwmax ? dist : bwmax;
                 }
-                ci2[o0 + (e - e0)] = c;
-                va2[o0 + (e - e0)] = v;
-                const int64_t dist = c > i ? c - i : i - c;
-                bwmax = dist > bwmax ? dist : bwmax;
+                ci2[o0] = (int32_t)i;
+                va2[o0] = dv;
+            } else {
+                for (int64_t e = e0; e < e1; e++, o++) {
+                    const int32_t c = ci[e];
+                    ci2[o] = c;
+                    va2[o] = alpha * va[e];
+                    const int64_t dist = c > i ? c - i : i - c;
+                    bwmax = dist > bwmax ? dist : bwmax;
+                }
             }
-            for (int64_t o = o0 + (e1 - e0); o < o1; o++) {  // padding: (i, 0.0); first: (i, -beta) if no diagonal
+            for (; o < o1; o++) {  // padding: (i, 0.0)
                 ci2[o] = (int32_t)i;
-                va2[o] = (!has && o == o0 + (e1 - e0)) ? -beta : 0.0;
+                va2[o] = 0.0;
             }
             if (u2) u2[i] = u ? u[i] : 1.0;
         }
@@ -653,7 +671,9 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr int NSL = G::NSL;
     constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
-    constexpr bool OWN_EARLY = DBL && !OWN_SMEM;   // else: loaded at the row start (L1/L2-hot)
+    // csr / rank-1 doubling: w_{j-1}[i] is the row's first gather (the prepped diagonal entry)
+    constexpr bool OWN_GATHER = DBL && !OWN_SMEM && MODE != MODE_BTB;
+    constexpr bool OWN_EARLY = DBL && !OWN_SMEM && !OWN_GATHER;  // loaded at the row start
     static_assert(VB == 0 || (MODE != MODE_BTB && !CG && !KEEP && (VB != 1 || !OWN_SMEM)),
                   "sign-bit probes: per-step csr/rank-1");
     constexpr bool HAS_S = (MODE == MODE_RANK1);
@@ -739,6 +759,10 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                             x[q][sl] = CG ? ldcg2(p + sl * G::SS) : ldg2(p + sl * G::SS);
                     }
                 }
+            }
+            if (OWN_GATHER && t0 == 0) {
+#pragma unroll
+                for (int sl = 0; sl < NSL; sl++) own[sl] = x[0][sl];
             }
 #pragma unroll
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++)
@@ -835,7 +859,7 @@ cheb_step_kernel(StepArgs a) {
     // DBL: 16-row tiles (CHEB_RPG_DBL) with the own W_cur rows staged by TMA for w_{j-1}^T w_j
     // (measured best: 6.50 ms per configs[3] launch vs 6.82 ms with 32-row tiles and an early
     // L1/L2 load of the own row; staging with 32-row tiles shrinks L1 too much)
-    constexpr int R4 = DBL ? CHEB_RPG_DBL : (RP ? RP : CHEB_RPG);
+    constexpr int R4 = RP ? RP : (DBL ? CHEB_RPG_DBL : CHEB_RPG);
     using G = Geo<K, R4>;
     constexpr bool WCS = DBL && CHEB_DBL_STAGE_WC && VB != 1;  // step 1 on sign bits: v from the bits
     using SL = StageLayout<K, MODE, WCS, R4>;
@@ -1654,7 +1678,7 @@ __device__ __forceinline__ void spin_until_geq(const unsigned int* p, unsigned i
 template <int K, int MODE, bool DBL = false, int RP = 0>
 __global__ void __launch_bounds__(kThreads, min_ctas(MODE, DBL))
 cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
-    constexpr int R4 = DBL ? CHEB_RPG_DBL : (RP ? RP : CHEB_RPG);  // same tile geometry as cheb_step_kernel
+    constexpr int R4 = RP ? RP : (DBL ? CHEB_RPG_DBL : CHEB_RPG);  // same tile geometry as cheb_step_kernel
     using G = Geo<K, R4>;
     using SL = StageLayout<K, MODE, false, R4>;
     constexpr bool HAS_S = (MODE == MODE_RANK1);

@@ -377,9 +377,10 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
               int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
     constexpr int R4S = RP ? RP : CHEB_RPG;
     using G = Geo<K, R4S>;  // per-step / fused geometry; the doubling kernels use Geo<K, CHEB_RPG_DBL>
-    using GD = Geo<K, CHEB_RPG_DBL>;
+    constexpr int R4D = RP ? RP : CHEB_RPG_DBL;  // doubling kernels: same RP rule
+    using GD = Geo<K, R4D>;
     using SL = StageLayout<K, MODE, false, R4S>;
-    using SLD = StageLayout<K, MODE, false, CHEB_RPG_DBL>;
+    using SLD = StageLayout<K, MODE, false, R4D>;
     const int64_t d = op->A.n_cols;
     double* w[2] = {(double*)(ws + L.w0), (double*)(ws + L.w1)};
     double* y = (double*)(ws + L.y);
@@ -423,11 +424,11 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     // dynamic shared memory: the staged tiles, reused as the reduction scratch at the end
     const size_t smem = std::max<size_t>(fp.doubling ? SLD::SMEM : SL::SMEM, red_scratch_bytes<K, 2>());  // persistent, fused
     const size_t smem_step = std::max<size_t>(
-        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, CHEB_RPG_DBL>::BYTES : SL::BYTES),
+        (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, R4D>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
-    const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true>, a.ntiles, sms, smem_step)
+    const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true, 0, RP>, a.ntiles, sms, smem_step)
                                        : grid_for(cheb_step_kernel<K, MODE, true, false, 0, RP>, a.ntiles, sms, smem_step);
-    const int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true>, a.ntiles, sms, smem_step)
+    const int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true, 0, RP>, a.ntiles, sms, smem_step)
                                       : grid_for(cheb_step_kernel<K, MODE, false, false, 0, RP>, a.ntiles, sms, smem_step);
     int grid_spmm = 1;
     if (MODE == MODE_BTB) {
@@ -438,7 +439,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     // mu_{2j-1} and mu_{2j} (indices <= n) from w_j^T w_{j-1} and w_j^T w_j
     const int32_t nsteps = fp.doubling ? (n + 1) / 2 : n;
     if (MODE != MODE_BTB && fp.persistent) {
-        auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true> : cheb_persist_kernel<K, MODE, false, RP>;
+        auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true, RP> : cheb_persist_kernel<K, MODE, false, RP>;
         const int grid_p = grid_for(pkern, a.ntiles, sms, smem);
         PersistArgs pp{};
         pp.w0 = w[0];
@@ -539,11 +540,11 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         const bool vb1 = fp.vbits && j == 1, vb2 = fp.vbits && j == 2 && !fp.power;
         if (fp.doubling) {
             if (j == 1) {
-                if (vb1) launch_step<K, MODE, true, true, V1>(grid_first, smem_step, st, a);
-                else cheb_step_kernel<K, MODE, true, true><<<grid_first, kThreads, smem_step, st>>>(a);
+                if (vb1) launch_step<K, MODE, true, true, V1, RP>(grid_first, smem_step, st, a);
+                else launch_step<K, MODE, true, true, 0, RP>(grid_first, smem_step, st, a);
             } else {
-                if (vb2) launch_step<K, MODE, false, true, V2>(grid_step, smem_step, st, a);
-                else cheb_step_kernel<K, MODE, false, true><<<grid_step, kThreads, smem_step, st>>>(a);
+                if (vb2) launch_step<K, MODE, false, true, V2, RP>(grid_step, smem_step, st, a);
+                else launch_step<K, MODE, false, true, 0, RP>(grid_step, smem_step, st, a);
             }
         } else if (j == 1 || fp.power) {  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
             if (vb1) launch_step<K, MODE, true, false, V1, RP>(grid_first, smem_step, st, a);
@@ -561,7 +562,7 @@ template <int K>
 int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
                    int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
                    int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
-    const bool small = fp.small && !fp.on && !fp.doubling;
+    const bool small = fp.small && !fp.on;
     switch (op->kind) {
         case CL_OP_CSR:
             if (small) return run_block<K, MODE_CSR, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);

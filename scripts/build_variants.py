@@ -10,6 +10,8 @@ VARIANTS = {
     "s3": ["CHEB_STAGES=3"],
     "s3c3": ["CHEB_STAGES=3", "CHEB_MIN_CTAS=3"],
     "c3": ["CHEB_MIN_CTAS=3"],
+    "dr2": ["CHEB_RPG_DBL=2"],
+    "dwc": ["CHEB_DBL_STAGE_WC=1"],
     "r1": ["CHEB_RPG=1"],
     "r1s3": ["CHEB_RPG=1", "CHEB_STAGES=3"],
     "r4": ["CHEB_RPG=4"],
