@@ -153,8 +153,21 @@ def test_rank1_explicit_u(orc):
     _check_moments(r.moments, mu, T.n_rows)
 
 
-def test_general_csr_without_diagonal_entries(orc):
-    """Rows without a stored diagonal and empty rows (the -beta*w term must still apply)."""
+@pytest.mark.parametrize("dbl", [False, True])
+@pytest.mark.parametrize("persist", [0, 2])
+def test_general_csr_without_diagonal_entries(orc, persistent_mode, dbl, persist):
+    """Rows without a stored diagonal and empty rows (the -beta*w term must still apply): the prep
+    adds an (i, -beta) entry at the head of such a row, and the doubling kernels read w_{j-1}[i]
+    from that first gather; per-step and persistent schedules."""
+    persistent_mode(persist)
+    P.set_doubling(dbl)
+    try:
+        _csr_without_diagonal(orc)
+    finally:
+        P.set_doubling(False)
+
+
+def _csr_without_diagonal(orc):
     S = W.random_spd(3000, 4)
     rows = np.repeat(np.arange(S.n_rows), np.diff(S.row_ptr))
     keep = (rows != S.col_idx) | (rows % 7 != 0)
