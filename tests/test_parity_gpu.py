@@ -171,7 +171,9 @@ def _csr_without_diagonal(orc):
     S = W.random_spd(3000, 4)
     rows = np.repeat(np.arange(S.n_rows), np.diff(S.row_ptr))
     keep = (rows != S.col_idx) | (rows % 7 != 0)
-    keep &= ~((rows % 101) == 5)  # some rows become empty
+    # some rows (and, to keep the operator symmetric -- moment doubling assumes it -- their
+    # columns) become empty
+    keep &= ~((rows % 101) == 5) & ~((S.col_idx % 101) == 5)
     C = W.csr.from_coo(S.n_rows, S.n_cols, rows[keep], S.col_idx[keep], S.val[keep])
     lam = 1.0 + np.abs(C.val).max() * 40
     op = _dev_op("csr", C)
