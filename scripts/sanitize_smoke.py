@@ -23,12 +23,15 @@ def main():
     op_b = P.Operator("btb", dev(B), dev(W.transpose(B)))
     a, b = P.bounds_btb(op_b)
     P.probes(1000, 3, 5, 16)
-    for persist in (0, 2):
-        P.set_persistent(persist)
-        for k in (8, 64):
-            P.logdet(op_g, 0.2, 1.8, 7, 11, seed=1, k=k)
-            P.logdet(op_t, 0.01, 8.5, 7, 11, seed=1, k=k)
-            P.taylor_logdet(op_g, 2.0, 5, 9, 1, k)
+    for small in (1, 0):  # 16-row tiles for L2-resident operators (default) and the standard geometry
+        P.set_small_tiles(small)
+        for persist in (0, 2):
+            P.set_persistent(persist)
+            for k in (8, 64):
+                P.logdet(op_g, 0.2, 1.8, 7, 11, seed=1, k=k)
+                P.logdet(op_t, 0.01, 8.5, 7, 11, seed=1, k=k)
+                P.taylor_logdet(op_g, 2.0, 5, 9, 1, k)
+    P.set_small_tiles(1)
     P.set_persistent(1)
     P.logdet(op_b, a, b, 5, 9, seed=1, k=16)
     P.set_doubling(True)  # moment-doubling kernels, per step and persistent
