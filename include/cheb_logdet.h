@@ -203,7 +203,8 @@ int cheb_set_persistent(int32_t mode);
 /* Tile geometry of the Algorithm-1 kernels (process-wide):
  *   1 = auto (default): operators whose working set fits in half of L2 use 16-row tiles (at
  *       k = 64; 256*4/k rows) in both the per-step and the persistent kernel -- more tiles per
- *       step shorten the critical path of a latency-bound step;
+ *       step shorten the critical path of a latency-bound step; so do Algorithm-1 runs with
+ *       probe blocks k <= 16 (64-row instead of 128-row tiles at k = 16);
  *   0 = always the standard geometry (32-row tiles at k = 64), which the fused-pair kernels use.
  * Moments are bit-identical between schedules that use the same geometry and grid.
  * CL_EINVAL for other values. */

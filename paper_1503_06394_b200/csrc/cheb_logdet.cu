@@ -960,7 +960,9 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         const double wset = 2.0 * op->A.n_cols * probe_block * 8.0 + 12.0 * op->A.nnz + 8.0 * op->A.n_cols;
-        fp.small = wset <= 0.5 * (double)l2 && g_small_tiles.load() != 0;
+        // 16-row-per-group tiles also pay for Algorithm 1 at k <= 16 (configs[3], k = 16: 1565 vs
+        // 1608 ms per estimate), where a standard tile has 128+ rows
+        fp.small = g_small_tiles.load() != 0 && (wset <= 0.5 * (double)l2 || (probe_block <= 16 && !fp.doubling));
         if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
