@@ -2,13 +2,16 @@
 """Benchmark of the Chebyshev-Hutchinson log-det hot path (BASELINE.json metric:
 probe*Chebyshev-steps/sec, HBM GB/s vs peak, log-det wall time at 25M vars).
 
-One bench "step" = one whole estimate on this GPU's probe shard: probe
-initialisation, `degree` fused Chebyshev steps per probe block, reductions, the
-moment all-reduce (N > 1) and the device accumulation of Gamma.  Default
-workload: BASELINE configs[3] (gmrf5000: d = 2.5e7, n = 100, m = 128 probes per
-GPU, k = 64) -- weak scaling over GPUs (m = 128 * N in total).
+One bench "step" = one whole estimate: probe initialisation, `degree` fused Chebyshev steps per
+probe block, reductions, the moment all-reduce (N > 1) and the device accumulation of Gamma.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--k K]
+Headline (default): BASELINE configs[3] as the config states it -- gmrf5000 (d = 2.5e7, n = 100),
+m = 128 probes IN TOTAL sharded across the N GPUs (strong scaling), probe block k = 16 at every N
+("scaling curves use fixed k = 16, so per-GPU bytes per probe-step are identical
+across G"; 16 probes per GPU at N = 8).  Beside it, in the same JSON line, `weak_scaling`: m = 128
+probes PER GPU at the best single-GPU block size k = 64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--k K] [--scaling weak]
     python bench.py --impl reference ...    # the CPU oracle as the reference arm
 
 Under torchrun each rank drives one GPU; rank 0 prints ONE JSON line.
@@ -43,14 +46,14 @@ def _peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
-def _traffic_per_launch(workload, k):
-    """dram read+write bytes per step launch from the committed ncu --set full summary."""
+def _traffic_per_launch(workload, k, kernel="step"):
+    """dram read+write bytes per launch from the committed ncu --set full summaries."""
     p = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         j = json.load(f)
-    e = j.get(f"{workload}/k{k}")
+    e = j.get(f"{workload}/k{k}" + ("" if kernel == "step" else f"/{kernel}"))
     return float(e["dram_bytes_per_launch"]) if e else None
 
 
@@ -67,10 +70,9 @@ def step_bytes(d, nnz, k, first=False, mode="csr", doubling=False):
     return 12 * nnz + 8 * (d + 1) + vec + (0 if doubling else d * max(4, k // 8))
 
 
-def fused_bytes(d, nnz, k):
-    """cheb_step2_kernel (two steps): w_{j-1}, w_j read; w_{j+1}, w_{j+2} written;
-    matrix and sign bits once per stage."""
-    return 32 * d * k + 2 * (12 * nnz + 8 * (d + 1) + d * max(4, k // 8))
+def spmm_bytes(d, nnz_b, k):
+    """Algorithmic HBM bytes of one spmm_kernel launch (B^T B: Y = B w): B once, w read, Y written."""
+    return 12 * nnz_b + 8 * (d + 1) + 16 * d * k
 
 
 class ClockSampler:
@@ -148,6 +150,17 @@ def cpu_model():
     return None
 
 
+def plan(args, wl, world):
+    """(m_total, k, scaling) of the headline line."""
+    if args.scaling == "strong":
+        m_total = args.probes or wl.num_probes
+        k = args.k or 16
+    else:
+        m_total = (args.probes or wl.num_probes) * world
+        k = args.k or next((kk for kk in (8, 16, 32, 64) if kk >= m_total // world), 64)
+    return m_total, k
+
+
 # ------------------------------------------------------------------------- oracle (CPU) arm
 def oracle_sample(wl, A, steps_per_probe, probes, workers):
     """Time the oracle AS IT STANDS on a bounded sample: `probes` probes x
@@ -180,9 +193,11 @@ def _oracle_plan(wl, budget_s=20.0):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     wl, A, At = build_workload(args.workload)
+    m_total, k = plan(args, wl, world)
     workers, steps = _oracle_plan(wl, budget_s=args.ref_budget)
     for _ in range(args.warmup):
         oracle_sample(wl, A, 1, workers, workers)
@@ -196,8 +211,9 @@ def run_reference(args):
               f"one single-threaded oracle process per probe")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": wl.name, "d": wl.d, "degree": wl.degree,
+                                            "num_probes": m_total, "probe_block": k,
                                             "num_probes_per_step": workers, "steps_per_probe": steps},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle", "cpu_model": cpu_model(),
                             "sample": sample},
@@ -207,6 +223,86 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------- GPU arm
+def timed_region(sh, steps, flush_buf, P, torch, dist, world, dev):
+    """Time `steps` whole estimates on the device (events on the launching stream; max over
+    ranks).  With flush_buf, a 2x-L2 write precedes each estimate outside its event pair.
+    Returns (ms, profile, launches, [stats])."""
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps if flush_buf is not None else 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n_launch0 = P.launch_count()
+    P.profile_begin()
+    all_stats = []
+    if flush_buf is not None:
+        for i in range(steps):
+            flush_buf.fill_(i)
+            evs[i][0].record(stream)
+            all_stats.append(sh.run(check=False)[1])
+            evs[i][1].record(stream)
+    else:
+        evs[0][0].record(stream)
+        for _ in range(steps):
+            all_stats.append(sh.run(check=False)[1])
+        evs[0][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    prof = P.profile_end()
+    launches = P.launch_count() - n_launch0
+    elapsed = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in evs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(elapsed, op=dist.ReduceOp.MAX)
+    for s in all_stats:  # every timed estimate must be valid (raises ChebError otherwise)
+        sh.check(s)
+    return float(elapsed.item()), prof, launches, all_stats
+
+
+def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind):
+    """Roofline of the dominant kernel from its measured launch times and algorithmic bytes."""
+    d = wl.d
+    gnnz = A.nnz if wl.mode != "btb" else At.nnz  # gather matrix of the step kernel
+    (s_ms, s_n), (b_ms, b_n), (p_ms, p_n) = prof["single"], prof["spmm"], prof["persistent"]
+    dbl = bool(args.doubling)
+    gather_aware = None
+    if p_ms > s_ms:  # persistent multi-step kernel: one launch = all steps of a block
+        kern = f"cheb_persist_kernel<{k},{wl.mode}>"
+        apps = (wl.degree + 1) // 2 if dbl else wl.degree  # applications of A~ per launch
+        bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode, dbl)
+                            + (apps - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode, dbl))
+        avg_launch_ms, dom_ms, nl = p_ms / max(p_n, 1), p_ms, p_n
+    else:
+        kern = f"cheb_step_kernel<{k},{wl.mode}>"
+        per_block = s_n / max(blocks * steps, 1)
+        if args.basis == "taylor":  # power recurrence: every launch reads w_{j-1}, writes w_j
+            tot = s_n * step_bytes(d, gnnz, k, True, wl.mode)
+        else:
+            tot = blocks * steps * (step_bytes(d, gnnz, k, True, wl.mode, dbl)
+                                    + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode, dbl))
+        nl = s_n
+        if wl.mode == "btb" and b_n:
+            # one B^T B application = spmm (Y = B w) + step (B^T Y, recurrence, dots): both halves
+            kern += f" + spmm_kernel<{k}>"
+            tot += b_n * spmm_bytes(d, A.nnz, k)
+            # random columns: every gathered row of w (spmm) and of Y (step) is an HBM access
+            # (8k bytes per nonzero) rather than an L2 hit
+            ga = tot - 8 * d * k * (s_n + b_n) + 8 * k * (gnnz * s_n + A.nnz * b_n)
+            gather_aware = {"bytes_per_application": ga / nl,
+                            "achieved": ga / ((s_ms + b_ms) / 1e3) / 1e9,
+                            "frac": ga / ((s_ms + b_ms) / 1e3) / 1e9 / hbm}
+            s_ms += b_ms
+        bytes_per_launch = tot / max(nl, 1)
+        avg_launch_ms, dom_ms = s_ms / max(nl, 1), s_ms
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "peak_kind": peak_kind, "frac_vs_nominal_8000": achieved / 8000.0, "kernel": kern,
+            "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
+            "launches": int(nl), "step_kernel_share": dom_ms / t_ms,
+            "traffic": _traffic_per_launch(wl.name, k), "gather_aware": gather_aware}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -218,10 +314,9 @@ def run_ours(args):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     wl, A, At = build_workload(args.workload)
-    m_per_gpu = args.probes or wl.num_probes
-    m_total = m_per_gpu * world
-    # one block when m <= 64 (smallest k >= m: matrix read once per step), else blocks of 64
-    k = args.k or next((kk for kk in (8, 16, 32, 64) if kk >= m_per_gpu), 64)
+    m_total, k = plan(args, wl, world)
+    p0, p1 = pdist.shard_range(m_total, world, rank)
+    m_mine = p1 - p0
 
     # CPU baseline first (fork-based pool before any CUDA context exists)
     cpu = None
@@ -242,19 +337,21 @@ def run_ours(args):
     a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
     torch.cuda.synchronize()
     upload_s = time.perf_counter() - t_up
-    group = None
-    sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, group=group, basis=args.basis)
     if args.doubling:
         P.set_doubling(True)
+    sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed, basis=args.basis)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # warm-up
     for _ in range(args.warmup):
-        sh.run()
+        sh.run(check=True)
     torch.cuda.synchronize()
+
+    # L2 between timed iterations: a working set (two probe blocks + matrix) larger than L2 needs
+    # no flush; a smaller one gets a 2x-L2 buffer write between iterations, outside the per-
+    # iteration event pairs (one pair per iteration, times summed)
+    l2_bytes = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 0) or 0)
+    wset = 2 * wl.d * k * 8 + 12 * int(A.nnz + (At.nnz if At is not None else 0)) + 8 * wl.d
+    flush = l2_bytes > 0 and wset < l2_bytes
+    flush_buf = torch.empty(2 * l2_bytes // 4, dtype=torch.int32, device=dev) if flush else None
 
     # ---- timed region (device events on the launching stream; max over ranks)
     clocks = ClockSampler(None)
@@ -263,41 +360,26 @@ def run_ours(args):
         bus = getattr(props, "pci_bus_id", None)
         clocks.bus_id = None if bus is None else f":{int(bus):02X}:00."
         clocks.start()
-    stream = torch.cuda.current_stream()
-    # L2 between timed iterations: a working set (two probe blocks + matrix) larger than L2 needs
-    # no flush; a smaller one gets a 2x-L2 buffer write between iterations, outside the per-
-    # iteration event pairs (one pair per iteration, times summed)
-    l2_bytes = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 0) or 0)
-    wset = 2 * wl.d * k * 8 + 12 * int(A.nnz + (At.nnz if At is not None else 0)) + 8 * wl.d
-    flush = l2_bytes > 0 and wset < l2_bytes
-    flush_buf = torch.empty(2 * l2_bytes // 4, dtype=torch.int32, device=dev) if flush else None
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps if flush else 1)]
-    barrier()
-    torch.cuda.synchronize()
-    n_launch0 = P.launch_count()
-    P.profile_begin()
-    if flush:
-        for i in range(args.steps):
-            flush_buf.fill_(i)
-            evs[i][0].record(stream)
-            gp, stats = sh.run()
-            evs[i][1].record(stream)
-    else:
-        evs[0][0].record(stream)
-        for _ in range(args.steps):
-            gp, stats = sh.run()
-        evs[0][1].record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    prof = P.profile_end()
-    launches = P.launch_count() - n_launch0
+    t_ms, prof, launches, all_stats = timed_region(sh, args.steps, flush_buf, P, torch, dist, world, dev)
     clk = clocks.stop() if rank == 0 else None
-    elapsed = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in evs)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(elapsed, op=dist.ReduceOp.MAX)
-    t_ms = float(elapsed.item())
-    st = stats.cpu().numpy()
+    st = all_stats[-1].cpu().numpy()
+
+    # ---- weak scaling beside the headline: m per GPU fixed, best single-GPU block size
+    weak = None
+    if args.scaling == "strong" and not args.no_weak:
+        m_w = (args.probes or wl.num_probes) * world
+        k_w = next((kk for kk in (8, 16, 32, 64) if kk >= m_w // world), 64)
+        sw = pdist.ShardedEstimator(op, a, b, wl.degree, m_w, k_w, seed=wl.seed, basis=args.basis)
+        sw.run(check=True)
+        reps = max(1, min(args.steps, 3))
+        tw, profw, _, stw = timed_region(sw, reps, flush_buf, P, torch, dist, world, dev)
+        hbm, peak_kind = _peaks()
+        rw = roofline(wl, A, At, k_w, math.ceil((m_w // world) / k_w), reps, tw, profw, args, hbm, peak_kind)
+        weak = {"scaling": "weak", "num_probes": m_w, "probes_per_gpu": m_w // world, "probe_block": k_w,
+                "value": m_w * wl.degree * reps / (tw / 1e3), "unit": UNIT, "ms_per_step": tw / reps,
+                "steps": reps, "logdet_wall_s": tw / reps / 1e3, "gamma": float(stw[-1].cpu().numpy()[0]),
+                "roofline_frac": rw["frac"], "roofline_achieved_gbs": rw["achieved"]}
+        del sw
 
     # ---- the other schedule on the same operator (Algorithm 1 <-> moment doubling)
     alt = None
@@ -307,7 +389,7 @@ def run_ours(args):
     # ---- end-to-end through the public C ABI with HOST buffers (pinned)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, torch, dist)
+        e2e = run_e2e(args, wl, A, At, a, b, m_total, k, rank, world, dev, P, pdist, torch, dist)
 
     if rank != 0:
         if world > 1:
@@ -316,70 +398,36 @@ def run_ours(args):
     units = m_total * wl.degree * args.steps  # degree-n Chebyshev moments delivered per probe
     value = units / (t_ms / 1e3)
     hbm, peak_kind = _peaks()
-    d, nnz = wl.d, (A.nnz + (At.nnz if At is not None else 0))
-    gnnz = A.nnz if wl.mode != "btb" else At.nnz  # gather matrix of the step kernel
-    blocks = math.ceil(m_per_gpu / k)
-    (s_ms, s_n), (f_ms, f_n), (p_ms, p_n) = prof["single"], prof["fused"], prof["persistent"]
-    if p_ms > max(s_ms, f_ms):  # persistent multi-step kernel: one launch = all steps of a block
-        kern = f"cheb_persist_kernel<{k},{wl.mode}>"
-        apps = (wl.degree + 1) // 2 if args.doubling else wl.degree  # applications of A~ per launch
-        dbl = bool(args.doubling)
-        bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode, dbl)
-                            + (apps - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode, dbl))
-        avg_launch_ms, dom_ms = p_ms / max(p_n, 1), p_ms
-    elif f_ms > s_ms:  # temporally fused pairs dominate (static / dynamic / warp-specialised)
-        kern = f"cheb_step2[w|d]_kernel<{k}> (fusion mode {os.environ.get('CHEB_FUSION', '1')})"
-        bytes_per_launch = fused_bytes(d, gnnz, k)
-        avg_launch_ms, dom_ms = f_ms / max(f_n, 1), f_ms
-    else:
-        kern = f"cheb_step_kernel<{k},{wl.mode}>"
-        # per block and estimate: one FIRST launch, the rest full steps
-        per_block = s_n / max(blocks * args.steps, 1)
-        if args.basis == "taylor":  # power recurrence: every launch reads w_{j-1}, writes w_j
-            tot = s_n * step_bytes(d, gnnz, k, True, wl.mode)
-        else:
-            dbl = bool(args.doubling)
-            tot = blocks * args.steps * (step_bytes(d, gnnz, k, True, wl.mode, dbl)
-                                         + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode, dbl))
-        bytes_per_launch = tot / max(s_n, 1)
-        avg_launch_ms, dom_ms = s_ms / max(s_n, 1), s_ms
-    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
-    gather_aware = None
+    nnz = A.nnz + (At.nnz if At is not None else 0)
+    blocks = math.ceil(m_mine / k)
+    roof = roofline(wl, A, At, k, blocks, args.steps, t_ms, prof, args, hbm, peak_kind)
+    cfg = {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": wl.d,
+           "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total, "probes_per_gpu": m_mine,
+           "probe_block": k, "a": a, "b": b, "basis": args.basis,
+           "schedule": ("moment doubling: ceil(n/2) applications of A~ per probe, value counts "
+                        "the n Chebyshev steps delivered" if args.doubling else
+                        "Algorithm 1: n applications of A~ per probe"),
+           "applications_per_probe": (wl.degree + 1) // 2 if args.doubling else wl.degree,
+           "parallelism": f"probe-dp{world}",
+           "l2": (f"L2 flushed between timed iterations ({2 * l2_bytes / 1e6:.0f} MB write outside the "
+                  f"per-iteration events; working set {wset / 1e6:.1f} MB < L2 {l2_bytes / 1e6:.0f} MB)"
+                  if flush else f"inputs larger than L2 (working set {wset / 1e9:.1f} GB/GPU > L2), "
+                  "no flush needed"),
+           "logdet_wall_s": t_ms / args.steps / 1e3,
+           "logdet_wall_incl_generation_upload_s": build_workload.gen_s + upload_s + t_ms / args.steps / 1e3,
+           "generation_s": build_workload.gen_s, "upload_s": upload_s, "gamma": float(st[0]),
+           "stderr": float(st[1])}
     if wl.mode == "btb":
-        # random columns: every gathered row of Y is an HBM access (8k bytes) instead of an
-        # L2 hit; this is the traffic the step kernel actually has to move
-        ga = bytes_per_launch - 8 * d * k + 8 * k * gnnz
-        gather_aware = {"bytes_per_launch": ga, "achieved": ga / (avg_launch_ms / 1e3) / 1e9,
-                        "frac": ga / (avg_launch_ms / 1e3) / 1e9 / hbm}
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "peak_kind": peak_kind, "frac_vs_nominal_8000": achieved / 8000.0, "kernel": kern, "bytes_per_launch": bytes_per_launch,
-            "avg_launch_ms": avg_launch_ms, "step_kernel_share": dom_ms / t_ms,
-            "traffic": _traffic_per_launch(wl.name, k), "gather_aware": gather_aware}
+        cfg["log_abs_det_B"] = P.log_abs_det_from_btb(float(st[0]))  # Alg. 2's output
+        cfg["log_abs_det_B_stderr"] = 0.5 * float(st[1])
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-           "scaling": "weak",
+           "scaling": args.scaling,
            "vs_baseline": (value / wl.paper_probe_steps_per_s) if wl.paper_probe_steps_per_s else None,
-           "dtype": "f64", "data": "synthetic",
-           "config": {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": d,
-                      "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total,
-                      "probes_per_gpu": m_per_gpu, "probe_block": k, "a": a, "b": b,
-                      "basis": args.basis,
-                      "schedule": ("moment doubling: ceil(n/2) applications of A~ per probe, value counts "
-                                   "the n Chebyshev steps delivered" if args.doubling else
-                                   "Algorithm 1: n applications of A~ per probe"),
-                      "applications_per_probe": (wl.degree + 1) // 2 if args.doubling else wl.degree,
-                      "parallelism": f"probe-dp{world}",
-                      "l2": (f"L2 flushed between timed iterations ({2 * l2_bytes / 1e6:.0f} MB write outside the "
-                             f"per-iteration events; working set {wset / 1e6:.1f} MB < L2 {l2_bytes / 1e6:.0f} MB)"
-                             if flush else f"inputs larger than L2 (working set {wset / 1e9:.1f} GB/GPU > L2), "
-                             "no flush needed"),
-                      "logdet_wall_s": t_ms / args.steps / 1e3,
-                      "logdet_wall_incl_generation_upload_s": build_workload.gen_s + upload_s + t_ms / args.steps / 1e3,
-                      "generation_s": build_workload.gen_s, "upload_s": upload_s, "gamma": float(st[0]),
-                      "stderr": float(st[1])},
+           "dtype": "f64", "data": "synthetic", "config": cfg,
            "roofline": roof, "gpu_launches": int(launches),
            "gpu_launches_per_step": launches / args.steps, "clocks": clk, "cpu_baseline": cpu,
-           "e2e": e2e, "alt_schedule": alt}
+           "e2e": e2e, "weak_scaling": weak, "alt_schedule": alt}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -387,52 +435,48 @@ def run_ours(args):
 
 
 def run_alt_schedule(args, sh, P, torch, dist, world, dev, gamma_main):
-    """Time the other schedules on the same sharded estimator (device events, max over ranks),
-    reported beside the headline, never instead of it: moment doubling (G25) and temporally
-    fused step pairs (warp-specialised, fusion mode 2) when the headline is Algorithm 1."""
+    """Time the other moment schedule on the same sharded estimator (device events, max over
+    ranks), reported beside the headline, never instead of it: moment doubling (G25) when the
+    headline is Algorithm 1, and vice versa."""
     n = sh.est.degree
-    alts = []
     if not args.doubling:
-        alts.append(("moment doubling", (n + 1) // 2, lambda on: P.set_doubling(on)))
+        name, apps, switch = "moment doubling", (n + 1) // 2, (lambda on: P.set_doubling(on))
     else:
-        alts.append(("Algorithm 1 recurrence", n, lambda on: P.set_doubling(not on)))
-    if not args.doubling and sh.est.op.kind == "csr":
-        alts.append(("fused step pairs (fusion mode 2)", n, lambda on: P.set_fusion(2 if on else 1)))
-    out = []
-    for name, apps, switch in alts:
-        switch(True)
-        try:
-            sh.run()
-            torch.cuda.synchronize()
-            reps = max(1, min(args.steps, 3))
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if world > 1:
-                dist.barrier()
-            ev0.record()
-            for _ in range(reps):
-                gp, stats = sh.run()
-            ev1.record()
-            torch.cuda.synchronize()
-            el = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(el, op=dist.ReduceOp.MAX)
-            g = float(stats.cpu().numpy()[0])
-        finally:
-            switch(False)
-        wall = float(el.item()) / reps / 1e3
-        out.append({"schedule": name, "applications_per_probe": apps, "logdet_wall_s": wall,
-                    "chebyshev_steps_per_s": sh.est.m * n / wall, "gamma": g,
-                    "rel_diff_gamma_vs_headline": abs(g - gamma_main) / abs(gamma_main), "reps": reps})
-    return out
+        name, apps, switch = "Algorithm 1 recurrence", n, (lambda on: P.set_doubling(not on))
+    switch(True)
+    try:
+        sh.run(check=True)
+        torch.cuda.synchronize()
+        reps = max(1, min(args.steps, 3))
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        ev0.record()
+        for _ in range(reps):
+            gp, stats = sh.run(check=False)
+        ev1.record()
+        torch.cuda.synchronize()
+        sh.check(stats)
+        el = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        g = float(stats.cpu().numpy()[0])
+    finally:
+        switch(False)
+    wall = float(el.item()) / reps / 1e3
+    return [{"schedule": name, "applications_per_probe": apps, "logdet_wall_s": wall,
+             "chebyshev_steps_per_s": sh.est.m * n / wall, "gamma": g,
+             "rel_diff_gamma_vs_headline": abs(g - gamma_main) / abs(gamma_main), "reps": reps}]
 
 
-def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, torch, dist):
-    """Same metric end to end: every step copies the operator from pinned host
-    memory to the device, runs the estimate through the public API and reads the
-    result back to the host."""
+def run_e2e(args, wl, A, At, a, b, m_total, k, rank, world, dev, P, pdist, torch, dist):
+    """Same metric end to end through the C ABI with HOST buffers: every step copies the operator
+    from pinned host memory to the device, runs the estimate and reads the result back.
+    N = 1: cheb_logdet_host.  N > 1: every rank calls cheb_moments_host for its probe shard (H2D
+    of the CSR, moments, D2H of its moment rows), the zero-padded tables are summed with one NCCL
+    all_reduce and cheb_finalize accumulates Gamma (device), read back to the host."""
     def pin(x):
-        t = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
-        return t
+        return torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
 
     class HostCSR:
         pass
@@ -447,31 +491,34 @@ def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, tor
     hAt = host_csr(At) if At is not None else None
     h2d = sum(t.numel() * t.element_size() for h in (hA, hAt) if h is not None
               for t in (h.row_ptr, h.col_idx, h.val))
-    m_total = m_per_gpu * world
     steps = max(1, min(args.steps, args.e2e_steps))
+    n = wl.degree
     if world == 1:
         def one():
-            r = P.logdet_host(wl.mode, hA, a, b, wl.degree, m_total, seed=wl.seed, k=k, At=hAt,
-                              c=wl.r1_c)
-            return r
+            return P.logdet_host(wl.mode, hA, a, b, n, m_total, seed=wl.seed, k=k, At=hAt, c=wl.r1_c)
         one()  # warm
         t0 = time.perf_counter()
         for _ in range(steps):
             one()
         dt = time.perf_counter() - t0
         d2h = 8 * (3 + m_total)
+        h2d_mu = 0
     else:
+        p0, p1 = pdist.shard_range(m_total, world, rank)
+        c = torch.from_numpy(P.coeffs_log(a, b, n)).to(dev)
+        mu_h = torch.zeros((m_total, n + 1), dtype=torch.float64).pin_memory()
+
         def one():
-            dA = P.DeviceCSR(hA.n_rows, hA.n_cols, hA.row_ptr.to(dev, non_blocking=True),
-                             hA.col_idx.to(dev, non_blocking=True), hA.val.to(dev, non_blocking=True))
-            dAt = None
-            if hAt is not None:
-                dAt = P.DeviceCSR(hAt.n_rows, hAt.n_cols, hAt.row_ptr.to(dev, non_blocking=True),
-                                  hAt.col_idx.to(dev, non_blocking=True), hAt.val.to(dev, non_blocking=True))
-            op = P.Operator(wl.mode, dA, dAt, wl.r1_c)
-            sh = pdist.ShardedEstimator(op, a, b, wl.degree, m_total, k, seed=wl.seed)
-            gp, stats = sh.run()
-            return stats.cpu()
+            if p1 > p0:
+                P.moments_host(wl.mode, hA, a, b, n, p0, p1, wl.seed, k, At=hAt, c=wl.r1_c,
+                               out=mu_h[p0:p1].numpy())
+            mu = mu_h.to(dev, non_blocking=True)
+            pdist.combine_moments(mu)
+            gp, stats = P.finalize(mu, c)
+            s = stats.cpu()
+            if s[2].item() != 1.0:
+                raise P.ChebError(-5, "non-finite estimate on the e2e path")
+            return s
         one()
         dist.barrier()
         torch.cuda.synchronize()
@@ -483,15 +530,15 @@ def run_e2e(args, wl, A, At, a, b, m_per_gpu, k, rank, world, dev, P, pdist, tor
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         dt = float(dt.item())
-        d2h = 8 * 3
-    return {"value": m_total * wl.degree * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
+        d2h = 8 * (n + 1) * (p1 - p0) + 8 * 3
+        h2d_mu = 8 * (n + 1) * m_total
+    return {"value": m_total * n * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d + h2d_mu),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "wall_s_per_step": dt / steps,
             "api": "cheb_logdet_host (C ABI, pinned host CSR)" if world == 1 else
-                   "ShardedEstimator after pinned H2D of the CSR",
+                   "cheb_moments_host per rank (C ABI, pinned host CSR) + NCCL all_reduce + cheb_finalize",
             "includes": ("H2D copy of the CSR from pinned host memory, operator prep, all steps, D2H "
                          "of the result; device workspace from the library's per-thread arena "
-                         "(allocated by the warm-up call)" if world == 1 else
-                         "H2D CSR copy, estimator workspace alloc, all steps, all-reduce, D2H result")}
+                         "(allocated by the warm-up call)")}
 
 
 def main():
@@ -501,16 +548,21 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="gmrf5000")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong (default): the config's m probes in total over all GPUs, k = 16; "
+                         "weak: m probes per GPU at the best single-GPU block size")
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--basis", choices=["chebyshev", "taylor"], default="chebyshev",
                     help="taylor: the Fig. 1(d) power-series baseline on the same kernels")
-    ap.add_argument("--probes", type=int, default=0, help="probes per GPU (default: the config's m)")
+    ap.add_argument("--probes", type=int, default=0,
+                    help="probes (total for strong scaling, per GPU for weak; default: the config's m)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of oracle work per sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--doubling", action="store_true",
                     help="moment-doubling schedule (ceil(n/2) applications of A~) for the timed region")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other moment schedule")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

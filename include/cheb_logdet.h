@@ -97,7 +97,10 @@ size_t cheb_workspace_bytes(const cl_operator *op, int32_t probe_block);
  * changes a probe.  `stream` is a cudaStream_t (NULL = legacy default).
  * Allocates nothing; `workspace` must hold cheb_workspace_bytes(op, k) bytes and may be used
  * by one call at a time (calls on different streams need separate workspaces).
- * Non-finite moments are NOT detected here (see cheb_finalize / cheb_logdet). */
+ * Errors found on the device are reported without a host synchronisation: the call ends with a
+ * status epilogue that records them in the workspace status word (cheb_workspace_status) and,
+ * for a timed-out spin wait of the persistent kernel, overwrites every moment of the call with
+ * NaN, so cheb_finalize's stats[2] (all-finite flag) is 0 for any estimate that saw either. */
 int cheb_moments(const cl_operator *op, double a, double b, int32_t degree,
                  int64_t probe_begin, int64_t probe_end, uint64_t seed,
                  int32_t probe_block, void *workspace, size_t ws_bytes,
@@ -148,6 +151,14 @@ int cheb_gershgorin(const cl_csr *A, double *lo_hi, void *stream);
 int cheb_finalize(const double *mu, const double *c, int64_t m, int32_t degree,
                   double *gamma_p, double *stats, void *stream);
 
+/* Device status of the last cheb_moments / cheb_power_moments / cheb_affine_power_moments call
+ * that used `workspace` (DEVICE pointer; the word sits at a fixed offset of every workspace):
+ *   bit 0 (1) = a grid-wide spin wait of the persistent kernel gave up after ~seconds without
+ *               progress (CTAs not co-resident); that call's moments were set to NaN;
+ *   bit 1 (2) = a moment of that call is not finite ([a,b] does not enclose the spectrum).
+ * *status is a HOST uint32; synchronises `stream` (enqueue after the call, same stream). */
+int cheb_workspace_status(const void *workspace, uint32_t *status, void *stream);
+
 /* Synchronous single-GPU estimate in BASELINE's shape; operator pointers are
  * DEVICE pointers.  probe_block = 0 picks k automatically.  Allocates its own
  * workspace.  CL_ENONFINITE if any estimate is not finite. */
@@ -160,6 +171,14 @@ int cheb_logdet(const cl_operator *op, double a, double b, int32_t degree,
 int cheb_logdet_host(const cl_operator *op, double a, double b, int32_t degree,
                      int32_t num_probes, uint64_t seed, int32_t probe_block,
                      cl_result *out);
+
+/* Shard-level moments from a HOST operator (the end-to-end call of one rank of the multi-GPU
+ * driver): copies the operator to the device (per-thread arena, see cheb_release_cache), runs
+ * cheb_moments for global probes [probe_begin, probe_end) and copies the moments to the HOST
+ * array mu_out[(probe_end-probe_begin)*(degree+1)].  Synchronous.  CL_ECUDA on a device
+ * timeout, CL_ENONFINITE if a moment is not finite (mu_out is written in both cases). */
+int cheb_moments_host(const cl_operator *op, double a, double b, int32_t degree, int64_t probe_begin,
+                      int64_t probe_end, uint64_t seed, int32_t probe_block, double *mu_out);
 
 /* Spectral interval of B^T B for Algorithm 2, computed on the device
  * from B and B^T (DEVICE CSRs in op, kind must be CL_OP_BTB):
@@ -184,9 +203,9 @@ int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_blo
 int64_t cheb_launch_count(void);
 int cheb_profile_begin(void);
 int cheb_profile_end(double *step_ms, int64_t *step_launches);
-/* After cheb_profile_end(): summed milliseconds and launch count of the temporally fused
- * two-step kernel (each launch = 2 Chebyshev steps). */
-int cheb_profile_fused(double *ms, int64_t *launches);
+/* After cheb_profile_end(): summed milliseconds and launch count of the B^T B spmm kernel
+ * (Y = B w_{j-1}, the first half of every B^T B application; one launch per step). */
+int cheb_profile_spmm(double *ms, int64_t *launches);
 /* After cheb_profile_end(): milliseconds and launches of the persistent kernel (each launch
  * = all n Chebyshev steps of one probe block). */
 int cheb_profile_persistent(double *ms, int64_t *launches);
@@ -205,26 +224,11 @@ int cheb_set_persistent(int32_t mode);
  *       k = 64; 256*4/k rows) in both the per-step and the persistent kernel -- more tiles per
  *       step shorten the critical path of a latency-bound step; so do Algorithm-1 runs with
  *       probe blocks k <= 16 (64-row instead of 128-row tiles at k = 16);
- *   0 = always the standard geometry (32-row tiles at k = 64), which the fused-pair kernels use.
+ *   0 = always the standard geometry (32-row tiles at k = 64).
  * Moments are bit-identical between schedules that use the same geometry and grid.
  * CL_EINVAL for other values. */
 int cheb_set_small_tiles(int32_t mode);
 int cheb_get_small_tiles(void);
-
-/* Temporal fusion mode for CL_OP_CSR operators (process-wide; default 1, see DESIGN.md §7
- * for the measured status):
- *   1 = one launch per Chebyshev step;
- *   2 = auto: pairs of steps (w_{j+1}, w_{j+2}) in one cooperative launch when the
- *       operator's bandwidth max|i - col| is small enough for the two-step wavefront to
- *       stay in L2 and the matrix has enough row tiles to fill the pipeline; tiles are
- *       handed out by dynamic tickets (moments deterministic only up to rounding order);
- *   3 = always fuse pairs, dynamic tickets, warp-specialised producer (testing; correct
- *       for any bandwidth);
- *   4 = always fuse pairs, static tile->CTA map: moments bit-identical to mode 1;
- *   5 = always fuse pairs, dynamic tickets, thread-0 producer (comparison).
- * With modes 2-4, cheb_moments synchronises its stream once after the operator prep (to
- * read the bandwidth).  CL_EINVAL for other values. */
-int cheb_set_fusion(int32_t steps);
 
 /* Moment-doubling schedule for cheb_moments / cheb_logdet / cheb_logdet_host (process-wide;
  * default 0; env CHEB_DOUBLING sets the initial value).  DESIGN.md reading G25:
@@ -238,18 +242,6 @@ int cheb_set_fusion(int32_t steps);
  *       to the power-basis entry points.  CL_EINVAL for other values. */
 int cheb_set_doubling(int32_t on);
 int cheb_get_doubling(void);
-
-/* Gather-staged step kernels for CL_OP_CSR with probe blocks k >= 16 (process-wide; default 0;
- * env CHEB_GATHER).  A pass after the operator prep lists, per tile of 1024/k rows, the unique
- * rows of W_cur its nonzeros reference (at most 4096/k) and gives every nonzero a 16-bit slot
- * in that list; each step then fetches the listed rows into shared memory with TMA tile::gather4
- * (a tensor map over W_cur) and the compute warps read their neighbours from shared memory.
- * Applies to the per-step Algorithm-1 schedule only (not persistent / fused / doubling / power);
- * operators whose tiles exceed the capacity keep the regular kernels.  cheb_moments then
- * synchronises its stream once after the list pass.  Moments are deterministic (static tile map)
- * but round differently from the regular kernels.  CL_EINVAL for other values. */
-int cheb_set_gather(int32_t on);
-int cheb_get_gather(void);
 
 /* cheb_logdet / cheb_logdet_host keep their device workspace (and cheb_logdet_host the device
  * copy of the operator) in grow-only per-thread arenas, so repeated estimates do not pay a

@@ -8,14 +8,16 @@ library raises.
 from .api import (DeviceCSR, Operator, Result, Estimator, coeffs_log, workspace_bytes,
                   power_moments, taylor_coeffs, taylor_logdet, affine_power_moments, norm_bound,
                   spectrum_estimate,
-                  alloc_workspace, moments, finalize, logdet, logdet_host, bounds_btb, probes,
-                  launch_count, profile_begin, profile_end, set_fusion, set_persistent, set_small_tiles, get_small_tiles, set_doubling,
-                  get_doubling, set_gather, get_gather, release_cache, log_abs_det_from_btb, log_tau_from_rank1)
+                  alloc_workspace, moments, moments_host, finalize, logdet, logdet_host, bounds_btb, probes,
+                  launch_count, profile_begin, profile_end, set_persistent, set_small_tiles, get_small_tiles, set_doubling,
+                  get_doubling, release_cache, workspace_status, check_estimate, log_abs_det_from_btb, log_tau_from_rank1)
 from ._lib import ChebError, load as load_library
 
 __all__ = ["DeviceCSR", "Operator", "Result", "Estimator", "coeffs_log", "workspace_bytes",
            "power_moments", "taylor_coeffs", "taylor_logdet", "affine_power_moments", "norm_bound",
            "spectrum_estimate",
-           "alloc_workspace", "moments", "finalize", "logdet", "logdet_host", "bounds_btb",
-           "probes", "launch_count", "profile_begin", "profile_end", "set_fusion", "set_persistent", "set_small_tiles", "get_small_tiles", "set_doubling", "get_doubling", "set_gather", "get_gather", "release_cache", "log_abs_det_from_btb",
+           "alloc_workspace", "moments", "moments_host", "finalize", "logdet", "logdet_host", "bounds_btb",
+           "probes", "launch_count", "profile_begin", "profile_end", "set_persistent", "set_small_tiles",
+           "get_small_tiles", "set_doubling", "get_doubling", "release_cache", "workspace_status", "check_estimate",
+           "log_abs_det_from_btb",
            "log_tau_from_rank1", "ChebError", "load_library"]

@@ -71,13 +71,14 @@ def load():
         "cheb_gershgorin": (I, [ctypes.POINTER(CLCsr), P, P]),
         "cheb_logdet": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_logdet_host": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
+        "cheb_moments_host": (I, [OPP, D, D, I32, I64, I64, U64, I32, P]),
         "cheb_bounds_btb": (I, [OPP, P, P]),
         "cheb_probes": (I, [I64, U64, I64, I32, P, P]),
         "cheb_launch_count": (I64, []),
         "cheb_profile_begin": (I, []),
         "cheb_profile_end": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
-        "cheb_profile_fused": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
-        "cheb_set_fusion": (I, [I32]),
+        "cheb_profile_spmm": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
+        "cheb_workspace_status": (I, [P, ctypes.POINTER(ctypes.c_uint32), P]),
         "cheb_profile_persistent": (I, [ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "cheb_set_persistent": (I, [I32]),
         "cheb_set_small_tiles": (I, [I32]),
@@ -85,8 +86,6 @@ def load():
         "cheb_set_doubling": (I, [I32]),
         "cheb_get_doubling": (I, []),
         "cheb_release_cache": (I, []),
-        "cheb_set_gather": (I, [I32]),
-        "cheb_get_gather": (I, []),
         "cheb_last_error": (ctypes.c_char_p, []),
         "cheb_version": (I, []),
     }

@@ -248,12 +248,7 @@ def logdet(op: Operator, a: float, b: float, degree: int = 15, num_probes: int =
     return _result(r, gp, mu)
 
 
-def logdet_host(kind: str, A, a: float, b: float, degree: int = 15, num_probes: int = 30,
-                seed: int = 1, k: int = 0, At=None, c: float = 0.0, u: Optional[np.ndarray] = None,
-                want_moments: bool = False) -> Result:
-    """Synchronous estimate from HOST (numpy) CSR arrays: the library copies the
-    operator to the device inside the call (cheb_logdet_host)."""
-    keep = []
+def _host_operator(kind, A, At, c, u, keep) -> CLOperator:
     s = CLOperator()
     s.kind = OP_KIND[kind]
     s.A = _host_csr_struct(A, keep)
@@ -264,6 +259,32 @@ def logdet_host(kind: str, A, a: float, b: float, degree: int = 15, num_probes: 
         uu = np.ascontiguousarray(u, dtype=np.float64)
         keep.append(uu)
         s.r1_u = uu.ctypes.data
+    return s
+
+
+def moments_host(kind: str, A, a: float, b: float, degree: int, probe_begin: int, probe_end: int,
+                 seed: int, k: int, At=None, c: float = 0.0, u: Optional[np.ndarray] = None,
+                 out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Synchronous shard moments from HOST CSR arrays (cheb_moments_host): H2D copy of the
+    operator, moments of global probes [probe_begin, probe_end), D2H of mu[rows][n+1]."""
+    keep = []
+    s = _host_operator(kind, A, At, c, u, keep)
+    if out is None:
+        out = np.empty((probe_end - probe_begin, degree + 1))
+    if out.dtype != np.float64 or not out.flags.c_contiguous or out.shape != (probe_end - probe_begin, degree + 1):
+        raise TypeError("out must be a C-contiguous float64 array [rows][degree+1]")
+    check(_lib.load().cheb_moments_host(ctypes.byref(s), float(a), float(b), int(degree), int(probe_begin),
+                                        int(probe_end), int(seed) & (2 ** 64 - 1), int(k), out.ctypes.data))
+    return out
+
+
+def logdet_host(kind: str, A, a: float, b: float, degree: int = 15, num_probes: int = 30,
+                seed: int = 1, k: int = 0, At=None, c: float = 0.0, u: Optional[np.ndarray] = None,
+                want_moments: bool = False) -> Result:
+    """Synchronous estimate from HOST (numpy) CSR arrays: the library copies the
+    operator to the device inside the call (cheb_logdet_host)."""
+    keep = []
+    s = _host_operator(kind, A, At, c, u, keep)
     gp = np.empty(num_probes)
     mu = np.empty((num_probes, degree + 1)) if want_moments else None
     r = CLResult()
@@ -300,17 +321,44 @@ def profile_begin():
 
 
 def profile_end():
-    """Stop recording; returns {"single": (ms, launches), "fused": (ms, launches)} for the
-    single-step and the fused two-step kernels."""
+    """Stop recording; returns {"single": (ms, launches), "spmm": (ms, launches),
+    "persistent": (ms, launches)}: the Chebyshev step kernel, the B^T B spmm kernel (Y = B w) and
+    the persistent multi-step kernel, each summed over its launches (CUDA events on the launching
+    stream)."""
     L = _lib.load()
     ms, n = ctypes.c_double(), ctypes.c_int64()
     check(L.cheb_profile_end(ctypes.byref(ms), ctypes.byref(n)))
-    fms, fn = ctypes.c_double(), ctypes.c_int64()
-    check(L.cheb_profile_fused(ctypes.byref(fms), ctypes.byref(fn)))
+    sms, sn = ctypes.c_double(), ctypes.c_int64()
+    check(L.cheb_profile_spmm(ctypes.byref(sms), ctypes.byref(sn)))
     pms, pn = ctypes.c_double(), ctypes.c_int64()
     check(L.cheb_profile_persistent(ctypes.byref(pms), ctypes.byref(pn)))
-    return {"single": (ms.value, n.value), "fused": (fms.value, fn.value),
+    return {"single": (ms.value, n.value), "spmm": (sms.value, sn.value),
             "persistent": (pms.value, pn.value)}
+
+
+STATUS_TIMEOUT, STATUS_NONFINITE = 1, 2
+
+
+def workspace_status(workspace: torch.Tensor, stream=None) -> int:
+    """Device status word of the last moments call that used `workspace` (cheb_workspace_status):
+    bit 0 = a persistent-kernel spin wait timed out (its moments were set to NaN), bit 1 = a
+    non-finite moment.  Synchronises the stream."""
+    st = ctypes.c_uint32()
+    check(_lib.load().cheb_workspace_status(workspace.data_ptr(), ctypes.byref(st), _stream_ptr(stream)))
+    return int(st.value)
+
+
+def check_estimate(stats: torch.Tensor, workspace: Optional[torch.Tensor] = None, stream=None):
+    """Raise ChebError unless an estimate is valid (synchronises): CL_ECUDA if a device spin wait
+    timed out, CL_ENONFINITE if any Gamma_p is not finite (stats[2] from cheb_finalize is the
+    all-finite flag; the [a,b] interval likely misses the spectrum)."""
+    status = workspace_status(workspace, stream) if workspace is not None else 0
+    ok = float(stats[2].item()) == 1.0 and math.isfinite(float(stats[0].item()))
+    if status & STATUS_TIMEOUT:
+        raise _lib.ChebError(_lib.CL_ECUDA, "persistent-kernel grid wait timed out; moments set to NaN")
+    if not ok or status & STATUS_NONFINITE:
+        raise _lib.ChebError(_lib.CL_ENONFINITE,
+                             "non-finite estimate: [a,b] likely does not enclose the spectrum")
 
 
 def set_persistent(mode: int):
@@ -335,15 +383,6 @@ def set_doubling(on: bool):
     check(_lib.load().cheb_set_doubling(1 if on else 0))
 
 
-def set_gather(on: bool):
-    """Gather-staged step kernels (csr, k >= 16; TMA tile::gather4 of each tile's rows)."""
-    check(_lib.load().cheb_set_gather(1 if on else 0))
-
-
-def get_gather() -> bool:
-    return bool(_lib.load().cheb_get_gather())
-
-
 def release_cache():
     """Free this thread's device arenas of cheb_logdet / cheb_logdet_host."""
     check(_lib.load().cheb_release_cache())
@@ -351,12 +390,6 @@ def release_cache():
 
 def get_doubling() -> bool:
     return bool(_lib.load().cheb_get_doubling())
-
-
-def set_fusion(steps: int):
-    """Temporal fusion for CSR operators: 1 (off, default), 2 (auto), 3 (always fuse pairs,
-    dynamic tile tickets), 4 (always fuse pairs, static tile map: bit-identical to 1)."""
-    check(_lib.load().cheb_set_fusion(int(steps)))
 
 
 class Estimator:
@@ -396,17 +429,27 @@ class Estimator:
     def enqueue_finalize(self, stream=None):
         return finalize(self.mu, self.c, stream=stream)
 
-    def run(self, stream=None):
+    def run(self, stream=None, check: bool = False):
+        """Enqueue one whole estimate; returns device (gamma_p, stats).  check=True synchronises and
+        raises ChebError on a device timeout or a non-finite estimate (check_estimate)."""
         self.enqueue_moments(stream)
-        return self.enqueue_finalize(stream)
+        gp, stats = self.enqueue_finalize(stream)
+        if check:
+            self.check(stats, stream)
+        return gp, stats
+
+    def check(self, stats, stream=None):
+        """Raise ChebError if the estimate behind `stats` is invalid (synchronises)."""
+        check_estimate(stats, self.workspace, stream)
 
     def capture(self):
         """Capture one whole estimate (operator prep, probe init, every step launch, finalize) into
         a CUDA graph; returns (replay, gamma_p, stats): replay() re-runs it with one launch call on
         the capture stream's successors and refreshes gamma_p / stats in place.  Useful when many
         small estimates are served (launch gaps dominate below ~1 ms per estimate); the schedule
-        switches (persistent / fusion / doubling) in effect at capture time are baked in (fusion
-        mode 2 is not capturable: it synchronises to read the operator bandwidth)."""
+        switches (persistent / small tiles / doubling) in effect at capture time are baked in.  The
+        captured sequence performs no host synchronisation (cheb_moments never synchronises), so
+        every schedule is capturable; check a replay's stats with check()."""
         s = torch.cuda.Stream(device=self.mu.device)
         s.wait_stream(torch.cuda.current_stream(self.mu.device))
         with torch.cuda.stream(s):

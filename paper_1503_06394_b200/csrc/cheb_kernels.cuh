@@ -25,7 +25,6 @@
 #pragma once
 #include <cassert>
 #include <cstdint>
-#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 // CHEB_CHECKS=1 builds (scripts/build_variants.py "checked") turn on device-side bounds
@@ -142,24 +141,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrival
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {  // non-blocking
-    uint32_t done;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return done != 0;
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // release.cta
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
@@ -178,47 +159,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
             : "memory");
     } while (!done);
 }
-// mbar_wait with a bounded spin: sets *err and gives up instead of hanging the GPU (new kernels)
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t phase, unsigned int* err) {
-    const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0, spins = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(phase)
-            : "memory");
-        if (!done && ++spins > (1u << 22)) {
-            atomicExch(err, 1u);
-            return;
-        }
-    } while (!done);
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void st2_hint(double* p, double2 v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ double2 ldnc2_hint(const double* p, uint64_t pol) {
-    double2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-    return v;
-}
-#ifndef CHEB_FUSED_HINTS
-#define CHEB_FUSED_HINTS 0  // fused kernel: keep the L2 window (w_j gathers, w_{j+1} stores) evict_last
-#endif
-
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -267,26 +212,12 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// L2 prefetch of each staged tile's first-touch gather rows (CHEB_L2_PREFETCH, default 0): with
-// rows processed in ascending order, the rows a banded operator's tile touches for the first time
-// are [r0 + bw, r0 + bw + T) (bw = max |i - col|); the staging thread can prefetch them into L2.
-// Measured harmful on configs[3] (6.20 -> 9.36 ms per launch, DRAM 40.3 -> 60.8 GB): tiles are
-// staged two items per CTA ahead, i.e. ~2G tiles ahead of the chip-wide front, and the prefetched
-// rows are evicted by the ~60 MB of traffic before their use.  Kept as a build option.
-#ifndef CHEB_L2_PREFETCH
-#define CHEB_L2_PREFETCH 0
-#endif
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 struct StepArgs {
     int64_t d;            // rows of the gather matrix (= dimension of M)
     int64_t ntiles;
     const int64_t* rp;    // prepped gather matrix: padded row_ptr copy
     const int32_t* ci;    //   padded col copy
     const double* va;     //   padded scaled values (alpha*a, diagonal alpha*a_ii - beta)
-    const unsigned long long* bw;  // operator bandwidth max|i - col| (device), nullptr: no prefetch
     const double* xg;     // gather source: W_cur (csr/rank1) or Y = B W_cur (btb)
     const double* wcur;   // W_cur
     double* wnext;        // in: W_prev (unless FIRST); out: W_next (in place)
@@ -389,11 +320,10 @@ __device__ __forceinline__ int probe_of(int lg, int q) {
 
 // Epilogues of the last CTA:
 //   EPI_STEP  ch0 -> mu[p][col]                        (+ rank-1: ch1 -> s_next)
-//   EPI_PAIR  ch0 -> mu[p][col], ch1 -> mu[p][col+1]   (temporally fused pair)
 //   EPI_DBL   moment doubling, step j = col: ch0 = w_j^T w_j, ch1 = w_j^T w_{j-1}
 //             mu[p][2j] = 2 ch0 - mu[p][0],  mu[p][2j-1] = 2 ch1 - mu[p][1]  (j = 1: mu[p][1] = ch1)
 //             (indices > n = mu_stride - 1 are not written)   (+ rank-1: ch2 -> s_next)
-enum { EPI_STEP = 0, EPI_PAIR = 1, EPI_DBL = 2 };
+enum { EPI_STEP = 0, EPI_DBL = 2 };
 
 // Moment-doubling epilogue for one probe row (T_{2j} = 2 T_j^2 - I, T_{2j+1} = 2 T_{j+1} T_j - T_1
 // for the symmetric Ã; reading G25).
@@ -462,10 +392,6 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
         double* row = a.mu_out + (size_t)tid * a.mu_stride;
         if (tid < a.kvalid) {
             if (EPI == EPI_STEP) row[a.mu_col] = fin[0][tid];
-            if (EPI == EPI_PAIR) {
-                row[a.mu_col] = fin[0][tid];
-                row[a.mu_col + 1] = fin[1][tid];
-            }
             if (EPI == EPI_DBL) dbl_write(row, a.mu_col, a.mu_stride - 1, fin[0][tid], fin[1][tid]);
         }
         if (HAS_S) a.s_next[tid] = fin[NCH - 1][tid];
@@ -510,10 +436,8 @@ __global__ void __launch_bounds__(kThreads)
 prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ va, double alpha, double beta, int64_t* __restrict__ rp2,
             int64_t rp2_len, int32_t* __restrict__ ci2, double* __restrict__ va2,
-            const double* __restrict__ u, double* __restrict__ u2,
-            unsigned long long* __restrict__ bw) {
+            const double* __restrict__ u, double* __restrict__ u2) {
     const int64_t total = rp2[d];  // padded nnz
-    int64_t bwmax = 0;  // operator bandwidth max |i - col| (temporal fusion planning)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of 32
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < d; i0 += stride) {
         const int64_t i = i0 + threadIdx.x;
@@ -539,8 +463,6 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
                         va2[o] = alpha * va[e];
                         o++;
                     }
-                    const int64_t dist = c > i ? c - i : i - c;
-                    bwmax = dist > bwmax ? dist : bwmax;
                 }
                 ci2[o0] = (int32_t)i;
                 va2[o0] = dv;
@@ -549,8 +471,6 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
                     const int32_t c = ci[e];
                     ci2[o] = c;
                     va2[o] = alpha * va[e];
-                    const int64_t dist = c > i ? c - i : i - c;
-                    bwmax = dist > bwmax ? dist : bwmax;
                 }
             }
             for (; o < o1; o++) {  // padding: (i, 0.0)
@@ -559,14 +479,6 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
             }
             if (u2) u2[i] = u ? u[i] : 1.0;
         }
-    }
-    if (bw) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const int64_t o = __shfl_xor_sync(0xffffffffu, bwmax, off);
-            bwmax = o > bwmax ? o : bwmax;
-        }
-        if ((threadIdx.x & 31) == 0) atomicMax(bw, (unsigned long long)bwmax);
     }
     if (blockIdx.x == 0) {
         for (int64_t k = d + 1 + threadIdx.x; k < rp2_len; k += blockDim.x) rp2[k] = total;
@@ -661,7 +573,7 @@ __host__ __device__ constexpr int n_channels() { return (DBL ? 2 : 1) + (MODE ==
 // VB: the probe vector v = w_0 is never materialised in HBM on the per-step path, its sign bits
 // stand in for it: VB = 1 (step 1) gathers v from the bits, VB = 2 (step 2) takes w_{j-2} = v
 // from the staged bits.  x * (+-1) is exact, so results are bit-identical to reading v.
-template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool KEEP = false, bool DBL = false,
+template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool DBL = false,
           bool WCS = false, int R4 = CHEB_RPG, int VB = 0>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
@@ -674,7 +586,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     // csr / rank-1 doubling: w_{j-1}[i] is the row's first gather (the prepped diagonal entry)
     constexpr bool OWN_GATHER = DBL && !OWN_SMEM && MODE != MODE_BTB;
     constexpr bool OWN_EARLY = DBL && !OWN_SMEM && !OWN_GATHER;  // loaded at the row start
-    static_assert(VB == 0 || (MODE != MODE_BTB && !CG && !KEEP && (VB != 1 || !OWN_SMEM)),
+    static_assert(VB == 0 || (MODE != MODE_BTB && !CG && (VB != 1 || !OWN_SMEM)),
                   "sign-bit probes: per-step csr/rank-1");
     constexpr bool HAS_S = (MODE == MODE_RANK1);
     constexpr int SCH = n_channels<MODE, DBL>() - 1;  // rank-1 channel
@@ -752,12 +664,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                     // lane offset folded into the base: one IMAD.WIDE per gathered row
                     const double* p = xl + (size_t)(uint32_t)c[q] * K;
 #pragma unroll
-                    for (int sl = 0; sl < NSL; sl++) {
-                        if (KEEP && CHEB_FUSED_HINTS)
-                            x[q][sl] = ldnc2_hint(p + sl * G::SS, policy_evict_last());
-                        else
-                            x[q][sl] = CG ? ldcg2(p + sl * G::SS) : ldg2(p + sl * G::SS);
-                    }
+                    for (int sl = 0; sl < NSL; sl++) x[q][sl] = CG ? ldcg2(p + sl * G::SS) : ldg2(p + sl * G::SS);
                 }
             }
             if (OWN_GATHER && t0 == 0) {
@@ -813,16 +720,8 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         }
         double* out = wout + (size_t)i * K;
 #pragma unroll
-        for (int sl = 0; sl < NSL; sl++) {
-            if (KEEP) {  // re-read from L2 later in the same launch (fused kernel, stage 1)
-                if (CHEB_FUSED_HINTS)
-                    st2_hint(out + pp[sl], nw[sl], policy_evict_last());
-                else
-                    *reinterpret_cast<double2*>(out + pp[sl]) = nw[sl];
-            } else {     // streamed: next read is by a later launch
-                __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw[sl]);
-            }
-        }
+        for (int sl = 0; sl < NSL; sl++)  // streamed: the next read is by a later step
+            __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw[sl]);
 #pragma unroll
         for (int sl = 0; sl < NSL; sl++) {
             if (DBL) {
@@ -886,12 +785,6 @@ cheb_step_kernel(StepArgs a) {
     }
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-    // thread 0: bandwidth for the L2 prefetch (only for banded operators, bw < d/4)
-    int64_t pf_bw = -1;
-    if (CHEB_L2_PREFETCH && MODE != MODE_BTB && tid == 0 && a.bw) {
-        const int64_t bwv = (int64_t)*a.bw;
-        pf_bw = (4 * bwv < a.d) ? bwv : -1;
-    }
     // ---- producer (thread 0): issue the bulk copies of tile t into stage b
     auto issue = [&](int64_t t, int b, int64_t e0, int64_t e1) {
         unsigned char* st = smem + b * SL::BYTES;
@@ -923,10 +816,6 @@ cheb_step_kernel(StepArgs a) {
             bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
         }
         if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
-        if (CHEB_L2_PREFETCH && MODE != MODE_BTB && pf_bw >= 0) {  // first-touch gather rows -> L2
-            const int64_t p0 = r0 + pf_bw, p1 = imin64(p0 + rows, a.d);
-            if (p1 > p0) prefetch_l2(a.xg + (size_t)p0 * K, (uint32_t)(p1 - p0) * K * 8);
-        }
     };
     auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
     auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
@@ -965,10 +854,10 @@ cheb_step_kernel(StepArgs a) {
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
-            step_tile<K, MODE, FIRST, true, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+            step_tile<K, MODE, FIRST, true, false, DBL, WCS, R4, VB>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                acc, a.xg, a.wcur, a.wnext);
         else
-            step_tile<K, MODE, FIRST, false, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
+            step_tile<K, MODE, FIRST, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
                                                                 a.wnext);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) {
@@ -981,56 +870,26 @@ cheb_step_kernel(StepArgs a) {
 
 
 // ---------------------------------------------------------------------------------------
-// K2x2: temporally fused pair of Chebyshev steps (CSR mode, banded operators).
-//   stage 1 (tile P):      w_{j+1} = 2 Ã w_j     - w_{j-1}   (A: w_{j-1} -> w_{j+1}, gathers B)
-//   stage 2 (tile P - D):  w_{j+2} = 2 Ã w_{j+1} - w_j       (B: w_j -> w_{j+2},     gathers A)
-// Every element is computed with exactly the single-step arithmetic, in the same order, so
-// results are bit-identical to two cheb_step_kernel launches; only the schedule changes.
-// CTA c handles positions P = c + k*G (k = 0, 1, ...): stage 1 of tile P, then stage 2 of
-// tile u = P - D.  Stage 2 of u gathers w_{j+1} rows within the operator bandwidth of u and
-// overwrites w_j rows of u that stage 1 of tiles u-H..u+H read (H = ceil(bandwidth/T) + 1
-// tiles), so it needs every stage-1 tile t <= u + H complete.
-// Completion is tracked in chunks of 32 tiles: after stage 1 of tile t a CTA release-adds 1
-// to cnt[t/32]; a waiter keeps `known` = number of leading chunks seen full and advances it
-// with one warp-wide load of the next 32 chunk counters (ballot -> first non-full chunk).
-// Those loads are issued before the preceding stage-1 tile is computed, so in steady state
-// the check costs no latency.
-// D = (SLACK + ceil((H+2)/G)) * G >= H + 2 makes every dependency sit at an earlier position
-// (deadlock-free with all CTAs co-resident: cooperative launch), and D a multiple of G keeps
-// stage-2 tile u on CTA u mod G exactly like the single-step kernel: the per-CTA partial dot
-// products (hence the moments) are bit-identical too.  With SLACK = 0, D = G: the L2 window
-// between the stages is one wave of tiles plus the halo.  w_{j+1} stays in L2 between the
-// stages: per 2 steps HBM sees w_{j-1}, w_j read and w_{j+1}, w_{j+2} written (4 vector
-// streams instead of 6).
+// Status epilogue of a cheb_moments call (one launch per call).  status: the workspace status
+// word; bit 0 is set by a spin wait of the persistent kernel that gave up (it never hangs the
+// GPU).  Then every moment of the call becomes NaN, so cheb_finalize's finiteness flag and
+// cheb_logdet's CL_ENONFINITE/CL_ECUDA checks see it; otherwise bit 1 records any non-finite
+// moment (operator spectrum outside [a,b]).  mu: the call's rows, contiguous.
 // ---------------------------------------------------------------------------------------
-#ifndef CHEB_FUSED_SLACK
-#define CHEB_FUSED_SLACK 0
-#endif
-constexpr int kFusedSlack = CHEB_FUSED_SLACK;  // extra waves of lag between the stages
-constexpr int kChunkTiles = 32;                // tiles per completion counter
-// Consumer side of the dependency: the counters are read relaxed and the gathers that follow
-// are control-dependent on them (issued only after the counts are seen), and every w_{j+1}
-// row is written exactly once before its count is released and never changes afterwards, so
-// no L1 line of it can be stale (L1 starts empty at launch; stage 1 reads A only through TMA).
-// CHEB_FUSED_FENCE=1 adds the formal fence.acq_rel.gpu (an SM-wide L1 invalidate per item).
-#ifndef CHEB_FUSED_FENCE
-#define CHEB_FUSED_FENCE 0
-#endif
-
-struct FusedArgs {
-    double* A;                // in: w_{j-1}, out: w_{j+1}
-    double* B;                // in: w_j,     out: w_{j+2}
-    unsigned int* cnt;        // [ceil(ntiles/32)] completed stage-1 tiles per chunk (zeroed)
-    unsigned int* err;        // dependency-wait timeout flag
-    int64_t D;                // stage-2 lag in positions, a multiple of gridDim.x, >= H + 2
-    int64_t H;                // halo in tiles
-};
-
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+__global__ void __launch_bounds__(kThreads)
+moments_status_kernel(unsigned int* status, double* mu, int64_t nmu) {
+    const bool poison = (*reinterpret_cast<volatile unsigned int*>(status) & 1u) != 0;
+    int bad = 0;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nmu; x += (int64_t)gridDim.x * blockDim.x) {
+        if (poison) mu[x] = __longlong_as_double(0x7ff8000000000000ll);
+        else bad |= !isfinite(mu[x]);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, 2u);
 }
+
+// ---------------------------------------------------------------------------------------
+// Inter-CTA synchronisation primitives (persistent kernel)
+// ---------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -1041,600 +900,6 @@ __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v)
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-#ifndef CHEB_FUSED_MIN_CTAS
-#define CHEB_FUSED_MIN_CTAS CHEB_MIN_CTAS
-#endif
-template <int K>
-__global__ void __launch_bounds__(kThreads, CHEB_FUSED_MIN_CTAS)
-cheb_step2_kernel(StepArgs a, FusedArgs f) {
-    using G = Geo<K>;
-    using SL = StageLayout<K, MODE_CSR>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int64_t s_base_c[2], s_base_v[2];
-    __shared__ int s_fit[2];
-
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t Gd = gridDim.x;
-    double acc[2][kPPL];  // stage 1 / stage 2 moments
-#pragma unroll
-    for (int q = 0; q < kPPL; q++) acc[0][q] = acc[1][q] = 0.0;
-    double (&mu1)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[0]);
-    double (&mu2)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[1]);
-    double2 z2[G::NSL];
-#pragma unroll
-    for (int sl = 0; sl < G::NSL; sl++) z2[sl] = make_double2(0.0, 0.0);
-    const int64_t npos = a.ntiles + f.D;  // positions 0 .. ntiles + D - 1
-    const int64_t M = blockIdx.x < npos ? 2 * ((npos - 1 - blockIdx.x) / Gd + 1) : 0;
-    const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
-
-    auto item = [&](int64_t m, int& stg, int64_t& t) -> bool {
-        const int64_t P = (int64_t)blockIdx.x + (m >> 1) * Gd;
-        stg = (int)(m & 1);
-        t = stg ? P - f.D : P;
-        return t >= 0 && t < a.ntiles;
-    };
-    auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
-        const int64_t r0 = t * G::TILE;
-        e0 = __ldg(a.rp + r0);
-        e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
-    };
-    auto issue = [&](int64_t t, int b, const double* wsrc, int64_t e0, int64_t e1) {
-        unsigned char* st = smem + b * SL::BYTES;
-        const int64_t r0 = t * G::TILE;
-        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-        const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
-        const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
-        const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
-        s_fit[b] = fit;
-        s_base_c[b] = c0;
-        s_base_v[b] = v0;
-        const uint32_t wbytes = (uint32_t)rows * K * 8;
-        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
-        uint32_t bytes = G::RPBYTES + sgbytes + wbytes;
-        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
-        mbar_expect_tx(&bar[b], bytes);
-        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
-        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
-        bulk_g2s_hint(st + SL::OFF_WPREV, wsrc + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
-        if (fit) {
-            bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
-            bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
-        }
-    };
-    auto advance = [&](int64_t& m, int& stg, int64_t& t) -> bool {
-        for (; m < M; ++m)
-            if (item(m, stg, t)) return true;
-        return false;
-    };
-    // full count of chunk ch (the last chunk may be short); chunks past the end read as full
-    auto chunk_full = [&](int64_t ch) -> unsigned int {
-        return (unsigned int)imin64(kChunkTiles, a.ntiles - ch * kChunkTiles);
-    };
-
-    int64_t m_issue = 0, ne0 = 0, ne1 = 0, nt = 0;
-    int nstg = 0;
-    bool pending = false;
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-        for (int q = 0; q < 2; q++) {
-            int stg;
-            int64_t t, e0, e1;
-            if (!advance(m_issue, stg, t)) break;
-            bounds(t, e0, e1);
-            issue(t, q, stg ? f.B : f.A, e0, e1);
-            ++m_issue;
-        }
-    }
-    __syncthreads();
-
-    int64_t q = 0;
-    int64_t known = 0;       // warp 0: leading chunks known complete
-    unsigned int peek = 0;   // warp 0, per lane: prefetched counter of chunk known + lane
-    int64_t peek_base = -1;  // chunk index of lane 0's prefetched counter (-1: none)
-    for (int64_t m = 0; m < M; ++m) {
-        int stg;
-        int64_t t;
-        if (!item(m, stg, t)) continue;
-        const int b = (int)(q & 1);
-        const uint32_t phase = (uint32_t)((q >> 1) & 1);
-        if (tid == 0) {
-            pending = advance(m_issue, nstg, nt);
-            if (pending) bounds(nt, ne0, ne1);
-        }
-        if (stg == 1) {
-            // stage-1 tiles [0, need) must be complete
-            const int64_t need = imin64(t + f.H + 1, a.ntiles);
-            if (tid < 32) {
-                uint32_t spins = 0;
-                while (known * kChunkTiles < need) {
-                    const int64_t ch = known + lane;
-                    unsigned int v;
-                    if (peek_base == known) {
-                        v = peek;
-                    } else {
-                        v = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
-                    }
-                    const bool full = ch >= nchunks || v >= chunk_full(ch);
-                    const unsigned int notfull = __ballot_sync(0xffffffffu, !full);
-                    const int adv = notfull ? __ffs(notfull) - 1 : 32;
-                    known += adv;
-                    peek_base = -1;
-                    if (adv == 0) {
-                        __nanosleep(100);
-                        if ((++spins & 1023u) == 0 && (spins > (1u << 23) || ld_acquire_u32(f.err))) {
-                            if (lane == 0) atomicExch(f.err, 1u);  // ~seconds without progress: never hang
-                            break;
-                        }
-                    }
-                }
-#if CHEB_FUSED_FENCE
-                fence_acq_rel_gpu();  // formal acquire (costs an SM-wide L1 invalidate per item)
-#endif
-            }
-            __syncthreads();
-        }
-        mbar_wait(&bar[b], phase);
-        const unsigned char* st = smem + b * SL::BYTES;
-        const int64_t r0 = t * G::TILE;
-        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-        if (stg == 0) {
-            // prefetch the chunk counters the next stage-2 check will read (overlaps this tile)
-            if (tid < 32) {
-                const int64_t ch = known + lane;
-                peek = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
-                peek_base = known;
-            }
-            if (s_fit[b])
-                step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
-                                                                 mu1, f.B, f.B, f.A);
-            else
-                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, mu1, f.B,
-                                                                  f.B, f.A);
-        } else {
-            if (s_fit[b])
-                step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
-                                                                 mu2, f.A, f.A, f.B);
-            else
-                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, mu2, f.A,
-                                                                  f.A, f.B);
-        }
-        __syncthreads();  // every warp is done with stage b (and, for stage 1, with its stores)
-        if (tid == 0) {
-            if (pending) {
-                issue(nt, b, nstg ? f.B : f.A, ne0, ne1);
-                ++m_issue;
-            }
-            if (stg == 0) {  // publish: stage 1 of tile t is complete (release: the CTA's stores
-                             // are ordered before it by the barrier above)
-                red_release_add(f.cnt + t / kChunkTiles, 1u);
-            }
-        }
-        ++q;
-    }
-    grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
-}
-
-
-// ---------------------------------------------------------------------------------------
-// K2x2d: temporally fused pair with DYNAMIC tile tickets.  Same two stages as cheb_step2_kernel,
-// but tiles are handed out by two global counters instead of a static tile -> CTA map, so a slow
-// CTA delays only the one tile it holds (no accumulated skew):
-//   * a CTA takes a stage-1 ticket t1 = c1++; if t1 >= D it then takes one stage-2 ticket
-//     u = c2++ (alternating); once c1 is exhausted it drains stage-2 tickets;
-//   * every stage-2 ticket u taken this way satisfies u + D < c1, so the stage-1 tiles it needs
-//     (<= u + H < u + D) have all been handed out, and stage-1 work never waits;
-//   * a CTA's own pending stage-1 ticket is always > its current stage-2 need, and a wait chain
-//     X -> Y implies u_X > u_Y: no cycle, deadlock-free with all CTAs co-resident.
-// Tickets are taken when the TMA staging of the item is issued (two items ahead).
-// Moments: per-CTA partial sums as in the other kernels, but which tiles a CTA sums now depends
-// on the run, so the rounding of mu is run-dependent (still within the parity tolerances).
-// ---------------------------------------------------------------------------------------
-struct FusedDynArgs {
-    unsigned int* c1;         // stage-1 ticket counter (zeroed)
-    unsigned int* c2;         // stage-2 ticket counter (zeroed)
-};
-
-template <int K>
-__global__ void __launch_bounds__(kThreads, CHEB_FUSED_MIN_CTAS)
-cheb_step2d_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
-    using G = Geo<K>;
-    using SL = StageLayout<K, MODE_CSR>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int64_t s_base_c[2], s_base_v[2];
-    __shared__ int s_fit[2];
-    __shared__ int64_t s_t[2];   // tile of the item staged in buffer b (-1: no more items)
-    __shared__ int s_stg[2];     // its stage
-
-    const int tid = threadIdx.x, lane = tid & 31;
-    double acc[2][kPPL];  // stage 1 / stage 2 moments
-#pragma unroll
-    for (int q = 0; q < kPPL; q++) acc[0][q] = acc[1][q] = 0.0;
-    double (&mu1)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[0]);
-    double (&mu2)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[1]);
-    double2 z2[G::NSL];
-#pragma unroll
-    for (int sl = 0; sl < G::NSL; sl++) z2[sl] = make_double2(0.0, 0.0);
-    const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
-    const unsigned int ntl = (unsigned int)a.ntiles;
-
-    auto issue = [&](int64_t t, int b, const double* wsrc, int64_t e0, int64_t e1) {
-        unsigned char* st = smem + b * SL::BYTES;
-        const int64_t r0 = t * G::TILE;
-        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-        const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
-        const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
-        const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
-        s_fit[b] = fit;
-        s_base_c[b] = c0;
-        s_base_v[b] = v0;
-        const uint32_t wbytes = (uint32_t)rows * K * 8;
-        const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
-        uint32_t bytes = G::RPBYTES + sgbytes + wbytes;
-        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
-        mbar_expect_tx(&bar[b], bytes);
-        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
-        bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
-        bulk_g2s_hint(st + SL::OFF_WPREV, wsrc + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
-        if (fit) {
-            bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
-            bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
-        }
-    };
-    // thread 0: ticket policy (see above)
-    bool want2 = false, done1 = false, done2 = false;
-    auto take = [&](int& stg, int64_t& t) -> bool {
-        if (want2 || done1) {
-            want2 = false;
-            if (!done2) {
-                const unsigned int u = atomicAdd(dy.c2, 1u);
-                if (u < ntl) {
-                    stg = 1;
-                    t = u;
-                    return true;
-                }
-                done2 = true;
-            }
-        }
-        if (!done1) {
-            const unsigned int t1 = atomicAdd(dy.c1, 1u);
-            if (t1 < ntl) {
-                stg = 0;
-                t = t1;
-                want2 = (int64_t)t1 >= f.D;
-                return true;
-            }
-            done1 = true;
-        }
-        if (!done2) {
-            const unsigned int u = atomicAdd(dy.c2, 1u);
-            if (u < ntl) {
-                stg = 1;
-                t = u;
-                return true;
-            }
-            done2 = true;
-        }
-        return false;
-    };
-    auto stage_next = [&](int b) {  // thread 0: take the next item and stage it into buffer b
-        int stg;
-        int64_t t;
-        if (take(stg, t)) {
-            s_t[b] = t;
-            s_stg[b] = stg;
-            const int64_t r0 = t * G::TILE;
-            issue(t, b, stg ? f.B : f.A, __ldg(a.rp + r0), __ldg(a.rp + imin64(r0 + G::TILE, a.d)));
-        } else {
-            s_t[b] = -1;
-        }
-    };
-
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-        stage_next(0);
-        stage_next(1);
-    }
-    __syncthreads();
-
-    int64_t known = 0;       // warp 0: leading chunks known complete
-    for (int64_t q = 0;; ++q) {
-        const int b = (int)(q & 1);
-        const uint32_t phase = (uint32_t)((q >> 1) & 1);
-        const int64_t t = s_t[b];
-        if (t < 0) break;
-        const int stg = s_stg[b];
-        if (stg == 1) {
-            const int64_t need = imin64(t + f.H + 1, a.ntiles);  // stage-1 tiles [0, need) complete
-            if (tid < 32) {
-                uint32_t spins = 0;
-                while (known * kChunkTiles < need) {
-                    const int64_t ch = known + lane;
-                    const unsigned int v = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
-                    const bool full = ch >= nchunks || v >= (unsigned int)imin64(kChunkTiles, a.ntiles - ch * kChunkTiles);
-                    const unsigned int notfull = __ballot_sync(0xffffffffu, !full);
-                    const int adv = notfull ? __ffs(notfull) - 1 : 32;
-                    known += adv;
-                    if (adv == 0) {
-                        __nanosleep(64);
-                        if ((++spins & 1023u) == 0 && (spins > (1u << 23) || ld_acquire_u32(f.err))) {
-                            if (lane == 0) atomicExch(f.err, 1u);  // ~seconds without progress: never hang
-                            break;
-                        }
-                    }
-                }
-#if CHEB_FUSED_FENCE
-                fence_acq_rel_gpu();
-#endif
-            }
-            __syncthreads();
-        }
-        mbar_wait(&bar[b], phase);
-        const unsigned char* st = smem + b * SL::BYTES;
-        const int64_t r0 = t * G::TILE;
-        const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-        if (stg == 0) {
-            if (s_fit[b])
-                step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
-                                                                 mu1, f.B, f.B, f.A);
-            else
-                step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, mu1, f.B, f.B, f.A);
-        } else {
-            if (s_fit[b])
-                step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
-                                                                 mu2, f.A, f.A, f.B);
-            else
-                step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, mu2, f.A, f.A, f.B);
-        }
-        __syncthreads();  // every warp is done with buffer b (and, for stage 1, with its stores)
-        if (tid == 0) {
-            if (stg == 0) red_release_add(f.cnt + t / kChunkTiles, 1u);  // publish stage 1 of t
-            stage_next(b);
-        }
-        __syncthreads();  // s_t[b] / s_stg[b] of the next use of b are visible
-    }
-    grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
-}
-
-// ---------------------------------------------------------------------------------------
-// K2x2w: dynamic-ticket fused pair, warp-specialised.  Warps 0..7 only compute tiles; a ninth
-// (producer) warp takes the tickets (same policy as cheb_step2d_kernel), stages each item by TMA,
-// waits for a stage-2 item's dependencies and then arrives on the item's "full" mbarrier
-// (expect_tx first, so the phase completes when both the bytes and the arrival are in); the
-// compute warps arrive on the buffer's "empty" mbarrier when done, after which the producer
-// publishes a finished stage-1 tile (consumer stores -> arrive.release.cta -> producer
-// wait.acquire.cta -> red.release.gpu: cumulative).  No ticket atomic, bound load, fence or
-// dependency wait sits between two tiles of the compute warps.
-// ---------------------------------------------------------------------------------------
-#ifndef CHEB_FUSEDW_MIN_CTAS
-#define CHEB_FUSEDW_MIN_CTAS 3
-#endif
-constexpr int kFusedWThreads = kThreads + 32;
-#ifndef CHEB_FUSEDW_STAGES
-#define CHEB_FUSEDW_STAGES 3
-#endif
-constexpr int kWStages = CHEB_FUSEDW_STAGES;  // staged items in flight per CTA
-
-template <int K>
-__global__ void __launch_bounds__(kFusedWThreads, CHEB_FUSEDW_MIN_CTAS)
-cheb_step2w_kernel(StepArgs a, FusedArgs f, FusedDynArgs dy) {
-    using G = Geo<K>;
-    using SL = StageLayout<K, MODE_CSR>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int NS = kWStages;
-    __shared__ __align__(8) uint64_t full[NS], empty[NS];
-    __shared__ int64_t s_base_c[NS], s_base_v[NS], s_t[NS];
-    __shared__ int s_fit[NS], s_stg[NS];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double acc[2][kPPL];  // stage 1 / stage 2 moments (compute warps)
-#pragma unroll
-    for (int q = 0; q < kPPL; q++) acc[0][q] = acc[1][q] = 0.0;
-    if (tid == 0) {
-        for (int x = 0; x < NS; x++) {
-            mbar_init(&full[x], 1);
-            mbar_init(&empty[x], kThreads / 32);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == kThreads / 32) {
-        // ------------------------------------------------------------------ producer warp
-        const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
-        const unsigned int ntl = (unsigned int)a.ntiles;
-        // Ticket policy of cheb_step2d_kernel, split so the atomic for item q+1 is issued one item
-        // ahead and only examined in the next iteration (it overlaps this item's bound loads, TMA
-        // issue and dependency wait).  lane 0 state:
-        bool want2 = false, done1 = false, done2 = false;
-        auto choose = [&]() -> int {  // counter of the next ticket: 1, 2, or 0 (none left)
-            if ((want2 || done1) && !done2) {
-                want2 = false;
-                return 2;
-            }
-            if (!done1) return 1;
-            return done2 ? 0 : 2;
-        };
-        auto draw = [&](int ctr) -> unsigned int { return ctr == 1 ? atomicAdd(dy.c1, 1u) : ctr == 2 ? atomicAdd(dy.c2, 1u) : 0u; };
-        // classify a drawn ticket (falling back to the other counter when one is exhausted)
-        auto resolve = [&](int ctr, unsigned int raw, int& stg, int64_t& t) -> bool {
-            for (;;) {
-                if (ctr == 0) return false;
-                if (raw < ntl) {
-                    stg = ctr == 2 ? 1 : 0;
-                    t = raw;
-                    if (ctr == 1) want2 = (int64_t)raw >= f.D;
-                    return true;
-                }
-                if (ctr == 1) done1 = true;
-                else done2 = true;
-                ctr = choose();
-                raw = draw(ctr);
-            }
-        };
-        int64_t pf_bw = -1;  // lane 0: bandwidth for the L2 prefetch (banded operators only)
-        if (CHEB_L2_PREFETCH && lane == 0 && a.bw) {
-            const int64_t bwv = (int64_t)*a.bw;
-            pf_bw = (4 * bwv < a.d) ? bwv : -1;
-        }
-        int64_t known = 0;
-        int64_t prev_t[NS], pend[NS];  // pend: item in buffer x whose completion is not yet observed
-        int prev_stg[NS];
-        for (int x = 0; x < NS; x++) {
-            prev_t[x] = -1;
-            pend[x] = -1;
-            prev_stg[x] = 1;
-        }
-        // Publish finished stage-1 tiles as soon as the compute warps release them -- also while
-        // this warp spins on a dependency, so a wait never holds back this CTA's own finished
-        // tiles (else two CTAs could wait on each other's unpublished tiles).
-        auto retire = [&](int x, bool block) {
-            if (pend[x] < 0) return;
-            const uint32_t ph = (uint32_t)((pend[x] / NS) & 1);
-            if (block) mbar_wait(&empty[x], ph);
-            else if (!mbar_test(&empty[x], ph)) return;
-            if (lane == 0 && prev_stg[x] == 0) red_release_add(f.cnt + prev_t[x] / kChunkTiles, 1u);
-            pend[x] = -1;
-        };
-        int ctr_n = 0;          // lane 0: counter and raw value of the ticket drawn for the next item
-        unsigned int raw_n = 0;
-        if (lane == 0) {
-            ctr_n = choose();
-            raw_n = draw(ctr_n);
-        }
-        int64_t q = 0;
-        for (;; ++q) {
-            const int b = (int)(q % NS);
-            int stg = 0;
-            int64_t t = -1, e0 = 0, e1 = 0;
-            bool ok = false;
-            if (lane == 0) {
-                ok = resolve(ctr_n, raw_n, stg, t);
-                if (ok) {  // bound loads of this item, then the next ticket: both in flight below
-                    const int64_t r0 = t * G::TILE;
-                    e0 = __ldg(a.rp + r0);
-                    e1 = __ldg(a.rp + imin64(r0 + G::TILE, a.d));
-                    ctr_n = choose();
-                    raw_n = draw(ctr_n);
-                }
-            }
-            for (int x = 0; x < NS; x++)
-                if (x != b) retire(x, false);
-            retire(b, true);  // buffer b is free once the compute warps are done with item q-NS
-            ok = __shfl_sync(0xffffffffu, ok, 0);
-            if (!ok) {
-                if (lane == 0) {
-                    s_t[b] = -1;
-                    mbar_arrive(&full[b]);
-                }
-                break;
-            }
-            stg = __shfl_sync(0xffffffffu, stg, 0);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (lane == 0) {
-                unsigned char* st = smem + b * SL::BYTES;
-                const int64_t r0 = t * G::TILE;
-                const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-                const int64_t c0 = e0 & ~int64_t(3), c1 = (e1 + 3) & ~int64_t(3);
-                const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
-                const bool fit = (c1 - c0) <= G::CAP + 8 && (v1 - v0) <= G::CAP + 4;
-                s_fit[b] = fit;
-                s_base_c[b] = c0;
-                s_base_v[b] = v0;
-                s_t[b] = t;
-                s_stg[b] = stg;
-                const double* wsrc = stg ? f.B : f.A;
-                const uint32_t wbytes = (uint32_t)rows * K * 8;
-                const uint32_t sgbytes = ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u;
-                uint32_t bytes = G::RPBYTES + sgbytes + wbytes;
-                if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
-                mbar_expect_tx_only(&full[b], bytes);
-                bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &full[b]);
-                bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &full[b]);
-                bulk_g2s_hint(st + SL::OFF_WPREV, wsrc + (size_t)r0 * K, wbytes, &full[b], policy_evict_first());
-                if (fit) {
-                    bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &full[b]);
-                    bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &full[b]);
-                }
-                if (CHEB_L2_PREFETCH && stg == 0 && pf_bw >= 0) {  // stage-1 first-touch rows of w_j
-                    const int64_t p0 = r0 + pf_bw, p1 = imin64(p0 + rows, a.d);
-                    if (p1 > p0) prefetch_l2(f.B + (size_t)p0 * K, (uint32_t)(p1 - p0) * K * 8);
-                }
-            }
-            if (stg == 1) {  // stage-1 tiles [0, need) must be complete before the gathers
-                const int64_t need = imin64(t + f.H + 1, a.ntiles);
-                uint32_t spins = 0;
-                while (known * kChunkTiles < need) {
-                    const int64_t ch = known + lane;
-                    const unsigned int v = ch < nchunks ? ld_relaxed_u32(f.cnt + ch) : 0u;
-                    const bool fullc = ch >= nchunks || v >= (unsigned int)imin64(kChunkTiles, a.ntiles - ch * kChunkTiles);
-                    const unsigned int notfull = __ballot_sync(0xffffffffu, !fullc);
-                    const int adv = notfull ? __ffs(notfull) - 1 : 32;
-                    known += adv;
-                    if (adv == 0) {
-                        for (int x = 0; x < NS; x++)
-                            if (x != b) retire(x, false);  // keep publishing while waiting
-                        __nanosleep(64);
-                        if ((++spins & 1023u) == 0 && (spins > (1u << 23) || ld_acquire_u32(f.err))) {
-                            if (lane == 0) atomicExch(f.err, 1u);  // ~seconds without progress: never hang
-                            break;
-                        }
-                    }
-                }
-#if CHEB_FUSED_FENCE
-                fence_acq_rel_gpu();
-#endif
-            }
-            __syncwarp();
-            prev_t[b] = t;
-            prev_stg[b] = stg;
-            pend[b] = q;
-            if (lane == 0) mbar_arrive(&full[b]);  // release.cta: the smem metadata above
-        }
-        for (int x = 0; x < NS; x++) retire(x, true);  // the last items may still be computing
-    } else {
-        // ------------------------------------------------------------------ compute warps
-        double2 z2[G::NSL];
-#pragma unroll
-        for (int sl = 0; sl < G::NSL; sl++) z2[sl] = make_double2(0.0, 0.0);
-        double (&mu1)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[0]);
-        double (&mu2)[1][kPPL] = *reinterpret_cast<double(*)[1][kPPL]>(&acc[1]);
-        for (int64_t q = 0;; ++q) {
-            const int b = (int)(q % NS);
-            mbar_wait(&full[b], (uint32_t)((q / NS) & 1));
-            const int64_t t = s_t[b];
-            if (t < 0) break;
-            const int stg = s_stg[b];
-            const unsigned char* st = smem + b * SL::BYTES;
-            const int64_t r0 = t * G::TILE;
-            const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-            if (stg == 0) {
-                if (s_fit[b])
-                    step_tile<K, MODE_CSR, false, true, false, true>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
-                                                                     mu1, f.B, f.B, f.A);
-                else
-                    step_tile<K, MODE_CSR, false, false, false, true>(a, st, r0, rows, 0, 0, z2, mu1, f.B, f.B,
-                                                                      f.A);
-            } else {
-                if (s_fit[b])
-                    step_tile<K, MODE_CSR, false, true, true, false>(a, st, r0, rows, s_base_c[b], s_base_v[b], z2,
-                                                                     mu2, f.A, f.A, f.B);
-                else
-                    step_tile<K, MODE_CSR, false, false, true, false>(a, st, r0, rows, 0, 0, z2, mu2, f.A, f.A,
-                                                                      f.B);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[b]);  // release.cta: this warp's stores and smem reads
-        }
-    }
-    __syncthreads();  // all warps out of the loops; the stage buffers become the reduction scratch
-    grid_reduce_finish<K, kPPL, 2, EPI_PAIR, false, true>(acc, a, smem);
-}
 
 // ---------------------------------------------------------------------------------------
 // K2p: persistent multi-step kernel for small / L2-resident operators (csr, rank-1).
@@ -1777,17 +1042,17 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
             if (first) {
                 if (s_fit[b])
-                    step_tile<K, MODE, true, true, true, false, DBL, false, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+                    step_tile<K, MODE, true, true, true, DBL, false, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                      acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, true, false, true, false, DBL, false, R4>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
+                    step_tile<K, MODE, true, false, true, DBL, false, R4>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
                                                                       nxt);
             } else {
                 if (s_fit[b])
-                    step_tile<K, MODE, false, true, true, false, DBL, false, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
+                    step_tile<K, MODE, false, true, true, DBL, false, R4>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                       acc, cur, cur, nxt);
                 else
-                    step_tile<K, MODE, false, false, true, false, DBL, false, R4>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
+                    step_tile<K, MODE, false, false, true, DBL, false, R4>(a, st, r0, rows, 0, 0, r1, acc, cur, cur,
                                                                        nxt);
             }
             __syncthreads();
@@ -1866,293 +1131,6 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             __syncthreads();
         }
     }
-}
-
-// ---------------------------------------------------------------------------------------
-// Gather-staged step (opt-in, CSR): per tile of T = 1024/K rows, the sorted unique rows of W_cur the
-// tile's nonzeros reference ("gather list", at most S = 4096/K rows) are fetched into shared memory
-// by TMA tile::gather4 (4 rows per instruction); every nonzero carries a 16-bit slot into that
-// list instead of its column, so the compute warps read their neighbours from shared memory.
-// ---------------------------------------------------------------------------------------
-#ifndef CHEB_GS_LIST
-#define CHEB_GS_LIST 3328  // gather-list capacity x k: 52 rows at k = 64 (5-point stencil tiles need 50)
-#endif
-__host__ __device__ constexpr int next_pow2(int x) {
-    int p = 1;
-    while (p < x) p <<= 1;
-    return p;
-}
-
-template <int K>
-struct GsGeo {
-    static_assert(K >= 16, "gather-staged kernels: K >= 16");
-    static constexpr int T = 1024 / K;        // rows per tile (one row per lane group of 256 threads)
-    static constexpr int S = (CHEB_GS_LIST / K) & ~3;  // gather-list capacity (rows, multiple of 4)
-    static constexpr int CAPV = T * 8;        // staged nonzeros per tile (padded CSR)
-    static constexpr int WORDS = words_for(K);
-    static constexpr int OFF_GATH = 0;
-    static constexpr int OFF_WPREV = OFF_GATH + S * K * 8;
-    static constexpr int OFF_VAL = OFF_WPREV + T * K * 8;
-    static constexpr int OFF_SL = OFF_VAL + (CAPV + 4) * 8;
-    static constexpr int OFF_RP = OFF_SL + ((CAPV + 16) * 2 + 15) / 16 * 16;
-    static constexpr int OFF_SGN = OFF_RP + (T + 2) * 8;
-    static constexpr int BYTES = (OFF_SGN + ((T * WORDS * 4 + 15) / 16) * 16 + 1023) / 1024 * 1024;  // TMA dst alignment
-};
-
-// One warp per tile: sort the tile's (padded) columns in shared memory (bitonic), compact the
-// unique ones into gl[t*S ..], pad the list to a multiple of 4 with its last row, and write each
-// nonzero's slot (lower_bound in the list).  Tiles with more than CAPV nonzeros or S unique rows
-// set *ovf (the host then keeps the regular kernels for this operator).
-template <int K>
-__global__ void __launch_bounds__(kThreads)
-gather_list_kernel(int64_t d, int64_t ntiles, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                   int32_t* __restrict__ gl, int32_t* __restrict__ gl_len, uint16_t* __restrict__ sl,
-                   unsigned int* __restrict__ ovf) {
-    using GG = GsGeo<K>;
-    constexpr int C2 = next_pow2(GG::CAPV);
-    __shared__ int32_t buf[kThreads / 32][C2];
-    __shared__ int32_t uq[kThreads / 32][GG::S + 4];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t t = (int64_t)blockIdx.x * (kThreads / 32) + warp; t < ntiles; t += (int64_t)gridDim.x * (kThreads / 32)) {
-        const int64_t r0 = t * GG::T;
-        const int64_t r1 = imin64(r0 + GG::T, d);
-        const int64_t e0 = rp[r0], e1 = rp[r1];
-        const int n = (int)(e1 - e0);
-        if (n > GG::CAPV) {
-            if (lane == 0) {
-                gl_len[t] = -1;
-                atomicOr(ovf, 1u);
-            }
-            continue;
-        }
-        int32_t* b = buf[warp];
-        for (int x = lane; x < C2; x += 32) b[x] = x < n ? ci[e0 + x] : 0x7fffffff;
-        __syncwarp();
-        int np = 1;
-        while (np < n) np <<= 1;
-        for (int k2 = 2; k2 <= np; k2 <<= 1)
-            for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-                for (int x = lane; x < np; x += 32) {
-                    const int y = x ^ j2;
-                    if (y > x) {
-                        const bool up = (x & k2) == 0;
-                        const int32_t bx = b[x], by = b[y];
-                        if ((bx > by) == up) {
-                            b[x] = by;
-                            b[y] = bx;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        // compact the unique values (warp ballot prefix per 32-chunk)
-        int u = 0;
-        for (int base = 0; base < np; base += 32) {
-            const int x = base + lane;
-            const bool keep = x < n && (x == 0 || b[x] != b[x - 1]);
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            const int pos = u + __popc(m & ((1u << lane) - 1u));
-            if (keep && pos < GG::S) uq[warp][pos] = b[x];
-            u += __popc(m);
-        }
-        __syncwarp();
-        if (u > GG::S) {
-            if (lane == 0) {
-                gl_len[t] = -1;
-                atomicOr(ovf, 1u);
-            }
-            continue;
-        }
-        const int u4 = n == 0 ? 0 : (u + 3) & ~3;
-        for (int x = lane; x < u4; x += 32) gl[t * GG::S + x] = uq[warp][x < u ? x : u - 1];
-        if (lane == 0) gl_len[t] = u4;
-        for (int x = lane; x < n; x += 32) {  // slot of each nonzero: lower_bound in uq
-            const int32_t c = ci[e0 + x];
-            int lo = 0, hi = u;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (uq[warp][mid] < c) lo = mid + 1;
-                else hi = mid;
-            }
-            sl[e0 + x] = (uint16_t)lo;
-        }
-        __syncwarp();
-    }
-}
-
-struct GsArgs {
-    const int32_t* gl;      // [ntiles][S] gather rows of each tile (multiple of 4 used)
-    const int32_t* gl_len;  // [ntiles] used entries of gl (multiple of 4)
-    const uint16_t* sl;     // [padded nnz] slot of each nonzero in its tile's gather list
-    int64_t ntiles;         // tiles of GsGeo<K>::T rows
-    unsigned int* err;      // wait-timeout flag (never hang)
-};
-
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tmap, int32_t col, int4 rows,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-
-// Gather-staged fused Chebyshev step (CSR, Algorithm 1).  Warps 0..7 compute (one row per lane
-// group, T rows per tile), warp 8 stages tiles: gather list + row bounds (one warp-wide load),
-// expect_tx, then every lane issues its own gather4 of 4 list rows, lane 0 the bulk copies of
-// W_prev, the tile's values / slots, row pointers and sign words; NS-deep pipeline with
-// full/empty mbarriers.  Static tile -> CTA map (t = c + i*G) and per-CTA partial sums: moments are
-// deterministic.  The gather source W_cur is described by a 2D tensor map [d][K] fp64, box {K, 1}.
-#ifndef CHEB_GS_STAGES
-#define CHEB_GS_STAGES 3
-#endif
-template <int K, bool FIRST>
-__global__ void __launch_bounds__(kThreads + 32, 2)
-cheb_step_gs_kernel(StepArgs a, GsArgs g, const __grid_constant__ CUtensorMap tmap) {
-    using GG = GsGeo<K>;
-    using G = Geo<K>;
-    constexpr int NS = CHEB_GS_STAGES;
-    static_assert(G::GROUPS == GG::T, "one row per lane group");
-    extern __shared__ __align__(1024) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[NS], empty[NS];
-    __shared__ int64_t s_v0[NS], s_s0[NS], s_e0[NS];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t nmine = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    double acc[1][kPPL];
-#pragma unroll
-    for (int q = 0; q < kPPL; q++) acc[0][q] = 0.0;
-    if (tid == 0) {
-        for (int x = 0; x < NS; x++) {
-            mbar_init(&full[x], 1);
-            mbar_init(&empty[x], kThreads / 32);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (warp == kThreads / 32) {
-        // ------------------------------------------------------------------ producer warp
-        // metadata of a tile (list length, the list, row bounds): all loads issued together and
-        // one tile ahead, so their latency overlaps the current tile's staging
-        constexpr int LPL = (GG::S / 4 + 31) / 32;  // int4 list chunks per lane
-        struct Meta {
-            int len;
-            int4 gr[LPL];
-            int64_t e0, e1;
-        };
-        auto load_meta = [&](int64_t t, Meta& m) {
-            const int64_t r0 = t * GG::T;
-            const int rows = (int)imin64((int64_t)GG::T, a.d - r0);
-            m.len = __ldg(g.gl_len + t);
-#pragma unroll
-            for (int c = 0; c < LPL; c++) {
-                const int x = lane + 32 * c;
-                m.gr[c] = x < GG::S / 4 ? __ldg(reinterpret_cast<const int4*>(g.gl + t * GG::S) + x) : make_int4(0, 0, 0, 0);
-            }
-            m.e0 = __ldg(a.rp + r0);
-            m.e1 = __ldg(a.rp + r0 + rows);
-        };
-        Meta cur, nxt;
-        if (nmine > 0) load_meta(blockIdx.x, nxt);
-        for (int64_t it = 0; it < nmine; it++) {
-            const int b = (int)(it % NS);
-            cur = nxt;
-            if (it + 1 < nmine) load_meta((int64_t)blockIdx.x + (it + 1) * gridDim.x, nxt);
-            if (it >= NS) mbar_wait_bounded(&empty[b], (uint32_t)(((it / NS) - 1) & 1), g.err);
-            const int64_t t = (int64_t)blockIdx.x + it * gridDim.x;
-            const int64_t r0 = t * GG::T;
-            const int rows = (int)imin64((int64_t)GG::T, a.d - r0);
-            const int len = cur.len;  // multiple of 4, <= S
-            unsigned char* st = smem + b * GG::BYTES;
-            if (lane == 0) {
-                const int64_t e0 = cur.e0, e1 = cur.e1;
-                const int64_t v0 = e0 & ~int64_t(1), v1 = (e1 + 1) & ~int64_t(1);
-                const int64_t s0 = e0 & ~int64_t(7), s1 = (e1 + 7) & ~int64_t(7);
-                s_v0[b] = v0;
-                s_s0[b] = s0;
-                s_e0[b] = e0;
-                const uint32_t wbytes = (uint32_t)rows * K * 8;
-                const uint32_t sgbytes = ((uint32_t)rows * GG::WORDS * 4 + 15) & ~15u;
-                uint32_t bytes = (uint32_t)len * K * 8 + (uint32_t)(GG::T + 2) * 8 + sgbytes +
-                                 (uint32_t)(v1 - v0) * 8 + (uint32_t)(s1 - s0) * 2;
-                if (!FIRST) bytes += wbytes;
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[b])),
-                             "r"(bytes)
-                             : "memory");
-                bulk_g2s(st + GG::OFF_RP, a.rp + r0, (GG::T + 2) * 8, &full[b]);
-                bulk_g2s(st + GG::OFF_SGN, a.sbits + (size_t)r0 * GG::WORDS, sgbytes, &full[b]);
-                if (!FIRST)
-                    bulk_g2s_hint(st + GG::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &full[b], policy_evict_first());
-                bulk_g2s(st + GG::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &full[b]);
-                bulk_g2s(st + GG::OFF_SL, g.sl + s0, (uint32_t)(s1 - s0) * 2, &full[b]);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int c = 0; c < LPL; c++) {  // every 4-row chunk of the list: one gather4
-                const int x = lane + 32 * c;
-                if (4 * x < len) tma_gather4(st + GG::OFF_GATH + (size_t)x * 4 * K * 8, &tmap, 0, cur.gr[c], &full[b]);
-            }
-        }
-    } else {
-        // ------------------------------------------------------------------ compute warps
-        const int lg = tid % G::L, grp = tid / G::L;
-        int pp[G::NSL];
-#pragma unroll
-        for (int sl = 0; sl < G::NSL; sl++) pp[sl] = 2 * lg + sl * G::SS;
-        for (int64_t it = 0; it < nmine; it++) {
-            const int b = (int)(it % NS);
-            mbar_wait_bounded(&full[b], (uint32_t)((it / NS) & 1), g.err);
-            const unsigned char* st = smem + b * GG::BYTES;
-            const int64_t t = (int64_t)blockIdx.x + it * gridDim.x;
-            const int64_t r0 = t * GG::T;
-            const int rows = (int)imin64((int64_t)GG::T, a.d - r0);
-            const int lr = grp;
-            if (lr < rows) {
-                const int64_t i = r0 + lr;
-                const int64_t* rp_s = reinterpret_cast<const int64_t*>(st + GG::OFF_RP);
-                const double* val_s = reinterpret_cast<const double*>(st + GG::OFF_VAL);
-                const uint16_t* sl_s = reinterpret_cast<const uint16_t*>(st + GG::OFF_SL);
-                const double* gath = reinterpret_cast<const double*>(st + GG::OFF_GATH);
-                const double* wp_s = reinterpret_cast<const double*>(st + GG::OFF_WPREV);
-                const uint32_t* sg_s = reinterpret_cast<const uint32_t*>(st + GG::OFF_SGN);
-                const int ov = (int)(rp_s[lr] - s_v0[b]), os = (int)(rp_s[lr] - s_s0[b]);
-                const int nr = (int)(rp_s[lr + 1] - rp_s[lr]);
-                double2 g2[G::NSL];
-#pragma unroll
-                for (int sl = 0; sl < G::NSL; sl++) g2[sl] = make_double2(0.0, 0.0);
-                for (int t0 = 0; t0 < nr; t0 += CHEB_NNZ_UNROLL) {
-#pragma unroll
-                    for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
-                        const double v = val_s[ov + t0 + q];
-                        const double* xr = gath + (int)sl_s[os + t0 + q] * K;
-#pragma unroll
-                        for (int sl = 0; sl < G::NSL; sl++) {
-                            const double2 x = *reinterpret_cast<const double2*>(xr + pp[sl]);
-                            g2[sl].x = fma(v, x.x, g2[sl].x);
-                            g2[sl].y = fma(v, x.y, g2[sl].y);
-                        }
-                    }
-                }
-                double* out = a.wnext + (size_t)i * K;
-#pragma unroll
-                for (int sl = 0; sl < G::NSL; sl++) {
-                    double2 nw = g2[sl];
-                    if (!FIRST) {
-                        const double2 pv = *reinterpret_cast<const double2*>(wp_s + lr * K + pp[sl]);
-                        nw = make_double2(fma(2.0, g2[sl].x, -pv.x), fma(2.0, g2[sl].y, -pv.y));
-                    }
-                    __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw);
-                    const uint32_t bits = sg_s[lr * GG::WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
-                    acc[0][2 * sl] += signflip(nw.x, bits << 31);
-                    acc[0][2 * sl + 1] += signflip(nw.y, bits << 30);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[b]);
-        }
-    }
-    __syncthreads();  // stage buffers become the reduction scratch
-    grid_reduce_finish<K, kPPL, 1, EPI_STEP, false, true>(acc, a, smem);
 }
 
 // ---------------------------------------------------------------------------------------

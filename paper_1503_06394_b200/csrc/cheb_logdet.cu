@@ -48,8 +48,8 @@ int fail(int code, const char* fmt, ...) {
 struct Profiler {
     std::mutex mu;
     bool on = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];  // [0] single step, [1] fused pair,
-                                                               // [2] persistent (all n steps)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];  // [0] single step, [1] B^T B spmm
+                                                               // (Y = B w), [2] persistent (all n steps)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
     double ms[3] = {0.0, 0.0, 0.0};
     int64_t n[3] = {0, 0, 0};
@@ -59,12 +59,10 @@ int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
     return e ? atoi(e) : dflt;
 }
-// schedule controls (process-wide; CHEB_FUSION / CHEB_PERSISTENT env vars set the initial value)
-std::atomic<int> g_fusion{env_int("CHEB_FUSION", 1)};  // 1 off (default), 2 auto, 3 forced, 4 forced static
+// schedule controls (process-wide; the CHEB_* env vars set the initial value)
 std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
 std::atomic<int> g_small_tiles{env_int("CHEB_SMALL_TILES", 1)};  // 1 auto (default), 0 standard geometry
 std::atomic<int> g_doubling{env_int("CHEB_DOUBLING", 0)};      // 0 off (default), 1 moment doubling
-std::atomic<int> g_gather{env_int("CHEB_GATHER", 0)};          // 0 off (default), 1 gather-staged steps
 
 struct ProfScope {
     cudaStream_t s;
@@ -152,17 +150,23 @@ int tile_rows(int k, int r4 = CHEB_RPG) { return r4 * kThreads * 4 / k; }
 int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL)); }
 
 struct Layout {
-    size_t w0, w1, y, sbits, part, sbuf, ticket;
-    size_t rp2, ci2, va2, u2, cnt, misc, cnt64, scan, gl, gl_len, sl, total;
-    int64_t gs_ntiles;
+    size_t misc, w0, w1, y, sbits, part, sbuf, ticket;
+    size_t rp2, ci2, va2, u2, cnt64, scan, total;
     size_t scan_bytes;
     int64_t rp2_len;
 };
+
+// Status word at the start of every cheb_moments workspace (workspace offset kStatusOff, see
+// cheb_workspace_status): bit 0 = a spin wait of the persistent kernel gave up (timeout),
+// bit 1 = a moment written by the last call is not finite.
+constexpr size_t kStatusOff = 8;
 
 // Workspace of cheb_moments for dimension d, gather-matrix nnz, probe block k.
 Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     Layout L{};
     size_t off = 0;
+    L.misc = off; off += 256;  // [8] u32 status (kStatusOff), [16] barrier count, [20] barrier
+                               // generation, [24] rank-1 s_ready
     const size_t wbytes = align256((size_t)d * k * sizeof(double));
     const int words = k >= 32 ? k / 32 : 1;
     const size_t maxgrid = (size_t)sms * kMaxCtasPerSm;
@@ -187,19 +191,6 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     cub::DeviceScan::ExclusiveSum(nullptr, L.scan_bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(d + 1));
     L.scan = off; off += align256(L.scan_bytes);
     L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
-    L.cnt = off; off += align256(((size_t)ntiles + 64) * sizeof(unsigned int));  // fused wave counters
-    // gather-staged kernels (csr, k >= 16): per-tile gather lists and per-nonzero slots
-    L.gs_ntiles = 0;
-    L.gl = L.gl_len = L.sl = off;
-    if (kind == CL_OP_CSR && k >= 16) {
-        const int T = 1024 / k, S = (CHEB_GS_LIST / k) & ~3;
-        L.gs_ntiles = (d + T - 1) / T;
-        L.gl = off; off += align256((size_t)L.gs_ntiles * S * sizeof(int32_t));
-        L.gl_len = off; off += align256((size_t)L.gs_ntiles * sizeof(int32_t));
-        L.sl = off; off += align256((pnnz + 16) * sizeof(uint16_t));
-    }
-    L.misc = off; off += 256;  // [0] u64 bandwidth, [8] u32 wait-timeout flag, [16] barrier count,
-                               // [20] barrier generation, [24] rank-1 s_ready
     L.total = off;
     return L;
 }
@@ -297,87 +288,37 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
     prep_kernel<MODE><<<grid, kThreads, 0, st>>>(
         d, G2.row_ptr, G2.col_idx, G2.val, alpha, beta, (int64_t*)(ws + L.rp2), L.rp2_len,
         (int32_t*)(ws + L.ci2), (double*)(ws + L.va2),
-        MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr,
-        MODE != MODE_BTB ? (unsigned long long*)(ws + L.misc) : nullptr);
+        MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr);
     g_launches++;
 }
 
-// Fused pairs with dynamic tile tickets (cheb_step2d_kernel) instead of the static map
-// (CHEB_FUSED_DYN, default 1).
-// fusion modes: 2 auto / 3 forced -> warp-specialised dynamic kernel; 4 static map; 5 dynamic,
-// thread-0 producer
-bool fused_dynamic() { return g_fusion.load() != 4; }
-bool fused_ws() { return g_fusion.load() == 2 || g_fusion.load() == 3; }
-// Dynamic lag beyond the halo, in units of the grid size (CHEB_FUSED_LAG; default 1.5 for the
-// warp-specialised kernel, whose producer holds up to kWStages + 1 tickets, 1.0 otherwise): the
-// stage-1 tiles a stage-2 ticket needs were handed out D - H tiles earlier and may still be in
-// flight; measured optimum on configs[3] (profiles/r01_fusion_study.md).
-double fused_lag_waves() {
-    const char* e = getenv("CHEB_FUSED_LAG");
-    return e ? atof(e) : (fused_ws() ? 1.5 : 1.0);
-}
-
-// Temporal fusion plan (CSR mode): stage-2 halo H (tiles) and lag D (positions).
-struct FusionPlan {
-    bool on = false;          // temporally fused pairs
-    bool persistent = false;  // all steps in one persistent cooperative launch
-    int64_t H = 0, D = 0;
-    int G = 0;                // fused grid (= the single-step grid, for bit-identical moments)
+// Schedule of one cheb_moments call (chosen on the host before any launch).
+struct Schedule {
+    bool persistent = false;  // all steps of a probe block in one persistent cooperative launch
     bool power = false;       // power basis (Taylor baseline): w_j = Ã w_{j-1}, every step "FIRST"
     bool doubling = false;    // moment doubling: ceil(n/2) applications of Ã give mu_0..mu_n
     bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
-    bool gather = false;      // gather-staged step kernels (csr): TMA gather4 of each tile's rows
     bool small = false;       // L2-resident operator: 16-row tiles for the Algorithm-1 kernels (RP = 1)
-    CUtensorMap tmap[2];      // W buffers 0/1 as [d][k] fp64 tensors (gather mode)
 };
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda
-// dependency, so the library still loads on machines without a driver).
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-int encode_rows_map(CUtensorMap* m, void* base, int64_t d, int k) {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !p)
-            return fail(CL_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
-        fn = (EncodeTiledFn)p;
-    }
-    cuuint64_t gdim[2] = {(cuuint64_t)k, (cuuint64_t)d};
-    cuuint64_t gstride[1] = {(cuuint64_t)k * 8};
-    cuuint32_t box[2] = {(cuuint32_t)k, 1};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(CL_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return CL_OK;
-}
-
-// launch of a sign-bit step variant (own attribute for its dynamic shared memory)
+// Launch of one step-kernel variant.  The dynamic shared-memory opt-in is a per-device,
+// per-function attribute, so it is set on every launch (a few hundred ns, host side only).
 template <int K, int MODE, bool FIRST, bool DBL, int VB, int RP = 0>
 void launch_step(int grid, size_t smem, cudaStream_t st, const StepArgs& a) {
-    static bool attr = false;  // benign race: the attribute value is the same for every caller
-    if (!attr) {
-        cudaFuncSetAttribute(cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(200 * 1024));
-        attr = true;
-    }
+    cudaFuncSetAttribute(cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP><<<grid, kThreads, smem, st>>>(a);
 }
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
-// RP: tile geometry of the Algorithm-1 kernels (0: CHEB_RPG; 1: 16-row tiles for L2-resident
-// operators, FusionPlan::small); fused pairs always run with RP = 0
+// RP: tile geometry of the Algorithm-1 kernels (0: CHEB_RPG; 1: 16-row tiles, Schedule::small)
 template <int K, int MODE, int RP = 0>
 int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-              int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
+              int64_t mu_stride, cudaStream_t st, int sms, const Schedule& fp) {
     constexpr int R4S = RP ? RP : CHEB_RPG;
-    using G = Geo<K, R4S>;  // per-step / fused geometry; the doubling kernels use Geo<K, CHEB_RPG_DBL>
     constexpr int R4D = RP ? RP : CHEB_RPG_DBL;  // doubling kernels: same RP rule
+    using G = Geo<K, R4S>;  // Algorithm-1 geometry; the doubling kernels use Geo<K, R4D>
     using GD = Geo<K, R4D>;
     using SL = StageLayout<K, MODE, false, R4S>;
     using SLD = StageLayout<K, MODE, false, R4D>;
@@ -392,7 +333,6 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.rp = (const int64_t*)(ws + L.rp2);
     a.ci = (const int32_t*)(ws + L.ci2);
     a.va = (const double*)(ws + L.va2);
-    a.bw = (MODE != MODE_BTB && op->A.nnz > 0) ? (const unsigned long long*)(ws + L.misc) : nullptr;
     a.sbits = sbits;
     a.beta = beta;
     a.r1c_alpha = alpha * op->r1_c;
@@ -422,7 +362,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     const int tile = fp.doubling ? GD::TILE : G::TILE;
     a.ntiles = (d + tile - 1) / tile;
     // dynamic shared memory: the staged tiles, reused as the reduction scratch at the end
-    const size_t smem = std::max<size_t>(fp.doubling ? SLD::SMEM : SL::SMEM, red_scratch_bytes<K, 2>());  // persistent, fused
+    const size_t smem = std::max<size_t>(fp.doubling ? SLD::SMEM : SL::SMEM, red_scratch_bytes<K, 2>());  // persistent
     const size_t smem_step = std::max<size_t>(
         (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, R4D>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
@@ -449,7 +389,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         pp.s_buf = sbuf;
         pp.bar_count = (unsigned int*)(ws + L.misc + 16);
         pp.s_count = (unsigned int*)(ws + L.misc + 20);
-        pp.err = (unsigned int*)(ws + L.misc + 8);
+        pp.err = (unsigned int*)(ws + L.misc + kStatusOff);
         pp.power = fp.power ? 1 : 0;
         CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
         void* args[] = {&a, &pp};
@@ -458,49 +398,11 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         g_launches++;
         return CL_OK;
     }
-    int grid_fused = 0;
-    if (MODE == MODE_CSR && fp.on) grid_fused = fp.G;
     for (int32_t j = 1; j <= nsteps; j++) {
         const double* cur = w[(j - 1) & 1];
         double* nxt = w[j & 1];
-        if (MODE == MODE_CSR && RP == 0 && fp.on && !fp.doubling && j >= 2 && j + 1 <= n) {
-            // steps j and j+1 in one launch: A = w_{j-2} -> w_j, B = w_{j-1} -> w_{j+1}
-            FusedArgs f{};
-            f.A = nxt;
-            f.B = (double*)cur;
-            f.cnt = (unsigned int*)(ws + L.cnt);
-            f.err = (unsigned int*)(ws + L.misc + 8);
-            f.D = fp.D;
-            f.H = fp.H;
-            a.mu_col = j;
-            const int64_t nchunks = (a.ntiles + kChunkTiles - 1) / kChunkTiles;
-            CL_CUDA(cudaMemsetAsync(f.cnt, 0, ((size_t)nchunks + 1) * sizeof(unsigned int), st));
-            ProfScope ps(st, 1);
-            if (fused_dynamic()) {
-                FusedDynArgs dy{};
-                dy.c1 = (unsigned int*)(ws + L.misc + 32);
-                dy.c2 = (unsigned int*)(ws + L.misc + 36);
-                CL_CUDA(cudaMemsetAsync(ws + L.misc + 32, 0, 8, st));
-                void* args[] = {&a, &f, &dy};
-                if (fused_ws()) {
-                    const size_t smem_w = std::max<size_t>((size_t)kWStages * SL::BYTES, red_scratch_bytes<K, 2>());
-                    cudaFuncSetAttribute(cheb_step2w_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w);
-                    CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2w_kernel<K>, dim3(grid_fused),
-                                                        dim3(kFusedWThreads), args, smem_w, st));
-                } else {
-                    CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2d_kernel<K>, dim3(grid_fused),
-                                                        dim3(kThreads), args, smem, st));
-                }
-            } else {
-                void* args[] = {&a, &f};
-                CL_CUDA(cudaLaunchCooperativeKernel((const void*)cheb_step2_kernel<K>, dim3(grid_fused),
-                                                    dim3(kThreads), args, smem, st));
-            }
-            g_launches++;
-            j++;  // consumed two steps
-            continue;
-        }
         if (MODE == MODE_BTB) {
+            ProfScope ps(st, 1);
             spmm_kernel<K><<<grid_spmm, kThreads, 0, st>>>(op->A.n_rows, op->A.row_ptr, op->A.col_idx,
                                                           op->A.val, cur, y);
             g_launches++;
@@ -512,28 +414,6 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.s_next = sbuf + (j & 1) * K;
         a.mu_col = j;
         ProfScope ps(st);
-        if (MODE == MODE_CSR && fp.gather) {  // gather-staged steps (Algorithm 1, csr)
-            if constexpr (K >= 16) {
-                using GG = GsGeo<K>;
-                GsArgs gs{};
-                gs.gl = (const int32_t*)(ws + L.gl);
-                gs.gl_len = (const int32_t*)(ws + L.gl_len);
-                gs.sl = (const uint16_t*)(ws + L.sl);
-                gs.ntiles = L.gs_ntiles;
-                gs.err = (unsigned int*)(ws + L.misc + 8);
-                const size_t smem_gs = std::max<size_t>((size_t)CHEB_GS_STAGES * GG::BYTES, red_scratch_bytes<K, 1>());
-                const int grid_gs = (int)std::min<int64_t>((int64_t)sms * 2, L.gs_ntiles);
-                if (j == 1) {
-                    cudaFuncSetAttribute(cheb_step_gs_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gs);
-                    cheb_step_gs_kernel<K, true><<<grid_gs, kThreads + 32, smem_gs, st>>>(a, gs, fp.tmap[(j - 1) & 1]);
-                } else {
-                    cudaFuncSetAttribute(cheb_step_gs_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gs);
-                    cheb_step_gs_kernel<K, false><<<grid_gs, kThreads + 32, smem_gs, st>>>(a, gs, fp.tmap[(j - 1) & 1]);
-                }
-                g_launches++;
-                continue;
-            }
-        }
         // steps 1 and 2 read v = w_0 from the sign bits when it was not materialised (fp.vbits);
         // same grids as the plain kernels, so the moments are bit-identical either way
         constexpr int V1 = MODE != MODE_BTB ? 1 : 0, V2 = MODE != MODE_BTB ? 2 : 0;
@@ -561,14 +441,13 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
 template <int K>
 int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
                    int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-                   int64_t mu_stride, cudaStream_t st, int sms, const FusionPlan& fp) {
-    const bool small = fp.small && !fp.on;
+                   int64_t mu_stride, cudaStream_t st, int sms, const Schedule& fp) {
     switch (op->kind) {
         case CL_OP_CSR:
-            if (small) return run_block<K, MODE_CSR, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+            if (fp.small) return run_block<K, MODE_CSR, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
             return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         case CL_OP_CSR_RANK1:
-            if (small) return run_block<K, MODE_RANK1, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+            if (fp.small) return run_block<K, MODE_RANK1, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
             return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
         default:
             return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
@@ -581,51 +460,6 @@ void prep_mode(const cl_operator* op, double alpha, double beta, char* ws, const
         case CL_OP_CSR: run_prep<MODE_CSR>(op, alpha, beta, ws, L, st, sms); break;
         case CL_OP_CSR_RANK1: run_prep<MODE_RANK1>(op, alpha, beta, ws, L, st, sms); break;
         default: run_prep<MODE_BTB>(op, alpha, beta, ws, L, st, sms); break;
-    }
-}
-
-int fused_ws_occupancy(int k) {  // cheb_step2w_kernel: 288 threads per CTA
-    auto occ_of = [](auto kern, size_t smem) {
-        int occ = 0;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFusedWThreads, smem);
-        return occ < 1 ? 1 : (occ > kMaxCtasPerSm ? kMaxCtasPerSm : occ);
-    };
-    switch (k) {
-        case 8: return occ_of(cheb_step2w_kernel<8>, std::max<size_t>((size_t)kWStages * StageLayout<8, MODE_CSR>::BYTES, red_scratch_bytes<8, 2>()));
-        case 16: return occ_of(cheb_step2w_kernel<16>, std::max<size_t>((size_t)kWStages * StageLayout<16, MODE_CSR>::BYTES, red_scratch_bytes<16, 2>()));
-        case 32: return occ_of(cheb_step2w_kernel<32>, std::max<size_t>((size_t)kWStages * StageLayout<32, MODE_CSR>::BYTES, red_scratch_bytes<32, 2>()));
-        case 64: return occ_of(cheb_step2w_kernel<64>, std::max<size_t>((size_t)kWStages * StageLayout<64, MODE_CSR>::BYTES, red_scratch_bytes<64, 2>()));
-        default: return occ_of(cheb_step2w_kernel<128>, std::max<size_t>((size_t)kWStages * StageLayout<128, MODE_CSR>::BYTES, red_scratch_bytes<128, 2>()));
-    }
-}
-
-int fused_occupancy(int k) {
-    // both fused kernels (static map / dynamic tickets) run with the same shared memory; a
-    // cooperative grid must fit the smaller occupancy
-    auto occ_of = [](auto kern, size_t smem) {
-        int occ = 0;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-        return occ < 1 ? 1 : (occ > kMaxCtasPerSm ? kMaxCtasPerSm : occ);
-    };
-    auto both = [&](auto ks, auto kd, size_t smem) { return std::min(occ_of(ks, smem), occ_of(kd, smem)); };
-    switch (k) {
-        case 8: return both(cheb_step2_kernel<8>, cheb_step2d_kernel<8>, std::max<size_t>(StageLayout<8, MODE_CSR>::SMEM, red_scratch_bytes<8, 2>()));
-        case 16: return both(cheb_step2_kernel<16>, cheb_step2d_kernel<16>, std::max<size_t>(StageLayout<16, MODE_CSR>::SMEM, red_scratch_bytes<16, 2>()));
-        case 32: return both(cheb_step2_kernel<32>, cheb_step2d_kernel<32>, std::max<size_t>(StageLayout<32, MODE_CSR>::SMEM, red_scratch_bytes<32, 2>()));
-        case 64: return both(cheb_step2_kernel<64>, cheb_step2d_kernel<64>, std::max<size_t>(StageLayout<64, MODE_CSR>::SMEM, red_scratch_bytes<64, 2>()));
-        default: return both(cheb_step2_kernel<128>, cheb_step2d_kernel<128>, std::max<size_t>(StageLayout<128, MODE_CSR>::SMEM, red_scratch_bytes<128, 2>()));
-    }
-}
-
-int step_grid_csr(int k, int64_t ntiles, int sms) {
-    switch (k) {
-        case 8: return grid_for(cheb_step_kernel<8, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<8, MODE_CSR>::BYTES, red_scratch_bytes<8, 3>()));
-        case 16: return grid_for(cheb_step_kernel<16, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<16, MODE_CSR>::BYTES, red_scratch_bytes<16, 3>()));
-        case 32: return grid_for(cheb_step_kernel<32, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<32, MODE_CSR>::BYTES, red_scratch_bytes<32, 3>()));
-        case 64: return grid_for(cheb_step_kernel<64, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<64, MODE_CSR>::BYTES, red_scratch_bytes<64, 3>()));
-        default: return grid_for(cheb_step_kernel<128, MODE_CSR, false>, ntiles, sms, std::max<size_t>(kStepStages * StageLayout<128, MODE_CSR>::BYTES, red_scratch_bytes<128, 3>()));
     }
 }
 
@@ -688,7 +522,7 @@ int cheb_profile_end(double* step_ms, int64_t* step_launches) {
     return CL_OK;
 }
 
-int cheb_profile_fused(double* ms, int64_t* launches) {
+int cheb_profile_spmm(double* ms, int64_t* launches) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     if (ms) *ms = g_prof.ms[1];
     if (launches) *launches = g_prof.n[1];
@@ -723,20 +557,6 @@ int cheb_set_doubling(int32_t on) {
 }
 
 int cheb_get_doubling(void) { return g_doubling.load(); }
-
-int cheb_set_gather(int32_t on) {
-    if (on < 0 || on > 1) return fail(CL_EINVAL, "gather mode must be 0 or 1");
-    g_gather = on;
-    return CL_OK;
-}
-
-int cheb_get_gather(void) { return g_gather.load(); }
-
-int cheb_set_fusion(int32_t steps) {
-    if (steps < 1 || steps > 5) return fail(CL_EINVAL, "fusion mode must be 1..5");
-    g_fusion = steps;
-    return CL_OK;
-}
 
 // Host fp64 coefficient routine: accumulate, node by node, f(x_k)
 // times T_j(x_k) for all j with the scalar recurrence, then scale.
@@ -949,7 +769,7 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     CL_CUDA(cudaMemsetAsync(ws + L.ticket, 0, 256, st));
     CL_CUDA(cudaMemsetAsync(ws + L.misc, 0, 256, st));
     prep_mode(op, alpha, beta, ws, L, st, sms);
-    FusionPlan fp;
+    Schedule fp;
     fp.power = power;
     fp.doubling = !power && g_doubling.load() == 1;
     if (op->kind != CL_OP_BTB) {
@@ -966,57 +786,12 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
-    if (!fp.persistent && !power && !fp.doubling && op->kind == CL_OP_CSR && g_fusion.load() >= 2 && degree >= 3) {
-        // needs the operator bandwidth computed by the prep kernel: one small D2H per call
-        unsigned long long bw = 0;
-        CL_CUDA(cudaMemcpyAsync(&bw, ws + L.misc, sizeof(bw), cudaMemcpyDeviceToHost, st));
-        CL_CUDA(cudaStreamSynchronize(st));
-        const int T = tile_rows(probe_block);
-        const int64_t ntiles = (op->A.n_cols + T - 1) / T;
-        // same grid as the single-step kernel (bit-identical per-CTA partial sums), limited to
-        // what the fused kernel can keep co-resident
-        int64_t G = step_grid_csr(probe_block, ntiles, sms);
-        const int64_t Gmax = (int64_t)sms * (fused_ws() ? fused_ws_occupancy(probe_block) : fused_occupancy(probe_block));
-        if (G > Gmax) G = Gmax;
-        fp.G = (int)G;
-        fp.H = (int64_t)((bw + T - 1) / T) + 1;
-        fp.D = (kFusedSlack + (fp.H + 2 + G - 1) / G) * G;
-        if (fused_dynamic()) fp.D = fp.H + 2 + (int64_t)(G * fused_lag_waves());  // tickets: any D > H
-        if (getenv("CHEB_FUSED_NOWAIT")) fp.H = -1;  // TIMING DIAGNOSTIC ONLY: wrong results
-        const double window = (double)(fp.D + fp.H + 2) * T * probe_block * 8.0 * 2.0;
-        int l2 = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        fp.on = g_fusion.load() >= 3 || (ntiles >= 4 * fp.D && window <= 0.4 * (double)l2);
-    }
-    // gather-staged steps (opt-in): csr, Algorithm 1, per-step schedule, k >= 16; needs every tile's
-    // nonzeros / unique rows within capacity (checked by the list-building pass: one sync)
-    if (g_gather.load() == 1 && op->kind == CL_OP_CSR && probe_block >= 16 && !fp.persistent && !fp.on && !power &&
-        !fp.doubling && L.gs_ntiles > 0) {
-        unsigned int* ovf = (unsigned int*)(ws + L.misc + 44);
-        const int grid = (int)std::min<int64_t>((L.gs_ntiles + 7) / 8, (int64_t)sms * 16);
-        switch (probe_block) {
-            case 16: gather_list_kernel<16><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
-            case 32: gather_list_kernel<32><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
-            case 64: gather_list_kernel<64><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
-            default: gather_list_kernel<128><<<grid, kThreads, 0, st>>>(op->A.n_rows, L.gs_ntiles, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2), (int32_t*)(ws + L.gl), (int32_t*)(ws + L.gl_len), (uint16_t*)(ws + L.sl), ovf); break;
-        }
-        g_launches++;
-        unsigned int hovf = 1;
-        CL_CUDA(cudaMemcpyAsync(&hovf, ovf, sizeof(hovf), cudaMemcpyDeviceToHost, st));
-        CL_CUDA(cudaStreamSynchronize(st));
-        fp.gather = (hovf == 0);
-        if (fp.gather) {
-            if ((rc = encode_rows_map(&fp.tmap[0], ws + L.w0, op->A.n_cols, probe_block))) return rc;
-            if ((rc = encode_rows_map(&fp.tmap[1], ws + L.w1, op->A.n_cols, probe_block))) return rc;
-        }
-    }
-    // per-step csr/rank-1 without fused pairs: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
-    fp.vbits = !fp.persistent && !fp.on && !fp.gather && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
+    // per-step csr/rank-1: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
+    fp.vbits = !fp.persistent && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
     if (getenv("CHEB_DEBUG"))
-        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d fused=%d doubling=%d gather=%d H=%lld D=%lld\n",
+        fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d doubling=%d small=%d\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
-                (int)fp.on, (int)fp.doubling, (int)fp.gather, (long long)fp.H, (long long)fp.D);
+                (int)fp.doubling, (int)fp.small);
     for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
         const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
@@ -1028,6 +803,17 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
             default: rc = run_block_mode<128>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
         }
         if (rc) return rc;
+    }
+    // status epilogue: a timed-out spin wait poisons this call's moment rows with NaN (so every
+    // finiteness check downstream fires); a non-finite moment sets status bit 1.
+    // CHEB_INJECT_TIMEOUT=1 (tests only) raises bit 0 as a timed-out wait would: the call then
+    // fails loudly (NaN moments, CL_ECUDA from cheb_logdet), it can never return wrong numbers.
+    if (getenv("CHEB_INJECT_TIMEOUT")) CL_CUDA(cudaMemsetAsync(ws + L.misc + kStatusOff, 1, 1, st));
+    {
+        const int64_t nmu = (probe_end - probe_begin) * stride;
+        const int grid = (int)std::min<int64_t>((nmu + kThreads - 1) / kThreads, 64);
+        moments_status_kernel<<<grid, kThreads, 0, st>>>((unsigned int*)(ws + L.misc + kStatusOff), mu_out, nmu);
+        g_launches++;
     }
     CL_CUDA(cudaGetLastError());
     return CL_OK;
@@ -1044,8 +830,17 @@ int cheb_finalize(const double* mu, const double* c, int64_t m, int32_t degree,
     return CL_OK;
 }
 
-namespace {
+int cheb_workspace_status(const void* workspace, uint32_t* status, void* stream) {
+    if (!workspace || !status) return fail(CL_EINVAL, "NULL pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t h = 0;
+    CL_CUDA(cudaMemcpyAsync(&h, (const char*)workspace + kStatusOff, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    *status = h;
+    return CL_OK;
+}
 
+namespace {
 
 int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
                   uint64_t seed, int32_t probe_block, cl_result* out, cudaStream_t st) {
@@ -1073,8 +868,7 @@ int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int
     double hstats[3];
     unsigned int ferr = 0;
     CL_CUDA(cudaMemcpyAsync(hstats, stats, sizeof(hstats), cudaMemcpyDeviceToHost, st));
-    CL_CUDA(cudaMemcpyAsync(&ferr, (char*)ws.p + plan(op->A.n_cols, gather_nnz(op), k, op->kind, sm_count()).misc + 8,
-                            sizeof(ferr), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaMemcpyAsync(&ferr, (char*)ws.p + kStatusOff, sizeof(ferr), cudaMemcpyDeviceToHost, st));
     if (out->per_probe)
         CL_CUDA(cudaMemcpyAsync(out->per_probe, gp, sizeof(double) * num_probes, cudaMemcpyDeviceToHost, st));
     if (out->moments)
@@ -1085,7 +879,7 @@ int logdet_device(const cl_operator* op, double a, double b, int32_t degree, int
     out->num_probes = num_probes;
     out->degree = degree;
     out->probe_block = k;
-    if (ferr) return fail(CL_ECUDA, "fused-step dependency wait timed out (CTAs not co-resident?)");
+    if (ferr & 1u) return fail(CL_ECUDA, "persistent-kernel grid wait timed out (CTAs not co-resident?)");
     if (hstats[2] != 1.0 || !std::isfinite(hstats[0]))
         return fail(CL_ENONFINITE, "non-finite estimate: [a,b]=[%g,%g] likely does not enclose the spectrum", a, b);
     return CL_OK;
@@ -1109,17 +903,10 @@ int cheb_logdet(const cl_operator* op, double a, double b, int32_t degree, int32
     return rc;
 }
 
-int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
-                     uint64_t seed, int32_t probe_block, cl_result* out) {
-    auto t0 = std::chrono::steady_clock::now();
-    int rc;
-    if ((rc = check_op(op))) return rc;
-    if ((rc = check_ab(a, b, degree))) return rc;
-    if (num_probes < 1) return fail(CL_EINVAL, "num_probes < 1");
-    if (!out) return fail(CL_EINVAL, "out is NULL");
-    cudaStream_t st;
-    CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    cl_operator dop = *op;
+namespace {
+// Device copy of a HOST operator in the calling thread's operator arena (slot 1), enqueued on st.
+int upload_operator(const cl_operator* op, cl_operator* dop, cudaStream_t st) {
+    *dop = *op;
     // one arena block holds the device copy of every operator array
     auto csr_bytes = [](const cl_csr& A) {
         return align256(sizeof(int64_t) * (A.n_rows + 1)) + align256(sizeof(int32_t) * A.nnz) +
@@ -1129,11 +916,8 @@ int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, 
     if (op->kind == CL_OP_BTB) need += csr_bytes(op->At);
     if (op->kind == CL_OP_CSR_RANK1 && op->r1_u) need += align256(sizeof(double) * op->A.n_cols);
     void* blk = nullptr;
-    const double t_alloc = now_s();
-    if ((rc = arena_get(1, need, &blk))) {
-        cudaStreamDestroy(st);
-        return rc;
-    }
+    int rc;
+    if ((rc = arena_get(1, need, &blk))) return rc;
     size_t used = 0;
     auto up = [&](const void* h, size_t bytes, const void** dptr) -> int {
         if (!h || bytes == 0) return CL_OK;
@@ -1149,15 +933,30 @@ int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, 
         if ((r = up(A.col_idx, sizeof(int32_t) * A.nnz, (const void**)&A.col_idx))) return r;
         return up(A.val, sizeof(double) * A.nnz, (const void**)&A.val);
     };
-    rc = up_csr(dop.A);
-    if (!rc && dop.kind == CL_OP_BTB) rc = up_csr(dop.At);
-    if (!rc && dop.kind == CL_OP_CSR_RANK1 && dop.r1_u)
-        rc = up(dop.r1_u, sizeof(double) * dop.A.n_cols, (const void**)&dop.r1_u);
+    rc = up_csr(dop->A);
+    if (!rc && dop->kind == CL_OP_BTB) rc = up_csr(dop->At);
+    if (!rc && dop->kind == CL_OP_CSR_RANK1 && dop->r1_u)
+        rc = up(dop->r1_u, sizeof(double) * dop->A.n_cols, (const void**)&dop->r1_u);
+    return rc;
+}
+}  // namespace
+
+int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, int32_t num_probes,
+                     uint64_t seed, int32_t probe_block, cl_result* out) {
+    auto t0 = std::chrono::steady_clock::now();
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if ((rc = check_ab(a, b, degree))) return rc;
+    if (num_probes < 1) return fail(CL_EINVAL, "num_probes < 1");
+    if (!out) return fail(CL_EINVAL, "out is NULL");
+    cudaStream_t st;
+    CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cl_operator dop;
     const double t_h2d = now_s();
+    rc = upload_operator(op, &dop, st);
     if (getenv("CHEB_DEBUG")) {
         cudaStreamSynchronize(st);
-        fprintf(stderr, "[chebld] host call: arena %.1f ms, H2D %.1f ms (%zu B)\n", (t_h2d - t_alloc) * 1e3,
-                (now_s() - t_h2d) * 1e3, used);
+        fprintf(stderr, "[chebld] host call: arena + H2D %.1f ms\n", (now_s() - t_h2d) * 1e3);
     }
     const double t_est = now_s();
     if (!rc) rc = logdet_device(&dop, a, b, degree, num_probes, seed, probe_block, out, st);
@@ -1166,6 +965,45 @@ int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, 
     if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] host call: estimate %.1f ms\n", (now_s() - t_est) * 1e3);
     out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return rc;
+}
+
+int cheb_moments_host(const cl_operator* op, double a, double b, int32_t degree, int64_t probe_begin,
+                      int64_t probe_end, uint64_t seed, int32_t probe_block, double* mu_out) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if ((rc = check_ab(a, b, degree))) return rc;
+    if (probe_begin < 0 || probe_end <= probe_begin) return fail(CL_EINVAL, "need 0 <= probe_begin < probe_end");
+    if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32, 64 or 128");
+    if (!mu_out) return fail(CL_EINVAL, "mu_out is NULL");
+    cudaStream_t st;
+    CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cl_operator dop;
+    rc = upload_operator(op, &dop, st);
+    const size_t ws_bytes = plan(op->A.n_cols, gather_nnz(op), probe_block, op->kind, sm_count()).total;
+    const size_t mu_bytes = sizeof(double) * (size_t)(probe_end - probe_begin) * ((size_t)degree + 1);
+    void* ws = nullptr;
+    if (!rc) rc = arena_get(0, align256(ws_bytes) + mu_bytes, &ws);
+    uint32_t status = 0;
+    if (!rc) {
+        double* mu = (double*)((char*)ws + align256(ws_bytes));
+        rc = moments_impl(&dop, 2.0 / (b - a), (b + a) / (b - a), false, degree, probe_begin, probe_end, seed,
+                          probe_block, ws, ws_bytes, mu, st);
+        if (!rc) {
+            cudaError_t e1 = cudaMemcpyAsync(&status, (char*)ws + kStatusOff, sizeof(status), cudaMemcpyDeviceToHost, st);
+            cudaError_t e2 = cudaMemcpyAsync(mu_out, mu, mu_bytes, cudaMemcpyDeviceToHost, st);
+            cudaError_t e3 = cudaStreamSynchronize(st);
+            if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+                rc = fail(CL_ECUDA, "D2H of moments: %s",
+                          cudaGetErrorString(e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3)));
+        }
+    }
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (rc) return rc;
+    if (status & 1u) return fail(CL_ECUDA, "persistent-kernel grid wait timed out (CTAs not co-resident?)");
+    if (status & 2u)
+        return fail(CL_ENONFINITE, "non-finite moment: [a,b]=[%g,%g] likely does not enclose the spectrum", a, b);
+    return CL_OK;
 }
 
 int cheb_bounds_btb(const cl_operator* op, double* ab_out, void* stream) {
@@ -1218,11 +1056,11 @@ int cheb_probes(int64_t d, uint64_t seed, int64_t probe_begin, int32_t probe_blo
     CL_CUDA(cudaMemsetAsync((char*)ws.p + L.ticket, 0, 256, st));
     int rc;
     switch (probe_block) {
-        case 8: rc = run_block<8, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 8, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
-        case 16: rc = run_block<16, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 16, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
-        case 32: rc = run_block<32, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 32, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
-        case 64: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
-        default: rc = run_block<128, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 128, (char*)ws.p, L, (double*)mu.p, 1, st, sms, FusionPlan()); break;
+        case 8: rc = run_block<8, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 8, (char*)ws.p, L, (double*)mu.p, 1, st, sms, Schedule()); break;
+        case 16: rc = run_block<16, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 16, (char*)ws.p, L, (double*)mu.p, 1, st, sms, Schedule()); break;
+        case 32: rc = run_block<32, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 32, (char*)ws.p, L, (double*)mu.p, 1, st, sms, Schedule()); break;
+        case 64: rc = run_block<64, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 64, (char*)ws.p, L, (double*)mu.p, 1, st, sms, Schedule()); break;
+        default: rc = run_block<128, MODE_CSR>(&op, 1.0, 0.0, 0, seed, probe_begin, 128, (char*)ws.p, L, (double*)mu.p, 1, st, sms, Schedule()); break;
     }
     if (rc) return rc;
     CL_CUDA(cudaMemcpyAsync(v_out, (char*)ws.p + L.w0, sizeof(double) * d * probe_block,

@@ -86,7 +86,7 @@ def likelihood_scan(family: PrecisionFamily, thetas: Sequence[float], xs: Sequen
         if not a > 0:
             raise ValueError(f"J({th}) not certified positive definite by Gershgorin (lo={a})")
         est = Estimator(Operator("csr", J), a, b, degree, num_probes, k, seed)
-        _, stats = est.run()
+        _, stats = est.run(check=True)  # raises on a device timeout / non-finite estimate
         st = stats.cpu().numpy()
         q = sum(quadform(J, x) for x in xs)
         out["logdet"].append(st[0])

@@ -42,10 +42,6 @@ def main():
     P.set_persistent(1)
     P.logdet(op_b, a, b, 5, 9, seed=1, k=16)
     P.set_doubling(False)
-    for mode in (3, 4, 5):  # fused pairs: warp-specialised, static, dynamic
-        P.set_fusion(mode)
-        P.moments(op_g, 0.2, 1.8, 6, 0, 9, 1, 16)
-    P.set_fusion(1)
     torch.cuda.synchronize()
     print("sanitize smoke ok")
 

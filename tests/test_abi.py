@@ -87,6 +87,7 @@ def test_validation_before_device_work(L):
     r = _lib.CLResult()
     assert L.cheb_logdet(ctypes.byref(op), 0.5, 1.5, 3, 0, 1, 0, ctypes.byref(r)) == -1
     assert L.cheb_finalize(None, None, 1, 1, None, None, None) == -1
+    assert L.cheb_workspace_status(None, None, None) == -1
 
 
 def test_schedule_controls_validate(L):
@@ -95,10 +96,6 @@ def test_schedule_controls_validate(L):
     assert L.cheb_set_doubling(-1) == _lib.CL_EINVAL
     assert L.cheb_set_doubling(1) == 0 and L.cheb_get_doubling() == 1
     assert L.cheb_set_doubling(0) == 0 and L.cheb_get_doubling() == 0
-    assert L.cheb_set_fusion(0) == _lib.CL_EINVAL
-    assert L.cheb_set_fusion(6) == _lib.CL_EINVAL
-    for mode in (1, 2, 3, 4, 5, 1):
-        assert L.cheb_set_fusion(mode) == 0
     assert L.cheb_set_persistent(3) == _lib.CL_EINVAL
     assert L.cheb_set_persistent(1) == 0
     assert L.cheb_set_small_tiles(2) == _lib.CL_EINVAL

@@ -63,3 +63,42 @@ def test_gloo_world2_combine_equals_single_process(tmp_path, orc):
     for r in range(world):
         got = np.load(tmp_path / f"mu{r}.npy")
         assert np.array_equal(got, full)  # zero padding + sum is exact
+
+
+def _worker_poison(rank, world, port, out_dir):
+    """Rank 1's shard comes back poisoned (NaN rows: what cheb_moments' status epilogue writes
+    after a timed-out spin wait); after the all-reduce EVERY rank holds non-finite moments, so
+    every rank's finalize flags the estimate and ShardedEstimator.check raises on all of them."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import workloads as W
+    from paper_1503_06394_b200.api import check_estimate
+    from paper_1503_06394_b200._lib import ChebError
+    wl = W.get_workload("gmrf_s")
+    A, _ = wl.matrices()
+    m, n = 10, 6
+    b0, b1 = shard_range(m, world, rank)
+    mu = torch.zeros((m, n + 1), dtype=torch.float64)
+    mu[b0:b1] = torch.from_numpy(oracle.moments(oracle.Op("csr", A), wl.a, wl.b, n, wl.seed, range(b0, b1)))
+    if rank == 1:
+        mu[b0:b1] = float("nan")
+    combine_moments(mu)
+    g, gp, se = oracle.gamma_from_moments(oracle.coeffs_log(wl.a, wl.b, n), mu.numpy())
+    stats = torch.tensor([g, se, 1.0 if np.all(np.isfinite(gp)) else 0.0], dtype=torch.float64)
+    try:
+        check_estimate(stats)
+        raised = 0
+    except ChebError as e:
+        raised = e.code
+    np.save(os.path.join(out_dir, f"raised{rank}.npy"), np.array([raised]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_error_reaches_every_rank(tmp_path):
+    world, port = 2, _free_port()
+    tmp.spawn(_worker_poison, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert int(np.load(tmp_path / f"raised{r}.npy")[0]) == -5

@@ -127,48 +127,14 @@ def test_doubling_off_restores_algorithm1(orc):
     try:
         n0 = P.launch_count()
         P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-        assert P.launch_count() - n0 == 2 + 1 + 10 + 1
+        assert P.launch_count() - n0 == 2 + 1 + 10 + 1 + 1  # prep, init, steps, status, finalize
         P.set_doubling(True)
         n0 = P.launch_count()
         P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-        assert P.launch_count() - n0 == 2 + 1 + 5 + 1
+        assert P.launch_count() - n0 == 2 + 1 + 5 + 1 + 1
     finally:
         P.set_doubling(False)
         P.set_persistent(1)
 
-
-def _full(orc, name, k, sample):
-    wl = W.get_workload(name)
-    A, At = wl.matrices()
-    op = _dev_op(wl.mode, A, At, wl.r1_c)
-    a, b = (wl.a, wl.b) if wl.a is not None else P.bounds_btb(op)
-    est = P.Estimator(op, a, b, wl.degree, wl.num_probes, k, seed=wl.seed)
-    gp, stats = est.run()
-    torch.cuda.synchronize()
-    mu = est.mu.cpu().numpy()
-    assert stats.cpu().numpy()[2] == 1.0
-    omu = orc.moments(orc.Op(wl.mode, A, wl.r1_c), a, b, wl.degree, wl.seed, sample, workers=len(sample))
-    _check(mu[list(sample)], omu, wl.d)
-    c = orc.coeffs_log(a, b, wl.degree)
-    gpn = gp.cpu().numpy()
-    for i, p in enumerate(sample):
-        og = orc.gamma_from_moments(c, omu[i:i + 1])[0]
-        assert abs(gpn[p] - og) <= GAMMA_RTOL * abs(og) + 1e-12 * wl.d
-
-
-def test_doubling_full_config1_torus256(orc, doubling):
-    _full(orc, "torus256", 32, [0, 31])
-
-
-def test_doubling_full_config2_gmrf1000(orc, doubling):
-    _full(orc, "gmrf1000", 64, [0, 63])
-
-
-@pytest.mark.slow
-def test_doubling_full_config3_gmrf5000(orc, doubling):
-    _full(orc, "gmrf5000", 64, [0, 127])
-
-
-@pytest.mark.slow
-def test_doubling_full_config4_btb4m(orc, doubling):
-    _full(orc, "btb4m", 64, [0, 63])
+# Full-size doubling parity (every probe of configs[0..4] vs the oracle's tables) lives in
+# tests/test_parity_full_gpu.py.

@@ -360,6 +360,22 @@ def test_variance_law(orc):
     assert abs(gp.mean() - np.trace(P)) < 4 * sd / math.sqrt(m)
     ratio = gp.std(ddof=1) / sd
     assert 0.9 < ratio < 1.1  # chi^2 band for 1279 dof is ~ +-4%
+    # the oracle's reported standard error is the estimator's sd, i.e. the per-sample sd of the
+    # variance law over sqrt(m) (P:187-190 with G8's 1/m): stderr * sqrt(m) ~ sqrt(2(|P|_F^2 - sum P_ii^2))
+    assert 0.9 < r["stderr"] * math.sqrt(m) / sd < 1.1
+    assert 0.9 < r["stderr"] / (sd / math.sqrt(m)) < 1.1
+
+
+def test_stderr_two_probes_closed_form(orc):
+    """m = 2: the sample sd of {x, y} is |x - y|/sqrt(2), so the standard error of the mean is
+    |x - y|/2 exactly; m = 1 reports 0 (a single probe has no spread estimate)."""
+    wl = W.get_workload("gmrf_s")
+    A, _ = wl.matrices()
+    r = orc.logdet(orc.Op("csr", A), wl.a, wl.b, 15, 2, 5, workers=2)
+    x, y = r["gamma_p"]
+    assert abs(r["stderr"] - abs(x - y) / 2) <= 1e-15 * abs(x - y)
+    assert abs(r["gamma"] - (x + y) / 2) <= 1e-15 * abs(x + y)
+    assert orc.logdet(orc.Op("csr", A), wl.a, wl.b, 15, 1, 5)["stderr"] == 0.0
 
 
 # ---------------------------------------------------------------- Alg. 2 setup bounds

@@ -1,0 +1,115 @@
+"""Full-size, full-m GPU parity: EVERY probe of BASELINE.json configs[0..4] against the oracle.
+
+The oracle's tables (tests/golden/oracle_mu/<name>.npz) were written by
+scripts/oracle_golden.py, which calls only oracle/ (the pinned CPU implementation) on all host
+cores -- SURVEY §4.5's "compute once, cache keyed by (config, seed, probe, n)".  A table is only
+used if the regenerated matrix hashes to the table's matrix_sha256 and oracle/cheb_oracle.c to its
+oracle_sha256; probe 0 is also recomputed live by the oracle and must equal the table bit for bit.
+
+The CUDA path runs in the bench launch configurations (Estimator, the object bench.py times):
+k = 16 (the strong-scaling headline, 8 blocks at configs[3]) and the weak-scaling / single-GPU
+block size (k = 64, or the smallest k >= m), for Algorithm 1 and for the moment-doubling
+schedule.  Tolerances (north_star): Gamma within 1e-10 relative; every Gamma_p
+within 1e-10 |Gamma_p| + 1e-12 d; every moment within 1e-11 d; stderr within 1e-8 relative.
+
+Set PARITY_REPORT=<path> to append one JSON line per case with the measured margins
+(profiles/r02_parity.json is assembled from these lines).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_1503_06394_b200 as P  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden", "oracle_mu")
+
+# (config, probe blocks k, slow)
+CASES = [("gmrf32", (16, 64), False), ("torus256", (16, 32), False), ("gmrf1000", (16, 64), False),
+         ("gmrf5000", (16, 64), True), ("btb4m", (16, 64), True)]
+PARAMS = [pytest.param(name, k, dbl, marks=[pytest.mark.slow] if slow else [])
+          for name, ks, slow in CASES for k in ks for dbl in (False, True)]
+
+_cache = {}
+
+
+def _sha(A, At):
+    h = hashlib.sha256()
+    for M in (A, At):
+        if M is None:
+            continue
+        for arr in (M.row_ptr, M.col_idx, M.val):
+            h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()
+
+
+def _golden(orc, name):
+    """(workload, A, At, table) with the table's provenance checked."""
+    if name in _cache:
+        return _cache[name]
+    z = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    wl = W.get_workload(name)
+    A, At = wl.matrices()
+    assert str(z["matrix_sha256"]) == _sha(A, At), f"stale golden table for {name}: rerun scripts/oracle_golden.py"
+    with open(os.path.join(ROOT, "oracle", "cheb_oracle.c"), "rb") as f:
+        assert str(z["oracle_sha256"]) == hashlib.sha256(f.read()).hexdigest(), \
+            f"oracle changed since {name}.npz was written: rerun scripts/oracle_golden.py"
+    a, b, n = float(z["a"]), float(z["b"]), int(z["degree"])
+    assert (n, int(z["seed"]), z["mu"].shape[0]) == (wl.degree, wl.seed, wl.num_probes)
+    # the table is the oracle's: probe 0 recomputed live, bit for bit
+    live = orc.moments(orc.Op(wl.mode, A, wl.r1_c), a, b, n, wl.seed, [0], workers=1)
+    assert np.array_equal(live[0], z["mu"][0])
+    _cache.clear()  # keep at most one full-size matrix alive
+    _cache[name] = (wl, A, At, z)
+    return _cache[name]
+
+
+@pytest.fixture
+def schedule():
+    yield
+    P.set_doubling(False)
+
+
+@pytest.mark.parametrize("name,k,dbl", PARAMS)
+def test_full_m_parity(orc, schedule, name, k, dbl):
+    wl, A, At, z = _golden(orc, name)
+    a, b, n, m, d = float(z["a"]), float(z["b"]), wl.degree, wl.num_probes, wl.d
+    op = P.Operator(wl.mode, P.DeviceCSR.from_host(A), P.DeviceCSR.from_host(At) if At is not None else None,
+                    wl.r1_c)
+    if wl.mode == "btb":  # the path's own a0 step agrees with the oracle's bounds
+        ga, gb = P.bounds_btb(op)
+        assert abs(ga - a) <= 1e-13 * a and abs(gb - b) <= 1e-13 * b
+    P.set_doubling(dbl)
+    est = P.Estimator(op, a, b, n, m, k, seed=wl.seed)
+    gp, stats = est.run(check=True)
+    mu = est.mu.cpu().numpy()
+    gp = gp.cpu().numpy()
+    st = stats.cpu().numpy()
+    omu, ogp, og, ose = z["mu"], z["gamma_p"], float(z["gamma"]), float(z["stderr"])
+    dmu = np.abs(mu - omu)
+    dgp = np.abs(gp - ogp)
+    rep = {"config": name, "notes": wl.notes, "k": k, "schedule": "doubling" if dbl else "algorithm1",
+           "m": m, "degree": n, "d": d, "gamma_gpu": float(st[0]), "gamma_oracle": og,
+           "rel_err_gamma": abs(st[0] - og) / abs(og), "max_rel_err_gamma_p": float((dgp / np.abs(ogp)).max()),
+           "max_abs_err_mu_over_d": float(dmu.max() / d), "rel_err_stderr": abs(st[1] - ose) / ose,
+           "tolerances": {"gamma": 1e-10, "gamma_p": "1e-10|G_p| + 1e-12 d", "mu": "1e-11 d", "stderr": 1e-8}}
+    path = os.environ.get("PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rep) + "\n")
+    assert st[2] == 1.0
+    assert np.all(dmu <= 1e-11 * d), rep
+    assert np.all(dgp <= 1e-10 * np.abs(ogp) + 1e-12 * d), rep
+    assert abs(st[0] - og) <= 1e-10 * abs(og), rep
+    assert abs(st[1] - ose) <= 1e-8 * ose, rep

@@ -88,61 +88,6 @@ def persistent_mode():
     P.set_persistent(1)
 
 
-@pytest.fixture
-def fusion_mode():
-    """Restore the default temporal-fusion mode after a test.  The fused-pair kernels use the
-    standard tile geometry, so the per-step references of these tests do too."""
-    P.set_small_tiles(0)
-    yield P.set_fusion
-    P.set_fusion(1)
-    P.set_small_tiles(1)
-
-
-@pytest.mark.parametrize("k", [8, 16, 32, 64, 128])
-@pytest.mark.parametrize("degree", [3, 4, 9, 40])
-def test_fused_pairs_bit_identical_and_parity(orc, fusion_mode, persistent_mode, k, degree):
-    """The temporally fused two-step kernel, static tile map (mode 4), gives moments
-    bit-identical to one launch per step; the dynamic-ticket kernel (mode 3) agrees to
-    rounding; all match the oracle (odd and even step counts)."""
-    persistent_mode(0)
-    wl = W.get_workload("gmrf_s")
-    A, _ = _mats(wl)
-    op = _dev_op("csr", A)
-    m = 11
-    fusion_mode(1)
-    single = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
-    mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, degree, wl.seed, range(m), workers=4)
-    for mode in (4, 3, 5):
-        fusion_mode(mode)
-        n0 = P.launch_count()
-        fused = P.moments(op, wl.a, wl.b, degree, 0, m, wl.seed, k).cpu().numpy()
-        nl = P.launch_count() - n0
-        blocks = -(-m // k)
-        assert nl == 2 + blocks * (1 + 1 + (degree - 1) // 2 + (degree - 1) % 2)  # prep (2); init, first, pairs, tail
-        if mode == 4:
-            assert np.array_equal(single, fused)
-        else:
-            assert np.allclose(single, fused, rtol=1e-13, atol=1e-13 * wl.d)
-        _check_moments(fused, mu, wl.d)
-
-
-def test_fused_wide_band_forced(orc, fusion_mode, persistent_mode):
-    """Forced fusion stays correct for an operator with a wide band (random SPD:
-    bandwidth ~ d) -- the dependency wait covers the whole matrix."""
-    persistent_mode(0)
-    S = W.random_spd(20000, 6)
-    op = _dev_op("csr", S)
-    lam = 1.0 + 2.0 * np.abs(S.val).max() * 12
-    fusion_mode(1)
-    single = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
-    fusion_mode(4)
-    assert np.array_equal(single, P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy())
-    for mode in (3, 5):
-        fusion_mode(mode)
-        fused = P.moments(op, 0.01, lam, 7, 0, 16, 3, 16).cpu().numpy()
-        assert np.allclose(single, fused, rtol=1e-12, atol=1e-12 * S.n_rows)
-
-
 def test_rank1_explicit_u(orc):
     T = W.torus_laplacian(21)
     u = np.linspace(0.5, 1.5, T.n_rows)
@@ -259,11 +204,12 @@ def test_launch_count_increases(persistent_mode):
     persistent_mode(0)
     n0 = P.launch_count()
     P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-    assert P.launch_count() - n0 == 2 + 1 + 10 + 1  # prep (count + scatter) + init + 10 steps + finalize
+    # prep (count + scatter) + init + 10 steps + status epilogue + finalize
+    assert P.launch_count() - n0 == 2 + 1 + 10 + 1 + 1
     persistent_mode(2)
     n0 = P.launch_count()
     P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-    assert P.launch_count() - n0 == 2 + 1 + 1 + 1  # prep (2) + init + persistent + finalize
+    assert P.launch_count() - n0 == 2 + 1 + 1 + 1 + 1  # prep (2) + init + persistent + status + finalize
 
 
 @pytest.mark.parametrize("name", ["gmrf32", "torus_s", "gmrf_s"])
@@ -481,26 +427,6 @@ def test_sharded_estimators_sum_to_single_run(world):
     assert torch.equal(st_full, st_sum)
 
 
-def test_fusion_auto_at_config2_size(orc, fusion_mode, persistent_mode):
-    """Fusion mode 2 (auto) engages the warp-specialised fused kernel at configs[2] size
-    (d = 1e6, banded); moments agree with per-step launches to rounding and with the oracle on
-    sampled probes."""
-    wl = W.get_workload("gmrf1000")
-    A, _ = _mats(wl)
-    op = _dev_op("csr", A)
-    n, m = 21, 64
-    fusion_mode(1)
-    single = P.moments(op, wl.a, wl.b, n, 0, m, wl.seed, 64).cpu().numpy()
-    fusion_mode(2)
-    P.profile_begin()
-    fused = P.moments(op, wl.a, wl.b, n, 0, m, wl.seed, 64).cpu().numpy()
-    prof = P.profile_end()
-    assert prof["fused"][1] == (n - 1) // 2  # pairs (2,3), (4,5), ... launched as fused kernels
-    assert np.allclose(single, fused, rtol=1e-13, atol=1e-13 * wl.d)
-    mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, wl.seed, [0, 63], workers=2)
-    _check_moments(fused[[0, 63]], mu, wl.d)
-
-
 @pytest.mark.parametrize("name", ["gmrf32", "torus_s", "btb_s", "gmrf_s"])
 def test_cuda_graph_replay_identical(name):
     """A captured estimate replays to the bit-identical result of an eager run."""
@@ -552,48 +478,119 @@ def test_host_entry_arena_reuse_across_operators(orc):
     P.release_cache()
 
 
+# ------------------------------------------------------------------ instantiations no other test reaches
+def test_rank1_standard_tile_geometry_per_step(orc, persistent_mode):
+    """Rank-1 on the standard tile geometry (cheb_step_kernel<64, RANK1, ..., RP = 0>): a 1024^2
+    torus + c 11^T at k = 64 has a working set above half of L2, so neither the small-tile rule nor
+    the persistent kernel applies.  Every probe against the oracle."""
+    persistent_mode(1)
+    N = 1024
+    T = W.torus_laplacian(N)
+    lam2 = 2.0 - 2.0 * math.cos(2.0 * math.pi / N)
+    c = lam2 / (N * N)
+    op = _dev_op("rank1", T, None, c)
+    n, m = 24, 64
+    P.profile_begin()
+    r = P.logdet(op, lam2, 8.0, n, m, seed=13, k=64, want_moments=True)
+    prof = P.profile_end()
+    assert prof["persistent"][1] == 0 and prof["single"][1] == n  # per-step launches
+    mu = orc.moments(orc.Op("rank1", T, c), lam2, 8.0, n, 13, range(m), workers=8)
+    _check_moments(r.moments, mu, T.n_rows)
+    g, _, _ = orc.gamma_from_moments(orc.coeffs_log(lam2, 8.0, n), mu)
+    _check_gamma(r.logdet, g)
+
+
 @pytest.fixture
-def gather_mode():
-    yield P.set_gather
-    P.set_gather(False)
+def small_tiles_mode():
+    yield P.set_small_tiles
+    P.set_small_tiles(1)
 
 
-@pytest.mark.parametrize("name", ["gmrf_s", "gmrf32", "spd"])
-@pytest.mark.parametrize("k", [16, 32, 64, 128])
-def test_gather_staged_parity(orc, gather_mode, persistent_mode, name, k):
-    """Gather-staged steps (TMA gather4 of each tile's unique rows) against the oracle, and
-    deterministic run to run; 'spd' is the paper's 5.1 random SPD matrix as a CSR operator
-    (random columns: long gather lists, ragged rows) with its Gershgorin interval."""
-    persistent_mode(0)
-    gather_mode(True)
-    if name == "spd":
-        A = W.random_spd(3001, 4)
-        op = _dev_op("csr", A)
-        a, b, n, m, seed, d = 1e-3, P.norm_bound(op), 20, 20, 3, A.n_rows
-    else:
-        wl = W.get_workload(name)
-        A, _ = _mats(wl)
-        op = _dev_op("csr", A)
-        a, b, n, m, seed, d = wl.a, wl.b, wl.degree, wl.num_probes, wl.seed, wl.d
-    r = P.logdet(op, a, b, n, m, seed=seed, k=k, want_moments=True)
-    mu = orc.moments(orc.Op("csr", A), a, b, n, seed, range(m), workers=4)
-    _check_moments(r.moments, mu, d)
-    g, _, _ = orc.gamma_from_moments(orc.coeffs_log(a, b, n), mu)
-    assert abs(r.logdet - g) <= GAMMA_RTOL * abs(g)
-    r2 = P.logdet(op, a, b, n, m, seed=seed, k=k, want_moments=True)
-    assert np.array_equal(r.moments, r2.moments)
+@pytest.mark.parametrize("name", ["gmrf32", "gmrf_s", "torus_s"])
+@pytest.mark.parametrize("k", [8, 64])
+@pytest.mark.parametrize("dbl", [False, True])
+def test_persistent_standard_geometry(orc, persistent_mode, small_tiles_mode, name, k, dbl):
+    """cheb_persist_kernel<..., RP = 0> (persistent forced, small tiles off): vs the oracle and
+    bit-identical to per-step launches on the same geometry."""
+    small_tiles_mode(0)
+    wl = W.get_workload(name)
+    A, _ = _mats(wl)
+    op = _dev_op(wl.mode, A, None, wl.r1_c)
+    m = wl.num_probes
+    P.set_doubling(dbl)
+    try:
+        out = {}
+        for mode in (0, 2):
+            persistent_mode(mode)
+            out[mode] = P.moments(op, wl.a, wl.b, wl.degree, 0, m, wl.seed, k).cpu().numpy()
+    finally:
+        P.set_doubling(False)
+    assert np.array_equal(out[0], out[2])
+    mu = orc.moments(orc.Op(wl.mode, A, wl.r1_c), wl.a, wl.b, wl.degree, wl.seed, range(m), workers=4)
+    _check_moments(out[2], mu, wl.d)
 
 
-def test_gather_staged_full_config2(orc, gather_mode, persistent_mode):
-    persistent_mode(0)
-    gather_mode(True)
-    _full_size(orc, "gmrf1000", 64, [0, 63])
+# ------------------------------------------------------------------ device errors on the async path
+def test_timeout_status_poisons_and_raises(persistent_mode, monkeypatch):
+    """A timed-out spin wait (injected: CHEB_INJECT_TIMEOUT raises the status bit the persistent
+    kernel's bailout sets) must never come back as a normal value: cheb_moments' status epilogue
+    turns the call's moments into NaN, the status word reports it, Estimator.run(check=True),
+    ShardedEstimator.run() and cheb_logdet raise."""
+    from paper_1503_06394_b200.dist import ShardedEstimator
+    wl = W.get_workload("gmrf_s")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    monkeypatch.setenv("CHEB_INJECT_TIMEOUT", "1")
+    est = P.Estimator(op, wl.a, wl.b, 12, 16, 16, seed=3)
+    gp, stats = est.run()
+    assert P.workspace_status(est.workspace) & 1
+    assert np.all(np.isnan(est.mu.cpu().numpy()))
+    assert stats.cpu().numpy()[2] == 0.0
+    with pytest.raises(P.ChebError) as ei:
+        est.run(check=True)
+    assert ei.value.code == -4
+    with pytest.raises(P.ChebError) as ei:
+        ShardedEstimator(op, wl.a, wl.b, 12, 16, 16, seed=3).run()
+    assert ei.value.code == -4
+    with pytest.raises(P.ChebError) as ei:
+        P.logdet(op, wl.a, wl.b, 12, 16, seed=3, k=16)
+    assert ei.value.code == -4
+    monkeypatch.delenv("CHEB_INJECT_TIMEOUT")
+    gp, stats = est.run(check=True)  # status word is per call: clean again
+    assert P.workspace_status(est.workspace) == 0
 
 
-@pytest.mark.slow
-def test_fused_pairs_full_config3(orc, fusion_mode, persistent_mode):
-    """Fused step pairs (fusion mode 2: warp-specialised, dynamic tickets) at the headline size
-    in the bench launch configuration (k = 64, two blocks), sampled probes vs the oracle."""
-    persistent_mode(0)
-    fusion_mode(2)
-    _full_size(orc, "gmrf5000", 64, [0, 127])
+def test_nonfinite_status_on_async_path():
+    """b below lambda_max on the asynchronous path: status bit 1, check raises CL_ENONFINITE."""
+    from paper_1503_06394_b200.dist import ShardedEstimator
+    A = W.csr.from_coo(50, 50, np.arange(50), np.arange(50), np.full(50, 1e6))
+    op = _dev_op("csr", A)
+    est = P.Estimator(op, 0.5, 1.0, 200, 8, 8, seed=1)
+    est.run()
+    assert P.workspace_status(est.workspace) & 2
+    with pytest.raises(P.ChebError) as ei:
+        est.run(check=True)
+    assert ei.value.code == -5
+    with pytest.raises(P.ChebError):
+        ShardedEstimator(op, 0.5, 1.0, 200, 8, 8, seed=1).run()
+
+
+def test_dist_entry_point_one_rank_torchrun(orc):
+    """`torchrun --nproc-per-node 1 -m paper_1503_06394_b200.dist` (the multi-GPU driver's launch
+    path, NCCL process group of one rank): its estimate equals the oracle's on the same probes."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", "--master-port=29517", "-m", "paper_1503_06394_b200.dist",
+           "--workload", "gmrf_s", "--k", "8"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    wl = W.get_workload("gmrf_s")
+    A, _ = _mats(wl)
+    og = orc.logdet(orc.Op("csr", A), wl.a, wl.b, wl.degree, wl.num_probes, wl.seed, workers=4)["gamma"]
+    assert out["world"] == 1 and out["num_probes"] == wl.num_probes
+    _check_gamma(out["logdet"], og)
