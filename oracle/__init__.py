@@ -12,10 +12,12 @@ from .runner import (Op, build_oracle, lib, cheb_nodes, coeffs_from_values,
                      coeffs_log, cheb_eval, splitmix64, rademacher, apply_tilde,
                      moments_vec, moments, logdet, bounds_btb, gamma_from_moments,
                      taylor_coeffs, power_moments_vec, taylor_logdet, affine_power_moments,
-                     affine_power_moments_vec, gershgorin, quadform)
+                     affine_power_moments_vec, gershgorin, quadform,
+                     lanczos, ritz, spectrum_bounds)
 
 __all__ = ["Op", "build_oracle", "lib", "cheb_nodes", "coeffs_from_values",
            "coeffs_log", "cheb_eval", "splitmix64", "rademacher", "apply_tilde",
            "moments_vec", "moments", "logdet", "bounds_btb", "gamma_from_moments",
            "taylor_coeffs", "power_moments_vec", "taylor_logdet", "affine_power_moments",
-           "affine_power_moments_vec", "gershgorin", "quadform"]
+           "affine_power_moments_vec", "gershgorin", "quadform",
+           "lanczos", "ritz", "spectrum_bounds"]

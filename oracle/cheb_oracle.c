@@ -449,3 +449,70 @@ double orc_quadform(const orc_csr *A, const double *x)
     free(ax);
     return r;
 }
+
+/* ---------------------------------------------------------------------- */
+/* Spectral interval by Lanczos (sigma_max "by the    */
+/* power iteration", sigma_min "by the inverse power iteration"; reading    */
+/* G26 replaces both by the Lanczos process, which contains the power       */
+/* iteration's Krylov space and converges first at both ends of the         */
+/* spectrum).  Plain Lanczos on Ã = alpha*M - beta*I ([a,b] map, reading    */
+/* G1) with FULL re-orthogonalisation (classical Gram-Schmidt, twice):      */
+/*   q_1 = v/|v|,  w = Ã q_j - beta_{j-1} q_{j-1},  alpha_j = q_j.w,        */
+/*   w -= alpha_j q_j, w -= sum_i (q_i.w) q_i (twice),                      */
+/*   beta_j = |w|,  q_{j+1} = w / beta_j,                j = 1..N.           */
+/* alpha_out[j-1] = alpha_j (diagonal of the Jacobi matrix T_N),            */
+/* beta_out[j-1] = beta_j (off-diagonal; beta_N is the residual factor:     */
+/* |Ã y - theta y| = beta_N |s_N| for a Ritz pair (theta, y = Q s)).        */
+/* Returns ORC_OK, or the number of completed steps as -(100+j) when w      */
+/* vanished at step j (invariant subspace found).                           */
+/* ---------------------------------------------------------------------- */
+int32_t orc_lanczos_tilde(const orc_op *op, double a, double b, int32_t N, const double *v,
+                          double *alpha_out, double *beta_out)
+{
+    int64_t d = op_dim(op);
+    double *Q = (double *)malloc(sizeof(double) * (size_t)d * (size_t)(N + 1));
+    double *w = (double *)malloc(sizeof(double) * (size_t)d);
+    if (!Q || !w) { free(Q); free(w); return ORC_ENOMEM; }
+    double nv = sqrt(dot(v, v, d));
+    for (int64_t i = 0; i < d; i++) Q[i] = v[i] / nv;
+    int32_t rc = ORC_OK;
+    for (int32_t j = 0; j < N; j++) {
+        double *q = Q + (size_t)j * d;
+        int32_t e = orc_apply_tilde(op, a, b, q, w);
+        if (e) { rc = e; break; }
+        if (j > 0) {
+            const double *qm = Q + (size_t)(j - 1) * d;
+            for (int64_t i = 0; i < d; i++) w[i] -= beta_out[j - 1] * qm[i];
+        }
+        double al = dot(q, w, d);
+        alpha_out[j] = al;
+        for (int64_t i = 0; i < d; i++) w[i] -= al * q[i];
+        for (int pass = 0; pass < 2; pass++) {
+            for (int32_t t = 0; t <= j; t++) {
+                const double *qt = Q + (size_t)t * d;
+                double h = dot(qt, w, d);
+                for (int64_t i = 0; i < d; i++) w[i] -= h * qt[i];
+            }
+        }
+        double be = sqrt(dot(w, w, d));
+        beta_out[j] = be;
+        if (!(be > 0.0)) { rc = -(100 + j + 1); break; }
+        double *qn = Q + (size_t)(j + 1) * d;
+        for (int64_t i = 0; i < d; i++) qn[i] = w[i] / be;
+    }
+    free(Q);
+    free(w);
+    return rc;
+}
+
+int32_t orc_lanczos_probe(const orc_op *op, double a, double b, int32_t N, uint64_t seed, int64_t p,
+                          double *alpha_out, double *beta_out)
+{
+    int64_t d = op_dim(op);
+    double *v = (double *)malloc(sizeof(double) * (size_t)d);
+    if (!v) return ORC_ENOMEM;
+    orc_rademacher(seed, p, d, v);
+    int32_t rc = orc_lanczos_tilde(op, a, b, N, v, alpha_out, beta_out);
+    free(v);
+    return rc;
+}

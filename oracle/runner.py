@@ -86,6 +86,10 @@ def lib():
         L.orc_gershgorin.restype = D
         L.orc_quadform.argtypes = [ctypes.POINTER(_CSR), P]
         L.orc_quadform.restype = D
+        L.orc_lanczos_tilde.argtypes = [ctypes.POINTER(_OP), D, D, I32, P, P, P]
+        L.orc_lanczos_tilde.restype = I32
+        L.orc_lanczos_probe.argtypes = [ctypes.POINTER(_OP), D, D, I32, U64, I64, P, P]
+        L.orc_lanczos_probe.restype = I32
         _lib = L
     return _lib
 
@@ -329,3 +333,50 @@ def bounds_btb(B) -> tuple:
     if rc != 0:
         raise ValueError(f"orc_bounds_btb rc={rc} (Johnson bound not positive?)")
     return float(a[0]), float(b[0])
+
+
+# ---- spectral interval by Lanczos (reading G26) ----
+def lanczos(op: Op, a: float, b: float, N: int, v: np.ndarray = None, seed: int = None, p: int = None):
+    """N Lanczos steps on Ã = alpha M - beta I ([a,b] map) with full re-orthogonalisation from the
+    start vector v (or the Rademacher probe p of `seed`): returns (alpha[N], beta[N]) -- the Jacobi
+    matrix T_N (diagonal alpha, off-diagonal beta[:-1]) and the residual factor beta[N-1]."""
+    al, be = np.empty(N), np.empty(N)
+    st = op._struct()
+    if v is not None:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        rc = lib().orc_lanczos_tilde(ctypes.byref(st), a, b, N, _ptr(v), _ptr(al), _ptr(be))
+    else:
+        rc = lib().orc_lanczos_probe(ctypes.byref(st), a, b, N, seed, p, _ptr(al), _ptr(be))
+    if rc <= -100:  # invariant subspace after -rc - 100 steps: T_j is exact (beta_j = 0)
+        j = -rc - 100
+        return al[:j], be[:j]
+    if rc != 0:
+        raise RuntimeError(f"orc_lanczos rc={rc}")
+    return al, be
+
+
+def ritz(alpha: np.ndarray, beta: np.ndarray):
+    """Ritz values theta (ascending) of T_N and their residual bounds beta_N |s_N| (an eigenvalue of
+    Ã lies within the bound of each theta), by numpy's symmetric eigensolver."""
+    N = alpha.size
+    T = np.diag(alpha) + np.diag(beta[:N - 1], 1) + np.diag(beta[:N - 1], -1)
+    th, S = np.linalg.eigh(T)
+    return th, beta[N - 1] * np.abs(S[N - 1, :])
+
+
+def spectrum_bounds(op: Op, lo: float, hi: float, N: int, seed: int, probes: Sequence[int]):
+    """Interval [a, b] for the estimator from Lanczos on each probe, in M-space (lambda = (theta +
+    beta)/alpha for the map of [lo, hi]): a = min_p (theta_min - r_min) / ..., b = min(max_p
+    (theta_max + r_max), hi); also the extreme Ritz values and residuals themselves."""
+    alpha, beta = 2.0 / (hi - lo), (hi + lo) / (hi - lo)
+    lmin, lmax, rmin, rmax, rows = np.inf, -np.inf, 0.0, 0.0, []
+    for p in probes:
+        al, be = lanczos(op, lo, hi, N, seed=seed, p=p)
+        th, r = ritz(al, be)
+        rows.append((al, be))
+        if (th[0] + beta) / alpha < lmin:
+            lmin, rmin = (th[0] + beta) / alpha, r[0] / alpha
+        if (th[-1] + beta) / alpha > lmax:
+            lmax, rmax = (th[-1] + beta) / alpha, r[-1] / alpha
+    return {"lambda_min": lmin, "lambda_max": lmax, "res_min": rmin, "res_max": rmax,
+            "a": max(lmin - rmin, 0.0), "b": min(lmax + rmax, hi), "jacobi": rows}

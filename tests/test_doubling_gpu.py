@@ -78,7 +78,8 @@ def test_doubling_degrees_odd_even(orc, doubling, n, persist):
     steps = (n + 1) // 2
     blocks = 2
     if persist == 0:
-        assert nl == 2 + blocks * (1 + steps) + 1  # prep (count + scatter), (init + ceil(n/2) steps) per block, finalize
+        # prep (count + scatter), (init + ceil(n/2) steps) per block, status epilogue, finalize
+        assert nl == 2 + blocks * (1 + steps) + 1 + 1
     mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, 2, range(9))
     _check(r.moments, mu, wl.d)
 

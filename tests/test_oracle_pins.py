@@ -491,3 +491,78 @@ def test_quadform_matches_dense(orc):
     x = np.random.default_rng(5).standard_normal(63)
     D = W.to_dense(A)
     assert abs(orc.quadform(A, x) - x @ D @ x) < 1e-12 * abs(x @ D @ x)
+
+
+# ---------------------------------------------------------------- Lanczos spectral interval (f4, G26)
+def _tridiag_csr(diag, off):
+    d = diag.size
+    r = np.concatenate([np.arange(d), np.arange(d - 1), np.arange(1, d)])
+    c = np.concatenate([np.arange(d), np.arange(1, d), np.arange(d - 1)])
+    v = np.concatenate([diag, off, off])
+    return W.csr.from_coo(d, d, r, c, v)
+
+
+def test_lanczos_reproduces_tridiagonal_from_e1(orc):
+    """Textbook identity: Lanczos on a symmetric tridiagonal matrix with positive off-diagonal,
+    started at e_1, returns that matrix (here Ã = alpha T - beta I of it)."""
+    rng = np.random.default_rng(4)
+    d = 30
+    diag, off = rng.uniform(1.0, 3.0, d), rng.uniform(0.1, 0.5, d - 1)
+    T = _tridiag_csr(diag, off)
+    a, b = 0.5, 4.5
+    al, be = orc.lanczos(orc.Op("csr", T), a, b, 12, v=np.eye(d)[0])
+    alpha, beta = 2 / (b - a), (b + a) / (b - a)
+    assert np.allclose(al, alpha * diag[:12] - beta, rtol=0, atol=1e-14)
+    assert np.allclose(be, alpha * off[:12], rtol=0, atol=1e-14)
+
+
+def test_lanczos_finds_distinct_eigenvalues_exactly(orc):
+    """M diagonal with 6 distinct eigenvalues (each repeated): the Krylov space of any start vector
+    has dimension 6, so after 6 steps the Ritz values are exactly those eigenvalues and the process
+    stops (beta_6 = 0)."""
+    vals = np.array([0.3, 0.7, 1.1, 2.0, 2.9, 3.5])
+    diag = np.repeat(vals, 17)
+    D = W.csr.from_coo(diag.size, diag.size, np.arange(diag.size), np.arange(diag.size), diag)
+    a, b = 0.0, 4.0
+    al, be = orc.lanczos(orc.Op("csr", D), a, b, 6, seed=3, p=0)
+    th, r = orc.ritz(al, be)
+    lam = (th + (b + a) / (b - a)) * (b - a) / 2
+    assert np.allclose(lam, vals, atol=1e-12)
+    assert be[5] < 1e-12 and np.all(r < 1e-12)
+
+
+def test_lanczos_gauss_quadrature_matches_moments(orc):
+    """Gauss quadrature from T_N (nodes theta_i, weights s_{1,i}^2) integrates polynomials of degree
+    <= 2N-1 exactly against the probe's spectral measure: sum_i w_i T_j(theta_i) = mu_j / mu_0 with
+    mu_j = v^T T_j(Ã) v from the (independently pinned) moment routine."""
+    wl = W.get_workload("gmrf_s")
+    A, _ = wl.matrices()
+    op = orc.Op("csr", A)
+    N = 12
+    v = orc.rademacher(7, 0, wl.d)
+    al, be = orc.lanczos(op, wl.a, wl.b, N, v=v)
+    T = np.diag(al) + np.diag(be[:-1], 1) + np.diag(be[:-1], -1)
+    th, S = np.linalg.eigh(T)
+    w = S[0, :] ** 2
+    mu = orc.moments_vec(op, wl.a, wl.b, 2 * N - 1, v)
+    quad = np.array([np.sum(w * np.cos(j * np.arccos(np.clip(th, -1, 1)))) for j in range(2 * N)])
+    assert np.allclose(quad * mu[0], mu, rtol=0, atol=1e-11 * wl.d)
+
+
+def test_lanczos_grid_extremes_and_interval(orc):
+    """20x20 GMRF grid (closed-form spectrum): the extreme Ritz values converge to lambda_min /
+    lambda_max, each residual bound covers the distance to the eigenvalue, and the interval
+    spectrum_bounds returns encloses the whole spectrum."""
+    N, theta = 20, 0.2
+    A = W.grid_gmrf(N, theta)
+    lam = cf.grid_eigs(N, theta)
+    lo, hi = 0.0, orc.gershgorin(A)
+    sb = orc.spectrum_bounds(orc.Op("csr", A), lo, hi, 80, 5, range(4))
+    assert abs(sb["lambda_min"] - lam.min()) < 1e-9 and abs(sb["lambda_max"] - lam.max()) < 1e-9
+    assert sb["lambda_min"] >= lam.min() - 1e-12 and sb["lambda_max"] <= lam.max() + 1e-12  # Ritz: inside
+    assert sb["a"] <= lam.min() and sb["b"] >= lam.max() and sb["b"] <= hi
+    al, be = sb["jacobi"][0]
+    th, r = orc.ritz(al, be)
+    lt = 2 / hi * lam - 1
+    for t, rr in zip(th, r):  # Kahan: some eigenvalue within each residual bound
+        assert np.min(np.abs(lt - t)) <= rr + 1e-12
