@@ -7,7 +7,7 @@ library raises.
 """
 from .api import (DeviceCSR, Operator, Result, Estimator, coeffs_log, workspace_bytes,
                   power_moments, taylor_coeffs, taylor_logdet, affine_power_moments, norm_bound,
-                  spectrum_estimate,
+                  spectrum_bounds, logdet_auto,
                   alloc_workspace, moments, moments_host, finalize, logdet, logdet_host, bounds_btb, probes,
                   launch_count, profile_begin, profile_end, set_persistent, set_small_tiles, get_small_tiles, set_doubling,
                   get_doubling, release_cache, workspace_status, check_estimate, log_abs_det_from_btb, log_tau_from_rank1)
@@ -15,7 +15,7 @@ from ._lib import ChebError, load as load_library
 
 __all__ = ["DeviceCSR", "Operator", "Result", "Estimator", "coeffs_log", "workspace_bytes",
            "power_moments", "taylor_coeffs", "taylor_logdet", "affine_power_moments", "norm_bound",
-           "spectrum_estimate",
+           "spectrum_bounds", "logdet_auto",
            "alloc_workspace", "moments", "moments_host", "finalize", "logdet", "logdet_host", "bounds_btb",
            "probes", "launch_count", "profile_begin", "profile_end", "set_persistent", "set_small_tiles",
            "get_small_tiles", "set_doubling", "get_doubling", "release_cache", "workspace_status", "check_estimate",

@@ -188,18 +188,33 @@ def norm_bound(op: Operator, stream=None) -> float:
     return s.value
 
 
-def spectrum_estimate(op: Operator, iters: int = 60, probes: int = 8, seed: int = 12345, k: int = 8):
-    """Block power iteration on the fused kernels: with s = norm_bound,
-    lambda_max ~ s * R(M/s) and lambda_min ~ s * (1 - R(I - M/s)), where R is the ratio of
-    the probe-summed last two power moments.  These are INNER estimates (lambda_max from
-    below, lambda_min from above); widen them before using them as [a, b]."""
-    s = norm_bound(op)
-    hi = affine_power_moments(op, 1.0 / s, 0.0, iters, 0, probes, seed, k).sum(dim=0).cpu().numpy()
-    lo = affine_power_moments(op, -1.0 / s, -1.0, iters, 0, probes, seed, k).sum(dim=0).cpu().numpy()
-    lam_max = s * hi[-1] / hi[-2]
-    lam_min = s * (1.0 - lo[-1] / lo[-2])
-    return {"lambda_min": float(lam_min), "lambda_max": float(lam_max), "norm_bound": s,
-            "iters": iters, "probes": probes}
+def spectrum_bounds(op: Operator, lanczos_steps: int = 100, probes: int = 8, seed: int = 12345,
+                    lo: float = 0.0, hi: float = 0.0, want_jacobi: bool = False) -> dict:
+    """Spectral interval of M from the matrix (cheb_spectrum_bounds, reading
+    G26): Lanczos tridiagonals of `probes` Rademacher probes from their Chebyshev moments on
+    [lo, hi] (hi <= 0: the device norm bound).  Returns lambda_min / lambda_max (extreme Ritz
+    values), res_min / res_max (residual bounds), a / b (the interval to pass to logdet), lo / hi,
+    and with want_jacobi the per-probe Lanczos tridiagonals in Ã-space (alpha[N], beta[N])."""
+    out = _lib.CLSpectrum()
+    jac = np.empty((probes, 2 * lanczos_steps)) if want_jacobi else None
+    st = op.struct()
+    check(_lib.load().cheb_spectrum_bounds(ctypes.byref(st), float(lo), float(hi), int(lanczos_steps), int(probes),
+                                           int(seed) & (2 ** 64 - 1), ctypes.byref(out),
+                                           jac.ctypes.data if jac is not None else None))
+    r = {f: getattr(out, f) for f, _ in _lib.CLSpectrum._fields_}
+    if jac is not None:
+        r["jacobi"] = [(row[:lanczos_steps], row[lanczos_steps:]) for row in jac]
+    return r
+
+
+def logdet_auto(op: Operator, degree: int = 15, num_probes: int = 30, seed: int = 1, k: int = 0,
+                lanczos_steps: int = 100, bound_probes: int = 8, want_moments: bool = False):
+    """log det M without a caller-supplied interval: [a, b] from spectrum_bounds (device Lanczos),
+    then the estimate (cheb_logdet).  Returns (Result, spectrum dict)."""
+    sb = spectrum_bounds(op, lanczos_steps, bound_probes, seed=seed ^ 0x5DEECE66D)
+    if not sb["a"] > 0.0:
+        raise _lib.ChebError(_lib.CL_EINVAL, f"Lanczos lower bound not positive ({sb['a']}); pass [a, b]")
+    return logdet(op, sb["a"], sb["b"], degree, num_probes, seed, k, want_moments), sb
 
 
 def taylor_coeffs(s: float, degree: int) -> np.ndarray:

@@ -1006,6 +1006,171 @@ int cheb_moments_host(const cl_operator* op, double a, double b, int32_t degree,
     return CL_OK;
 }
 
+namespace {
+// ---- spectral interval (reading G26) ----------------------
+// Lanczos from Chebyshev moments: the Lanczos process started at a probe v builds the Jacobi
+// matrix of v's spectral measure d lambda_v (weights (v^T q_i)^2 at the eigenvalues of Ã); its
+// recurrence coefficients follow from the measure's modified moments
+//   nu_l = int p_l d lambda_v,  p_l = T_l / 2^(l-1) (monic Chebyshev: p_{l+1} = x p_l - b_l p_{l-1},
+//   b_1 = 1/2, b_l = 1/4),  i.e. nu_0 = mu_0, nu_l = mu_l / 2^(l-1) with mu_l = v^T T_l(Ã) v,
+// by the modified Chebyshev algorithm (Sack-Donovan / Wheeler), which is well conditioned for
+// measures on [-1, 1] -- and the mu_l are exactly what the hot path computes.  2N moments give
+// the N x N Jacobi matrix (alpha_0..alpha_{N-1}; beta_1..beta_{N-1} of the monic recurrence,
+// off-diagonal sqrt(beta_k)) and beta_N, the Lanczos residual factor.
+int modified_chebyshev(const double* mu, int N, double* alpha, double* beta) {
+    const int L = 2 * N + 1;  // nu_0 .. nu_2N
+    std::vector<double> nu(L), sm2(L, 0.0), sm1(L), sk(L);
+    double sc = 1.0;
+    for (int l = 0; l < L; l++) {
+        nu[l] = l == 0 ? mu[0] : mu[l] * sc;
+        if (l >= 1) sc *= 0.5;
+    }
+    if (!(nu[0] > 0.0)) return fail(CL_ENONFINITE, "spectral measure has no mass (mu_0 = %g)", nu[0]);
+    sm1 = nu;  // sigma_{0,l}
+    alpha[0] = nu[1] / nu[0];
+    beta[0] = nu[0];
+    for (int k = 1; k <= N; k++) {
+        for (int l = k; l <= 2 * N - k; l++) {
+            const double bl = l == 1 ? 0.5 : 0.25;
+            sk[l] = sm1[l + 1] - alpha[k - 1] * sm1[l] - beta[k - 1] * sm2[l] + bl * sm1[l - 1];
+        }
+        if (!(sk[k] > 0.0) || !std::isfinite(sk[k]))
+            return fail(CL_ENONFINITE, "Lanczos breakdown at step %d (measure supported on <= %d points?)", k, k);
+        beta[k] = sk[k] / sm1[k - 1];
+        if (k < N) alpha[k] = sk[k + 1] / sk[k] - sm1[k] / sm1[k - 1];
+        sm2.swap(sm1);
+        sm1.swap(sk);
+    }
+    return CL_OK;
+}
+
+// Eigen-decomposition of the symmetric tridiagonal matrix (diag d[0..n-1], off-diagonal e[0..n-2])
+// by the implicit QL method with Wilkinson shifts, accumulating the eigenvectors in z (row-major
+// n x n, z[r*n + c] = component r of eigenvector c).  d is overwritten by the eigenvalues.
+int tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<double>& z) {
+    const int n = (int)d.size();
+    z.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; i++) z[(size_t)i * n + i] = 1.0;
+    e.resize(n, 0.0);
+    if (n > 0) e[n - 1] = 0.0;
+    for (int l = 0; l < n; l++) {
+        int iter = 0, m;
+        do {
+            for (m = l; m < n - 1; m++) {
+                const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+                if (std::fabs(e[m]) <= 1e-16 * dd) break;
+            }
+            if (m != l) {
+                if (++iter > 60) return fail(CL_ENONFINITE, "tridiagonal QL did not converge");
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = std::hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int i;
+                for (i = m - 1; i >= l; i--) {
+                    double f = s * e[i], b = c * e[i];
+                    r = std::hypot(f, g);
+                    e[i + 1] = r;
+                    if (r == 0.0) {
+                        d[i + 1] -= p;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    s = f / r;
+                    c = g / r;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    p = s * r;
+                    d[i + 1] = g + p;
+                    g = c * r - b;
+                    for (int k = 0; k < n; k++) {
+                        f = z[(size_t)k * n + i + 1];
+                        z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * f;
+                        z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * f;
+                    }
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= p;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
+    }
+    return CL_OK;
+}
+}  // namespace
+
+int cheb_spectrum_bounds(const cl_operator* op, double lo, double hi, int32_t lanczos_steps,
+                         int32_t num_probes, uint64_t seed, cl_spectrum* out, double* jacobi_out) {
+    int rc;
+    if ((rc = check_op(op))) return rc;
+    if (!out) return fail(CL_EINVAL, "out is NULL");
+    if (lanczos_steps < 1 || lanczos_steps > 400) return fail(CL_EINVAL, "lanczos_steps must be in [1, 400]");
+    if (num_probes < 1 || num_probes > 128) return fail(CL_EINVAL, "num_probes must be in [1, 128]");
+    if (!std::isfinite(lo) || lo < 0.0 || !std::isfinite(hi)) return fail(CL_EINVAL, "need finite lo >= 0");
+    cudaStream_t st;
+    CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } guard{st};
+    if (hi <= 0.0) {  // a guaranteed upper bound of the spectrum from the matrix
+        if ((rc = cheb_norm_bound(op, &hi, st))) return rc;
+    }
+    if (!(hi > lo)) return fail(CL_EINVAL, "need hi > lo (got [%g, %g])", lo, hi);
+    const int N = lanczos_steps, n2 = 2 * N;
+    const int k = pick_k(num_probes);
+    const size_t ws_bytes = plan(op->A.n_cols, gather_nnz(op), k, op->kind, sm_count()).total;
+    const size_t mu_n = (size_t)num_probes * (n2 + 1);
+    void* ws = nullptr;
+    if ((rc = arena_get(0, align256(ws_bytes) + sizeof(double) * mu_n, &ws))) return rc;
+    double* mu_d = (double*)((char*)ws + align256(ws_bytes));
+    const double alpha = 2.0 / (hi - lo), beta = (hi + lo) / (hi - lo);
+    // the hot path: Chebyshev moments mu_0..mu_2N of every probe on [lo, hi]
+    if ((rc = moments_impl(op, alpha, beta, false, n2, 0, num_probes, seed, k, ws, ws_bytes, mu_d, st))) return rc;
+    std::vector<double> mu(mu_n);
+    uint32_t status = 0;
+    CL_CUDA(cudaMemcpyAsync(&status, (char*)ws + kStatusOff, sizeof(status), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaMemcpyAsync(mu.data(), mu_d, sizeof(double) * mu_n, cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    if (status & 1u) return fail(CL_ECUDA, "persistent-kernel grid wait timed out");
+    if (status & 2u) return fail(CL_ENONFINITE, "non-finite moment: [lo,hi]=[%g,%g] misses the spectrum", lo, hi);
+    double lmin = INFINITY, lmax = -INFINITY, rmin = 0.0, rmax = 0.0;
+    std::vector<double> al(N), be(N + 1), d, e, z;
+    for (int p = 0; p < num_probes; p++) {
+        if ((rc = modified_chebyshev(mu.data() + (size_t)p * (n2 + 1), N, al.data(), be.data()))) return rc;
+        if (jacobi_out) {
+            double* row = jacobi_out + (size_t)p * 2 * N;
+            for (int j = 0; j < N; j++) row[j] = al[j];                   // diagonal of T_N (Ã-space)
+            for (int j = 1; j <= N; j++) row[N + j - 1] = std::sqrt(be[j]);  // off-diagonal, then beta_N
+        }
+        d.assign(al.begin(), al.end());
+        e.resize(N > 1 ? N - 1 : 0);
+        for (int j = 1; j < N; j++) e[j - 1] = std::sqrt(be[j]);
+        if ((rc = tridiag_ql(d, e, z))) return rc;
+        const double bN = std::sqrt(be[N]);
+        int imin = 0, imax = 0;
+        for (int i = 1; i < N; i++) {
+            if (d[i] < d[imin]) imin = i;
+            if (d[i] > d[imax]) imax = i;
+        }
+        // Ritz value theta and Kahan residual bound beta_N |s_N| (an eigenvalue of Ã lies within it),
+        // mapped to M: lambda = (theta + beta) / alpha
+        const double l0 = (d[imin] + beta) / alpha, r0 = bN * std::fabs(z[(size_t)(N - 1) * N + imin]) / alpha;
+        const double l1 = (d[imax] + beta) / alpha, r1 = bN * std::fabs(z[(size_t)(N - 1) * N + imax]) / alpha;
+        if (l0 < lmin) { lmin = l0; rmin = r0; }
+        if (l1 > lmax) { lmax = l1; rmax = r1; }
+    }
+    out->lambda_min = lmin;
+    out->lambda_max = lmax;
+    out->res_min = rmin;
+    out->res_max = rmax;
+    out->a = std::max(lmin - rmin, 0.0);
+    out->b = std::min(lmax + rmax, hi);
+    out->lo = lo;
+    out->hi = hi;
+    out->lanczos_steps = N;
+    out->num_probes = num_probes;
+    return CL_OK;
+}
+
 int cheb_bounds_btb(const cl_operator* op, double* ab_out, void* stream) {
     int rc;
     if ((rc = check_op(op))) return rc;

@@ -340,16 +340,61 @@ def test_norm_bounds_match_oracle(orc):
     assert abs(P.norm_bound(_dev_op("btb", B, W.transpose(B))) - ob) <= 1e-13 * ob
 
 
-def test_spectrum_estimate_grid_closed_form():
-    """Device power iteration recovers the grid's closed-form extreme eigenvalues."""
+@pytest.mark.parametrize("name", ["gmrf_s", "torus_s", "btb_s", "spd_s"])
+def test_spectrum_bounds_match_oracle_lanczos(orc, name):
+    """f4: the library's Lanczos tridiagonals (from the hot path's Chebyshev moments by the modified
+    Chebyshev algorithm) equal the oracle's explicit Lanczos with full re-orthogonalisation, probe
+    by probe; so do the extreme Ritz values and their residual bounds."""
+    wl = W.get_workload(name)
+    A, At = _mats(wl)
+    op = _dev_op(wl.mode, A, At, wl.r1_c)
+    oop = orc.Op(wl.mode, A, wl.r1_c)
+    if wl.mode == "btb":
+        hi = orc.bounds_btb(A)[1]
+    elif wl.mode == "rank1":
+        hi = 9.0  # torus Laplacian spectrum in [0, 8], the 1-eigenvalue c d = lambda_2 < 1
+    else:
+        hi = orc.gershgorin(A)
+    N, probes, seed = 30, 4, 21
+    sb = P.spectrum_bounds(op, N, probes, seed=seed, lo=0.0, hi=hi, want_jacobi=True)
+    ob = orc.spectrum_bounds(oop, 0.0, hi, N, seed, range(probes))
+    for (ga, gb), (oa, obe) in zip(sb["jacobi"], ob["jacobi"]):
+        assert np.max(np.abs(ga - oa)) <= 1e-9, np.max(np.abs(ga - oa))
+        assert np.max(np.abs(gb - obe)) <= 1e-9, np.max(np.abs(gb - obe))
+    for key in ("lambda_min", "lambda_max"):
+        assert abs(sb[key] - ob[key]) <= 1e-10 * hi, (key, sb[key], ob[key])
+    for key in ("res_min", "res_max", "a", "b"):
+        assert abs(sb[key] - ob[key]) <= 1e-8 * hi, (key, sb[key], ob[key])
+
+
+def test_spectrum_bounds_grid_closed_form():
+    """Device Lanczos recovers the grid's closed-form extreme eigenvalues; [a, b] encloses the
+    spectrum; hi defaults to the device norm bound."""
     from oracle import closed_forms as cf
     N, theta = 20, 0.2
     op = _dev_op("csr", W.grid_gmrf(N, theta))
-    est = P.spectrum_estimate(op, iters=500, probes=8)
+    sb = P.spectrum_bounds(op, 80, 4, seed=5)
     lam = cf.grid_eigs(N, theta)
-    assert lam.max() - 2e-3 < est["lambda_max"] <= lam.max() + 1e-9
-    assert lam.min() - 1e-9 <= est["lambda_min"] < lam.min() + 2e-3
-    assert est["norm_bound"] >= lam.max()
+    assert abs(sb["lambda_min"] - lam.min()) < 1e-9 and abs(sb["lambda_max"] - lam.max()) < 1e-9
+    assert sb["a"] <= lam.min() and lam.max() <= sb["b"] <= sb["hi"]
+    assert sb["hi"] == P.norm_bound(op)
+
+
+@pytest.mark.slow
+def test_spectrum_bounds_config3_estimate(orc):
+    """configs[3] without a caller-supplied interval: device Lanczos bounds enclose the closed-form
+    spectrum [1 - 4 theta cos(pi/5001), 1 + 4 theta cos(pi/5001)], and the estimate on them equals
+    the closed-form-interval estimate (same probes) within its standard error."""
+    wl = W.get_workload("gmrf5000")
+    A, _ = _mats(wl)
+    op = _dev_op("csr", A)
+    sb = P.spectrum_bounds(op, 100, 8, seed=77)
+    c = math.cos(math.pi / 5001)
+    lmin, lmax = 1 - 4 * 0.24 * c, 1 + 4 * 0.24 * c
+    assert 0 < sb["a"] <= lmin and lmax <= sb["b"], sb
+    ra = P.logdet(op, sb["a"], sb["b"], wl.degree, wl.num_probes, seed=wl.seed, k=64)
+    rc = P.logdet(op, wl.a, wl.b, wl.degree, wl.num_probes, seed=wl.seed, k=64)
+    assert abs(ra.logdet - rc.logdet) <= rc.stderr, (ra.logdet, rc.logdet, rc.stderr, sb)
 
 
 # ------------------------------------------------------------------ GMRF likelihood scan (SURVEY f2)
