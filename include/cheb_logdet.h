@@ -84,9 +84,11 @@ typedef struct {
     double res_min, res_max;       /* their Lanczos residual bounds |M y - lambda y| (Kahan: an  */
                                    /* eigenvalue of M lies within res of each)                   */
     double a, b;                   /* interval for cheb_logdet: max(lambda_min - res_min, 0),    */
-                                   /* min(lambda_max + res_max, hi)                              */
-    double lo, hi;                 /* enclosing interval the moments were computed on            */
-    int32_t lanczos_steps, num_probes;
+                                   /* min(lambda_max + res_max, hi_bound)                        */
+    double hi_bound;               /* guaranteed upper bound of the spectrum (cheb_norm_bound)   */
+    int32_t lanczos_steps;         /* Lanczos steps used (min over probes; fewer than requested  */
+                                   /* when a run reached an invariant subspace)                  */
+    int32_t num_probes;
 } cl_spectrum;
 
 /* Chebyshev interpolation coefficients c_0..c_n of f(x) = log(((b-a)x+(b+a))/2)
@@ -186,18 +188,18 @@ int cheb_logdet_host(const cl_operator *op, double a, double b, int32_t degree,
  * ("run the power iteration to estimate a better bound", "use the inverse
  * power iteration to estimate [sigma_min]"; reading G26 uses the Lanczos process instead, whose
  * Krylov space contains the power iterates and which converges first at both ends).
- * For each of num_probes Rademacher probes v (seed, global probes 0..num_probes-1) the hot path
- * computes the Chebyshev moments mu_j = v^T T_j(Ã) v, j = 0..2N (N = lanczos_steps), on the
- * enclosing interval [lo, hi] (Ã = alpha M - beta I for it); the modified Chebyshev algorithm turns
- * them into the N-step Lanczos tridiagonal T_N of v (exactly, in exact arithmetic), whose extreme
- * eigenvalues and residual bounds give out (see cl_spectrum).  hi <= 0 takes hi = cheb_norm_bound
- * (a guaranteed upper bound); lo = 0 is valid for any positive semi-definite M.  jacobi_out: NULL
- * or a HOST array [num_probes][2N] receiving T_N in Ã-space per probe: diagonal alpha_0..alpha_{N-1},
- * then off-diagonal beta_1..beta_{N-1} and the residual factor beta_N.  Synchronous; device memory
- * from the calling thread's arena.  CL_EINVAL for N outside [1, 400] or probes outside [1, 128];
- * CL_ENONFINITE if [lo, hi] misses the spectrum or the Lanczos process breaks down. */
-int cheb_spectrum_bounds(const cl_operator *op, double lo, double hi, int32_t lanczos_steps,
-                         int32_t num_probes, uint64_t seed, cl_spectrum *out, double *jacobi_out);
+ * num_probes independent Lanczos runs on M, started at the Rademacher probes of `seed` (global
+ * probes 0..num_probes-1; the path's splitmix64 generator), N = lanczos_steps steps each, without
+ * re-orthogonalisation, run as blocks of k probes ([d][k] columns) on the device: the operator
+ * products by the spmm kernel, the recurrence and its three reductions per step by
+ * lanczos_vec_kernel; only the Jacobi matrices T_N (k x 2N doubles per block) return to the host,
+ * whose QL eigen-solver gives the extreme Ritz values and their residual bounds (see cl_spectrum).
+ * jacobi_out: NULL or a HOST array [num_probes][2N] receiving T_N per probe: diagonal
+ * alpha_0..alpha_{N-1}, then beta_1..beta_N (off-diagonal, the last is the residual factor); NaN
+ * beyond an early stop.  Synchronous; device memory from the calling thread's arena.
+ * CL_EINVAL for N outside [1, 2000] or probes outside [1, 4096]. */
+int cheb_spectrum_bounds(const cl_operator *op, int32_t lanczos_steps, int32_t num_probes, uint64_t seed,
+                         cl_spectrum *out, double *jacobi_out);
 
 /* Shard-level moments from a HOST operator (the end-to-end call of one rank of the multi-GPU
  * driver): copies the operator to the device (per-thread arena, see cheb_release_cache), runs

@@ -34,8 +34,8 @@ class CLOperator(ctypes.Structure):
 class CLSpectrum(ctypes.Structure):
     _fields_ = [("lambda_min", ctypes.c_double), ("lambda_max", ctypes.c_double),
                 ("res_min", ctypes.c_double), ("res_max", ctypes.c_double),
-                ("a", ctypes.c_double), ("b", ctypes.c_double), ("lo", ctypes.c_double), ("hi", ctypes.c_double),
-                ("lanczos_steps", ctypes.c_int32), ("num_probes", ctypes.c_int32)]
+                ("a", ctypes.c_double), ("b", ctypes.c_double),
+                ("hi_bound", ctypes.c_double), ("lanczos_steps", ctypes.c_int32), ("num_probes", ctypes.c_int32)]
 
 
 class CLResult(ctypes.Structure):
@@ -79,7 +79,7 @@ def load():
         "cheb_logdet": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_logdet_host": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_moments_host": (I, [OPP, D, D, I32, I64, I64, U64, I32, P]),
-        "cheb_spectrum_bounds": (I, [OPP, D, D, I32, I32, U64, ctypes.POINTER(CLSpectrum), P]),
+        "cheb_spectrum_bounds": (I, [OPP, I32, I32, U64, ctypes.POINTER(CLSpectrum), P]),
         "cheb_bounds_btb": (I, [OPP, P, P]),
         "cheb_probes": (I, [I64, U64, I64, I32, P, P]),
         "cheb_launch_count": (I64, []),

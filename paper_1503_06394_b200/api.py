@@ -189,16 +189,16 @@ def norm_bound(op: Operator, stream=None) -> float:
 
 
 def spectrum_bounds(op: Operator, lanczos_steps: int = 100, probes: int = 8, seed: int = 12345,
-                    lo: float = 0.0, hi: float = 0.0, want_jacobi: bool = False) -> dict:
+                    want_jacobi: bool = False) -> dict:
     """Spectral interval of M from the matrix (cheb_spectrum_bounds, reading
-    G26): Lanczos tridiagonals of `probes` Rademacher probes from their Chebyshev moments on
-    [lo, hi] (hi <= 0: the device norm bound).  Returns lambda_min / lambda_max (extreme Ritz
-    values), res_min / res_max (residual bounds), a / b (the interval to pass to logdet), lo / hi,
-    and with want_jacobi the per-probe Lanczos tridiagonals in Ã-space (alpha[N], beta[N])."""
+    G26): `probes` Lanczos runs of `lanczos_steps` steps on the device.  Returns lambda_min /
+    lambda_max (extreme Ritz values), res_min / res_max (residual bounds), a / b (the interval to
+    pass to logdet), hi_bound (device norm bound), lanczos_steps (used), and with want_jacobi the
+    per-probe Lanczos tridiagonals (alpha[N], beta[N])."""
     out = _lib.CLSpectrum()
     jac = np.empty((probes, 2 * lanczos_steps)) if want_jacobi else None
     st = op.struct()
-    check(_lib.load().cheb_spectrum_bounds(ctypes.byref(st), float(lo), float(hi), int(lanczos_steps), int(probes),
+    check(_lib.load().cheb_spectrum_bounds(ctypes.byref(st), int(lanczos_steps), int(probes),
                                            int(seed) & (2 ** 64 - 1), ctypes.byref(out),
                                            jac.ctypes.data if jac is not None else None))
     r = {f: getattr(out, f) for f, _ in _lib.CLSpectrum._fields_}

@@ -25,6 +25,7 @@
 #pragma once
 #include <cassert>
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 // CHEB_CHECKS=1 builds (scripts/build_variants.py "checked") turn on device-side bounds
@@ -40,6 +41,8 @@
 #endif
 
 namespace chebld {
+
+namespace cg = cooperative_groups;
 
 constexpr int kThreads = 256;
 #ifndef CHEB_MIN_CTAS
@@ -227,7 +230,10 @@ struct StepArgs {
     const double* r1u;    // padded u copy (nullptr = ones)
     const double* s_cur;  // [K] u^T w_{j-1}
     double* s_next;       // [K] u^T w_j
-    double* part;         // per-CTA partials [NCH][gridDim.x][K] (persistent: [2][NCH][G][K])
+    double* part;         // per-CTA partials [NCH][gridDim.x][K]
+    double* gpart;        // reduction-group sums [NCH][ng][K] (persistent: [2][NCH][ng][K])
+    int32_t rg;           // reduction group size (0: red_group(gridDim.x)); the persistent kernel's
+                          // cluster size, so per-step launches of the same grid reduce identically
     unsigned int* ticket;
     double* mu_out;       // mu_out[p*mu_stride + mu_col]
     int64_t mu_stride;
@@ -236,16 +242,16 @@ struct StepArgs {
 };
 
 // ---------------------------------------------------------------------------------------
-// Deterministic CTA + grid reduction of per-lane accumulators for probes pl..pl+PPL-1
-// (lane group size LG = K/PPL).  Fixed shuffle tree in a warp, warps in index order, CTAs
-// in a fixed strided order; the last CTA to finish (atomic ticket) writes the result.
-// ---------------------------------------------------------------------------------------
-// ---------------------------------------------------------------------------------------
-// Canonical (deterministic) reduction of the per-CTA partials part[c][p], c < G, for one
-// probe p:  thread t sums c = t, t+256, ... ascending; lanes combine with the xor-butterfly
-// 16, 8, 4, 2, 1 (every lane ends with the bitwise-same sum); warps 0..7 are added in order.
-// Every kernel that produces moments (per-step, fused, persistent) uses exactly this order,
-// so the result depends only on the grid size G -- not on which kernel or CTA computed it.
+// Canonical (deterministic) reduction of the per-CTA partials part[c][p], c < G.
+// Reduction groups of RG = red_group(G) consecutive CTAs: group q covers c in
+// [q*RG, min(G, (q+1)*RG)).  For probe p:
+//     S_q = (((0 + part[q*RG][p]) + part[q*RG+1][p]) + ...)      (ascending c)
+//     mu  = the fixed tree of group_tree_sum over S_0 .. S_{ng-1}
+// Every kernel that produces moments uses exactly this order, so the result depends only on
+// the grid size G -- not on which kernel or CTA computed it.  The per-step kernels form the S_q
+// in their last CTA from global partials; the persistent kernel runs each group as a thread-
+// block cluster and forms S_q from its CTAs' shared memory (DSMEM), so one grid-wide barrier
+// per step suffices (every CTA then sums the ng = ceil(G/RG) group sums itself).
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ double warp_sum_xor(double v) {
 #pragma unroll
@@ -253,61 +259,45 @@ __device__ __forceinline__ double warp_sum_xor(double v) {
     return v;
 }
 
-// All K probes of NCH channels by one CTA (last-CTA-done epilogue).  part: [NCH][G][K];
-// out: shared [NCH][K].  Each channel is summed in the canonical order independently.
-template <int K, int NCH>
-__device__ __forceinline__ void reduce_partials_all(const double* part, int G, double (*out)[K],
-                                                    double (*wsum)[kThreads / 32][8]) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int p0 = 0; p0 < K; p0 += 8) {
-        double m[NCH][8];
+constexpr int kRedGroup = 8;  // portable cluster size: the default reduction group
+__host__ __device__ constexpr int red_group(int G, int rg = kRedGroup) { return G < rg ? (G < 1 ? 1 : G) : rg; }
+
+// Second level of the canonical order for one channel: gp = that channel's group sums [ng][K].
+// Thread t handles probe t / T and the groups q = t % T, t % T + T, ... (ascending), T = 256 / K
+// consecutive lanes per probe; their partial sums are combined by the xor butterfly T/2, ..., 1,
+// so every lane of the probe ends with the same value.  All kThreads threads must call it.
+template <int K>
+__device__ __forceinline__ double group_tree_sum(const double* gp, int ng) {
+    constexpr int T = kThreads / K;
+    const int p = threadIdx.x / T, u = threadIdx.x % T;
+    double t = 0.0;
+    for (int q = u; q < ng; q += T) t += __ldcg(gp + (size_t)q * K + p);
 #pragma unroll
-        for (int ch = 0; ch < NCH; ch++)
-#pragma unroll
-            for (int q = 0; q < 8; q++) m[ch][q] = 0.0;
-        for (int c = tid; c < G && tid < kThreads; c += kThreads) {  // extra (producer) warps: none
-#pragma unroll
-            for (int ch = 0; ch < NCH; ch++)
-#pragma unroll
-                for (int q = 0; q < 8; q++) m[ch][q] += __ldcg(part + ((size_t)ch * G + c) * K + p0 + q);
-        }
-#pragma unroll
-        for (int ch = 0; ch < NCH; ch++)
-#pragma unroll
-            for (int q = 0; q < 8; q++) m[ch][q] = warp_sum_xor(m[ch][q]);
-        if (lane == 0 && warp < kThreads / 32) {
-#pragma unroll
-            for (int ch = 0; ch < NCH; ch++)
-#pragma unroll
-                for (int q = 0; q < 8; q++) wsum[ch][warp][q] = m[ch][q];
-        }
-        __syncthreads();
-        if (tid < 8 * NCH) {
-            const int ch = tid >> 3, q = tid & 7;
-            double mm = 0.0;
-#pragma unroll
-            for (int w = 0; w < kThreads / 32; w++) mm += wsum[ch][w][q];
-            out[ch][p0 + q] = mm;
-        }
-        __syncthreads();
-    }
+    for (int off = T / 2; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    return t;
 }
 
-// One probe p by one CTA (persistent kernel); returns the sum in thread 0.
-__device__ __forceinline__ double reduce_partials_one(const double* part, int K, int G, int p, double* wbuf) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double m = 0.0;
-    for (int c = tid; c < G; c += kThreads) m += __ldcg(part + (size_t)c * K + p);
-    m = warp_sum_xor(m);
-    if (lane == 0) wbuf[warp] = m;
-    __syncthreads();
-    double r = 0.0;
-    if (tid == 0) {
+// All K probes of NCH channels by one CTA (last-CTA-done epilogue).  part: [NCH][G][K] (global,
+// written by other CTAs); gpart: [NCH][ng][K] global scratch; out: shared [NCH][K].
+template <int K, int NCH>
+__device__ __forceinline__ void reduce_partials_grouped(const double* part, int G, int RG, double* gpart,
+                                                        double (*out)[K]) {
+    const int ng = (G + RG - 1) / RG;
+    for (int x = threadIdx.x; x < NCH * ng * K; x += kThreads) {
+        const int p = x % K, q = (x / K) % ng, ch = x / (K * ng);
+        const int c0 = q * RG, cn = (G - c0) < RG ? (G - c0) : RG;
+        const double* src = part + ((size_t)ch * G + c0) * K + p;
+        double sq = 0.0;
+        for (int r = 0; r < cn; r++) sq += __ldcg(src + (size_t)r * K);
+        gpart[((size_t)ch * ng + q) * K + p] = sq;
+    }
+    __syncthreads();  // block-level visibility of the gpart stores
 #pragma unroll
-        for (int w = 0; w < kThreads / 32; w++) r += wbuf[w];
+    for (int ch = 0; ch < NCH; ch++) {
+        const double t = group_tree_sum<K>(gpart + (size_t)ch * ng * K, ng);
+        if (threadIdx.x % (kThreads / K) == 0) out[ch][threadIdx.x / (kThreads / K)] = t;
     }
     __syncthreads();
-    return r;
 }
 
 // Lane lg of a row group owns probes probe_of<K,PPL,SPLIT>(lg, q), q < PPL: contiguous
@@ -337,10 +327,10 @@ __device__ __forceinline__ void dbl_write(double* row, int j, int64_t n, double 
 }
 
 // Shared-memory scratch of grid_reduce_finish (aliases the callers' dynamic shared memory,
-// which is idle once every tile is consumed): red[NCH][8][K], fin[NCH][K], wsum[NCH][8][8].
+// which is idle once every tile is consumed): red[NCH][8][K], fin[NCH][K].
 template <int K, int NCH>
 __host__ __device__ constexpr int red_scratch_bytes() {
-    return 8 * (NCH * (kThreads / 32) * K + NCH * K + NCH * (kThreads / 32) * 8);
+    return 8 * (NCH * (kThreads / 32) * K + NCH * K);
 }
 
 template <int K, int PPL, int NCH, int EPI, bool HAS_S, bool SPLIT = false>
@@ -349,7 +339,6 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
     constexpr int LG = K / PPL;
     auto red = reinterpret_cast<double(*)[kThreads / 32][K]>(scratch);
     auto fin = reinterpret_cast<double(*)[K]>(scratch + 8 * NCH * (kThreads / 32) * K);
-    auto wsum = reinterpret_cast<double(*)[kThreads / 32][8]>(scratch + 8 * (NCH * (kThreads / 32) * K + NCH * K));
     __shared__ bool is_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = lane % LG;
@@ -387,7 +376,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    reduce_partials_all<K, NCH>(a.part, (int)gridDim.x, fin, wsum);
+    reduce_partials_grouped<K, NCH>(a.part, (int)gridDim.x, a.rg > 0 ? a.rg : red_group((int)gridDim.x), a.gpart, fin);
     if (tid < K) {
         double* row = a.mu_out + (size_t)tid * a.mu_stride;
         if (tid < a.kvalid) {
@@ -870,6 +859,115 @@ cheb_step_kernel(StepArgs a) {
 
 
 // ---------------------------------------------------------------------------------------
+// Lanczos process on the device (reading G26): K independent Lanczos runs,
+// one per column of a [d][K] block (one Rademacher probe per column), on M itself (no interval
+// needed).  Per step j, with q = q_j (normalised), qp = q_{j-1}, s = u^T q_j (rank-1):
+//   z = M_S q                                   (spmm_kernel; B^T B: two of them)
+//   LZ_DOT:  alpha_j = q^T (z + c u s)
+//   LZ_UPD:  qp <- z + c u s - alpha_j q - beta_j qp,  beta_{j+1} = |qp|
+//   LZ_NRM:  qp <- qp / beta_{j+1},  s <- u^T qp   (then q and qp swap roles)
+// No re-orthogonalisation (loss of orthogonality only duplicates converged extreme Ritz values).
+// Every per-column scalar stays on the device; one reduction per pass: per-CTA partials, the last
+// CTA sums them in CTA order (deterministic).
+// ---------------------------------------------------------------------------------------
+enum { LZ_DOT = 0, LZ_UPD = 1, LZ_NRM = 2 };
+
+struct LzArgs {
+    int64_t d;
+    double* q;            // q_j            [d][K]
+    double* qp;           // q_{j-1} / work [d][K]
+    const double* z;      // M_S q_j        [d][K]
+    const double* u;      // rank-1 u (nullptr: ones)
+    double r1c;           // rank-1 weight c (0: no rank-1 term)
+    double* s;            // [K] u^T q_j
+    const double* alpha;  // [K] alpha_j (LZ_UPD)
+    const double* beta;   // [K] beta_j  (LZ_UPD: coefficient of qp; LZ_NRM: the divisor)
+    double* out;          // [K] reduction result: alpha_j (DOT), beta_{j+1} (UPD), s (NRM)
+    double* part;         // [gridDim.x][K] per-CTA partials
+    unsigned int* ticket;
+};
+
+template <int K, int OP>
+__global__ void __launch_bounds__(kThreads)
+lanczos_vec_kernel(LzArgs a) {
+    constexpr int CP = K / 2;  // column pairs; a thread keeps one pair for every row it visits
+    __shared__ double red[kThreads][2];
+    __shared__ bool is_last;
+    const int tid = threadIdx.x;
+    const int64_t n2 = a.d * CP;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;  // multiple of CP: the pair is fixed
+    double acc0 = 0.0, acc1 = 0.0;
+    const int cp = (int)(((int64_t)blockIdx.x * kThreads + tid) % CP);
+    const int c0 = 2 * cp;
+    double s0 = 0.0, s1 = 0.0, al0 = 0.0, al1 = 0.0, be0 = 0.0, be1 = 0.0;
+    if (OP != LZ_NRM && a.r1c != 0.0) { s0 = a.r1c * a.s[c0]; s1 = a.r1c * a.s[c0 + 1]; }
+    if (OP == LZ_UPD) { al0 = a.alpha[c0]; al1 = a.alpha[c0 + 1]; be0 = a.beta[c0]; be1 = a.beta[c0 + 1]; }
+    if (OP == LZ_NRM) { be0 = 1.0 / a.beta[c0]; be1 = 1.0 / a.beta[c0 + 1]; }
+    for (int64_t x = (int64_t)blockIdx.x * kThreads + tid; x < n2; x += stride) {
+        const int64_t i = x / CP;
+        const size_t o = (size_t)i * K + c0;
+        const double ui = a.u ? a.u[i] : 1.0;
+        if (OP == LZ_DOT) {
+            const double2 q = *reinterpret_cast<const double2*>(a.q + o);
+            const double2 z = *reinterpret_cast<const double2*>(a.z + o);
+            acc0 = fma(q.x, fma(ui, s0, z.x), acc0);
+            acc1 = fma(q.y, fma(ui, s1, z.y), acc1);
+        } else if (OP == LZ_UPD) {
+            const double2 q = *reinterpret_cast<const double2*>(a.q + o);
+            const double2 z = *reinterpret_cast<const double2*>(a.z + o);
+            double2 w = *reinterpret_cast<const double2*>(a.qp + o);
+            w.x = fma(-be0, w.x, fma(-al0, q.x, fma(ui, s0, z.x)));
+            w.y = fma(-be1, w.y, fma(-al1, q.y, fma(ui, s1, z.y)));
+            *reinterpret_cast<double2*>(a.qp + o) = w;
+            acc0 = fma(w.x, w.x, acc0);
+            acc1 = fma(w.y, w.y, acc1);
+        } else {
+            double2 w = *reinterpret_cast<const double2*>(a.qp + o);
+            w.x *= be0;
+            w.y *= be1;
+            *reinterpret_cast<double2*>(a.qp + o) = w;
+            acc0 = fma(ui, w.x, acc0);
+            acc1 = fma(ui, w.y, acc1);
+        }
+    }
+    red[tid][0] = acc0;
+    red[tid][1] = acc1;
+    __syncthreads();
+    // per-CTA partial of column c: threads t = c/2 (mod CP) in ascending order
+    if (tid < K) {
+        double m = 0.0;
+        const int pr = tid / 2, h = tid & 1;  // kThreads % CP == 0: thread t holds pair t % CP
+        for (int t = pr; t < kThreads; t += CP) m += red[t][h];
+        a.part[(size_t)blockIdx.x * K + tid] = m;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (tid < K) {
+        double t = 0.0;
+        for (unsigned int c = 0; c < gridDim.x; c++) t += __ldcg(a.part + (size_t)c * K + tid);
+        a.out[tid] = (OP == LZ_UPD) ? sqrt(t) : t;
+    }
+    if (tid == 0) *a.ticket = 0u;
+}
+
+// v_p[i] = +-1 for global probes p0 .. p0+K-1 (the path's splitmix64 generator), written to w
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+lanczos_probe_kernel(int64_t d, uint64_t seed, uint64_t p0, double* w) {
+    const int64_t n = d * K;
+    for (int64_t x = (int64_t)blockIdx.x * kThreads + threadIdx.x; x < n; x += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = x / K;
+        const int c = (int)(x % K);
+        const uint64_t z = splitmix64_at(seed, (p0 + (uint64_t)c) * (uint64_t)d + (uint64_t)i + 1ull);
+        w[x] = (z >> 63) ? -1.0 : 1.0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Status epilogue of a cheb_moments call (one launch per call).  status: the workspace status
 // word; bit 0 is set by a spin wait of the persistent kernel that gave up (it never hangs the
 // GPU).  Then every moment of the call becomes NaN, so cheb_finalize's finiteness flag and
@@ -903,25 +1001,27 @@ __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v)
 
 // ---------------------------------------------------------------------------------------
 // K2p: persistent multi-step kernel for small / L2-resident operators (csr, rank-1).
-// One cooperative launch runs steps j = 1..n of a probe block: each step walks the same
-// static tile schedule as cheb_step_kernel (tile t on CTA t mod G, same staged pipeline) and
-// writes per-CTA partial dot products; CTAs then arrive at a grid barrier (monotone
-// counter: step j is complete when it reaches j*G).  Before waiting, each CTA already issues
-// the TMA copies of its first tiles of step j+1 (W_prev = w_{j-1} and the matrix are final),
-// so the barrier latency overlaps the next step's staging.  After the barrier every CTA
-// reduces the rank-1 partials itself (s_j = u^T w_j, same fixed order everywhere) and CTA 0
-// reduces mu_j, in the order grid_reduce_finish uses: moments are bit-identical to per-step
-// launches with the same grid.  Removes the n launch/drain gaps that dominate when one step
-// is a few microseconds of L2 traffic.
+// One cooperative launch, in thread-block clusters of RG = red_group(G) CTAs, runs steps
+// j = 1..n of a probe block: each step walks the same static tile schedule as cheb_step_kernel
+// (tile t on CTA t mod G, same staged pipeline).  Step tail, ONE grid-wide synchronisation:
+//   1. every CTA reduces its accumulators to a per-CTA partial in its shared memory;
+//   2. cluster barrier; the cluster's rank 0 sums its CTAs' partials over DSMEM (ascending
+//      rank = ascending c: the group sums S_q of the canonical order), stores them and
+//      release-adds 1 to the grid counter (step j complete at j * ng);
+//   3. every CTA issues the TMA copies of its first tiles of step j+1 (W_prev = w_{j-1} and the
+//      matrix are final), waits for the counter, and sums the ng group sums itself: the rank-1
+//      s_j = u^T w_j that gates step j+1 and (the last CTA) the moments mu_j.
+// Moments are bit-identical to per-step launches with the same grid.  Removes the n launch /
+// drain gaps that dominate when one step is a few microseconds of L2 traffic, and (rank-1) the
+// second grid-wide wait that publishing s_j from a few reducer CTAs needed.
 // ---------------------------------------------------------------------------------------
 struct PersistArgs {
     double* w0;               // holds v (from probe_init) at entry
     double* w1;
     int32_t n;                // degree
-    double* part;             // [2][NCH][gridDim.x][K] partials (double-buffered by step parity)
-    double* s_buf;            // [2][K] s_j by step parity (s_0 from probe_init in s_buf[0])
-    unsigned int* bar_count;  // grid barrier arrivals (zeroed; monotone)
-    unsigned int* s_count;    // rank-1: probes whose s_j is published (zeroed; monotone)
+    double* gpart;            // [2][NCH][ng][K] group sums (double-buffered by step parity)
+    double* s_buf;            // s_0 (from probe_init) in s_buf[0..K)
+    unsigned int* bar_count;  // grid barrier: arrivals of cluster leaders (zeroed; monotone)
     unsigned int* err;        // wait timeout flag
     int32_t power;            // power basis (Taylor baseline): every step is w_j = Ã w_{j-1}
 };
@@ -953,7 +1053,8 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     __shared__ int64_t s_base_c[2], s_base_v[2];
     __shared__ int s_fit[2];
     __shared__ double red[NCH][kThreads / 32][K];
-    __shared__ double wbuf[kThreads / 32];
+    __shared__ double cpart[2][NCH][K];  // this CTA's partial of step j (parity j & 1), read over DSMEM
+    __shared__ double fin[NCH][K];
     __shared__ double s_sh[HAS_S ? K : 1];
     // row bounds of this CTA's tiles, loaded once (they are the same every step): staging a tile
     // then needs no global load on thread 0 (a per-tile ~1 us stall of warp 0, which the end-of-tile
@@ -965,6 +1066,10 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     const int lg = tid % G::L;
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     uint32_t uses[2] = {0u, 0u};
+    // reduction groups = clusters of RG consecutive CTAs (the host launches clusters of RG)
+    cg::cluster_group cluster = cg::this_cluster();
+    const int RG = a.rg, ng = (int)gridDim.x / RG;
+    const int crank = (int)cluster.block_rank(), cid = (int)blockIdx.x / RG;
 
     const bool cached = nmine <= kBoundsCache;
     if (cached) {
@@ -1058,7 +1163,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             __syncthreads();
             if (tid == 0 && it + 2 < nmine) issue(j, it + 2, b);
         }
-        // ---- per-CTA partials (same tree as grid_reduce_finish)
+        // ---- per-CTA partial (same tree as grid_reduce_finish), into shared memory
 #pragma unroll
         for (int off = G::L; off < 32; off <<= 1) {
 #pragma unroll
@@ -1075,20 +1180,32 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             }
         }
         __syncthreads();
-        double* part = pa_.part + (size_t)(j & 1) * NCH * gridDim.x * K;  // [NCH][G][K] of step j
+        const int par = j & 1;
         if (tid < K) {
 #pragma unroll
             for (int ch = 0; ch < NCH; ch++) {
                 double m = 0.0;
 #pragma unroll
                 for (int w = 0; w < kThreads / 32; w++) m += red[ch][w][tid];
-                part[((size_t)ch * gridDim.x + blockIdx.x) * K + tid] = m;
+                cpart[par][ch][tid] = m;
             }
         }
-        // ---- grid barrier, split: arrive, stage step j+1, wait
-        __syncthreads();
+        // ---- cluster (reduction group) barrier: the group's partials and w_j rows are complete;
+        // rank 0 forms the group sum S_q over DSMEM (ascending rank = ascending CTA index)
+        cluster.sync();
+        double* gp = pa_.gpart + (size_t)par * NCH * ng * K;  // [NCH][ng][K] of step j
+        if (crank == 0) {
+            for (int x = tid; x < NCH * K; x += kThreads) {
+                const int ch = x / K, p = x % K;
+                double sq = 0.0;
+                for (int r = 0; r < RG; r++) sq += *cluster.map_shared_rank(&cpart[par][ch][p], r);
+                gp[((size_t)ch * ng + cid) * K + p] = sq;
+            }
+            __syncthreads();
+            if (tid == 0) red_release_add(pa_.bar_count, 1u);  // release: the cluster's step-j stores
+        }
+        // ---- stage step j+1, then the single grid-wide wait
         if (tid == 0) {
-            red_release_add(pa_.bar_count, 1u);  // release: the CTA's stores of step j (barrier above)
             if (j < pa_.n) {
                 // w_{j-1} (W_prev of step j+1) and the matrix are final: stage ahead.  The
                 // proxy fence orders other CTAs' generic stores of w_{j-1} (step j-1, already
@@ -1096,40 +1213,26 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 for (int64_t i = 0; i < 2 && i < nmine; i++) issue(j + 1, i, (int)i);  // stages are all consumed
             }
-            spin_until_geq(pa_.bar_count, (unsigned int)j * gridDim.x, pa_.err);  // + acquire (L1 invalidated)
+            spin_until_geq(pa_.bar_count, (unsigned int)j * ng, pa_.err);  // + acquire (L1 invalidated)
         }
         __syncthreads();
-        // ---- canonical reductions of step j's partials: CTA c owns probes c, c+G, ...
-        // rank-1: s_j = u^T w_j gates the next step, so it is reduced and published first; the
-        // moments follow off the critical path (the parity-double-buffered partials of step j are
-        // next overwritten in step j+2, which starts after this CTA publishes s_{j+1})
-        if (HAS_S) {
-            for (int p = blockIdx.x; p < K; p += gridDim.x) {
-                const double sv = reduce_partials_one(part + (size_t)(NCH - 1) * gridDim.x * K, K, (int)gridDim.x, p, wbuf);
-                if (tid == 0) pa_.s_buf[(j & 1) * K + p] = sv;
-            }
-            if (tid == 0) {
-                const unsigned int mine = blockIdx.x < K ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-                if (mine) red_release_add(pa_.s_count, mine);
-            }
-        }
-        for (int p = blockIdx.x; p < K; p += gridDim.x) {
-            double v[NCH];
+        // ---- canonical sums over the ng group sums (every CTA: s_j; the last CTA: the moments)
+        constexpr int T = kThreads / K;
+        const bool want_mu = blockIdx.x == gridDim.x - 1;
 #pragma unroll
-            for (int ch = 0; ch < (HAS_S ? NCH - 1 : NCH); ch++)
-                v[ch] = reduce_partials_one(part + (size_t)ch * gridDim.x * K, K, (int)gridDim.x, p, wbuf);
-            if (tid == 0 && p < a.kvalid) {
-                double* row = a.mu_out + (size_t)p * a.mu_stride;
-                if (DBL) dbl_write(row, j, a.mu_stride - 1, v[0], v[1]);
-                else row[j] = v[0];
-            }
+        for (int ch = 0; ch < NCH; ch++) {
+            if (!want_mu && !(HAS_S && ch == NCH - 1)) continue;
+            const double t = group_tree_sum<K>(gp + (size_t)ch * ng * K, ng);
+            if (tid % T == 0) fin[ch][tid / T] = t;
         }
-        if (HAS_S) {
-            if (tid == 0) spin_until_geq(pa_.s_count, (unsigned int)j * K, pa_.err);  // every s_j published
-            __syncthreads();
-            if (tid < K) s_sh[tid] = __ldcg(pa_.s_buf + (j & 1) * K + tid);
-            __syncthreads();
+        __syncthreads();
+        if (want_mu && tid < a.kvalid) {
+            double* row = a.mu_out + (size_t)tid * a.mu_stride;
+            if (DBL) dbl_write(row, j, a.mu_stride - 1, fin[0][tid], fin[1][tid]);
+            else row[j] = fin[0][tid];
         }
+        if (HAS_S && tid < K) s_sh[tid] = fin[NCH - 1][tid];
+        __syncthreads();
     }
 }
 

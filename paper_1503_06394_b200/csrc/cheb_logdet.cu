@@ -150,7 +150,7 @@ int tile_rows(int k, int r4 = CHEB_RPG) { return r4 * kThreads * 4 / k; }
 int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL)); }
 
 struct Layout {
-    size_t misc, w0, w1, y, sbits, part, sbuf, ticket;
+    size_t misc, w0, w1, y, sbits, part, gpart, sbuf, ticket;
     size_t rp2, ci2, va2, u2, cnt64, scan, total;
     size_t scan_bytes;
     int64_t rp2_len;
@@ -165,8 +165,7 @@ constexpr size_t kStatusOff = 8;
 Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     Layout L{};
     size_t off = 0;
-    L.misc = off; off += 256;  // [8] u32 status (kStatusOff), [16] barrier count, [20] barrier
-                               // generation, [24] rank-1 s_ready
+    L.misc = off; off += 256;  // [8] u32 status (kStatusOff), [16] persistent-kernel grid barrier
     const size_t wbytes = align256((size_t)d * k * sizeof(double));
     const int words = k >= 32 ? k / 32 : 1;
     const size_t maxgrid = (size_t)sms * kMaxCtasPerSm;
@@ -176,7 +175,9 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.y = off; if (kind == CL_OP_BTB) off += wbytes;
     L.sbits = off; off += align256((size_t)d * words * sizeof(uint32_t) + 16);
     // per-CTA partials: up to 3 channels (doubling + rank-1) x 2 step parities (persistent kernel)
-    L.part = off; off += align256(6 * maxgrid * k * sizeof(double));
+    L.part = off; off += align256(3 * maxgrid * k * sizeof(double));
+    // reduction-group sums: up to 3 channels x 2 step parities (persistent kernel)
+    L.gpart = off; off += align256(6 * (maxgrid / kRedGroup + 1) * k * sizeof(double));
     L.sbuf = off; off += align256(2 * (size_t)k * sizeof(double));
     L.ticket = off; off += 256;
     L.rp2_len = ntiles * tile_rows_max(k) + 2;
@@ -267,6 +268,9 @@ int grid_for(Kern kern, int64_t ntiles, int sms, size_t dyn_smem = 0) {
         if (g > cap) g = cap;
     }
     if (g > ntiles) g = ntiles;
+    // staged step / persistent kernels: a multiple of the reduction group (cluster) size, so the
+    // persistent kernel's clusters tile the grid and both schedules share one canonical order
+    if (dyn_smem > 0 && g >= kRedGroup) g -= g % kRedGroup;
     return (int)(g < 1 ? 1 : g);
 }
 
@@ -298,7 +302,8 @@ struct Schedule {
     bool power = false;       // power basis (Taylor baseline): w_j = Ã w_{j-1}, every step "FIRST"
     bool doubling = false;    // moment doubling: ceil(n/2) applications of Ã give mu_0..mu_n
     bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
-    bool small = false;       // L2-resident operator: 16-row tiles for the Algorithm-1 kernels (RP = 1)
+    bool small = false;       // 16-row tiles for the Algorithm-1 kernels (RP = 1)
+    bool l2res = false;       // csr / rank-1 working set within half of L2 (persistent schedule's home)
 };
 
 // Launch of one step-kernel variant.  The dynamic shared-memory opt-in is a per-device,
@@ -308,6 +313,55 @@ void launch_step(int grid, size_t smem, cudaStream_t st, const StepArgs& a) {
     cudaFuncSetAttribute(cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cheb_step_kernel<K, MODE, FIRST, DBL, VB, RP><<<grid, kThreads, smem, st>>>(a);
+}
+
+// Launch configuration of the persistent kernel: clusters of rg CTAs (attribute 0).
+void cluster_config(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* at, int grid, int rg, size_t smem,
+                    cudaStream_t st) {
+    cfg->gridDim = dim3(grid);
+    cfg->blockDim = dim3(kThreads);
+    cfg->dynamicSmemBytes = smem;
+    cfg->stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)rg;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg->attrs = at;
+    cfg->numAttrs = 1;
+}
+
+// Grid and reduction-group (cluster) size of the persistent kernel: the occupancy grid, cut to
+// what co-resident clusters hold.  Clusters of 8 strand CTAs at 3 CTAs/SM (GPCs of 16/18/20
+// SMs), so 8, 4 and 2 are tried and the one with the fewest tiles on the busiest CTA wins (ties:
+// the larger cluster, fewer group sums to add after the barrier).
+template <typename Kern>
+int persist_grid(Kern pk, int64_t ntiles, int sms, size_t smem, int* grid_out, int* rg_out) {
+    const int g0 = grid_for(pk, ntiles, sms, smem);
+    int best_g = 0, best_rg = 1;
+    int64_t best_span = INT64_MAX;
+    for (int rg : {kRedGroup, 4, 2}) {
+        const int r = red_group(g0, rg);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        cluster_config(&cfg, at, g0 - g0 % r, r, smem, 0);
+        int maxc = 0;
+        if (cudaOccupancyMaxActiveClusters(&maxc, pk, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        const int g = (int)std::min<int64_t>(g0 - g0 % r, (int64_t)maxc * r);
+        if (g < 1) continue;
+        const int64_t span = (ntiles + g - 1) / g;
+        if (span < best_span) {
+            best_span = span;
+            best_g = g;
+            best_rg = r;
+        }
+    }
+    if (best_g < 1) return fail(CL_ECUDA, "persistent kernel: no co-resident cluster configuration");
+    *grid_out = best_g;
+    *rg_out = best_rg;
+    return CL_OK;
 }
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
@@ -328,6 +382,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     uint32_t* sbits = (uint32_t*)(ws + L.sbits);
     double* sbuf = (double*)(ws + L.sbuf);
 
+    int rc_persist = CL_OK;
     StepArgs a{};
     a.d = d;
     a.rp = (const int64_t*)(ws + L.rp2);
@@ -338,6 +393,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.r1c_alpha = alpha * op->r1_c;
     a.r1u = (MODE == MODE_RANK1 && op->r1_u) ? (const double*)(ws + L.u2) : nullptr;
     a.part = (double*)(ws + L.part);
+    a.gpart = (double*)(ws + L.gpart);
     a.ticket = (unsigned int*)(ws + L.ticket);
     a.mu_out = mu_rows;
     a.mu_stride = mu_stride;
@@ -366,10 +422,22 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     const size_t smem_step = std::max<size_t>(
         (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, R4D>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
-    const int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true, 0, RP>, a.ntiles, sms, smem_step)
-                                       : grid_for(cheb_step_kernel<K, MODE, true, false, 0, RP>, a.ntiles, sms, smem_step);
-    const int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true, 0, RP>, a.ntiles, sms, smem_step)
-                                      : grid_for(cheb_step_kernel<K, MODE, false, false, 0, RP>, a.ntiles, sms, smem_step);
+    int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true, 0, RP>, a.ntiles, sms, smem_step)
+                                 : grid_for(cheb_step_kernel<K, MODE, true, false, 0, RP>, a.ntiles, sms, smem_step);
+    int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true, 0, RP>, a.ntiles, sms, smem_step)
+                                : grid_for(cheb_step_kernel<K, MODE, false, false, 0, RP>, a.ntiles, sms, smem_step);
+    // L2-resident csr / rank-1 operators: the persistent schedule's grid and reduction groups
+    // (clusters) are used by the per-step launches too, so both schedules reduce identically
+    int grid_p = 0;
+    a.rg = 0;  // default reduction groups (red_group(G))
+    if (MODE != MODE_BTB && (fp.persistent || fp.l2res)) {
+        auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true, RP> : cheb_persist_kernel<K, MODE, false, RP>;
+        int rg = 1;
+        if ((rc_persist = persist_grid(pkern, a.ntiles, sms, smem, &grid_p, &rg))) return rc_persist;
+        a.rg = rg;
+        if (!fp.persistent) grid_first = grid_step = grid_p;
+        if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] persistent grid %d, reduction groups of %d\n", grid_p, rg);
+    }
     int grid_spmm = 1;
     if (MODE == MODE_BTB) {
         const int64_t ng = (op->A.n_rows + SpmmGeo<K>::GROUPS - 1) / SpmmGeo<K>::GROUPS;
@@ -380,21 +448,25 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     const int32_t nsteps = fp.doubling ? (n + 1) / 2 : n;
     if (MODE != MODE_BTB && fp.persistent) {
         auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true, RP> : cheb_persist_kernel<K, MODE, false, RP>;
-        const int grid_p = grid_for(pkern, a.ntiles, sms, smem);
         PersistArgs pp{};
         pp.w0 = w[0];
         pp.w1 = w[1];
         pp.n = nsteps;
-        pp.part = (double*)(ws + L.part);
+        pp.gpart = (double*)(ws + L.gpart);
         pp.s_buf = sbuf;
         pp.bar_count = (unsigned int*)(ws + L.misc + 16);
-        pp.s_count = (unsigned int*)(ws + L.misc + 20);
         pp.err = (unsigned int*)(ws + L.misc + kStatusOff);
         pp.power = fp.power ? 1 : 0;
         CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
-        void* args[] = {&a, &pp};
+        // clusters of a.rg CTAs (the reduction groups), all co-resident (cooperative launch)
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        cluster_config(&cfg, at, grid_p, a.rg, smem, st);
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        cfg.numAttrs = 2;
         ProfScope ps(st, 2);
-        CL_CUDA(cudaLaunchCooperativeKernel((const void*)pkern, dim3(grid_p), dim3(kThreads), args, smem, st));
+        CL_CUDA(cudaLaunchKernelEx(&cfg, pkern, a, pp));
         g_launches++;
         return CL_OK;
     }
@@ -783,7 +855,8 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         // 16-row-per-group tiles also pay for Algorithm 1 at k <= 16 (configs[3], k = 16: 1565 vs
         // 1608 ms per estimate), where a standard tile has 128+ rows
         fp.small = g_small_tiles.load() != 0 && (wset <= 0.5 * (double)l2 || (probe_block <= 16 && !fp.doubling));
-        if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || wset <= 0.5 * (double)l2;
+        fp.l2res = wset <= 0.5 * (double)l2;
+        if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || fp.l2res;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
     // per-step csr/rank-1: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
@@ -1007,50 +1080,13 @@ int cheb_moments_host(const cl_operator* op, double a, double b, int32_t degree,
 }
 
 namespace {
-// ---- spectral interval (SURVEY f4; P:300-310; DESIGN.md reading G26) ----------------------
-// Lanczos from Chebyshev moments: the Lanczos process started at a probe v builds the Jacobi
-// matrix of v's spectral measure d lambda_v (weights (v^T q_i)^2 at the eigenvalues of Ã); its
-// recurrence coefficients follow from the measure's modified moments
-//   nu_l = int p_l d lambda_v,  p_l = T_l / 2^(l-1) (monic Chebyshev: p_{l+1} = x p_l - b_l p_{l-1},
-//   b_1 = 1/2, b_l = 1/4),  i.e. nu_0 = mu_0, nu_l = mu_l / 2^(l-1) with mu_l = v^T T_l(Ã) v,
-// by the modified Chebyshev algorithm (Sack-Donovan / Wheeler), which is well conditioned for
-// measures on [-1, 1] -- and the mu_l are exactly what the hot path computes.  2N moments give
-// the N x N Jacobi matrix (alpha_0..alpha_{N-1}; beta_1..beta_{N-1} of the monic recurrence,
-// off-diagonal sqrt(beta_k)) and beta_N, the Lanczos residual factor.
-int modified_chebyshev(const double* mu, int N, double* alpha, double* beta) {
-    const int L = 2 * N + 1;  // nu_0 .. nu_2N
-    std::vector<double> nu(L), sm2(L, 0.0), sm1(L), sk(L);
-    double sc = 1.0;
-    for (int l = 0; l < L; l++) {
-        nu[l] = l == 0 ? mu[0] : mu[l] * sc;
-        if (l >= 1) sc *= 0.5;
-    }
-    if (!(nu[0] > 0.0)) return fail(CL_ENONFINITE, "spectral measure has no mass (mu_0 = %g)", nu[0]);
-    sm1 = nu;  // sigma_{0,l}
-    alpha[0] = nu[1] / nu[0];
-    beta[0] = nu[0];
-    for (int k = 1; k <= N; k++) {
-        for (int l = k; l <= 2 * N - k; l++) {
-            const double bl = l == 1 ? 0.5 : 0.25;
-            sk[l] = sm1[l + 1] - alpha[k - 1] * sm1[l] - beta[k - 1] * sm2[l] + bl * sm1[l - 1];
-        }
-        if (!(sk[k] > 0.0) || !std::isfinite(sk[k]))
-            return fail(CL_ENONFINITE, "Lanczos breakdown at step %d (measure supported on <= %d points?)", k, k);
-        beta[k] = sk[k] / sm1[k - 1];
-        if (k < N) alpha[k] = sk[k + 1] / sk[k] - sm1[k] / sm1[k - 1];
-        sm2.swap(sm1);
-        sm1.swap(sk);
-    }
-    return CL_OK;
-}
-
 // Eigen-decomposition of the symmetric tridiagonal matrix (diag d[0..n-1], off-diagonal e[0..n-2])
 // by the implicit QL method with Wilkinson shifts, accumulating the eigenvectors in z (row-major
 // n x n, z[r*n + c] = component r of eigenvector c).  d is overwritten by the eigenvalues.
-int tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<double>& z) {
+int tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<double>& z, bool vectors = true) {
     const int n = (int)d.size();
-    z.assign((size_t)n * n, 0.0);
-    for (int i = 0; i < n; i++) z[(size_t)i * n + i] = 1.0;
+    z.assign(vectors ? (size_t)n * n : 0, 0.0);
+    for (int i = 0; vectors && i < n; i++) z[(size_t)i * n + i] = 1.0;
     e.resize(n, 0.0);
     if (n > 0) e[n - 1] = 0.0;
     for (int l = 0; l < n; l++) {
@@ -1083,7 +1119,7 @@ int tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<double
                     p = s * r;
                     d[i + 1] = g + p;
                     g = c * r - b;
-                    for (int k = 0; k < n; k++) {
+                    for (int k = 0; vectors && k < n; k++) {
                         f = z[(size_t)k * n + i + 1];
                         z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * f;
                         z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * f;
@@ -1100,63 +1136,161 @@ int tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<double
 }
 }  // namespace
 
-int cheb_spectrum_bounds(const cl_operator* op, double lo, double hi, int32_t lanczos_steps,
-                         int32_t num_probes, uint64_t seed, cl_spectrum* out, double* jacobi_out) {
+extern "C++" {
+namespace {
+// ---- spectral interval (SURVEY f4; P:300-310; DESIGN.md reading G26) ----------------------
+// N Lanczos steps for the k probes of one block (columns of [d][k] buffers), on the device;
+// hist receives alpha_j (row 2j) and beta_{j+1} (row 2j+1), j < N, k doubles per row.
+template <int K>
+int lanczos_block(const cl_operator* op, int N, uint64_t seed, int64_t p0, char* ws, size_t wbytes,
+                  double* hist_d, cudaStream_t st, int sms) {
+    const int64_t d = op->A.n_cols;
+    double* Q = (double*)ws;
+    double* Pb = (double*)(ws + wbytes);
+    double* Z = (double*)(ws + 2 * wbytes);
+    double* T = (double*)(ws + 3 * wbytes);  // B^T B: Y = B q
+    double* part = (double*)(ws + 4 * wbytes);
+    const int gv = (int)std::min<int64_t>((d * (K / 2) + kThreads - 1) / kThreads, (int64_t)sms * 8);
+    double* s_d = part + (size_t)gv * K;
+    double* beta0 = s_d + K;                  // [K] sqrt(d) (normalises the probe), then zeros
+    unsigned int* ticket = (unsigned int*)(beta0 + 2 * K);
+    const int64_t ngs = (std::max(op->A.n_rows, op->At.n_rows) + SpmmGeo<K>::GROUPS - 1) / SpmmGeo<K>::GROUPS;
+    const int gs = grid_for(spmm_kernel<K>, ngs, sms);
+    const int gp = (int)std::min<int64_t>((d * K + kThreads - 1) / kThreads, (int64_t)sms * 8);
+    std::vector<double> hb(2 * K);
+    for (int c = 0; c < K; c++) {
+        hb[c] = std::sqrt((double)d);  // |v| for a +-1 probe
+        hb[K + c] = 0.0;
+    }
+    CL_CUDA(cudaMemcpyAsync(beta0, hb.data(), sizeof(double) * 2 * K, cudaMemcpyHostToDevice, st));
+    CL_CUDA(cudaMemsetAsync(ticket, 0, 256, st));
+    lanczos_probe_kernel<K><<<gp, kThreads, 0, st>>>(d, seed, (uint64_t)p0, Pb);
+    LzArgs a{};
+    a.d = d;
+    a.u = op->kind == CL_OP_CSR_RANK1 ? op->r1_u : nullptr;
+    a.r1c = op->kind == CL_OP_CSR_RANK1 ? op->r1_c : 0.0;
+    a.s = s_d;
+    a.part = part;
+    a.ticket = ticket;
+    // q_0 = v / |v|, s = u^T q_0
+    a.qp = Pb;
+    a.beta = beta0;
+    a.out = s_d;
+    lanczos_vec_kernel<K, LZ_NRM><<<gv, kThreads, 0, st>>>(a);
+    std::swap(Q, Pb);
+    CL_CUDA(cudaMemsetAsync(Pb, 0, wbytes, st));  // q_{-1} = 0 (beta_0 = 0: row K.. of beta0)
+    g_launches += 2;
+    for (int j = 0; j < N; j++) {
+        double* al = hist_d + (size_t)(2 * j) * K;
+        double* bn = hist_d + (size_t)(2 * j + 1) * K;
+        const double* bj = j == 0 ? beta0 + K : hist_d + (size_t)(2 * j - 1) * K;
+        if (op->kind == CL_OP_BTB) {
+            spmm_kernel<K><<<gs, kThreads, 0, st>>>(op->A.n_rows, op->A.row_ptr, op->A.col_idx, op->A.val, Q, T);
+            spmm_kernel<K><<<gs, kThreads, 0, st>>>(op->At.n_rows, op->At.row_ptr, op->At.col_idx, op->At.val, T, Z);
+            g_launches += 2;
+        } else {
+            spmm_kernel<K><<<gs, kThreads, 0, st>>>(op->A.n_rows, op->A.row_ptr, op->A.col_idx, op->A.val, Q, Z);
+            g_launches++;
+        }
+        a.q = Q;
+        a.qp = Pb;
+        a.z = Z;
+        a.out = al;
+        lanczos_vec_kernel<K, LZ_DOT><<<gv, kThreads, 0, st>>>(a);
+        a.alpha = al;
+        a.beta = bj;
+        a.out = bn;
+        lanczos_vec_kernel<K, LZ_UPD><<<gv, kThreads, 0, st>>>(a);
+        a.beta = bn;
+        a.out = s_d;
+        lanczos_vec_kernel<K, LZ_NRM><<<gv, kThreads, 0, st>>>(a);
+        g_launches += 3;
+        std::swap(Q, Pb);
+    }
+    CL_CUDA(cudaGetLastError());
+    return CL_OK;
+}
+
+size_t lanczos_ws_bytes(int64_t d, int k, int sms) {
+    const size_t wbytes = align256((size_t)d * k * sizeof(double));
+    return 4 * wbytes + align256(((size_t)sms * 8 + 3) * k * sizeof(double) + 256);
+}
+}  // namespace
+}  // extern "C++"
+
+int cheb_spectrum_bounds(const cl_operator* op, int32_t lanczos_steps, int32_t num_probes, uint64_t seed,
+                         cl_spectrum* out, double* jacobi_out) {
     int rc;
     if ((rc = check_op(op))) return rc;
     if (!out) return fail(CL_EINVAL, "out is NULL");
-    if (lanczos_steps < 1 || lanczos_steps > 400) return fail(CL_EINVAL, "lanczos_steps must be in [1, 400]");
-    if (num_probes < 1 || num_probes > 128) return fail(CL_EINVAL, "num_probes must be in [1, 128]");
-    if (!std::isfinite(lo) || lo < 0.0 || !std::isfinite(hi)) return fail(CL_EINVAL, "need finite lo >= 0");
+    if (lanczos_steps < 1 || lanczos_steps > 2000) return fail(CL_EINVAL, "lanczos_steps must be in [1, 2000]");
+    if (num_probes < 1 || num_probes > 4096) return fail(CL_EINVAL, "num_probes must be in [1, 4096]");
     cudaStream_t st;
     CL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } guard{st};
-    if (hi <= 0.0) {  // a guaranteed upper bound of the spectrum from the matrix
-        if ((rc = cheb_norm_bound(op, &hi, st))) return rc;
-    }
-    if (!(hi > lo)) return fail(CL_EINVAL, "need hi > lo (got [%g, %g])", lo, hi);
-    const int N = lanczos_steps, n2 = 2 * N;
-    const int k = pick_k(num_probes);
-    const size_t ws_bytes = plan(op->A.n_cols, gather_nnz(op), k, op->kind, sm_count()).total;
-    const size_t mu_n = (size_t)num_probes * (n2 + 1);
+    double hi = 0.0;  // a guaranteed upper bound of the spectrum from the matrix
+    if ((rc = cheb_norm_bound(op, &hi, st))) return rc;
+    const int N = lanczos_steps, k = pick_k(num_probes), sms = sm_count();
+    const int64_t d = op->A.n_cols;
+    const size_t wbytes = align256((size_t)d * k * sizeof(double));
+    const size_t ws_bytes = lanczos_ws_bytes(d, k, sms);
+    const size_t hist_n = (size_t)2 * N * k;
     void* ws = nullptr;
-    if ((rc = arena_get(0, align256(ws_bytes) + sizeof(double) * mu_n, &ws))) return rc;
-    double* mu_d = (double*)((char*)ws + align256(ws_bytes));
-    const double alpha = 2.0 / (hi - lo), beta = (hi + lo) / (hi - lo);
-    // the hot path: Chebyshev moments mu_0..mu_2N of every probe on [lo, hi]
-    if ((rc = moments_impl(op, alpha, beta, false, n2, 0, num_probes, seed, k, ws, ws_bytes, mu_d, st))) return rc;
-    std::vector<double> mu(mu_n);
-    uint32_t status = 0;
-    CL_CUDA(cudaMemcpyAsync(&status, (char*)ws + kStatusOff, sizeof(status), cudaMemcpyDeviceToHost, st));
-    CL_CUDA(cudaMemcpyAsync(mu.data(), mu_d, sizeof(double) * mu_n, cudaMemcpyDeviceToHost, st));
-    CL_CUDA(cudaStreamSynchronize(st));
-    if (status & 1u) return fail(CL_ECUDA, "persistent-kernel grid wait timed out");
-    if (status & 2u) return fail(CL_ENONFINITE, "non-finite moment: [lo,hi]=[%g,%g] misses the spectrum", lo, hi);
+    if ((rc = arena_get(0, ws_bytes + sizeof(double) * hist_n, &ws))) return rc;
+    double* hist_d = (double*)((char*)ws + ws_bytes);
+    std::vector<double> hist(hist_n), dd, ee, z;
     double lmin = INFINITY, lmax = -INFINITY, rmin = 0.0, rmax = 0.0;
-    std::vector<double> al(N), be(N + 1), d, e, z;
-    for (int p = 0; p < num_probes; p++) {
-        if ((rc = modified_chebyshev(mu.data() + (size_t)p * (n2 + 1), N, al.data(), be.data()))) return rc;
-        if (jacobi_out) {
-            double* row = jacobi_out + (size_t)p * 2 * N;
-            for (int j = 0; j < N; j++) row[j] = al[j];                   // diagonal of T_N (Ã-space)
-            for (int j = 1; j <= N; j++) row[N + j - 1] = std::sqrt(be[j]);  // off-diagonal, then beta_N
+    int used = N;
+    for (int64_t p0 = 0; p0 < num_probes; p0 += k) {
+        const int kvalid = (int)std::min<int64_t>(k, num_probes - p0);
+        switch (k) {
+            case 8: rc = lanczos_block<8>(op, N, seed, p0, (char*)ws, wbytes, hist_d, st, sms); break;
+            case 16: rc = lanczos_block<16>(op, N, seed, p0, (char*)ws, wbytes, hist_d, st, sms); break;
+            case 32: rc = lanczos_block<32>(op, N, seed, p0, (char*)ws, wbytes, hist_d, st, sms); break;
+            case 64: rc = lanczos_block<64>(op, N, seed, p0, (char*)ws, wbytes, hist_d, st, sms); break;
+            default: rc = lanczos_block<128>(op, N, seed, p0, (char*)ws, wbytes, hist_d, st, sms); break;
         }
-        d.assign(al.begin(), al.end());
-        e.resize(N > 1 ? N - 1 : 0);
-        for (int j = 1; j < N; j++) e[j - 1] = std::sqrt(be[j]);
-        if ((rc = tridiag_ql(d, e, z))) return rc;
-        const double bN = std::sqrt(be[N]);
-        int imin = 0, imax = 0;
-        for (int i = 1; i < N; i++) {
-            if (d[i] < d[imin]) imin = i;
-            if (d[i] > d[imax]) imax = i;
+        if (rc) return rc;
+        CL_CUDA(cudaMemcpyAsync(hist.data(), hist_d, sizeof(double) * hist_n, cudaMemcpyDeviceToHost, st));
+        CL_CUDA(cudaStreamSynchronize(st));
+        for (int c = 0; c < kvalid; c++) {
+            // T_Nv: diagonal alpha_0..alpha_{Nv-1}, off-diagonal beta_1..beta_{Nv-1}, residual beta_Nv;
+            // the process stops early at an invariant subspace (beta = 0) or a non-finite value
+            int Nv = 0;
+            double bmax = 0.0;
+            for (int j = 0; j < N; j++) {
+                const double al = hist[(size_t)(2 * j) * k + c], bn = hist[(size_t)(2 * j + 1) * k + c];
+                if (!std::isfinite(al) || !std::isfinite(bn)) break;
+                Nv = j + 1;
+                bmax = std::max(bmax, bn);
+                if (!(bn > 1e-14 * bmax)) break;
+            }
+            if (Nv < 1) return fail(CL_ENONFINITE, "Lanczos step 1 not finite (probe %lld)", (long long)(p0 + c));
+            used = std::min(used, Nv);
+            if (jacobi_out) {
+                double* row = jacobi_out + (size_t)(p0 + c) * 2 * N;
+                for (int j = 0; j < N; j++) {
+                    row[j] = j < Nv ? hist[(size_t)(2 * j) * k + c] : NAN;
+                    row[N + j] = j < Nv ? hist[(size_t)(2 * j + 1) * k + c] : NAN;
+                }
+            }
+            dd.resize(Nv);
+            ee.resize(Nv > 1 ? Nv - 1 : 0);
+            for (int j = 0; j < Nv; j++) dd[j] = hist[(size_t)(2 * j) * k + c];
+            for (int j = 0; j + 1 < Nv; j++) ee[j] = hist[(size_t)(2 * j + 1) * k + c];
+            const double bN = hist[(size_t)(2 * (Nv - 1) + 1) * k + c];
+            if ((rc = tridiag_ql(dd, ee, z))) return rc;
+            int imin = 0, imax = 0;
+            for (int i = 1; i < Nv; i++) {
+                if (dd[i] < dd[imin]) imin = i;
+                if (dd[i] > dd[imax]) imax = i;
+            }
+            // Ritz value and Kahan residual bound beta_Nv |s_Nv| (an eigenvalue of M lies within it)
+            const double r0 = bN * std::fabs(z[(size_t)(Nv - 1) * Nv + imin]);
+            const double r1 = bN * std::fabs(z[(size_t)(Nv - 1) * Nv + imax]);
+            if (dd[imin] < lmin) { lmin = dd[imin]; rmin = r0; }
+            if (dd[imax] > lmax) { lmax = dd[imax]; rmax = r1; }
         }
-        // Ritz value theta and Kahan residual bound beta_N |s_N| (an eigenvalue of Ã lies within it),
-        // mapped to M: lambda = (theta + beta) / alpha
-        const double l0 = (d[imin] + beta) / alpha, r0 = bN * std::fabs(z[(size_t)(N - 1) * N + imin]) / alpha;
-        const double l1 = (d[imax] + beta) / alpha, r1 = bN * std::fabs(z[(size_t)(N - 1) * N + imax]) / alpha;
-        if (l0 < lmin) { lmin = l0; rmin = r0; }
-        if (l1 > lmax) { lmax = l1; rmax = r1; }
     }
     out->lambda_min = lmin;
     out->lambda_max = lmax;
@@ -1164,9 +1298,8 @@ int cheb_spectrum_bounds(const cl_operator* op, double lo, double hi, int32_t la
     out->res_max = rmax;
     out->a = std::max(lmin - rmin, 0.0);
     out->b = std::min(lmax + rmax, hi);
-    out->lo = lo;
-    out->hi = hi;
-    out->lanczos_steps = N;
+    out->hi_bound = hi;
+    out->lanczos_steps = used;
     out->num_probes = num_probes;
     return CL_OK;
 }

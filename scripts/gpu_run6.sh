@@ -1,0 +1,4 @@
+#!/bin/bash
+CHEB_DEBUG=1 timeout 600 python scripts/exp_rank1.py > gpurun_out/exp_rank1.jsonl 2> gpurun_out/exp_rank1.err; echo "exp rc=$?"; cat gpurun_out/exp_rank1.jsonl; grep "persistent grid" gpurun_out/exp_rank1.err | sort | uniq -c
+timeout 1500 python -m pytest tests -m gpu -q -k "spectrum or persistent or graph or shard or standard_geometry or torus" > gpurun_out/t_sel.log 2>&1; echo "pytest rc=$?"; tail -12 gpurun_out/t_sel.log
+timeout 900 python scripts/accuracy_51.py > gpurun_out/acc.jsonl 2> gpurun_out/acc.err; echo "acc rc=$?"; tail -3 gpurun_out/acc.err
