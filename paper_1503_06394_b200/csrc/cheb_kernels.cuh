@@ -271,7 +271,13 @@ __device__ __forceinline__ double group_tree_sum(const double* gp, int ng) {
     constexpr int T = kThreads / K;
     const int p = threadIdx.x / T, u = threadIdx.x % T;
     double t = 0.0;
-    for (int q = u; q < ng; q += T) t += __ldcg(gp + (size_t)q * K + p);
+    for (int q0 = u; q0 < ng; q0 += 8 * T) {  // 8 loads in flight, then the adds in ascending q
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) v[r] = q0 + r * T < ng ? __ldcg(gp + (size_t)(q0 + r * T) * K + p) : 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) t += v[r];
+    }
 #pragma unroll
     for (int off = T / 2; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
     return t;
@@ -287,8 +293,11 @@ __device__ __forceinline__ void reduce_partials_grouped(const double* part, int 
         const int p = x % K, q = (x / K) % ng, ch = x / (K * ng);
         const int c0 = q * RG, cn = (G - c0) < RG ? (G - c0) : RG;
         const double* src = part + ((size_t)ch * G + c0) * K + p;
-        double sq = 0.0;
-        for (int r = 0; r < cn; r++) sq += __ldcg(src + (size_t)r * K);
+        double v[kRedGroup], sq = 0.0;
+#pragma unroll
+        for (int r = 0; r < kRedGroup; r++) v[r] = r < cn ? __ldcg(src + (size_t)r * K) : 0.0;
+#pragma unroll
+        for (int r = 0; r < kRedGroup; r++) sq += v[r];
         gpart[((size_t)ch * ng + q) * K + p] = sq;
     }
     __syncthreads();  // block-level visibility of the gpart stores
@@ -514,8 +523,8 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
                 bits |= bq << ((pl + q) & 31);
                 acc[0][q] += v[q] * v[q];
             }
-#pragma unroll
             if (w0)  // nullptr: the per-step path reads v from the sign bits only
+#pragma unroll
                 for (int q = 0; q < PPL; q += 2)
                     *reinterpret_cast<double2*>(w0 + (size_t)i * K + pl + q) = make_double2(v[q], v[q + 1]);
             if (HAS_S) {
@@ -734,8 +743,12 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
 }
 
 // resident CTAs per SM each mode is register-budgeted for (BTB is smem-limited to 2)
+#ifndef CHEB_MIN_CTAS_R1
+#define CHEB_MIN_CTAS_R1 3  // rank-1 Algorithm 1 (two accumulator channels)
+#endif
 __host__ __device__ constexpr int min_ctas(int mode, bool dbl = false) {
-    return mode == MODE_CSR ? (dbl ? CHEB_MIN_CTAS_DBL : CHEB_MIN_CTAS) : (mode == MODE_RANK1 && !dbl ? 3 : 2);
+    return mode == MODE_CSR ? (dbl ? CHEB_MIN_CTAS_DBL : CHEB_MIN_CTAS)
+                            : (mode == MODE_RANK1 && !dbl ? CHEB_MIN_CTAS_R1 : 2);
 }
 
 // RP: rows per lane group of the Algorithm-1 kernels (0: CHEB_RPG).  L2-resident operators use
@@ -1197,8 +1210,11 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         if (crank == 0) {
             for (int x = tid; x < NCH * K; x += kThreads) {
                 const int ch = x / K, p = x % K;
-                double sq = 0.0;
-                for (int r = 0; r < RG; r++) sq += *cluster.map_shared_rank(&cpart[par][ch][p], r);
+                double v[kRedGroup], sq = 0.0;  // all DSMEM loads in flight, then the adds in rank order
+#pragma unroll
+                for (int r = 0; r < kRedGroup; r++) v[r] = r < RG ? *cluster.map_shared_rank(&cpart[par][ch][p], r) : 0.0;
+#pragma unroll
+                for (int r = 0; r < kRedGroup; r++) sq += v[r];
                 gp[((size_t)ch * ng + cid) * K + p] = sq;
             }
             __syncthreads();
@@ -1216,12 +1232,15 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             spin_until_geq(pa_.bar_count, (unsigned int)j * ng, pa_.err);  // + acquire (L1 invalidated)
         }
         __syncthreads();
-        // ---- canonical sums over the ng group sums (every CTA: s_j; the last CTA: the moments)
+        // ---- canonical sums over the ng group sums: the rank-1 s_j by each cluster's rank 0, handed
+        // to its cluster over DSMEM (one load of the group sums per cluster, not per CTA); the
+        // moments by the last CTA
         constexpr int T = kThreads / K;
         const bool want_mu = blockIdx.x == gridDim.x - 1;
 #pragma unroll
         for (int ch = 0; ch < NCH; ch++) {
-            if (!want_mu && !(HAS_S && ch == NCH - 1)) continue;
+            const bool is_s = HAS_S && ch == NCH - 1;
+            if (!(is_s ? (crank == 0 && j < pa_.n) : want_mu)) continue;
             const double t = group_tree_sum<K>(gp + (size_t)ch * ng * K, ng);
             if (tid % T == 0) fin[ch][tid / T] = t;
         }
@@ -1231,8 +1250,12 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             if (DBL) dbl_write(row, j, a.mu_stride - 1, fin[0][tid], fin[1][tid]);
             else row[j] = fin[0][tid];
         }
-        if (HAS_S && tid < K) s_sh[tid] = fin[NCH - 1][tid];
-        __syncthreads();
+        if (HAS_S && j < pa_.n) {  // (after the last step nobody needs s_n; rank 0 may have exited)
+            if (crank == 0 && tid < K) s_sh[tid] = fin[NCH - 1][tid];
+            cluster.sync();  // rank 0's s_j visible to the cluster
+            if (crank != 0 && tid < K) s_sh[tid] = *cluster.map_shared_rank(&s_sh[tid], 0);
+            __syncthreads();
+        }
     }
 }
 

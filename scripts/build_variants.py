@@ -10,6 +10,7 @@ VARIANTS = {
     "s3": ["CHEB_STAGES=3"],
     "s3c3": ["CHEB_STAGES=3", "CHEB_MIN_CTAS=3"],
     "c3": ["CHEB_MIN_CTAS=3"],
+    "r1c4": ["CHEB_MIN_CTAS_R1=4"],
     "r1": ["CHEB_RPG=1"],
     "r4": ["CHEB_RPG=4"],
     "checked": ["CHEB_CHECKS=1"],
