@@ -58,11 +58,12 @@ typedef struct {
     const double *val;      /* [nnz]      */
 } cl_csr;
 
-typedef enum { CL_OP_CSR = 0, CL_OP_CSR_RANK1 = 1, CL_OP_BTB = 2 } cl_op_kind;
+typedef enum { CL_OP_CSR = 0, CL_OP_CSR_RANK1 = 1, CL_OP_BTB = 2, CL_OP_FAMILY = 3 } cl_op_kind;
 
 typedef struct {
-    int32_t kind;      /* cl_op_kind                                              */
-    cl_csr A;          /* A (CSR, RANK1) or B (BTB); d = A.n_cols                 */
+    int32_t kind;      /* cl_op_kind (FAMILY: only for cheb_workspace_bytes, see      */
+                       /* cheb_family_moments)                                       */
+    cl_csr A;          /* A (CSR, RANK1), B (BTB) or the family base; d = A.n_cols  */
     cl_csr At;         /* BTB only: exact CSR of B^T (n_rows = B.n_cols)          */
     double r1_c;       /* RANK1 only: weight c                                    */
     const double *r1_u;/* RANK1 only: u[d], NULL = all ones                       */
@@ -148,6 +149,31 @@ int cheb_norm_bound(const cl_operator *op, double *s_out, void *stream);
  * log-likelihood scan (§5.2) is
  *   log p(x | rho) = 1/2 log det J(rho) - 1/2 x^T J(rho) x - d/2 log(2 pi). */
 int cheb_quadform(const cl_csr *A, const double *x, double *out, void *stream);
+
+/* x^T D x and x^T O x for a DEVICE CSR A = D + O (D its diagonal entries, O the rest): out2[0],
+ * out2[1] (HOST).  For the family M(theta) = D + theta O, x^T M(theta) x = out2[0] + theta out2[1].
+ * Deterministic; synchronous on `stream`. */
+int cheb_quadform_split(const cl_csr *A, const double *x, double *out2, void *stream);
+
+/* One-parameter operator family for the GMRF likelihood scan (§5.2):
+ * M_r = D + theta_r O, r < R, from a DEVICE base CSR = D + O (D its diagonal entries, O the rest;
+ * the grid GMRF: base = I - Adj, M_r = I - theta_r Adj).
+ *   cheb_family_gershgorin: lo_hi[2r], lo_hi[2r+1] = the Gershgorin interval of M_r (HOST array
+ *     [R][2]); synchronous.
+ *   cheb_family_moments: the R members in the COLUMNS of one probe block, so all R share every pass
+ *     over the matrix: with R_pad = R rounded up to a power of two and kp = probe_block / R_pad
+ *     (>= 2), column c of a block carries member c / kp and probe p0 + c % kp (common random
+ *     numbers: every member sees the same probes).  Per column the step applies
+ *     Ã_r = alpha_r M_r - beta_r I for the member's interval ab[2r], ab[2r+1] (HOST [R][2]):
+ *     (alpha_r d_i - beta_r) w_i + alpha_r theta_r (O w)_i.  mu_out (DEVICE) receives
+ *     mu[r][p - probe_begin][j] = v_p^T T_j(Ã_r) v_p, layout [R][probe_end-probe_begin][degree+1].
+ *     Workspace: cheb_workspace_bytes of an operator {kind = CL_OP_FAMILY, A = base}.  Algorithm 1,
+ *     per-step launches; asynchronous like cheb_moments (same status word / NaN poisoning).
+ *     CL_EINVAL for probe_block < 16 or < 2 R_pad, or an invalid interval. */
+int cheb_family_gershgorin(const cl_csr *base, int32_t R, const double *theta, double *lo_hi, void *stream);
+int cheb_family_moments(const cl_csr *base, int32_t R, const double *theta, const double *ab, int32_t degree,
+                        int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                        void *workspace, size_t ws_bytes, double *mu_out, void *stream);
 
 /* Gershgorin interval of a DEVICE CSR: lo_hi[0] = min_i (a_ii - sum_{j!=i} |a_ij|),
  * lo_hi[1] = max_i sum_j |a_ij| (HOST array[2]); for a symmetric A it encloses spec(A)

@@ -12,7 +12,7 @@ SO_PATH = os.environ.get("CHEB_LIB") or os.path.join(PKG, "libchebld.so")  # CHE
 HEADER = os.path.join(ROOT, "include", "cheb_logdet.h")
 
 CL_OK, CL_EINVAL, CL_EDIM, CL_ENOMEM, CL_ECUDA, CL_ENONFINITE = 0, -1, -2, -3, -4, -5
-OP_KIND = {"csr": 0, "rank1": 1, "btb": 2}
+OP_KIND = {"csr": 0, "rank1": 1, "btb": 2, "family": 3}
 
 
 class ChebError(RuntimeError):
@@ -76,6 +76,9 @@ def load():
         "cheb_norm_bound": (I, [OPP, P, P]),
         "cheb_quadform": (I, [ctypes.POINTER(CLCsr), P, P, P]),
         "cheb_gershgorin": (I, [ctypes.POINTER(CLCsr), P, P]),
+        "cheb_quadform_split": (I, [ctypes.POINTER(CLCsr), P, P, P]),
+        "cheb_family_gershgorin": (I, [ctypes.POINTER(CLCsr), I32, P, P, P]),
+        "cheb_family_moments": (I, [ctypes.POINTER(CLCsr), I32, P, P, I32, I64, I64, U64, I32, P, SZ, P, P]),
         "cheb_logdet": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_logdet_host": (I, [OPP, D, D, I32, I32, U64, I32, ctypes.POINTER(CLResult)]),
         "cheb_moments_host": (I, [OPP, D, D, I32, I64, I64, U64, I32, P]),

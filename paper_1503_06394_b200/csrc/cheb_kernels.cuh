@@ -68,7 +68,9 @@ constexpr int kStepStages = CHEB_STAGES;
 #define CHEB_NNZ_UNROLL 5  // nnz of a row whose gathers are in flight together (5-point stencil: 1 chunk)
 #endif
 
-enum { MODE_CSR = 0, MODE_RANK1 = 1, MODE_BTB = 2 };
+// MODE_FAM: a one-parameter family M_r = D + theta_r O of a base CSR (D its diagonal, O the rest),
+// R values of theta in the columns of one probe block (the rho-likelihood scan)
+enum { MODE_CSR = 0, MODE_RANK1 = 1, MODE_BTB = 2, MODE_FAM = 3 };
 
 __host__ __device__ constexpr int words_for(int K) { return K >= 32 ? K / 32 : 1; }
 
@@ -128,7 +130,7 @@ struct StageLayout {
     static constexpr int OFF_COL = OFF_RP + G::RPBYTES;
     static constexpr int OFF_SGN = OFF_COL + G::COLBYTES;
     static constexpr int OFF_U = OFF_SGN + G::SGNBYTES;                          // RANK1 only
-    static constexpr int BYTES = OFF_U + (MODE == MODE_RANK1 ? G::UBYTES : 0);
+    static constexpr int BYTES = OFF_U + (MODE == MODE_RANK1 || MODE == MODE_FAM ? G::UBYTES : 0);  // u / D
     static constexpr int SMEM = 2 * BYTES;                                       // double buffer
 };
 
@@ -232,6 +234,11 @@ struct StepArgs {
     double* s_next;       // [K] u^T w_j
     double* part;         // per-CTA partials [NCH][gridDim.x][K]
     double* gpart;        // reduction-group sums [NCH][ng][K] (persistent: [2][NCH][ng][K])
+    int32_t fam_kp;       // MODE_FAM: probes per family member in a block (column c: member c / fam_kp,
+                          // probe c % fam_kp); 0 otherwise
+    int32_t fam_r;        // MODE_FAM: family members with output rows (columns of padding members skipped)
+    int64_t fam_rstride;  // MODE_FAM: doubles between the mu rows of consecutive members
+    const double* fam_coef;  // MODE_FAM: [3][K] per column: alpha_c, beta_c, alpha_c * theta_c
     int32_t rg;           // reduction group size (0: red_group(gridDim.x)); the persistent kernel's
                           // cluster size, so per-step launches of the same grid reduce identically
     unsigned int* ticket;
@@ -387,8 +394,10 @@ __device__ __forceinline__ void grid_reduce_finish(double (&acc)[NCH][PPL], cons
     __threadfence();
     reduce_partials_grouped<K, NCH>(a.part, (int)gridDim.x, a.rg > 0 ? a.rg : red_group((int)gridDim.x), a.gpart, fin);
     if (tid < K) {
-        double* row = a.mu_out + (size_t)tid * a.mu_stride;
-        if (tid < a.kvalid) {
+        // MODE_FAM: column tid is probe tid % fam_kp of family member tid / fam_kp
+        const int pc = a.fam_kp ? tid % a.fam_kp : tid, mc = a.fam_kp ? tid / a.fam_kp : 0;
+        double* row = a.mu_out + (size_t)mc * a.fam_rstride + (size_t)pc * a.mu_stride;
+        if (pc < a.kvalid && (!a.fam_kp || mc < a.fam_r)) {
             if (EPI == EPI_STEP) row[a.mu_col] = fin[0][tid];
             if (EPI == EPI_DBL) dbl_write(row, a.mu_col, a.mu_stride - 1, fin[0][tid], fin[1][tid]);
         }
@@ -445,7 +454,25 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
             const int64_t o0 = rp2[i], o1 = rp2[i + 1];
             has = (MODE == MODE_BTB);
             int64_t o = o0;
-            if (MODE != MODE_BTB) {
+            if (MODE == MODE_FAM) {
+                // family: raw off-diagonal values O (each member scales them by its alpha theta in
+                // the kernel); the head slot (i, 0.0) gathers w_{j-1}[i], D_i goes to u2[i]
+                double dv = 0.0;
+                o = o0 + 1;
+                for (int64_t e = e0; e < e1; e++) {
+                    const int32_t c = ci[e];
+                    if (c == i) {
+                        dv = va[e];
+                    } else {
+                        ci2[o] = c;
+                        va2[o] = va[e];
+                        o++;
+                    }
+                }
+                ci2[o0] = (int32_t)i;
+                va2[o0] = 0.0;
+                u2[i] = dv;
+            } else if (MODE != MODE_BTB) {
                 // csr / rank-1: the diagonal entry first (alpha a_ii - beta, or -beta when none is
                 // stored), then the off-diagonal entries in CSR order: the doubling kernels take
                 // w_{j-1}[i] from the row's first gather
@@ -475,7 +502,7 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
                 ci2[o] = (int32_t)i;
                 va2[o] = 0.0;
             }
-            if (u2) u2[i] = u ? u[i] : 1.0;
+            if (u2 && MODE != MODE_FAM) u2[i] = u ? u[i] : 1.0;
         }
     }
     if (blockIdx.x == 0) {
@@ -517,7 +544,8 @@ probe_init_kernel(StepArgs a, uint64_t seed, uint64_t p0, double* w0, uint32_t* 
             double v[PPL];
 #pragma unroll
             for (int q = 0; q < PPL; q++) {
-                const uint64_t z = splitmix64_at(seed, (p0 + pl + q) * d + (uint64_t)i + 1ull);
+                const uint64_t pc = MODE == MODE_FAM ? (uint64_t)((pl + q) % a.fam_kp) : (uint64_t)(pl + q);
+                const uint64_t z = splitmix64_at(seed, (p0 + pc) * d + (uint64_t)i + 1ull);
                 const uint32_t bq = (uint32_t)(z >> 63);
                 v[q] = bq ? -1.0 : 1.0;
                 bits |= bq << ((pl + q) & 31);
@@ -576,13 +604,13 @@ template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool DBL = 
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
                                           double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
-                                          const double* wcur, double* wout) {
+                                          const double* wcur, double* wout, const double* fcoef = nullptr) {
     using G = Geo<K, R4>;
     using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr int NSL = G::NSL;
     constexpr bool OWN_SMEM = SL::HAS_WC;          // w_{j-1}[i] rows staged in shared memory
     // csr / rank-1 doubling: w_{j-1}[i] is the row's first gather (the prepped diagonal entry)
-    constexpr bool OWN_GATHER = DBL && !OWN_SMEM && MODE != MODE_BTB;
+    constexpr bool OWN_GATHER = (DBL && !OWN_SMEM && MODE != MODE_BTB) || MODE == MODE_FAM;
     constexpr bool OWN_EARLY = DBL && !OWN_SMEM && !OWN_GATHER;  // loaded at the row start
     static_assert(VB == 0 || (MODE != MODE_BTB && !CG && (VB != 1 || !OWN_SMEM)),
                   "sign-bit probes: per-step csr/rank-1");
@@ -690,6 +718,18 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                 g[sl].y = fma(-a.beta, own[sl].y, g[sl].y);
             }
         }
+        if (MODE == MODE_FAM) {
+            // member of column p: (alpha_p d_i - beta_p) w_{j-1}[i] + alpha_p theta_p (O w_{j-1})_i
+            const double di = u_s[lr];
+#pragma unroll
+            for (int sl = 0; sl < NSL; sl++) {
+                const double2 ca = *reinterpret_cast<const double2*>(fcoef + pp[sl]);
+                const double2 cb = *reinterpret_cast<const double2*>(fcoef + K + pp[sl]);
+                const double2 cc = *reinterpret_cast<const double2*>(fcoef + 2 * K + pp[sl]);
+                g[sl].x = fma(fma(ca.x, di, -cb.x), own[sl].x, cc.x * g[sl].x);
+                g[sl].y = fma(fma(ca.y, di, -cb.y), own[sl].y, cc.y * g[sl].y);
+            }
+        }
         double ui = 1.0;
         if (HAS_S) {
             ui = a.r1u ? u_s[lr] : 1.0;
@@ -774,6 +814,9 @@ cheb_step_kernel(StepArgs a) {
     __shared__ __align__(16) int64_t s_ne[2];  // row bounds of the next tile to stage (cp.async)
 
     const int tid = threadIdx.x;
+    __shared__ __align__(16) double s_fcoef[MODE == MODE_FAM ? 3 * K : 2];  // family: alpha, beta, alpha*theta
+    if (MODE == MODE_FAM)
+        for (int x = tid; x < 3 * K; x += kThreads) s_fcoef[x] = a.fam_coef[x];
     double acc[NCH][kPPL];
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++)
@@ -806,7 +849,7 @@ cheb_step_kernel(StepArgs a) {
         if (SL::HAS_WC) bytes += wbytes;
         if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
         const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
-        if (HAS_S && a.r1u) bytes += ubytes;
+        if ((HAS_S || MODE == MODE_FAM) && a.r1u) bytes += ubytes;
         mbar_expect_tx(&bar[b], bytes);
         bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
         if (SIGNS) bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
@@ -817,7 +860,7 @@ cheb_step_kernel(StepArgs a) {
             bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
             bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
         }
-        if (HAS_S && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
+        if ((HAS_S || MODE == MODE_FAM) && a.r1u) bulk_g2s(st + SL::OFF_U, a.r1u + r0, ubytes, &bar[b]);
     };
     auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
     auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
@@ -857,10 +900,10 @@ cheb_step_kernel(StepArgs a) {
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
         if (s_fit[b])
             step_tile<K, MODE, FIRST, true, false, DBL, WCS, R4, VB>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
-                                                               acc, a.xg, a.wcur, a.wnext);
+                                                               acc, a.xg, a.wcur, a.wnext, s_fcoef);
         else
             step_tile<K, MODE, FIRST, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
-                                                                a.wnext);
+                                                                a.wnext, s_fcoef);
         __syncthreads();  // every warp is done with stage b
         if (tid == 0 && it + NS < nmine) {
             cp_async_wait_all();
@@ -1359,32 +1402,43 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
 // Quadratic form x^T A x for the GMRF likelihood scan: per-CTA partials
 // (grid-stride rows, warp xor-butterfly, warps in order) then quadform_final_kernel sums
 // the partials in CTA order -- deterministic.
+// SPLIT: two sums, x^T D x (diagonal entries) and x^T O x (off-diagonal entries) -- the family
+// M(theta) = D + theta O of the likelihood scan needs x^T M(theta) x = x^T D x + theta x^T O x.
+template <bool SPLIT>
 __global__ void __launch_bounds__(kThreads)
 quadform_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                 const double* __restrict__ va, const double* __restrict__ x, double* __restrict__ part) {
-    __shared__ double wsum[kThreads / 32];
-    double acc = 0.0;
+    constexpr int NO = SPLIT ? 2 : 1;
+    __shared__ double wsum[NO][kThreads / 32];
+    double acc[NO] = {};
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double r = 0.0;
-        for (int64_t e = rp[i]; e < rp[i + 1]; e++) r = fma(va[e], x[ci[e]], r);
-        acc = fma(x[i], r, acc);
+        double r[NO] = {};
+        for (int64_t e = rp[i]; e < rp[i + 1]; e++) {
+            const int k = SPLIT && ci[e] != i ? 1 : 0;
+            r[k] = fma(va[e], x[ci[e]], r[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < NO; k++) acc[k] = fma(x[i], r[k], acc[k]);
     }
-    acc = warp_sum_xor(acc);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+#pragma unroll
+    for (int k = 0; k < NO; k++) {
+        acc[k] = warp_sum_xor(acc[k]);
+        if ((threadIdx.x & 31) == 0) wsum[k][threadIdx.x >> 5] = acc[k];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < NO) {
         double t = 0.0;
-        for (int w = 0; w < kThreads / 32; w++) t += wsum[w];
-        part[blockIdx.x] = t;
+        for (int w = 0; w < kThreads / 32; w++) t += wsum[threadIdx.x][w];
+        part[(size_t)blockIdx.x * NO + threadIdx.x] = t;
     }
 }
-
-__global__ void quadform_final_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
+// sums the per-CTA partials in CTA order: out[k] = sum_c part[c * nout + k]
+__global__ void quadform_final_kernel(const double* __restrict__ part, int n, int nout, double* __restrict__ out) {
+    if (blockIdx.x == 0 && threadIdx.x < nout) {
         double t = 0.0;
-        for (int c = 0; c < n; c++) t += part[c];
-        *out = t;
+        for (int c = 0; c < n; c++) t += part[(size_t)c * nout + threadIdx.x];
+        out[threadIdx.x] = t;
     }
 }
 
@@ -1393,15 +1447,17 @@ __global__ void quadform_final_kernel(const double* __restrict__ part, int n, do
 // out[2] <- min_i (a_ii - sum_{j != i} |a_ij|) (Gershgorin lower end; ordered-key min).
 __global__ void __launch_bounds__(kThreads)
 gershgorin_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                  const double* __restrict__ va, const double* __restrict__ u, unsigned long long* out) {
+                  const double* __restrict__ va, const double* __restrict__ u, unsigned long long* out,
+                  double off_scale = 1.0) {  // off_scale: |theta| of a family member D + theta O
     double rmax = 0.0, umax = 0.0, lmin = INFINITY;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
          i += (int64_t)gridDim.x * blockDim.x) {
         double r = 0.0, off = 0.0, dg = 0.0;
         for (int64_t e = rp[i]; e < rp[i + 1]; e++) {
-            const double x = fabs(va[e]);
+            const bool diag = ci[e] == i;
+            const double x = diag ? fabs(va[e]) : off_scale * fabs(va[e]);
             r += x;
-            if (ci[e] == i) dg = va[e]; else off += x;
+            if (diag) dg = va[e]; else off += x;
         }
         rmax = fmax(rmax, r);
         lmin = fmin(lmin, dg - off);

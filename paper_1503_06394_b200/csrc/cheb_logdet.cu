@@ -151,7 +151,7 @@ int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL))
 
 struct Layout {
     size_t misc, w0, w1, y, sbits, part, gpart, sbuf, ticket;
-    size_t rp2, ci2, va2, u2, cnt64, scan, total;
+    size_t rp2, ci2, va2, u2, fcoef, cnt64, scan, total;
     size_t scan_bytes;
     int64_t rp2_len;
 };
@@ -191,7 +191,8 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     L.scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, L.scan_bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(d + 1));
     L.scan = off; off += align256(L.scan_bytes);
-    L.u2 = off; if (kind == CL_OP_CSR_RANK1) off += align256(((size_t)d + 2) * sizeof(double));
+    L.u2 = off; if (kind == CL_OP_CSR_RANK1 || kind == CL_OP_FAMILY) off += align256(((size_t)d + 2) * sizeof(double));
+    L.fcoef = off; if (kind == CL_OP_FAMILY) off += align256(3 * (size_t)k * sizeof(double));
     L.total = off;
     return L;
 }
@@ -210,7 +211,7 @@ int check_csr(const cl_csr& A, const char* name) {
 
 int check_op(const cl_operator* op) {
     if (!op) return fail(CL_EINVAL, "operator is NULL");
-    if (op->kind != CL_OP_CSR && op->kind != CL_OP_CSR_RANK1 && op->kind != CL_OP_BTB)
+    if (op->kind != CL_OP_CSR && op->kind != CL_OP_CSR_RANK1 && op->kind != CL_OP_BTB && op->kind != CL_OP_FAMILY)
         return fail(CL_EINVAL, "unknown operator kind %d", op->kind);
     int rc = check_csr(op->A, "A");
     if (rc) return rc;
@@ -292,7 +293,8 @@ void run_prep(const cl_operator* op, double alpha, double beta, char* ws, const 
     prep_kernel<MODE><<<grid, kThreads, 0, st>>>(
         d, G2.row_ptr, G2.col_idx, G2.val, alpha, beta, (int64_t*)(ws + L.rp2), L.rp2_len,
         (int32_t*)(ws + L.ci2), (double*)(ws + L.va2),
-        MODE == MODE_RANK1 ? op->r1_u : nullptr, MODE == MODE_RANK1 ? (double*)(ws + L.u2) : nullptr);
+        MODE == MODE_RANK1 ? op->r1_u : nullptr,
+        MODE == MODE_RANK1 || MODE == MODE_FAM ? (double*)(ws + L.u2) : nullptr);
     g_launches++;
 }
 
@@ -304,6 +306,8 @@ struct Schedule {
     bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
     bool small = false;       // 16-row tiles for the Algorithm-1 kernels (RP = 1)
     bool l2res = false;       // csr / rank-1 working set within half of L2 (persistent schedule's home)
+    int fam_kp = 0, fam_r = 0;  // family: probes per member per block, members with output rows
+    int64_t fam_rstride = 0;    // family: doubles between consecutive members' mu rows
 };
 
 // Launch of one step-kernel variant.  The dynamic shared-memory opt-in is a per-device,
@@ -391,7 +395,11 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.sbits = sbits;
     a.beta = beta;
     a.r1c_alpha = alpha * op->r1_c;
-    a.r1u = (MODE == MODE_RANK1 && op->r1_u) ? (const double*)(ws + L.u2) : nullptr;
+    a.r1u = ((MODE == MODE_RANK1 && op->r1_u) || MODE == MODE_FAM) ? (const double*)(ws + L.u2) : nullptr;
+    a.fam_kp = MODE == MODE_FAM ? fp.fam_kp : 0;
+    a.fam_r = fp.fam_r;
+    a.fam_rstride = fp.fam_rstride;
+    a.fam_coef = MODE == MODE_FAM ? (const double*)(ws + L.fcoef) : nullptr;
     a.part = (double*)(ws + L.part);
     a.gpart = (double*)(ws + L.gpart);
     a.ticket = (unsigned int*)(ws + L.ticket);
@@ -422,15 +430,20 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     const size_t smem_step = std::max<size_t>(
         (size_t)kStepStages * (fp.doubling ? StageLayout<K, MODE, CHEB_DBL_STAGE_WC, R4D>::BYTES : SL::BYTES),
         red_scratch_bytes<K, 3>());  // cheb_step_kernel
-    int grid_first = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, true, true, 0, RP>, a.ntiles, sms, smem_step)
-                                 : grid_for(cheb_step_kernel<K, MODE, true, false, 0, RP>, a.ntiles, sms, smem_step);
-    int grid_step = fp.doubling ? grid_for(cheb_step_kernel<K, MODE, false, true, 0, RP>, a.ntiles, sms, smem_step)
-                                : grid_for(cheb_step_kernel<K, MODE, false, false, 0, RP>, a.ntiles, sms, smem_step);
+    constexpr bool CAN_DBL = MODE != MODE_FAM;  // the family mode runs Algorithm 1 only
+    int grid_first = grid_for(cheb_step_kernel<K, MODE, true, false, 0, RP>, a.ntiles, sms, smem_step);
+    int grid_step = grid_for(cheb_step_kernel<K, MODE, false, false, 0, RP>, a.ntiles, sms, smem_step);
+    if constexpr (CAN_DBL) {
+        if (fp.doubling) {
+            grid_first = grid_for(cheb_step_kernel<K, MODE, true, true, 0, RP>, a.ntiles, sms, smem_step);
+            grid_step = grid_for(cheb_step_kernel<K, MODE, false, true, 0, RP>, a.ntiles, sms, smem_step);
+        }
+    }
     // L2-resident csr / rank-1 operators: the persistent schedule's grid and reduction groups
     // (clusters) are used by the per-step launches too, so both schedules reduce identically
     int grid_p = 0;
     a.rg = 0;  // default reduction groups (red_group(G))
-    if (MODE != MODE_BTB && (fp.persistent || fp.l2res)) {
+    if constexpr (MODE == MODE_CSR || MODE == MODE_RANK1) if (fp.persistent || fp.l2res) {
         auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true, RP> : cheb_persist_kernel<K, MODE, false, RP>;
         int rg = 1;
         if ((rc_persist = persist_grid(pkern, a.ntiles, sms, smem, &grid_p, &rg))) return rc_persist;
@@ -446,7 +459,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     // moment doubling (reading G25): steps j = 1..ceil(n/2); the epilogue of step j writes
     // mu_{2j-1} and mu_{2j} (indices <= n) from w_j^T w_{j-1} and w_j^T w_j
     const int32_t nsteps = fp.doubling ? (n + 1) / 2 : n;
-    if (MODE != MODE_BTB && fp.persistent) {
+    if constexpr (MODE == MODE_CSR || MODE == MODE_RANK1) if (fp.persistent) {
         auto pkern = fp.doubling ? cheb_persist_kernel<K, MODE, true, RP> : cheb_persist_kernel<K, MODE, false, RP>;
         PersistArgs pp{};
         pp.w0 = w[0];
@@ -490,14 +503,20 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         // same grids as the plain kernels, so the moments are bit-identical either way
         constexpr int V1 = MODE != MODE_BTB ? 1 : 0, V2 = MODE != MODE_BTB ? 2 : 0;
         const bool vb1 = fp.vbits && j == 1, vb2 = fp.vbits && j == 2 && !fp.power;
-        if (fp.doubling) {
-            if (j == 1) {
-                if (vb1) launch_step<K, MODE, true, true, V1, RP>(grid_first, smem_step, st, a);
-                else launch_step<K, MODE, true, true, 0, RP>(grid_first, smem_step, st, a);
-            } else {
-                if (vb2) launch_step<K, MODE, false, true, V2, RP>(grid_step, smem_step, st, a);
-                else launch_step<K, MODE, false, true, 0, RP>(grid_step, smem_step, st, a);
+        bool done = false;
+        if constexpr (CAN_DBL) {
+            if (fp.doubling) {
+                if (j == 1) {
+                    if (vb1) launch_step<K, MODE, true, true, V1, RP>(grid_first, smem_step, st, a);
+                    else launch_step<K, MODE, true, true, 0, RP>(grid_first, smem_step, st, a);
+                } else {
+                    if (vb2) launch_step<K, MODE, false, true, V2, RP>(grid_step, smem_step, st, a);
+                    else launch_step<K, MODE, false, true, 0, RP>(grid_step, smem_step, st, a);
+                }
+                done = true;
             }
+        }
+        if (done) {
         } else if (j == 1 || fp.power) {  // power basis: w_j = Ã w_{j-1} (no w_{j-2} term), ping-pong
             if (vb1) launch_step<K, MODE, true, false, V1, RP>(grid_first, smem_step, st, a);
             else launch_step<K, MODE, true, false, 0, RP>(grid_first, smem_step, st, a);
@@ -521,6 +540,12 @@ int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, 
         case CL_OP_CSR_RANK1:
             if (fp.small) return run_block<K, MODE_RANK1, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
             return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+        case CL_OP_FAMILY:
+            if constexpr (K >= 16) {  // >= 2 probes per member of an 8-member block
+                if (fp.small) return run_block<K, MODE_FAM, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+                return run_block<K, MODE_FAM>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+            }
+            return fail(CL_EINVAL, "family moments need probe_block >= 16");
         default:
             return run_block<K, MODE_BTB>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
     }
@@ -531,6 +556,7 @@ void prep_mode(const cl_operator* op, double alpha, double beta, char* ws, const
     switch (op->kind) {
         case CL_OP_CSR: run_prep<MODE_CSR>(op, alpha, beta, ws, L, st, sms); break;
         case CL_OP_CSR_RANK1: run_prep<MODE_RANK1>(op, alpha, beta, ws, L, st, sms); break;
+        case CL_OP_FAMILY: run_prep<MODE_FAM>(op, alpha, beta, ws, L, st, sms); break;
         default: run_prep<MODE_BTB>(op, alpha, beta, ws, L, st, sms); break;
     }
 }
@@ -721,6 +747,7 @@ double unkey(unsigned long long k) {
 int cheb_norm_bound(const cl_operator* op, double* s_out, void* stream) {
     int rc;
     if ((rc = check_op(op))) return rc;
+    if (op->kind == CL_OP_FAMILY) return fail(CL_EINVAL, "family operators: use cheb_family_moments");
     if (!s_out) return fail(CL_EINVAL, "s_out is NULL");
     if (op->kind == CL_OP_BTB) {
         double ab[2];
@@ -792,23 +819,146 @@ int cheb_gershgorin(const cl_csr* A, double* lo_hi, void* stream) {
     return CL_OK;
 }
 
-int cheb_quadform(const cl_csr* A, const double* x, double* out, void* stream) {
+namespace {
+int quadform_impl(const cl_csr* A, const double* x, double* out, bool split, void* stream) {
     int rc;
     if (!A || !x || !out) return fail(CL_EINVAL, "NULL pointer");
     if ((rc = check_csr(*A, "A"))) return rc;
     if (A->n_rows != A->n_cols || A->n_rows < 1) return fail(CL_EDIM, "A must be square and non-empty");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t d = A->n_rows;
+    const int nout = split ? 2 : 1;
     const int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
     DevBuf buf;
-    CL_CUDA(cudaMalloc(&buf.p, sizeof(double) * (grid + 1)));
+    CL_CUDA(cudaMalloc(&buf.p, sizeof(double) * ((size_t)grid * nout + nout)));
     double* part = (double*)buf.p;
-    quadform_kernel<<<grid, kThreads, 0, st>>>(d, A->row_ptr, A->col_idx, A->val, x, part);
-    quadform_final_kernel<<<1, 32, 0, st>>>(part, grid, part + grid);
+    if (split) quadform_kernel<true><<<grid, kThreads, 0, st>>>(d, A->row_ptr, A->col_idx, A->val, x, part);
+    else quadform_kernel<false><<<grid, kThreads, 0, st>>>(d, A->row_ptr, A->col_idx, A->val, x, part);
+    quadform_final_kernel<<<1, 32, 0, st>>>(part, grid, nout, part + (size_t)grid * nout);
     g_launches += 2;
     CL_CUDA(cudaGetLastError());
-    CL_CUDA(cudaMemcpyAsync(out, part + grid, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaMemcpyAsync(out, part + (size_t)grid * nout, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
     CL_CUDA(cudaStreamSynchronize(st));
+    return CL_OK;
+}
+}  // namespace
+
+int cheb_quadform(const cl_csr* A, const double* x, double* out, void* stream) {
+    return quadform_impl(A, x, out, false, stream);
+}
+
+int cheb_quadform_split(const cl_csr* A, const double* x, double* out2, void* stream) {
+    return quadform_impl(A, x, out2, true, stream);
+}
+
+int cheb_family_gershgorin(const cl_csr* base, int32_t R, const double* theta, double* lo_hi, void* stream) {
+    int rc;
+    if (!base || !theta || !lo_hi) return fail(CL_EINVAL, "NULL pointer");
+    if ((rc = check_csr(*base, "base"))) return rc;
+    if (base->n_rows != base->n_cols || base->n_rows < 1) return fail(CL_EDIM, "base must be square and non-empty");
+    if (R < 1) return fail(CL_EINVAL, "R < 1");
+    for (int r = 0; r < R; r++)
+        if (!std::isfinite(theta[r])) return fail(CL_EINVAL, "theta[%d] not finite", r);
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf buf;
+    CL_CUDA(cudaMalloc(&buf.p, 3 * sizeof(unsigned long long) * R));
+    std::vector<unsigned long long> init(3 * (size_t)R);
+    for (int r = 0; r < R; r++) {
+        init[3 * r] = 0ull;
+        init[3 * r + 1] = 0ull;
+        init[3 * r + 2] = ~0ull;
+    }
+    CL_CUDA(cudaMemcpyAsync(buf.p, init.data(), sizeof(unsigned long long) * init.size(), cudaMemcpyHostToDevice, st));
+    const int64_t d = base->n_rows;
+    const int grid = (int)std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    for (int r = 0; r < R; r++)
+        gershgorin_kernel<<<grid, kThreads, 0, st>>>(d, base->row_ptr, base->col_idx, base->val, nullptr,
+                                                      (unsigned long long*)buf.p + 3 * r, std::fabs(theta[r]));
+    g_launches += R;
+    CL_CUDA(cudaGetLastError());
+    CL_CUDA(cudaMemcpyAsync(init.data(), buf.p, sizeof(unsigned long long) * init.size(), cudaMemcpyDeviceToHost, st));
+    CL_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < R; r++) {
+        lo_hi[2 * r] = unkey(init[3 * r + 2]);
+        lo_hi[2 * r + 1] = unkey(init[3 * r]);
+    }
+    return CL_OK;
+}
+
+int cheb_family_moments(const cl_csr* base, int32_t R, const double* theta, const double* ab, int32_t degree,
+                        int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
+                        void* workspace, size_t ws_bytes, double* mu_out, void* stream) {
+    int rc;
+    if (!base || !theta || !ab) return fail(CL_EINVAL, "NULL pointer");
+    cl_operator fop{};
+    fop.kind = CL_OP_FAMILY;
+    fop.A = *base;
+    if ((rc = check_op(&fop))) return rc;
+    if (R < 1) return fail(CL_EINVAL, "R < 1");
+    for (int r = 0; r < R; r++) {
+        if (!std::isfinite(theta[r])) return fail(CL_EINVAL, "theta[%d] not finite", r);
+        if ((rc = check_ab(ab[2 * r], ab[2 * r + 1], degree))) return rc;
+    }
+    if (probe_begin < 0 || probe_end <= probe_begin) return fail(CL_EINVAL, "need 0 <= probe_begin < probe_end");
+    if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32, 64 or 128");
+    int rpad = 1;
+    while (rpad < R) rpad *= 2;
+    const int kp = probe_block / rpad;
+    if (kp < 2) return fail(CL_EINVAL, "probe_block %d too small for %d family members (need >= 2 probes each)",
+                            probe_block, R);
+    if (!workspace || !mu_out) return fail(CL_EINVAL, "NULL workspace or mu_out");
+    const int sms = sm_count();
+    const Layout L = plan(base->n_cols, base->nnz, probe_block, CL_OP_FAMILY, sms);
+    if (ws_bytes < L.total) return fail(CL_ENOMEM, "workspace too small: %zu < %zu", ws_bytes, L.total);
+    if ((uintptr_t)workspace & 255) return fail(CL_EINVAL, "workspace must be 256-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    const int64_t stride = (int64_t)degree + 1, mrows = probe_end - probe_begin;
+    CL_CUDA(cudaGetLastError());
+    CL_CUDA(cudaMemsetAsync(ws + L.ticket, 0, 256, st));
+    CL_CUDA(cudaMemsetAsync(ws + L.misc, 0, 256, st));
+    prep_mode(&fop, 0.0, 0.0, ws, L, st, sms);
+    // per column c: member r = c / kp (padding columns repeat the last member), its map of
+    // [a_r, b_r] onto [-1, 1] and theta_r
+    std::vector<double> coef(3 * (size_t)probe_block);
+    for (int c = 0; c < probe_block; c++) {
+        const int r = std::min(c / kp, R - 1);
+        const double a = ab[2 * r], b = ab[2 * r + 1];
+        const double alpha = 2.0 / (b - a), beta = (b + a) / (b - a);
+        coef[c] = alpha;
+        coef[probe_block + c] = beta;
+        coef[2 * probe_block + c] = alpha * theta[r];
+    }
+    CL_CUDA(cudaMemcpyAsync(ws + L.fcoef, coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice, st));
+    Schedule fp;
+    int l2 = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const double wset = 2.0 * base->n_cols * probe_block * 8.0 + 12.0 * base->nnz + 8.0 * base->n_cols;
+    fp.small = g_small_tiles.load() != 0 && (wset <= 0.5 * (double)l2 || probe_block <= 16);
+    fp.vbits = env_int("CHEB_VBITS", 1) != 0;
+    fp.fam_kp = kp;
+    fp.fam_r = R;
+    fp.fam_rstride = mrows * stride;
+    for (int64_t p0 = probe_begin; p0 < probe_end; p0 += kp) {
+        const int kvalid = (int)std::min<int64_t>(kp, probe_end - p0);
+        double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
+        switch (probe_block) {
+            case 16: rc = run_block_mode<16>(&fop, 0.0, 0.0, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 32: rc = run_block_mode<32>(&fop, 0.0, 0.0, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 64: rc = run_block_mode<64>(&fop, 0.0, 0.0, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 128: rc = run_block_mode<128>(&fop, 0.0, 0.0, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            default: rc = fail(CL_EINVAL, "family moments need probe_block >= 16"); break;
+        }
+        if (rc) return rc;
+    }
+    {
+        const int64_t nmu = (int64_t)R * mrows * stride;
+        const int grid = (int)std::min<int64_t>((nmu + kThreads - 1) / kThreads, 64);
+        moments_status_kernel<<<grid, kThreads, 0, st>>>((unsigned int*)(ws + L.misc + kStatusOff), mu_out, nmu);
+        g_launches++;
+    }
+    CL_CUDA(cudaGetLastError());
     return CL_OK;
 }
 
@@ -825,6 +975,7 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
                  int64_t probe_begin, int64_t probe_end, uint64_t seed, int32_t probe_block,
                  void* workspace, size_t ws_bytes, double* mu_out, void* stream) {
     int rc;
+    if (op->kind == CL_OP_FAMILY) return fail(CL_EINVAL, "family operators: use cheb_family_moments");
     if (probe_begin < 0 || probe_end <= probe_begin)
         return fail(CL_EINVAL, "need 0 <= probe_begin < probe_end");
     if (!valid_k(probe_block)) return fail(CL_EINVAL, "probe_block must be 8, 16, 32, 64 or 128");
@@ -965,6 +1116,7 @@ int cheb_logdet(const cl_operator* op, double a, double b, int32_t degree, int32
     auto t0 = std::chrono::steady_clock::now();
     int rc;
     if ((rc = check_op(op))) return rc;
+    if (op->kind == CL_OP_FAMILY) return fail(CL_EINVAL, "family operators: use cheb_family_moments");
     if ((rc = check_ab(a, b, degree))) return rc;
     if (num_probes < 1) return fail(CL_EINVAL, "num_probes < 1");
     if (!out) return fail(CL_EINVAL, "out is NULL");
@@ -1019,6 +1171,7 @@ int cheb_logdet_host(const cl_operator* op, double a, double b, int32_t degree, 
     auto t0 = std::chrono::steady_clock::now();
     int rc;
     if ((rc = check_op(op))) return rc;
+    if (op->kind == CL_OP_FAMILY) return fail(CL_EINVAL, "family operators: use cheb_family_moments");
     if ((rc = check_ab(a, b, degree))) return rc;
     if (num_probes < 1) return fail(CL_EINVAL, "num_probes < 1");
     if (!out) return fail(CL_EINVAL, "out is NULL");
@@ -1222,6 +1375,7 @@ int cheb_spectrum_bounds(const cl_operator* op, int32_t lanczos_steps, int32_t n
                          cl_spectrum* out, double* jacobi_out) {
     int rc;
     if ((rc = check_op(op))) return rc;
+    if (op->kind == CL_OP_FAMILY) return fail(CL_EINVAL, "family operators: not supported here");
     if (!out) return fail(CL_EINVAL, "out is NULL");
     if (lanczos_steps < 1 || lanczos_steps > 2000) return fail(CL_EINVAL, "lanczos_steps must be in [1, 2000]");
     if (num_probes < 1 || num_probes > 4096) return fail(CL_EINVAL, "num_probes must be in [1, 4096]");

@@ -1,16 +1,18 @@
 """GMRF log-likelihood scan (§5.2).
 
-For the precision family J(theta) = D + theta*O (the grid GMRF: D = I, O = -Adj) and an
-observed field x, the Gaussian log-likelihood is
+For the precision family J(theta) = D + theta*O (the grid GMRF: D = I, O = -Adj) and observed
+fields x_s, the Gaussian log-likelihood is
 
     log p(x | theta) = 1/2 log det J(theta) - 1/2 x^T J(theta) x - d/2 log(2 pi)
 
-(the paper's display, lacks the 1/2 factors -- reading G16).  Each log det is a
-Chebyshev-Hutchinson estimate on the device; every theta uses the SAME probes (same seed:
-common random numbers), so differences across theta carry little Monte-Carlo noise.
-Every arithmetic step runs in libchebld.so kernels: J(theta)'s values are built on the
-device from the base pattern (input construction), the interval comes from the device
-Gershgorin kernel, x^T J x from cheb_quadform.
+(the paper's display, lacks the 1/2 factors -- reading G16).  All values of theta are
+estimated in ONE batched pass (cheb_family_moments): the R members ride in the columns of every
+probe block, so each pass over the matrix serves all of them, and every member sees the SAME probes
+(common random numbers), so differences across theta carry little Monte-Carlo noise.  The
+intervals come from the device Gershgorin kernel (cheb_family_gershgorin), x^T J x = x^T D x +
+theta x^T O x from cheb_quadform_split, the Chebyshev coefficients per member from cheb_coeffs_log,
+Gamma_r from cheb_finalize.  The only arithmetic here is the log-likelihood formula above (finishing
+scalars, like a7).
 """
 import ctypes
 import math
@@ -22,7 +24,7 @@ import torch
 
 from . import _lib
 from ._lib import check
-from .api import DeviceCSR, Estimator, Operator, _stream_ptr
+from .api import DeviceCSR, Operator, _stream_ptr, alloc_workspace, coeffs_log, finalize, check_estimate
 
 
 def quadform(A: DeviceCSR, x: torch.Tensor) -> float:
@@ -34,6 +36,17 @@ def quadform(A: DeviceCSR, x: torch.Tensor) -> float:
     check(_lib.load().cheb_quadform(ctypes.byref(s), x.contiguous().data_ptr(), ctypes.byref(out),
                                     _stream_ptr()))
     return out.value
+
+
+def quadform_split(A: DeviceCSR, x: torch.Tensor):
+    """(x^T D x, x^T O x) for A = D + O on the device (cheb_quadform_split)."""
+    if x.dtype != torch.float64 or not x.is_cuda or x.numel() != A.n_rows:
+        raise TypeError("x must be a CUDA float64 vector of length d")
+    out = np.empty(2)
+    s = A.struct()
+    check(_lib.load().cheb_quadform_split(ctypes.byref(s), x.contiguous().data_ptr(), out.ctypes.data,
+                                          _stream_ptr()))
+    return float(out[0]), float(out[1])
 
 
 def gershgorin(A: DeviceCSR):
@@ -55,8 +68,36 @@ class PrecisionFamily:
         self.is_diag = rows == base.col_idx.to(torch.int64)
 
     def at(self, theta: float) -> DeviceCSR:
+        """One member as its own CSR (input construction; the scan itself never builds one)."""
         val = torch.where(self.is_diag, self.base.val, self.base.val * theta)
         return DeviceCSR(self.base.n_rows, self.base.n_cols, self.base.row_ptr, self.base.col_idx, val)
+
+    def gershgorin(self, thetas: Sequence[float]) -> np.ndarray:
+        """[R][2] Gershgorin intervals of the members (cheb_family_gershgorin)."""
+        th = np.ascontiguousarray(thetas, dtype=np.float64)
+        lh = np.empty((th.size, 2))
+        s = self.base.struct()
+        check(_lib.load().cheb_family_gershgorin(ctypes.byref(s), int(th.size), th.ctypes.data, lh.ctypes.data,
+                                                 _stream_ptr()))
+        return lh
+
+    def moments(self, thetas: Sequence[float], intervals: np.ndarray, degree: int, probe_begin: int,
+                probe_end: int, seed: int, k: int, workspace=None, stream=None) -> torch.Tensor:
+        """mu[r][p - probe_begin][j] = v_p^T T_j(Ã_r) v_p for every member in one batched pass
+        (cheb_family_moments); asynchronous."""
+        th = np.ascontiguousarray(thetas, dtype=np.float64)
+        ab = np.ascontiguousarray(intervals, dtype=np.float64).reshape(th.size, 2)
+        R = th.size
+        mu = torch.empty((R, probe_end - probe_begin, degree + 1), dtype=torch.float64, device=self.base.val.device)
+        if workspace is None:
+            workspace = alloc_workspace(Operator("family", self.base), k)
+        s = self.base.struct()
+        check(_lib.load().cheb_family_moments(ctypes.byref(s), int(R), th.ctypes.data, ab.ctypes.data, int(degree),
+                                              int(probe_begin), int(probe_end), int(seed) & (2 ** 64 - 1), int(k),
+                                              workspace.data_ptr(), workspace.numel(), mu.data_ptr(),
+                                              _stream_ptr(stream)))
+        self._workspace = workspace
+        return mu
 
 
 @dataclass
@@ -73,25 +114,38 @@ class ScanResult:
         return float(self.thetas[int(np.argmax(self.loglik))])
 
 
+def scan_probe_block(R: int, num_probes: int) -> int:
+    """Probe block of the batched scan: R members (padded to a power of two) x up to 16 probes
+    each, at least 16 and at most 128 columns."""
+    rpad = 1 << max(0, (R - 1).bit_length())
+    if 2 * rpad > 128:
+        raise ValueError(f"at most 64 family members per scan (got {R})")
+    kp = min(max(2, 1 << max(0, (num_probes - 1).bit_length())), 16, 128 // rpad)
+    return max(16, rpad * kp)
+
+
 def likelihood_scan(family: PrecisionFamily, thetas: Sequence[float], xs: Sequence[torch.Tensor],
                     degree: int, num_probes: int, seed: int = 1, k: int = 0) -> ScanResult:
-    """Log-likelihood of the samples xs under J(theta) for every theta (common probes)."""
-    d = family.base.n_rows
-    k = k or next((kk for kk in (8, 16, 32, 64) if kk >= num_probes), 64)
-    R = len(xs)
+    """Log-likelihood of the samples xs under J(theta) for every theta: one batched estimate of all
+    log det J(theta) (common probes), device quadratic forms, device Gershgorin intervals."""
+    th = np.asarray(thetas, dtype=np.float64)
+    R, d, S = th.size, family.base.n_rows, len(xs)
+    k = k or scan_probe_block(R, num_probes)
+    lh = family.gershgorin(th)
+    if not np.all(lh[:, 0] > 0):
+        bad = th[~(lh[:, 0] > 0)]
+        raise ValueError(f"J(theta) not certified positive definite by Gershgorin for theta in {bad}")
+    mu = family.moments(th, lh, degree, 0, num_probes, seed, k)
     out = {"logdet": [], "stderr": [], "quad": [], "loglik": []}
-    for th in thetas:
-        J = family.at(float(th))
-        a, b = gershgorin(J)
-        if not a > 0:
-            raise ValueError(f"J({th}) not certified positive definite by Gershgorin (lo={a})")
-        est = Estimator(Operator("csr", J), a, b, degree, num_probes, k, seed)
-        _, stats = est.run(check=True)  # raises on a device timeout / non-finite estimate
+    qs = [quadform_split(family.base, x) for x in xs]
+    for r in range(R):
+        c = torch.from_numpy(coeffs_log(lh[r, 0], lh[r, 1], degree)).to(mu.device)
+        _, stats = finalize(mu[r].contiguous(), c)
+        check_estimate(stats, family._workspace if r == 0 else None)
         st = stats.cpu().numpy()
-        q = sum(quadform(J, x) for x in xs)
+        q = sum(qd + th[r] * qo for qd, qo in qs)
         out["logdet"].append(st[0])
         out["stderr"].append(st[1])
         out["quad"].append(q)
-        out["loglik"].append(0.5 * R * st[0] - 0.5 * q - 0.5 * R * d * math.log(2 * math.pi))
-    return ScanResult(np.asarray(thetas, dtype=float), *(np.array(out[k_]) for k_ in
-                                                          ("logdet", "stderr", "quad", "loglik")), R)
+        out["loglik"].append(0.5 * S * st[0] - 0.5 * q - 0.5 * S * d * math.log(2 * math.pi))
+    return ScanResult(th, *(np.array(out[k_]) for k_ in ("logdet", "stderr", "quad", "loglik")), S)

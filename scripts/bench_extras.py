@@ -2,7 +2,8 @@
 
   f1  paper §5.1 scaling sweep: Algorithm 2 (B^T B, m=10, n=15) on the paper's random SPD
       generator for d = 1e3 .. 3e7 (Fig. 1(a) analogue; the paper: 500 s at d = 3e7)
-  f2  GMRF rho-likelihood scan at 5000 x 5000 (BASELINE configs[3] matrix): 8 thetas x 64 probes
+  f2  GMRF rho-likelihood scan at 5000 x 5000 (BASELINE configs[3] matrix): 8 thetas x 64 probes,
+      batched (one pass serves all thetas) vs separate estimates
   f3  Taylor baseline on configs[3] (power recurrence on the same kernels)
   f4  spectral-bound estimate (block power iteration) on configs[3]
 
@@ -64,14 +65,26 @@ def _gmrf5000():
 
 
 def f2():
+    """5000 x 5000 GMRF likelihood scan, 8 thetas x 64 probes, n = 100: all members batched in the
+    columns of each probe block (cheb_family_moments, k = 128: 8 members x 16 probes), against the
+    same scan done as 8 separate estimates (k = 64) on one box."""
     import paper_1503_06394_b200.gmrf as G
     base = W.grid_gmrf(5000, 1.0)
     fam = G.PrecisionFamily(P.DeviceCSR.from_host(base))
     x = torch.randn(base.n_rows, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
     thetas = np.linspace(-0.24, -0.20, 8)
-    t = timed(lambda: G.likelihood_scan(fam, thetas, [x], 100, 64, seed=1), reps=1, warm=1)
+    t = timed(lambda: G.likelihood_scan(fam, thetas, [x], 100, 64, seed=1), reps=2, warm=1)
+    lh = fam.gershgorin(thetas)
+    ws = P.alloc_workspace(P.Operator("csr", fam.base), 64)
+
+    def separate():
+        for th, (lo, hi) in zip(thetas, lh):
+            P.moments(P.Operator("csr", fam.at(float(th))), lo, hi, 100, 0, 64, 1, 64, workspace=ws)
+    ts = timed(separate, reps=2, warm=1)
     print(json.dumps({"row": "f2", "what": "rho-likelihood scan, 5000x5000 GMRF, 8 thetas x 64 probes, n=100",
-                      "seconds": t, "probe_steps_per_s": 8 * 64 * 100 / t}), flush=True)
+                      "batched_seconds": t, "batched_probe_steps_per_s": 8 * 64 * 100 / t,
+                      "separate_estimates_seconds": ts, "separate_probe_steps_per_s": 8 * 64 * 100 / ts}),
+          flush=True)
 
 
 def f3():
@@ -90,14 +103,20 @@ def f3():
 
 
 def f4():
+    """Lanczos spectral interval of configs[3] (cheb_spectrum_bounds), and the estimate on it vs the
+    closed-form interval (same probes)."""
     wl, A = _gmrf5000()
     op = P.Operator("csr", P.DeviceCSR.from_host(A))
-    res = {}
-    t = timed(lambda: res.update(P.spectrum_estimate(op, iters=200, probes=8)), reps=1)
     lam_max = 1 + 4 * 0.24 * math.cos(math.pi / 5001)
-    print(json.dumps({"row": "f4", "what": "block power iteration bounds on configs[3], 200 iters x 8 probes",
-                      "seconds": t, **res, "closed_form_lambda_max": lam_max,
-                      "closed_form_lambda_min": 2 - lam_max}), flush=True)
+    for steps in (50, 100):
+        res = {}
+        t = timed(lambda: res.update(P.spectrum_bounds(op, steps, 8, seed=77)), reps=1)
+        ra = P.logdet(op, res["a"], res["b"], wl.degree, wl.num_probes, seed=wl.seed, k=64)
+        rc = P.logdet(op, wl.a, wl.b, wl.degree, wl.num_probes, seed=wl.seed, k=64)
+        print(json.dumps({"row": "f4", "what": f"Lanczos bounds on configs[3], {steps} steps x 8 probes",
+                          "seconds": t, **res, "closed_form_lambda_max": lam_max,
+                          "closed_form_lambda_min": 2 - lam_max, "gamma_on_lanczos_interval": ra.logdet,
+                          "gamma_on_closed_form_interval": rc.logdet, "stderr": rc.stderr}), flush=True)
 
 
 if __name__ == "__main__":

@@ -432,6 +432,37 @@ def test_quadform_and_gershgorin_parity(orc):
     assert abs(lo - (1 - 4 * 0.22)) < 1e-15 and abs(hi - (1 + 4 * 0.22)) < 1e-15
 
 
+def test_family_moments_batched_parity(orc):
+    """f2: R = 5 members J(theta) = I - theta Adj in the columns of one probe block (padded to 8
+    members, kp = 8 probes each at k = 64; 13 probes: a ragged second block), every member's moments
+    vs the oracle on its own matrix and interval; Gershgorin intervals of the family kernel vs the
+    closed form; common probes (member r's probe p is the oracle's probe p)."""
+    G, fam, base = _grid_family(37)
+    thetas = [-0.24, -0.1, 0.05, 0.2, 0.23]
+    lh = fam.gershgorin(thetas)
+    for (lo, hi), th in zip(lh, thetas):
+        assert abs(lo - (1 - 4 * abs(th))) < 1e-15 and abs(hi - (1 + 4 * abs(th))) < 1e-15
+    n, m, seed = 30, 13, 4
+    for k in (64, 128):
+        mu = fam.moments(thetas, lh, n, 0, m, seed, k).cpu().numpy()
+        assert mu.shape == (5, m, n + 1)
+        for r, th in enumerate(thetas):
+            A = W.grid_gmrf(37, th)
+            want = orc.moments(orc.Op("csr", A), lh[r, 0], lh[r, 1], n, seed, range(m), workers=4)
+            _check_moments(mu[r], want, A.n_rows)
+    with pytest.raises(P.ChebError):  # 5 members need k >= 16 (8 x 2 probes)
+        fam.moments(thetas, lh, n, 0, m, seed, 8)
+
+
+def test_quadform_split_parity(orc):
+    G, fam, base = _grid_family(29)
+    x = np.random.default_rng(5).standard_normal(base.n_rows)
+    qd, qo = G.quadform_split(fam.base, torch.from_numpy(x).cuda())
+    for th in (-0.2, 0.15):
+        oq = orc.quadform(W.grid_gmrf(29, th), x)
+        assert abs(qd + th * qo - oq) <= 1e-13 * abs(oq)
+
+
 def test_likelihood_scan_parity(orc):
     """Scan values vs the oracle's (same probes, same formula, P:670 with reading G16)."""
     import math
