@@ -63,6 +63,13 @@ constexpr int kThreads = 256;
 #ifndef CHEB_STAGES
 #define CHEB_STAGES 2  // shared-memory pipeline depth of cheb_step_kernel
 #endif
+#ifndef CHEB_DECOUPLE
+// per-stage "consumed" mbarriers instead of a CTA barrier after each tile of cheb_step_kernel:
+// 0 never, 1 always, 2 (default) on the small-tile geometry (RP = 1: k <= 16 and L2-resident
+// operators; configs[3] at k = 16: 1541 vs 1575 ms per estimate, at k = 64 with 32-row tiles
+// 1276 vs 1253 ms, so not there)
+#define CHEB_DECOUPLE 2
+#endif
 constexpr int kStepStages = CHEB_STAGES;
 #ifndef CHEB_NNZ_UNROLL
 #define CHEB_NNZ_UNROLL 5  // nnz of a row whose gathers are in flight together (5-point stencil: 1 chunk)
@@ -145,6 +152,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {  // release.cta
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -604,7 +614,8 @@ template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool DBL = 
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
                                           double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
-                                          const double* wcur, double* wout, const double* fcoef = nullptr) {
+                                          const double* wcur, double* wout,
+                                          const double2 (*fcoef)[kPPL / 2] = nullptr) {
     using G = Geo<K, R4>;
     using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr int NSL = G::NSL;
@@ -723,9 +734,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             const double di = u_s[lr];
 #pragma unroll
             for (int sl = 0; sl < NSL; sl++) {
-                const double2 ca = *reinterpret_cast<const double2*>(fcoef + pp[sl]);
-                const double2 cb = *reinterpret_cast<const double2*>(fcoef + K + pp[sl]);
-                const double2 cc = *reinterpret_cast<const double2*>(fcoef + 2 * K + pp[sl]);
+                const double2 ca = fcoef[0][sl], cb = fcoef[1][sl], cc = fcoef[2][sl];
                 g[sl].x = fma(fma(ca.x, di, -cb.x), own[sl].x, cc.x * g[sl].x);
                 g[sl].y = fma(fma(ca.y, di, -cb.y), own[sl].y, cc.y * g[sl].y);
             }
@@ -783,12 +792,15 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
 }
 
 // resident CTAs per SM each mode is register-budgeted for (BTB is smem-limited to 2)
+#ifndef CHEB_MIN_CTAS_FAM
+#define CHEB_MIN_CTAS_FAM 3  // family mode: the lane's per-column scalars live in registers
+#endif
 #ifndef CHEB_MIN_CTAS_R1
 #define CHEB_MIN_CTAS_R1 3  // rank-1 Algorithm 1 (two accumulator channels)
 #endif
 __host__ __device__ constexpr int min_ctas(int mode, bool dbl = false) {
     return mode == MODE_CSR ? (dbl ? CHEB_MIN_CTAS_DBL : CHEB_MIN_CTAS)
-                            : (mode == MODE_RANK1 && !dbl ? CHEB_MIN_CTAS_R1 : 2);
+                            : (mode == MODE_RANK1 && !dbl ? CHEB_MIN_CTAS_R1 : (mode == MODE_FAM ? CHEB_MIN_CTAS_FAM : 2));
 }
 
 // RP: rows per lane group of the Algorithm-1 kernels (0: CHEB_RPG).  L2-resident operators use
@@ -814,9 +826,16 @@ cheb_step_kernel(StepArgs a) {
     __shared__ __align__(16) int64_t s_ne[2];  // row bounds of the next tile to stage (cp.async)
 
     const int tid = threadIdx.x;
-    __shared__ __align__(16) double s_fcoef[MODE == MODE_FAM ? 3 * K : 2];  // family: alpha, beta, alpha*theta
-    if (MODE == MODE_FAM)
-        for (int x = tid; x < 3 * K; x += kThreads) s_fcoef[x] = a.fam_coef[x];
+    // family: the lane's columns' alpha, beta, alpha*theta, held in registers for the whole launch
+    double2 s_fcoef[3][kPPL / 2];
+#pragma unroll
+    for (int sl = 0; sl < kPPL / 2; sl++) {
+        const int p = 2 * (tid % G::L) + sl * G::SS;
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+            s_fcoef[q][sl] = MODE == MODE_FAM ? make_double2(a.fam_coef[q * K + p], a.fam_coef[q * K + p + 1])
+                                              : make_double2(0.0, 0.0);
+    }
     double acc[NCH][kPPL];
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++)
@@ -877,9 +896,16 @@ cheb_step_kernel(StepArgs a) {
         cp_async8(&s_ne[1], a.rp + imin64(r0 + G::TILE, a.d));
         cp_async_commit();
     };
+    // "stage consumed" barriers, one arrival per warp: warps are not held at a CTA-wide barrier
+    // after every tile, only thread 0 waits (for the stage it refills, one tile later)
+    constexpr bool DEC = CHEB_DECOUPLE == 1 || (CHEB_DECOUPLE == 2 && RP == 1);
+    __shared__ __align__(8) uint64_t ebar[NS];
     if (tid == 0) {
 #pragma unroll
-        for (int i = 0; i < NS; i++) mbar_init(&bar[i], 1);
+        for (int i = 0; i < NS; i++) {
+            mbar_init(&bar[i], 1);
+            if (DEC) mbar_init(&ebar[i], kThreads / 32);
+        }
         fence_mbar_init();
         for (int64_t i = 0; i < NS && i < nmine; i++) {
             int64_t e0, e1;
@@ -893,6 +919,12 @@ cheb_step_kernel(StepArgs a) {
         const int b = (int)(it % NS);
         const uint32_t phase = (uint32_t)((it / NS) & 1);
         const int64_t t = tile_of(it);
+        if (DEC && tid == 0 && it >= 1 && it - 1 + NS < nmine) {  // refill the stage of tile it-1 with it-1+NS
+            const int pb = (int)((it - 1) % NS);
+            mbar_wait(&ebar[pb], (uint32_t)(((it - 1) / NS) & 1));
+            cp_async_wait_all();
+            issue(tile_of(it - 1 + NS), pb, s_ne[0], s_ne[1]);
+        }
         if (tid == 0 && it + NS < nmine) bounds_async(tile_of(it + NS));  // consumed below
         mbar_wait(&bar[b], phase);
         const unsigned char* st = smem + b * SL::BYTES;
@@ -904,12 +936,18 @@ cheb_step_kernel(StepArgs a) {
         else
             step_tile<K, MODE, FIRST, false, false, DBL, WCS, R4, VB>(a, st, r0, rows, 0, 0, r1, acc, a.xg, a.wcur,
                                                                 a.wnext, s_fcoef);
-        __syncthreads();  // every warp is done with stage b
-        if (tid == 0 && it + NS < nmine) {
-            cp_async_wait_all();
-            issue(tile_of(it + NS), b, s_ne[0], s_ne[1]);
+        if (DEC) {
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&ebar[b]);  // this warp is done with stage b
+        } else {
+            __syncthreads();  // every warp is done with stage b
+            if (tid == 0 && it + NS < nmine) {
+                cp_async_wait_all();
+                issue(tile_of(it + NS), b, s_ne[0], s_ne[1]);
+            }
         }
     }
+    if (DEC) __syncthreads();  // the reduction scratch below aliases the stages
     grid_reduce_finish<K, kPPL, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, true>(acc, a, smem);
 }
 
@@ -1300,6 +1338,9 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             __syncthreads();
         }
     }
+    // no CTA leaves while a cluster peer may still read its shared memory (also after a timed-out
+    // grid wait, when the steps were no longer in lockstep)
+    cluster.sync();
 }
 
 // ---------------------------------------------------------------------------------------

@@ -116,11 +116,13 @@ class ScanResult:
 
 def scan_probe_block(R: int, num_probes: int) -> int:
     """Probe block of the batched scan: R members (padded to a power of two) x up to 16 probes
-    each, at least 16 and at most 128 columns."""
+    each, 16..64 columns (64-column blocks are the fastest step kernels on B200; 128 only when 33-64
+    members need 2 probes each)."""
     rpad = 1 << max(0, (R - 1).bit_length())
     if 2 * rpad > 128:
         raise ValueError(f"at most 64 family members per scan (got {R})")
-    kp = min(max(2, 1 << max(0, (num_probes - 1).bit_length())), 16, 128 // rpad)
+    cap = 64 if 2 * rpad <= 64 else 128
+    kp = min(max(2, 1 << max(0, (num_probes - 1).bit_length())), 16, cap // rpad)
     return max(16, rpad * kp)
 
 

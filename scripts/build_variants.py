@@ -11,6 +11,9 @@ VARIANTS = {
     "s3c3": ["CHEB_STAGES=3", "CHEB_MIN_CTAS=3"],
     "c3": ["CHEB_MIN_CTAS=3"],
     "r1c4": ["CHEB_MIN_CTAS_R1=4"],
+    "dec": ["CHEB_DECOUPLE=1"],
+    "fam4": ["CHEB_MIN_CTAS_FAM=4"],
+    "dec3": ["CHEB_DECOUPLE=1", "CHEB_STAGES=3"],
     "r1": ["CHEB_RPG=1"],
     "r4": ["CHEB_RPG=4"],
     "checked": ["CHEB_CHECKS=1"],
