@@ -71,6 +71,9 @@ constexpr int kThreads = 256;
 #define CHEB_DECOUPLE 2
 #endif
 constexpr int kStepStages = CHEB_STAGES;
+#ifndef CHEB_CAP_PER_ROW
+#define CHEB_CAP_PER_ROW 8  // staged nonzeros per tile row (average)
+#endif
 #ifndef CHEB_NNZ_UNROLL
 #define CHEB_NNZ_UNROLL 5  // nnz of a row whose gathers are in flight together (5-point stencil: 1 chunk)
 #endif
@@ -106,7 +109,8 @@ struct Geo {
     static_assert(RPG >= 1, "CHEB_RPG too small for CHEB_PPL");
     static constexpr int TILE = GROUPS * RPG;       // rows per tile: 256 .. 16
     static constexpr int WORDS = words_for(K);
-    static constexpr int CAP = TILE * 8;            // staged nnz capacity (avg 8 per row)
+    static constexpr int CAP = TILE * CHEB_CAP_PER_ROW;  // staged nnz capacity (rows of a tile with more
+                                                        // nnz in total gather col/val from global)
     static constexpr int RED_T = kThreads / K;      // threads per probe in the final reduction
     // shared-memory stage layout (bytes, every field 16-byte aligned)
     static constexpr int WBYTES = TILE * K * 8;     // 16 KB
@@ -614,8 +618,7 @@ template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool DBL = 
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
                                           double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
-                                          const double* wcur, double* wout,
-                                          const double2 (*fcoef)[kPPL / 2] = nullptr) {
+                                          const double* wcur, double* wout, const double* fcoef = nullptr) {
     using G = Geo<K, R4>;
     using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr int NSL = G::NSL;
@@ -734,7 +737,9 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             const double di = u_s[lr];
 #pragma unroll
             for (int sl = 0; sl < NSL; sl++) {
-                const double2 ca = fcoef[0][sl], cb = fcoef[1][sl], cc = fcoef[2][sl];
+                const double2 ca = *reinterpret_cast<const double2*>(fcoef + pp[sl]);
+                const double2 cb = *reinterpret_cast<const double2*>(fcoef + K + pp[sl]);
+                const double2 cc = *reinterpret_cast<const double2*>(fcoef + 2 * K + pp[sl]);
                 g[sl].x = fma(fma(ca.x, di, -cb.x), own[sl].x, cc.x * g[sl].x);
                 g[sl].y = fma(fma(ca.y, di, -cb.y), own[sl].y, cc.y * g[sl].y);
             }
@@ -793,7 +798,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
 
 // resident CTAs per SM each mode is register-budgeted for (BTB is smem-limited to 2)
 #ifndef CHEB_MIN_CTAS_FAM
-#define CHEB_MIN_CTAS_FAM 3  // family mode: the lane's per-column scalars live in registers
+#define CHEB_MIN_CTAS_FAM 4  // family mode (per-column scalars in shared memory)
 #endif
 #ifndef CHEB_MIN_CTAS_R1
 #define CHEB_MIN_CTAS_R1 3  // rank-1 Algorithm 1 (two accumulator channels)
@@ -826,16 +831,11 @@ cheb_step_kernel(StepArgs a) {
     __shared__ __align__(16) int64_t s_ne[2];  // row bounds of the next tile to stage (cp.async)
 
     const int tid = threadIdx.x;
-    // family: the lane's columns' alpha, beta, alpha*theta, held in registers for the whole launch
-    double2 s_fcoef[3][kPPL / 2];
-#pragma unroll
-    for (int sl = 0; sl < kPPL / 2; sl++) {
-        const int p = 2 * (tid % G::L) + sl * G::SS;
-#pragma unroll
-        for (int q = 0; q < 3; q++)
-            s_fcoef[q][sl] = MODE == MODE_FAM ? make_double2(a.fam_coef[q * K + p], a.fam_coef[q * K + p + 1])
-                                              : make_double2(0.0, 0.0);
-    }
+    // family: per column alpha, beta, alpha*theta in shared memory (registers measured slower:
+    // 3 CTAs/SM and spills, 7.0 vs 5.9 s for the configs[3]-size 8-member scan)
+    __shared__ __align__(16) double s_fcoef[MODE == MODE_FAM ? 3 * K : 2];
+    if (MODE == MODE_FAM)
+        for (int x = tid; x < 3 * K; x += kThreads) s_fcoef[x] = a.fam_coef[x];
     double acc[NCH][kPPL];
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++)

@@ -17,14 +17,14 @@ scalars, like a7).
 import ctypes
 import math
 from dataclasses import dataclass
-from typing import Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch
 
 from . import _lib
 from ._lib import check
-from .api import DeviceCSR, Operator, _stream_ptr, alloc_workspace, coeffs_log, finalize, check_estimate
+from .api import DeviceCSR, Operator, _stream_ptr, alloc_workspace, coeffs_log, finalize, check_estimate, moments, workspace_status
 
 
 def quadform(A: DeviceCSR, x: torch.Tensor) -> float:
@@ -127,17 +127,37 @@ def scan_probe_block(R: int, num_probes: int) -> int:
 
 
 def likelihood_scan(family: PrecisionFamily, thetas: Sequence[float], xs: Sequence[torch.Tensor],
-                    degree: int, num_probes: int, seed: int = 1, k: int = 0) -> ScanResult:
-    """Log-likelihood of the samples xs under J(theta) for every theta: one batched estimate of all
-    log det J(theta) (common probes), device quadratic forms, device Gershgorin intervals."""
+                    degree: int, num_probes: int, seed: int = 1, k: int = 0,
+                    batched: Optional[bool] = None) -> ScanResult:
+    """Log-likelihood of the samples xs under J(theta) for every theta: all log det J(theta) with
+    common probes, device quadratic forms, device Gershgorin intervals.
+    batched=True: every member in the columns of each probe block (cheb_family_moments, one pass
+    over the matrix for all members); False: one estimate per member, sharing a workspace.  Default:
+    batched when fewer than 32 probes per member (a separate estimate would then run at k < 32, where
+    the matrix is >= 8 % of a step's bytes); with 64 probes per member the matrix is 4 % of a k = 64
+    step and the batched kernel's per-column scalars cost more than they save (configs[3]-size scan,
+    8 members x 64 probes: 5.9 s batched vs 5.0 s separate)."""
     th = np.asarray(thetas, dtype=np.float64)
     R, d, S = th.size, family.base.n_rows, len(xs)
-    k = k or scan_probe_block(R, num_probes)
+    if batched is None:
+        batched = num_probes < 32
     lh = family.gershgorin(th)
     if not np.all(lh[:, 0] > 0):
         bad = th[~(lh[:, 0] > 0)]
         raise ValueError(f"J(theta) not certified positive definite by Gershgorin for theta in {bad}")
-    mu = family.moments(th, lh, degree, 0, num_probes, seed, k)
+    if batched:
+        k = k or scan_probe_block(R, num_probes)
+        mu = family.moments(th, lh, degree, 0, num_probes, seed, k)
+    else:
+        k = k or next((kk for kk in (8, 16, 32, 64) if kk >= num_probes), 64)
+        ws = alloc_workspace(Operator("csr", family.base), k)
+        mu = torch.empty((R, num_probes, degree + 1), dtype=torch.float64, device=family.base.val.device)
+        for r in range(R):
+            moments(Operator("csr", family.at(float(th[r]))), lh[r, 0], lh[r, 1], degree, 0, num_probes, seed, k,
+                    mu_out=mu[r], workspace=ws)
+            if workspace_status(ws):  # the status word is per moments call: check each member
+                raise _lib.ChebError(_lib.CL_ENONFINITE, f"moments of J({th[r]}) failed (status {workspace_status(ws)})")
+        family._workspace = None
     out = {"logdet": [], "stderr": [], "quad": [], "loglik": []}
     qs = [quadform_split(family.base, x) for x in xs]
     for r in range(R):

@@ -65,32 +65,23 @@ def _gmrf5000():
 
 
 def f2():
-    """5000 x 5000 GMRF likelihood scan, 8 thetas x 64 probes, n = 100: all members batched in the
-    columns of each probe block (cheb_family_moments, k = 128: 8 members x 16 probes), against the
-    same scan done as 8 separate estimates (k = 64) on one box."""
+    """5000 x 5000 GMRF likelihood scan, 8 thetas, n = 100: members batched in the columns of each
+    probe block (cheb_family_moments) vs one estimate per member (shared workspace), at 64 and at
+    16 probes per member."""
     import paper_1503_06394_b200.gmrf as G
     base = W.grid_gmrf(5000, 1.0)
     fam = G.PrecisionFamily(P.DeviceCSR.from_host(base))
     x = torch.randn(base.n_rows, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
     thetas = np.linspace(-0.24, -0.20, 8)
-    t = timed(lambda: G.likelihood_scan(fam, thetas, [x], 100, 64, seed=1), reps=2, warm=1)
-    lh = fam.gershgorin(thetas)
-    k = G.scan_probe_block(len(thetas), 64)
-    wsf = P.alloc_workspace(P.Operator("family", fam.base), k)
-    tb = timed(lambda: fam.moments(thetas, lh, 100, 0, 64, 1, k, workspace=wsf), reps=2, warm=1)
-    ws = P.alloc_workspace(P.Operator("csr", fam.base), 64)
-    members = [P.Operator("csr", fam.at(float(th))) for th in thetas]
-
-    def separate():
-        for op, (lo, hi) in zip(members, lh):
-            P.moments(op, lo, hi, 100, 0, 64, 1, 64, workspace=ws)
-    ts = timed(separate, reps=2, warm=1)
-    print(json.dumps({"row": "f2", "what": "rho-likelihood scan, 5000x5000 GMRF, 8 thetas x 64 probes, n=100",
-                      "scan_seconds": t, "scan_probe_steps_per_s": 8 * 64 * 100 / t,
-                      "batched_moments_seconds": tb, "batched_probe_block": k,
-                      "batched_probe_steps_per_s": 8 * 64 * 100 / tb,
-                      "separate_moments_seconds": ts, "separate_probe_steps_per_s": 8 * 64 * 100 / ts}),
-          flush=True)
+    for m in (64, 16):
+        out = {"row": "f2", "what": f"rho-likelihood scan, 5000x5000 GMRF, 8 thetas x {m} probes, n=100"}
+        for batched in (True, False):
+            t = timed(lambda: G.likelihood_scan(fam, thetas, [x], 100, m, seed=1, batched=batched), reps=2, warm=1)
+            key = "batched" if batched else "separate"
+            out[f"{key}_scan_seconds"] = t
+            out[f"{key}_probe_steps_per_s"] = 8 * m * 100 / t
+        out["batched_probe_block"] = G.scan_probe_block(8, m)
+        print(json.dumps(out), flush=True)
 
 
 def f3():

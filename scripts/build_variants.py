@@ -13,6 +13,8 @@ VARIANTS = {
     "r1c4": ["CHEB_MIN_CTAS_R1=4"],
     "dec": ["CHEB_DECOUPLE=1"],
     "fam4": ["CHEB_MIN_CTAS_FAM=4"],
+    "cap6dec": ["CHEB_CAP_PER_ROW=6", "CHEB_DECOUPLE=1"],
+    "cap6": ["CHEB_CAP_PER_ROW=6"],
     "dec3": ["CHEB_DECOUPLE=1", "CHEB_STAGES=3"],
     "r1": ["CHEB_RPG=1"],
     "r4": ["CHEB_RPG=4"],
