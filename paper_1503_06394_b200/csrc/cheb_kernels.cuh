@@ -91,6 +91,21 @@ __host__ __device__ constexpr int words_for(int K) { return K >= 32 ? K / 32 : 1
 #define CHEB_PPL 4
 #endif
 constexpr int kPPL = CHEB_PPL;
+// 256-bit gathers and stores (sm_100 LDG/STG .ENL2.256): a lane's 4 probes are contiguous, so one
+// 32-byte access per gathered row instead of two 16-byte ones at stride K/2 (CHEB_WIDE=0: the split
+// layout {2l, 2l+1} + {K/2+2l, K/2+2l+1}).  Both cover whole 32-byte sectors per row.
+// 0 never, 1 always, 2 (default) for probe blocks k <= CHEB_WIDE_MAXK (configs[3]: k = 16 1534 vs
+// 1686 ms per estimate; k = 64 1388 vs 1328 ms, where a warp's two 16-byte accesses already cover
+// 8 whole rows' halves)
+#ifndef CHEB_WIDE
+#define CHEB_WIDE 2
+#endif
+#ifndef CHEB_WIDE_MAXK
+#define CHEB_WIDE_MAXK 32
+#endif
+__host__ __device__ constexpr bool wide_k(int K) {
+    return kPPL == 4 && (CHEB_WIDE == 1 || (CHEB_WIDE == 2 && K <= CHEB_WIDE_MAXK));
+}
 static_assert(kPPL == 4 || kPPL == 8, "CHEB_PPL must be 4 or 8");
 
 // Geometry of the step / spmm kernels: each lane owns PPL probes in PPL/2 slots of two
@@ -102,7 +117,12 @@ struct Geo {
     static_assert(K == 8 || K == 16 || K == 32 || K == 64 || K == 128, "K in {8,...,128}");
     static constexpr int PPL = kPPL;
     static constexpr int NSL = PPL / 2;             // 16-byte slots per lane and row
-    static constexpr int SS = K / NSL;              // probe stride between a lane's slots
+    static constexpr int SS = K / NSL;              // probe stride between a lane's slots (split layout)
+    static constexpr bool WIDE = wide_k(K);         // 256-bit accesses, a lane's probes contiguous
+    // first probe of slot sl of lane lg: contiguous with 256-bit accesses, split otherwise
+    __host__ __device__ static constexpr int lane_probe(int lg, int sl) {
+        return WIDE ? PPL * lg + 2 * sl : 2 * lg + sl * SS;
+    }
     static constexpr int L = K / PPL;               // lanes per row: 1..32
     static constexpr int GROUPS = kThreads / L;     // rows in flight per CTA
     static constexpr int RPG = R4 * 4 / PPL;        // rows per group per tile
@@ -230,6 +250,20 @@ __device__ __forceinline__ double signflip(double x, uint32_t m) {
 __device__ __forceinline__ double2 ldg2(const double* p) {
     return __ldg(reinterpret_cast<const double2*>(p));
 }
+// 32 contiguous bytes (32-byte aligned): read-only path / L1-allocating coherent path
+__device__ __forceinline__ void ldg4(const double* p, double2& lo, double2& hi) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y) : "l"(p));
+}
+__device__ __forceinline__ void ldca4(const double* p, double2& lo, double2& hi) {
+    asm volatile("ld.global.ca.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y) : "l"(p));
+}
+__device__ __forceinline__ void stcs4(double* p, double2 lo, double2 hi) {  // streaming store
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(lo.x), "d"(lo.y), "d"(hi.x),
+                 "d"(hi.y)
+                 : "memory");
+}
 
 struct StepArgs {
     int64_t d;            // rows of the gather matrix (= dimension of M)
@@ -280,7 +314,8 @@ __device__ __forceinline__ double warp_sum_xor(double v) {
     return v;
 }
 
-constexpr int kRedGroup = 8;  // portable cluster size: the default reduction group
+constexpr int kRedGroup = 8;      // portable cluster size: the default reduction group
+constexpr int kMaxRedGroup = 16;  // largest (non-portable) cluster the persistent kernel may use
 __host__ __device__ constexpr int red_group(int G, int rg = kRedGroup) { return G < rg ? (G < 1 ? 1 : G) : rg; }
 
 // Second level of the canonical order for one channel: gp = that channel's group sums [ng][K].
@@ -292,12 +327,13 @@ __device__ __forceinline__ double group_tree_sum(const double* gp, int ng) {
     constexpr int T = kThreads / K;
     const int p = threadIdx.x / T, u = threadIdx.x % T;
     double t = 0.0;
-    for (int q0 = u; q0 < ng; q0 += 8 * T) {  // 8 loads in flight, then the adds in ascending q
-        double v[8];
+    constexpr int B = 16;  // loads in flight per batch (one L2 round trip for ng <= 16 T), then the adds in ascending q
+    for (int q0 = u; q0 < ng; q0 += B * T) {
+        double v[B];
 #pragma unroll
-        for (int r = 0; r < 8; r++) v[r] = q0 + r * T < ng ? __ldcg(gp + (size_t)(q0 + r * T) * K + p) : 0.0;
+        for (int r = 0; r < B; r++) v[r] = q0 + r * T < ng ? __ldcg(gp + (size_t)(q0 + r * T) * K + p) : 0.0;
 #pragma unroll
-        for (int r = 0; r < 8; r++) t += v[r];
+        for (int r = 0; r < B; r++) t += v[r];
     }
 #pragma unroll
     for (int off = T / 2; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
@@ -314,11 +350,11 @@ __device__ __forceinline__ void reduce_partials_grouped(const double* part, int 
         const int p = x % K, q = (x / K) % ng, ch = x / (K * ng);
         const int c0 = q * RG, cn = (G - c0) < RG ? (G - c0) : RG;
         const double* src = part + ((size_t)ch * G + c0) * K + p;
-        double v[kRedGroup], sq = 0.0;
+        double v[kMaxRedGroup], sq = 0.0;
 #pragma unroll
-        for (int r = 0; r < kRedGroup; r++) v[r] = r < cn ? __ldcg(src + (size_t)r * K) : 0.0;
+        for (int r = 0; r < kMaxRedGroup; r++) v[r] = r < cn ? __ldcg(src + (size_t)r * K) : 0.0;
 #pragma unroll
-        for (int r = 0; r < kRedGroup; r++) sq += v[r];
+        for (int r = 0; r < kMaxRedGroup; r++) sq += v[r];
         gpart[((size_t)ch * ng + q) * K + p] = sq;
     }
     __syncthreads();  // block-level visibility of the gpart stores
@@ -634,7 +670,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
     const int grp = threadIdx.x / G::L;
     int pp[NSL];  // first probe of each slot: {2lg, 2lg+1} + s*SS
 #pragma unroll
-    for (int sl = 0; sl < NSL; sl++) pp[sl] = 2 * lg + sl * G::SS;
+    for (int sl = 0; sl < NSL; sl++) pp[sl] = G::lane_probe(lg, sl);
     const int64_t* rp_s = reinterpret_cast<const int64_t*>(st + SL::OFF_RP);
     const int32_t* col_s = reinterpret_cast<const int32_t*>(st + SL::OFF_COL);
     const double* val_s = reinterpret_cast<const double*>(st + SL::OFF_VAL);
@@ -704,7 +740,12 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
                     // lane offset folded into the base: one IMAD.WIDE per gathered row
                     const double* p = xl + (size_t)(uint32_t)c[q] * K;
 #pragma unroll
-                    for (int sl = 0; sl < NSL; sl++) x[q][sl] = CG ? ldcg2(p + sl * G::SS) : ldg2(p + sl * G::SS);
+                    if constexpr (G::WIDE) {
+                        if (CG) ldca4(p, x[q][0], x[q][1]);
+                        else ldg4(p, x[q][0], x[q][1]);
+                    } else {
+                        for (int sl = 0; sl < NSL; sl++) x[q][sl] = CG ? ldcg2(p + sl * G::SS) : ldg2(p + sl * G::SS);
+                    }
                 }
             }
             if (OWN_GATHER && t0 == 0) {
@@ -771,9 +812,12 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             }
         }
         double* out = wout + (size_t)i * K;
+        if constexpr (G::WIDE) {
+            stcs4(out + pp[0], nw[0], nw[1]);  // streamed: the next read is by a later step
+        } else {
 #pragma unroll
-        for (int sl = 0; sl < NSL; sl++)  // streamed: the next read is by a later step
-            __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw[sl]);
+            for (int sl = 0; sl < NSL; sl++) __stcs(reinterpret_cast<double2*>(out + pp[sl]), nw[sl]);
+        }
 #pragma unroll
         for (int sl = 0; sl < NSL; sl++) {
             if (DBL) {
@@ -797,6 +841,9 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
 }
 
 // resident CTAs per SM each mode is register-budgeted for (BTB is smem-limited to 2)
+#ifndef CHEB_DIAG_R1_NOSYNC
+#define CHEB_DIAG_R1_NOSYNC 0  // TIMING DIAGNOSTIC builds only (wrong rank-1 results): skip the s_j handoff
+#endif
 #ifndef CHEB_MIN_CTAS_FAM
 #define CHEB_MIN_CTAS_FAM 4  // family mode (per-column scalars in shared memory)
 #endif
@@ -844,7 +891,7 @@ cheb_step_kernel(StepArgs a) {
     double2 r1[G::NSL];  // alpha c s_{j-1}[p] of the lane's probes (rank-1)
 #pragma unroll
     for (int sl = 0; sl < G::NSL; sl++) {
-        const int p = 2 * (tid % G::L) + sl * G::SS;
+        const int p = G::lane_probe(tid % G::L, sl);
         r1[sl] = HAS_S ? make_double2(a.r1c_alpha * a.s_cur[p], a.r1c_alpha * a.s_cur[p + 1]) : make_double2(0.0, 0.0);
     }
     const int64_t nmine = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -948,7 +995,7 @@ cheb_step_kernel(StepArgs a) {
         }
     }
     if (DEC) __syncthreads();  // the reduction scratch below aliases the stages
-    grid_reduce_finish<K, kPPL, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, true>(acc, a, smem);
+    grid_reduce_finish<K, kPPL, NCH, DBL ? EPI_DBL : EPI_STEP, HAS_S, !G::WIDE>(acc, a, smem);
 }
 
 
@@ -1223,7 +1270,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         double2 r1[G::NSL];
 #pragma unroll
         for (int sl = 0; sl < G::NSL; sl++) {
-            const int p = 2 * lg + sl * G::SS;
+            const int p = G::lane_probe(lg, sl);
             r1[sl] = HAS_S ? make_double2(a.r1c_alpha * s_sh[p], a.r1c_alpha * s_sh[p + 1]) : make_double2(0.0, 0.0);
         }
         double acc[NCH][kPPL];
@@ -1268,7 +1315,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         if (lane < G::L) {
 #pragma unroll
             for (int q = 0; q < kPPL; q++) {
-                const int p = probe_of<K, kPPL, true>(lg, q);
+                const int p = probe_of<K, kPPL, !G::WIDE>(lg, q);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ch++) red[ch][warp][p] = acc[ch][q];
             }
@@ -1291,11 +1338,11 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
         if (crank == 0) {
             for (int x = tid; x < NCH * K; x += kThreads) {
                 const int ch = x / K, p = x % K;
-                double v[kRedGroup], sq = 0.0;  // all DSMEM loads in flight, then the adds in rank order
+                double v[kMaxRedGroup], sq = 0.0;  // all DSMEM loads in flight, then the adds in rank order
 #pragma unroll
-                for (int r = 0; r < kRedGroup; r++) v[r] = r < RG ? *cluster.map_shared_rank(&cpart[par][ch][p], r) : 0.0;
+                for (int r = 0; r < kMaxRedGroup; r++) v[r] = r < RG ? *cluster.map_shared_rank(&cpart[par][ch][p], r) : 0.0;
 #pragma unroll
-                for (int r = 0; r < kRedGroup; r++) sq += v[r];
+                for (int r = 0; r < kMaxRedGroup; r++) sq += v[r];
                 gp[((size_t)ch * ng + cid) * K + p] = sq;
             }
             __syncthreads();
@@ -1321,7 +1368,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ch++) {
             const bool is_s = HAS_S && ch == NCH - 1;
-            if (!(is_s ? (crank == 0 && j < pa_.n) : want_mu)) continue;
+            if (!(is_s ? (crank == 0 && j < pa_.n && !CHEB_DIAG_R1_NOSYNC) : want_mu)) continue;
             const double t = group_tree_sum<K>(gp + (size_t)ch * ng * K, ng);
             if (tid % T == 0) fin[ch][tid / T] = t;
         }
@@ -1331,7 +1378,7 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
             if (DBL) dbl_write(row, j, a.mu_stride - 1, fin[0][tid], fin[1][tid]);
             else row[j] = fin[0][tid];
         }
-        if (HAS_S && j < pa_.n) {  // (after the last step nobody needs s_n; rank 0 may have exited)
+        if (HAS_S && j < pa_.n && !CHEB_DIAG_R1_NOSYNC) {  // (after the last step nobody needs s_n)
             if (crank == 0 && tid < K) s_sh[tid] = fin[NCH - 1][tid];
             cluster.sync();  // rank 0's s_j visible to the cluster
             if (crank != 0 && tid < K) s_sh[tid] = *cluster.map_shared_rank(&s_sh[tid], 0);

@@ -15,6 +15,10 @@ VARIANTS = {
     "fam4": ["CHEB_MIN_CTAS_FAM=4"],
     "cap6dec": ["CHEB_CAP_PER_ROW=6", "CHEB_DECOUPLE=1"],
     "cap6": ["CHEB_CAP_PER_ROW=6"],
+    "narrow": ["CHEB_WIDE=0"],
+    "wide16": ["CHEB_WIDE_MAXK=16"],
+    "diag_r1nosync": ["CHEB_DIAG_R1_NOSYNC=1"],  # timing diagnostic: wrong rank-1 moments
+    "diag_r1nosync_c4": ["CHEB_DIAG_R1_NOSYNC=1", "CHEB_MIN_CTAS_R1=4"],
     "dec3": ["CHEB_DECOUPLE=1", "CHEB_STAGES=3"],
     "r1": ["CHEB_RPG=1"],
     "r4": ["CHEB_RPG=4"],

@@ -1,19 +1,22 @@
 #!/bin/bash
-# Round-end validation on one B200: GPU tests, smoke, headline bench, all configs, ncu evidence.
-# Large .ncu-rep files are summarised on the box and removed (gpurun copies back <= 64 MiB).
+# Round-end validation on one B200: GPU tests (full-m parity margins), smoke, headline bench, all
+# configs, f rows, ncu launch list of the headline bench.  Writes gpurun_out/*.
+rm -f gpurun_out/parity.jsonl
 SKIP_TESTS=${SKIP_TESTS:-0}
 if [ "$SKIP_TESTS" = 0 ]; then
-timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/t_gpu_full.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/t_gpu_full.log
+PARITY_REPORT=gpurun_out/parity.jsonl timeout 2700 python -m pytest tests -m gpu -q > gpurun_out/t_gpu_full.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/t_gpu_full.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 fi
 timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc=$?"
-bash scripts/bench_all.sh; echo "bench_all done"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 420 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-alt > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
-for V in step dbl; do
-  E=""; [ $V = dbl ] && E="CHEB_DOUBLING=1"
-  env $E timeout 900 ncu --set full --import-source on --clock-control none -k regex:"cheb_step_kernel" -s 10 -c 1 -o /tmp/full_$V python scripts/prof_step.py --workload gmrf5000 --k 64 --reps 1 > /dev/null 2>&1; echo "full $V rc=$?"
-  python scripts/ncu_brief.py /tmp/full_$V.ncu-rep > gpurun_out/full_${V}_brief.txt 2>&1
-  python scripts/ncu_summary.py /tmp/full_$V.ncu-rep >> gpurun_out/full_${V}_brief.txt 2>&1
+for W in gmrf32 torus256 gmrf1000 btb4m; do
+  timeout 600 python bench.py --workload $W --no-cpu-baseline > gpurun_out/all_$W.json 2> gpurun_out/all_$W.err; echo "bench $W rc=$?"
 done
-timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"cheb_step_kernel" -s 10 -c 3 --csv python scripts/prof_step.py --workload gmrf5000 --k 64 --reps 1 > gpurun_out/traffic.csv 2>/dev/null; echo "traffic rc=$?"
+timeout 600 python bench.py --doubling --no-cpu-baseline --no-e2e > gpurun_out/all_gmrf5000_dbl.json 2> gpurun_out/all_gmrf5000_dbl.err; echo "bench dbl rc=$?"
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-alt --no-weak"
+timeout 600 $B > gpurun_out/plain_bench.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
+S="python scripts/prof_step.py --workload gmrf5000 --k 16 --probes 16 --degree 12 --reps 1"
+timeout 300 $S > gpurun_out/plain_k16.log 2>&1 && \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:cheb_step_kernel -s 6 -c 1 -o gpurun_out/k16_full $S > gpurun_out/ncu_k16.log 2>&1; echo "k16 full rc=$?"
 du -sh gpurun_out
