@@ -94,14 +94,14 @@ constexpr int kPPL = CHEB_PPL;
 // 256-bit gathers and stores (sm_100 LDG/STG .ENL2.256): a lane's 4 probes are contiguous, so one
 // 32-byte access per gathered row instead of two 16-byte ones at stride K/2 (CHEB_WIDE=0: the split
 // layout {2l, 2l+1} + {K/2+2l, K/2+2l+1}).  Both cover whole 32-byte sectors per row.
-// 0 never, 1 always, 2 (default) for probe blocks k <= CHEB_WIDE_MAXK (configs[3]: k = 16 1534 vs
-// 1686 ms per estimate; k = 64 1388 vs 1328 ms, where a warp's two 16-byte accesses already cover
-// 8 whole rows' halves)
+// 0 never, 1 always, 2 (default) for probe blocks k <= CHEB_WIDE_MAXK (configs[3] per estimate:
+// k = 16 1534 vs 1686 ms; k = 32 1386 vs 1334 ms and k = 64 1388 vs 1328 ms in favour of the split
+// layout, whose 16-byte accesses already cover whole sectors of 2+ rows per warp instruction)
 #ifndef CHEB_WIDE
 #define CHEB_WIDE 2
 #endif
 #ifndef CHEB_WIDE_MAXK
-#define CHEB_WIDE_MAXK 32
+#define CHEB_WIDE_MAXK 16
 #endif
 __host__ __device__ constexpr bool wide_k(int K) {
     return kPPL == 4 && (CHEB_WIDE == 1 || (CHEB_WIDE == 2 && K <= CHEB_WIDE_MAXK));
