@@ -185,17 +185,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+#ifndef CHEB_MBAR_SUSPEND_NS
+#define CHEB_MBAR_SUSPEND_NS 0  // try_wait suspend-time hint (0: the hardware default)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done = 0;
     do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(phase)
-            : "memory");
+        if (CHEB_MBAR_SUSPEND_NS > 0) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(addr), "r"(phase), "r"((uint32_t)CHEB_MBAR_SUSPEND_NS)
+                : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(addr), "r"(phase)
+                : "memory");
+        }
     } while (!done);
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

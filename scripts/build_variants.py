@@ -17,6 +17,8 @@ VARIANTS = {
     "cap6": ["CHEB_CAP_PER_ROW=6"],
     "narrow": ["CHEB_WIDE=0"],
     "wide16": ["CHEB_WIDE_MAXK=16"],
+    "sus1k": ["CHEB_MBAR_SUSPEND_NS=1000"],
+    "sus20k": ["CHEB_MBAR_SUSPEND_NS=20000"],
     "diag_r1nosync": ["CHEB_DIAG_R1_NOSYNC=1"],  # timing diagnostic: wrong rank-1 moments
     "diag_r1nosync_c4": ["CHEB_DIAG_R1_NOSYNC=1", "CHEB_MIN_CTAS_R1=4"],
     "dec3": ["CHEB_DECOUPLE=1", "CHEB_STAGES=3"],
