@@ -260,7 +260,7 @@ def timed_region(sh, steps, flush_buf, P, torch, dist, world, dev):
     return float(elapsed.item()), prof, launches, all_stats
 
 
-def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind):
+def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind, sched="per_step"):
     """Roofline of the dominant kernel from its measured launch times and algorithmic bytes."""
     d = wl.d
     gnnz = A.nnz if wl.mode != "btb" else At.nnz  # gather matrix of the step kernel
@@ -268,7 +268,8 @@ def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind):
     dbl = bool(args.doubling)
     gather_aware = None
     if p_ms > s_ms:  # persistent multi-step kernel: one launch = all steps of a block
-        kern = f"cheb_persist_kernel<{k},{wl.mode}>"
+        kern = (f"cheb_resident_kernel<{k},{wl.mode}>" if sched == "resident" else
+                f"cheb_persist_kernel<{k},{wl.mode}>")
         apps = (wl.degree + 1) // 2 if dbl else wl.degree  # applications of A~ per launch
         bytes_per_launch = (step_bytes(d, gnnz, k, True, wl.mode, dbl)
                             + (apps - 1) * step_bytes(d, gnnz, k, args.basis == "taylor", wl.mode, dbl))
@@ -300,7 +301,11 @@ def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind):
             "peak_kind": peak_kind, "frac_vs_nominal_8000": achieved / 8000.0, "kernel": kern,
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
             "launches": int(nl), "step_kernel_share": dom_ms / t_ms,
-            "traffic": _traffic_per_launch(wl.name, k), "gather_aware": gather_aware}
+            "traffic": _traffic_per_launch(wl.name, k), "gather_aware": gather_aware,
+            "note": ("shared-memory-resident kernel: the vectors never reach HBM; achieved = the HBM step "
+                     "model's bytes / time (equivalent bandwidth)" if sched == "resident" else
+                     "L2-resident persistent kernel: HBM step-model bytes / time (equivalent bandwidth)"
+                     if p_ms > s_ms else None)}
 
 
 def run_ours(args):
@@ -362,6 +367,7 @@ def run_ours(args):
         clocks.start()
     t_ms, prof, launches, all_stats = timed_region(sh, args.steps, flush_buf, P, torch, dist, world, dev)
     clk = clocks.stop() if rank == 0 else None
+    sched = P.last_schedule()
     st = all_stats[-1].cpu().numpy()
 
     # ---- weak scaling beside the headline: m per GPU fixed, best single-GPU block size
@@ -373,12 +379,14 @@ def run_ours(args):
         sw.run(check=True)
         reps = max(1, min(args.steps, 3))
         tw, profw, _, stw = timed_region(sw, reps, flush_buf, P, torch, dist, world, dev)
+        sched_w = P.last_schedule()
         hbm, peak_kind = _peaks()
-        rw = roofline(wl, A, At, k_w, math.ceil((m_w // world) / k_w), reps, tw, profw, args, hbm, peak_kind)
+        rw = roofline(wl, A, At, k_w, math.ceil((m_w // world) / k_w), reps, tw, profw, args, hbm, peak_kind,
+                      sched_w)
         weak = {"scaling": "weak", "num_probes": m_w, "probes_per_gpu": m_w // world, "probe_block": k_w,
                 "value": m_w * wl.degree * reps / (tw / 1e3), "unit": UNIT, "ms_per_step": tw / reps,
                 "steps": reps, "logdet_wall_s": tw / reps / 1e3, "gamma": float(stw[-1].cpu().numpy()[0]),
-                "roofline_frac": rw["frac"], "roofline_achieved_gbs": rw["achieved"]}
+                "roofline_frac": rw["frac"], "roofline_achieved_gbs": rw["achieved"], "kernel_schedule": sched_w}
         del sw
 
     # ---- the other schedule on the same operator (Algorithm 1 <-> moment doubling)
@@ -400,7 +408,7 @@ def run_ours(args):
     hbm, peak_kind = _peaks()
     nnz = A.nnz + (At.nnz if At is not None else 0)
     blocks = math.ceil(m_mine / k)
-    roof = roofline(wl, A, At, k, blocks, args.steps, t_ms, prof, args, hbm, peak_kind)
+    roof = roofline(wl, A, At, k, blocks, args.steps, t_ms, prof, args, hbm, peak_kind, sched)
     cfg = {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": wl.d,
            "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total, "probes_per_gpu": m_mine,
            "probe_block": k, "a": a, "b": b, "basis": args.basis,
@@ -408,6 +416,7 @@ def run_ours(args):
                         "the n Chebyshev steps delivered" if args.doubling else
                         "Algorithm 1: n applications of A~ per probe"),
            "applications_per_probe": (wl.degree + 1) // 2 if args.doubling else wl.degree,
+           "kernel_schedule": sched,
            "parallelism": f"probe-dp{world}",
            "l2": (f"L2 flushed between timed iterations ({2 * l2_bytes / 1e6:.0f} MB write outside the "
                   f"per-iteration events; working set {wset / 1e6:.1f} MB < L2 {l2_bytes / 1e6:.0f} MB)"

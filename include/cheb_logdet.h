@@ -298,6 +298,25 @@ int cheb_get_small_tiles(void);
 int cheb_set_doubling(int32_t on);
 int cheb_get_doubling(void);
 
+/* Shared-memory-resident schedule for CL_OP_CSR / CL_OP_CSR_RANK1 (process-wide; default 1; env
+ * CHEB_RESIDENT sets the initial value).  Applies only in the automatic persistent mode
+ * (cheb_set_persistent(1)), to Algorithm 1 and the power basis (not moment doubling), k <= 64:
+ *   1 = auto: when one probe block (two d x k fp64 buffers + the CTAs' matrix rows) fits in the
+ *       shared memory of one CTA per SM, all n steps run in one cooperative cluster launch in
+ *       which every CTA keeps its rows of w_{j-1}, w_{j-2} on chip and gathers other rows over
+ *       DSMEM (same cluster) or from a global copy of the rows other clusters need
+ *       (cheb_resident_kernel); w_j is bit-identical to the other schedules, the
+ *       dot products follow this kernel's grid (deterministic run to run);
+ *   0 = off (the L2-resident persistent kernel or per-step launches).
+ * CL_EINVAL for other values. */
+int cheb_set_resident(int32_t mode);
+int cheb_get_resident(void);
+
+/* Schedule the calling thread's last cheb_moments-family call ran (set when it returns CL_OK):
+ * 0 = one launch per step, 1 = L2-resident persistent kernel, 2 = shared-memory-resident kernel;
+ * -1 before any call.  Diagnostics (tests, bench). */
+int cheb_last_schedule(void);
+
 /* cheb_logdet / cheb_logdet_host keep their device workspace (and cheb_logdet_host the device
  * copy of the operator) in grow-only per-thread arenas, so repeated estimates do not pay a
  * multi-GB cudaMalloc/cudaFree per call.  cheb_release_cache() frees the calling thread's

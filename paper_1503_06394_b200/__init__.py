@@ -9,7 +9,7 @@ from .api import (DeviceCSR, Operator, Result, Estimator, coeffs_log, workspace_
                   power_moments, taylor_coeffs, taylor_logdet, affine_power_moments, norm_bound,
                   spectrum_bounds, logdet_auto,
                   alloc_workspace, moments, moments_host, finalize, logdet, logdet_host, bounds_btb, probes,
-                  launch_count, profile_begin, profile_end, set_persistent, set_small_tiles, get_small_tiles, set_doubling,
+                  launch_count, profile_begin, profile_end, set_persistent, set_small_tiles, get_small_tiles, set_doubling, set_resident, get_resident, last_schedule,
                   get_doubling, release_cache, workspace_status, check_estimate, log_abs_det_from_btb, log_tau_from_rank1)
 from ._lib import ChebError, load as load_library
 
@@ -18,6 +18,6 @@ __all__ = ["DeviceCSR", "Operator", "Result", "Estimator", "coeffs_log", "worksp
            "spectrum_bounds", "logdet_auto",
            "alloc_workspace", "moments", "moments_host", "finalize", "logdet", "logdet_host", "bounds_btb",
            "probes", "launch_count", "profile_begin", "profile_end", "set_persistent", "set_small_tiles",
-           "get_small_tiles", "set_doubling", "get_doubling", "release_cache", "workspace_status", "check_estimate",
+           "get_small_tiles", "set_doubling", "get_doubling", "set_resident", "get_resident", "last_schedule", "release_cache", "workspace_status", "check_estimate",
            "log_abs_det_from_btb",
            "log_tau_from_rank1", "ChebError", "load_library"]

@@ -96,6 +96,9 @@ def load():
         "cheb_get_small_tiles": (I, []),
         "cheb_set_doubling": (I, [I32]),
         "cheb_get_doubling": (I, []),
+        "cheb_set_resident": (I, [I32]),
+        "cheb_get_resident": (I, []),
+        "cheb_last_schedule": (I, []),
         "cheb_release_cache": (I, []),
         "cheb_last_error": (ctypes.c_char_p, []),
         "cheb_version": (I, []),

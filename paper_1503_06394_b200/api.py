@@ -398,6 +398,24 @@ def set_doubling(on: bool):
     check(_lib.load().cheb_set_doubling(1 if on else 0))
 
 
+def set_resident(mode: int):
+    """Shared-memory-resident multi-step kernel (cheb_set_resident): 1 auto (default; csr/rank-1
+    probe blocks that fit in the SMs' shared memory, in the automatic persistent mode), 0 off."""
+    check(_lib.load().cheb_set_resident(int(mode)))
+
+
+def get_resident() -> int:
+    return int(_lib.load().cheb_get_resident())
+
+
+SCHEDULES = {0: "per_step", 1: "persistent", 2: "resident"}
+
+
+def last_schedule() -> str:
+    """Schedule of this thread's last moments call: "per_step", "persistent" or "resident"."""
+    return SCHEDULES.get(int(_lib.load().cheb_last_schedule()), "none")
+
+
 def release_cache():
     """Free this thread's device arenas of cheb_logdet / cheb_logdet_host."""
     check(_lib.load().cheb_release_cache())

@@ -25,6 +25,7 @@
 #pragma once
 #include <cassert>
 #include <cstdint>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -1401,6 +1402,435 @@ cheb_persist_kernel(StepArgs a, PersistArgs pa_) {
     // no CTA leaves while a cluster peer may still read its shared memory (also after a timed-out
     // grid wait, when the steps were no longer in lockstep)
     cluster.sync();
+}
+
+// ---------------------------------------------------------------------------------------
+// K2r: shared-memory-resident multi-step kernel (csr / rank-1, Algorithm 1 and the power basis).
+// For operators whose probe block fits in the chip's shared memory (two buffers of d x K fp64
+// over <= 148 SMs: configs[0] at every k, configs[1] at k <= 16) the vectors never leave the SMs:
+// CTA b owns rows [b*nr, (b+1)*nr) for all n steps and keeps w_{j-1}, w_{j-2} of its rows (and
+// its slice of the prepped matrix, its sign bits, u) in shared memory; w_j is written in place
+// over w_{j-2} (each element by the thread that reads it).  Two geometries:
+//   * one cluster (16 or 8 CTAs, small operators): rows of a peer CTA are gathered over DSMEM
+//     (ld.shared::cluster at the mapa'd address), the step tail is one cluster barrier after
+//     which every CTA sums the per-CTA partials over DSMEM in rank order;
+//   * a flat grid (one CTA per SM, cooperative): rows of other CTAs come from a global copy to
+//     which only the rows another CTA gathers ("exported" rows) are written (w_j into g[j & 1]);
+//     the step tail is one release-add on a grid counter and one wait; every CTA then sums the
+//     published partials of u^T w_j (rank-1) itself, and CTA p sums probe p's mu_j during the
+//     next step's reduction (off the critical path).
+// The column index of the prepped copy is encoded once per call by resident_prep_kernel
+// (>= 0 a global row, < 0 -(1 + (rank << 16 | offset)) a row of the own cluster / CTA).  w_j
+// values are bit-identical to the other schedules (same per-row FMA order); the dot products
+// follow this kernel's fixed reduction order (deterministic run to run).
+// ---------------------------------------------------------------------------------------
+#ifndef CHEB_RES_THREADS
+#define CHEB_RES_THREADS 512  // 128 registers per thread at one CTA per SM (768: 80, spills)
+#endif
+constexpr int kResThreads = CHEB_RES_THREADS;
+
+struct ResArgs {
+    double* g0;               // global copies of exported rows: w_j in g[j & 1]; g0 holds v at entry
+    double* g1;
+    int32_t n;                // steps
+    int32_t nr;               // rows per CTA
+    int32_t cap;              // staged nonzero capacity (dynamic shared memory)
+    int32_t power;            // power basis (Taylor baseline): w_j = Ã w_{j-1}
+    const uint8_t* exp;       // exp[i] != 0: row i is gathered by another cluster
+    double* gpart;            // [2][NCH][ng][K] group sums (step parity)
+    const double* s_buf;      // s_0 (rank-1, from probe_init)
+    unsigned int* bar_count;  // grid barrier: arrivals of cluster leaders (zeroed; monotone)
+    unsigned int* err;        // wait timeout flag
+};
+
+// shared-memory row stride (doubles): 256-bit-lane rows (k <= 16) get a 16-byte skew so the rows
+// of one quarter-warp fall on different banks
+template <int K>
+__host__ __device__ constexpr int res_row_stride() { return wide_k(K) ? K + 2 : K; }
+
+struct ResLayout {
+    size_t w0, w1, sg, u, ex, rp, col, val, total;
+};
+__host__ __device__ inline size_t res_a16(size_t x) { return (x + 15) & ~size_t(15); }
+template <int K>
+__host__ __device__ inline ResLayout res_layout(int nr, int cap, bool has_u) {
+    ResLayout l{};
+    const size_t wb = res_a16((size_t)nr * res_row_stride<K>() * 8);
+    l.w0 = 0;
+    l.w1 = l.w0 + wb;
+    l.sg = l.w1 + wb;
+    l.u = l.sg + res_a16((size_t)nr * words_for(K) * 4);
+    l.ex = l.u + (has_u ? res_a16((size_t)nr * 8) : 0);
+    l.rp = l.ex + res_a16((size_t)nr);
+    l.col = l.rp + res_a16((size_t)(nr + 1) * 4);
+    l.val = l.col + res_a16((size_t)cap * 4);
+    l.total = l.val + (size_t)cap * 8;
+    return l;
+}
+
+// Column encoding of the resident schedule (once per cheb_moments call, in place on the prepped
+// copy): columns owned by a CTA of the row's own cluster become -(1 + (rank << 16 | offset));
+// others stay global and mark their row as exported.
+__global__ void __launch_bounds__(kThreads)
+resident_prep_kernel(int64_t d, const int64_t* __restrict__ rp2, int32_t* __restrict__ ci2, int32_t nr,
+                     int32_t rg, int32_t dsmem, uint8_t* __restrict__ exp) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t oi = i / nr, cl = oi / rg;
+        for (int64_t e = rp2[i]; e < rp2[i + 1]; e++) {
+            const int32_t c = ci2[e];
+            const int64_t oc = c / nr;
+            if (dsmem ? oc / rg == cl : oc == oi)
+                ci2[e] = -1 - (int32_t)(((oc % rg) << 16) | (int64_t)(c - oc * nr));
+            else
+                exp[c] = 1;
+        }
+    }
+}
+
+// 16-byte loads of the resident kernel: own shared memory, a cluster peer's (DSMEM), global (L1)
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 ldcl2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ double2 ldca2(const double* p) {
+    double2 v;
+    asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
+#ifndef CHEB_RES_DIAG
+#define CHEB_RES_DIAG 0  // TIMING DIAGNOSTIC builds only (wrong results): 1 no gathers, 2 own-row gathers
+#endif
+#ifndef CHEB_RES_PROF
+#define CHEB_RES_PROF 0  // timing builds: per-CTA cycle counts of the step phases (g_res_prof)
+#endif
+#if CHEB_RES_PROF
+__device__ long long g_res_prof[1024 * 8];
+#define RES_T(i)                                                  \
+    do {                                                          \
+        if (tid == 0) {                                           \
+            const long long t_ = clock64();                       \
+            prof_acc[i] += t_ - prof_last;                        \
+            prof_last = t_;                                       \
+        }                                                         \
+    } while (0)
+#else
+#define RES_T(i) ((void)0)
+#endif
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kResThreads, 1)
+cheb_resident_kernel(StepArgs a, ResArgs ra) {
+    using G = Geo<K>;
+    constexpr int NT = kResThreads;
+    constexpr int L = G::L;          // lanes per row
+    constexpr int GR = NT / L;       // rows in flight
+    constexpr int NSL = G::NSL;
+    constexpr int RS = res_row_stride<K>();
+    constexpr int U = CHEB_NNZ_UNROLL;
+    constexpr int WORDS = G::WORDS;
+    constexpr bool HAS_S = (MODE == MODE_RANK1);
+    constexpr int NCH = HAS_S ? 2 : 1;
+    constexpr int NW = NT / 32;
+    static_assert(kPPL == 4, "resident kernel: 4 probes per lane");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[NCH][NW][K];
+    __shared__ double cpart[2][NCH][K];  // this CTA's partial of step j (parity j & 1), read over DSMEM
+    __shared__ double fin[NCH][K];
+    __shared__ double s_sh[HAS_S ? K : 1];
+    __shared__ double red2[HAS_S ? NT / K : 1][K];  // flat grid: s_j second level
+    __shared__ double red_mu[NW];                   // flat grid: mu_j of this CTA's probe
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lg = tid % L, grp = tid / L;
+    cg::cluster_group cluster = cg::this_cluster();
+    // one cluster (RG = G: DSMEM halos and reductions) or a flat grid (RG = 1: halos through the
+    // exported global rows, one grid counter per step)
+    const int RG = a.rg, NG = (int)gridDim.x;
+    const bool single = RG == NG;
+    const int crank = (int)cluster.block_rank();
+    double mu_pend = 0.0;  // flat grid: part[tid][p] of step mu_j, summed one step later
+    int32_t mu_j = 0;
+    const int64_t r0 = (int64_t)blockIdx.x * ra.nr;
+    const int nr = (int)(a.d - r0 < (int64_t)ra.nr ? (a.d - r0 > 0 ? a.d - r0 : 0) : ra.nr);
+    const ResLayout ly = res_layout<K>(ra.nr, ra.cap, a.r1u != nullptr);
+    double* const W0 = reinterpret_cast<double*>(smem + ly.w0);
+    double* const W1 = reinterpret_cast<double*>(smem + ly.w1);
+    uint32_t* sg_s = reinterpret_cast<uint32_t*>(smem + ly.sg);
+    double* u_s = reinterpret_cast<double*>(smem + ly.u);
+    uint8_t* ex_s = smem + ly.ex;
+    int32_t* rp_s = reinterpret_cast<int32_t*>(smem + ly.rp);
+    int32_t* col_s = reinterpret_cast<int32_t*>(smem + ly.col);
+    double* val_s = reinterpret_cast<double*>(smem + ly.val);
+    int pp[NSL];
+#pragma unroll
+    for (int sl = 0; sl < NSL; sl++) pp[sl] = G::lane_probe(lg, sl);
+
+    // ---- once per launch: the CTA's rows of the matrix, signs, u, export flags; w_0 = v
+    const int64_t e0 = nr > 0 ? a.rp[r0] : 0, e1 = nr > 0 ? a.rp[r0 + nr] : 0;
+    const bool fit = (e1 - e0) <= (int64_t)ra.cap;
+    for (int x = tid; x <= nr; x += NT) rp_s[x] = (int32_t)(a.rp[r0 + x] - e0);
+    if (fit)
+        for (int64_t e = tid; e < e1 - e0; e += NT) {
+            col_s[e] = a.ci[e0 + e];
+            val_s[e] = a.va[e0 + e];
+        }
+    for (int x = tid; x < nr * WORDS; x += NT) sg_s[x] = a.sbits[(size_t)r0 * WORDS + x];
+    if (a.r1u)
+        for (int x = tid; x < nr; x += NT) u_s[x] = a.r1u[r0 + x];
+    for (int x = tid; x < nr; x += NT) ex_s[x] = ra.exp[r0 + x];
+    if (HAS_S && tid < K) s_sh[tid] = __ldcg(ra.s_buf + tid);
+    __syncthreads();
+    for (int x = tid; x < nr * K; x += NT) {
+        const int lr = x / K, p = x % K;
+        W0[lr * RS + p] = pm1(sg_s[lr * WORDS + (p >> 5)], p & 31);
+    }
+    // kernel parameters used every step, pinned in registers: a parameter read from the constant
+    // bank after a barrier can miss (measured neutral, kept for predictability)
+    double* g0 = ra.g0;
+    double* g1 = ra.g1;
+    double* mu_out = a.mu_out;
+    double* gpart = ra.gpart;
+    unsigned int* bar_count = ra.bar_count;
+    unsigned int* err = ra.err;
+    const double* r1u = a.r1u;
+    double r1ca = a.r1c_alpha;
+    int64_t mu_stride = a.mu_stride;
+    int32_t n_steps = ra.n, power = ra.power, kvalid = a.kvalid;
+    const int32_t* ci_g = a.ci;
+    const double* va_g = a.va;
+    asm volatile("" : "+l"(g0), "+l"(g1), "+l"(mu_out), "+l"(gpart), "+l"(bar_count), "+l"(err), "+l"(r1u));
+    asm volatile("" : "+d"(r1ca), "+l"(mu_stride), "+r"(n_steps), "+r"(power), "+r"(kvalid), "+l"(ci_g), "+l"(va_g));
+    auto mu_flush = [&]() {  // flat grid, after the last step
+        double m = warp_sum_xor(mu_pend);
+        if (lane == 0) red_mu[warp] = m;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < NW; w++) t += red_mu[w];
+            mu_out[(size_t)blockIdx.x * mu_stride + mu_j] = t;
+        }
+    };
+    cluster.sync();  // every peer's w_0 rows are in place
+#if CHEB_RES_PROF
+    long long prof_acc[6] = {0, 0, 0, 0, 0, 0}, prof_last = clock64();
+#endif
+
+    for (int32_t j = 1; j <= n_steps; j++) {
+        const bool first = (j == 1) || power;
+        const double* Wo = (j & 1) ? W0 : W1;  // w_{j-1}
+        double* Wn = (j & 1) ? W1 : W0;        // w_{j-2} -> w_j
+        const double* go = ((j - 1) & 1) ? g1 : g0;
+        double* gn = (j & 1) ? g1 : g0;
+        double2 r1[NSL];
+#pragma unroll
+        for (int sl = 0; sl < NSL; sl++)
+            r1[sl] = HAS_S ? make_double2(r1ca * s_sh[pp[sl]], r1ca * s_sh[pp[sl] + 1])
+                           : make_double2(0.0, 0.0);
+        double acc[NCH][kPPL];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+            for (int q = 0; q < kPPL; q++) acc[ch][q] = 0.0;
+        const uint32_t wo_s = smem_u32(Wo);
+        // one row: gathers (own rows: ld.shared; cluster peers: ld.shared::cluster at the mapa'd
+        // address; other clusters: the exported global copy), rank-1 term, recurrence, dots
+        auto rows = [&](auto staged) {
+            constexpr bool STAGED = decltype(staged)::value;
+            for (int lr = grp; lr < nr; lr += GR) {
+                const int lo = rp_s[lr], hi = rp_s[lr + 1];
+                double2 g[NSL];
+#pragma unroll
+                for (int sl = 0; sl < NSL; sl++) g[sl] = make_double2(0.0, 0.0);
+                for (int t0 = lo; t0 < hi; t0 += U) {
+                    int32_t c[U];
+                    double v[U];
+#pragma unroll
+                    for (int q = 0; q < U; q++) {
+                        c[q] = STAGED ? col_s[t0 + q] : __ldg(ci_g + e0 + t0 + q);
+                        v[q] = STAGED ? val_s[t0 + q] : __ldg(va_g + e0 + t0 + q);
+                    }
+                    double2 x[U][NSL];
+#pragma unroll
+                    for (int q = 0; q < U; q++) {
+                        if (CHEB_RES_DIAG == 1) {  // timing diagnostic: no gathers
+                            x[q][0] = x[q][NSL - 1] = make_double2(v[q], 0.0);
+                        } else if (CHEB_RES_DIAG == 2) {  // timing diagnostic: every gather from the own row
+                            for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(wo_s + (lr * RS + pp[sl]) * 8);
+                        } else if (c[q] >= 0) {
+                            const double* p = go + (size_t)c[q] * K;
+#pragma unroll
+                            for (int sl = 0; sl < NSL; sl++) x[q][sl] = ldca2(p + pp[sl]);
+                        } else {
+                            const uint32_t e = (uint32_t)(-1 - c[q]);
+                            const uint32_t rk = e >> 16;
+                            const uint32_t ad = wo_s + (e & 0xFFFFu) * (RS * 8);
+                            if (rk == (uint32_t)crank) {
+#pragma unroll
+                                for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(ad + pp[sl] * 8);
+                            } else {
+                                const uint32_t adr = mapa_u32(ad, rk);
+#pragma unroll
+                                for (int sl = 0; sl < NSL; sl++) x[q][sl] = ldcl2(adr + pp[sl] * 8);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < U; q++)
+#pragma unroll
+                        for (int sl = 0; sl < NSL; sl++) {
+                            g[sl].x = fma(v[q], x[q][sl].x, g[sl].x);
+                            g[sl].y = fma(v[q], x[q][sl].y, g[sl].y);
+                        }
+                }
+                double ui = 1.0;
+                if (HAS_S) {
+                    ui = r1u ? u_s[lr] : 1.0;
+#pragma unroll
+                    for (int sl = 0; sl < NSL; sl++) {
+                        g[sl].x = fma(ui, r1[sl].x, g[sl].x);
+                        g[sl].y = fma(ui, r1[sl].y, g[sl].y);
+                    }
+                }
+                const bool ex = ex_s[lr] != 0;
+#pragma unroll
+                for (int sl = 0; sl < NSL; sl++) {
+                    double2* wp = reinterpret_cast<double2*>(Wn + lr * RS + pp[sl]);
+                    double2 nw = g[sl];
+                    if (!first) {
+                        const double2 pv = *wp;
+                        nw = make_double2(fma(2.0, g[sl].x, -pv.x), fma(2.0, g[sl].y, -pv.y));
+                    }
+                    *wp = nw;
+                    if (ex) __stcg(reinterpret_cast<double2*>(gn + (size_t)(r0 + lr) * K + pp[sl]), nw);
+                    const uint32_t bits = sg_s[lr * WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
+                    acc[0][2 * sl] += signflip(nw.x, bits << 31);
+                    acc[0][2 * sl + 1] += signflip(nw.y, bits << 30);
+                    if (HAS_S) {
+                        acc[NCH - 1][2 * sl] = fma(ui, nw.x, acc[NCH - 1][2 * sl]);
+                        acc[NCH - 1][2 * sl + 1] = fma(ui, nw.y, acc[NCH - 1][2 * sl + 1]);
+                    }
+                }
+            }
+        };
+        if (fit) rows(std::true_type{});
+        else rows(std::false_type{});
+        // ---- per-CTA partial: lanes of a warp -> warps in ascending order
+#pragma unroll
+        for (int off = L; off < 32; off <<= 1)
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch++)
+#pragma unroll
+                for (int q = 0; q < kPPL; q++) acc[ch][q] += __shfl_xor_sync(0xffffffffu, acc[ch][q], off);
+        if (lane < L) {
+#pragma unroll
+            for (int q = 0; q < kPPL; q++) {
+                const int p = probe_of<K, kPPL, !G::WIDE>(lg, q);
+#pragma unroll
+                for (int ch = 0; ch < NCH; ch++) red[ch][warp][p] = acc[ch][q];
+            }
+        }
+        if (!single && mu_j > 0) {  // the previous step's mu (flat grid): one butterfly, warps ascending
+            double m = warp_sum_xor(mu_pend);
+            if (lane == 0) red_mu[warp] = m;
+        }
+        __syncthreads();
+        RES_T(0);
+        if (!single && mu_j > 0) {
+            if (tid == 0) {
+                double m = 0.0;
+                for (int w = 0; w < NW; w++) m += red_mu[w];
+                mu_out[(size_t)blockIdx.x * mu_stride + mu_j] = m;
+            }
+            mu_j = 0;
+        }
+        const int par = j & 1;
+        if (tid < NCH * K) {
+            const int ch = tid / K, p = tid % K;
+            double m = 0.0;
+#pragma unroll 8
+            for (int w = 0; w < NW; w++) m += red[ch][w][p];
+            cpart[par][ch][p] = m;
+        }
+        RES_T(1);
+        const bool want_s = HAS_S && j < n_steps;
+        if (single) {
+            // ---- one cluster: barrier, then every CTA sums the partials over DSMEM in rank order
+            cluster.sync();  // the cluster's w_j rows and partials are complete
+            RES_T(2);
+            if (tid < NCH * K) {
+                const int ch = tid / K, p = tid % K;
+                double vr[kMaxRedGroup], sq = 0.0;
+#pragma unroll
+                for (int r = 0; r < kMaxRedGroup; r++) vr[r] = r < RG ? *cluster.map_shared_rank(&cpart[par][ch][p], r) : 0.0;
+#pragma unroll
+                for (int r = 0; r < kMaxRedGroup; r++) sq += vr[r];
+                fin[ch][p] = sq;
+            }
+            __syncthreads();
+            RES_T(3);
+            if (blockIdx.x == gridDim.x - 1 && tid < kvalid) mu_out[(size_t)tid * mu_stride + j] = fin[0][tid];
+            if (want_s && tid < K) s_sh[tid] = fin[NCH - 1][tid];
+        } else {
+            // ---- flat grid (one CTA per SM, no clusters): every CTA publishes its partial, one
+            // release-add on the grid counter, one wait.  pg: [NCH][NG][K] of step j.
+            double* pg = gpart + (size_t)par * NCH * NG * K;
+            if (tid < NCH * K) pg[((size_t)(tid / K) * NG + blockIdx.x) * K + tid % K] = cpart[par][tid / K][tid % K];
+            __syncthreads();
+            RES_T(2);
+            if (tid == 0) {
+                red_release_add(bar_count, 1u);                                  // release: w_j exports, partial
+                spin_until_geq(bar_count, (unsigned int)j * (unsigned)NG, err);  // + acquire
+            }
+            __syncthreads();
+            RES_T(5);
+            // mu_j of probe blockIdx.x (CTAs < K), summed during the next step's partial reduction:
+            // thread t holds part[t][p]
+            if (blockIdx.x < (unsigned)kvalid) {
+                mu_pend = tid < NG ? __ldcg(pg + (size_t)tid * K + blockIdx.x) : 0.0;
+                mu_j = j;
+            }
+            if (want_s) {
+                // s_j = sum over CTAs of part[c][S][p]: thread (u = tid / K, p = tid % K) sums
+                // c = u, u + U, ... ascending (coalesced rows of K), then u ascending
+                constexpr int UU = NT / K;
+                const double* ps = pg + (size_t)(NCH - 1) * NG * K;
+                const int p = tid % K, u = tid / K;
+                double t = 0.0;
+                for (int c = u; c < NG; c += UU) t += __ldcg(ps + (size_t)c * K + p);
+                red2[u][p] = t;
+                __syncthreads();
+                if (tid < K) {
+                    double sj = 0.0;
+                    for (int v = 0; v < UU; v++) sj += red2[v][tid];
+                    s_sh[tid] = sj;
+                }
+            }
+            RES_T(3);
+        }
+        __syncthreads();
+        RES_T(4);
+    }
+    if (!single && mu_j > 0) {  // mu_n
+        mu_flush();
+    }
+    // no CTA leaves while a cluster peer may still read its shared memory
+    cluster.sync();
+#if CHEB_RES_PROF
+    if (tid == 0)
+        for (int i = 0; i < 6; i++) g_res_prof[blockIdx.x * 8 + i] = prof_acc[i];
+#endif
 }
 
 // ---------------------------------------------------------------------------------------

@@ -63,6 +63,8 @@ int env_int(const char* name, int dflt) {
 std::atomic<int> g_persistent{env_int("CHEB_PERSISTENT", 1)};  // 0 off, 1 auto (default), 2 forced
 std::atomic<int> g_small_tiles{env_int("CHEB_SMALL_TILES", 1)};  // 1 auto (default), 0 standard geometry
 std::atomic<int> g_doubling{env_int("CHEB_DOUBLING", 0)};      // 0 off (default), 1 moment doubling
+thread_local int g_last_schedule = -1;  // cheb_last_schedule(): 0 per-step, 1 persistent, 2 resident
+std::atomic<int> g_resident{env_int("CHEB_RESIDENT", 1)};     // 0 off, 1 auto (default): shared-memory-resident kernel
 
 struct ProfScope {
     cudaStream_t s;
@@ -306,6 +308,9 @@ struct Schedule {
     bool vbits = false;       // per-step csr/rank-1: v = w_0 lives only as sign bits (steps 1, 2)
     bool small = false;       // 16-row tiles for the Algorithm-1 kernels (RP = 1)
     bool l2res = false;       // csr / rank-1 working set within half of L2 (persistent schedule's home)
+    bool resident = false;    // shared-memory-resident kernel (cheb_resident_kernel), plan below
+    int res_grid = 0, res_rg = 1, res_nr = 0, res_cap = 0;
+    size_t res_smem = 0;
     int fam_kp = 0, fam_r = 0;  // family: probes per member per block, members with output rows
     int64_t fam_rstride = 0;    // family: doubles between consecutive members' mu rows
 };
@@ -321,9 +326,9 @@ void launch_step(int grid, size_t smem, cudaStream_t st, const StepArgs& a) {
 
 // Launch configuration of the persistent kernel: clusters of rg CTAs (attribute 0).
 void cluster_config(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* at, int grid, int rg, size_t smem,
-                    cudaStream_t st) {
+                    cudaStream_t st, int threads = kThreads) {
     cfg->gridDim = dim3(grid);
-    cfg->blockDim = dim3(kThreads);
+    cfg->blockDim = dim3(threads);
     cfg->dynamicSmemBytes = smem;
     cfg->stream = st;
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -370,6 +375,96 @@ int persist_grid(Kern pk, int64_t ntiles, int sms, size_t smem, int* grid_out, i
         }
     }
     return fail(CL_ECUDA, "persistent kernel: no co-resident cluster configuration");
+}
+
+// ---- shared-memory-resident schedule (cheb_resident_kernel) ------------------------
+// One CTA of kResThreads per SM, all dynamic shared memory (the staged-matrix capacity takes what
+// the vectors leave).  A single cluster (16, else 8 CTAs) when its CTAs hold the whole probe block
+// with at most CHEB_RES_SINGLE_MAX (default 8192) row-probes per CTA: no grid-wide barrier at all
+// (configs[0]); otherwise clusters of 16/8/4/2 over the co-resident SMs, the largest cluster whose
+// grid is within 15 % of the best (configs[1] at k <= 16).  false: the block does not fit.
+template <int K, int MODE>
+bool resident_plan(int64_t d, int64_t nnz, bool has_u, Schedule* fp) {
+    auto kern = cheb_resident_kernel<K, MODE>;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    const size_t dyn_max = ((size_t)optin - fa.sharedSizeBytes) & ~size_t(127);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    auto cap_for = [&](int64_t nr) -> int {  // staged nonzero capacity, -1: the vectors do not fit
+        if (nr < 1 || nr > 65535) return -1;
+        const ResLayout l0 = res_layout<K>((int)nr, 0, has_u);
+        if (l0.total + 64 > dyn_max) return -1;
+        return (int)(((dyn_max - l0.total - 64) / 12) & ~size_t(3));
+    };
+    const int force_rg = env_int("CHEB_RG", 0);
+    const int64_t single_max = env_int("CHEB_RES_SINGLE_MAX", 8192);
+    auto take = [&](int grid, int rg) {
+        const int64_t nr = (d + grid - 1) / grid;
+        fp->res_grid = grid;
+        fp->res_rg = rg;
+        fp->res_nr = (int)nr;
+        // staged capacity: the expected padded slice (rows padded to the gather chunk, plus a
+        // missing diagonal) with room to spare, not all of shared memory
+        const int64_t want = nr * ((nnz + d - 1) / d + CHEB_NNZ_UNROLL);
+        fp->res_cap = (int)std::min<int64_t>(cap_for(nr), (want + 3) & ~int64_t(3));
+        fp->res_smem = res_layout<K>((int)nr, fp->res_cap, has_u).total;
+        const int cap_env = env_int("CHEB_RES_CAP", -1);  // tests: force the unstaged-matrix path
+        if (cap_env >= 0) fp->res_cap = std::min(fp->res_cap, cap_env & ~3);
+        return true;
+    };
+    // one cluster of 16 (non-portable), else 8 CTAs
+    for (int rg : {16, 8}) {
+        if (force_rg && rg != force_rg) continue;
+        const int64_t nr = (d + rg - 1) / rg;
+        if (nr * K > single_max || cap_for(nr) < 0) continue;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        cluster_config(&cfg, at, rg, rg, dyn_max, 0, kResThreads);
+        int maxc = 0;
+        if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (maxc >= 1) return take(rg, rg);
+    }
+    // flat grid: one CTA per SM, every SM (no cluster stranding), at most kResThreads CTAs
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kResThreads, dyn_max) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    const int grid = std::min(occ * sm_count(), kResThreads);
+    if (grid >= 2 && cap_for((d + grid - 1) / grid) >= 0) return take(grid, 1);
+    return false;
+}
+
+template <int K>
+int resident_setup(const cl_operator* op, char* ws, const Layout& L, cudaStream_t st, int sms, Schedule* fp) {
+    const int64_t d = op->A.n_cols;
+    const bool ok = op->kind == CL_OP_CSR ? resident_plan<K, MODE_CSR>(d, op->A.nnz, false, fp)
+                                          : resident_plan<K, MODE_RANK1>(d, op->A.nnz, op->r1_u != nullptr, fp);
+    if (!ok) return CL_OK;
+    fp->resident = true;
+    uint8_t* exp = (uint8_t*)(ws + L.cnt64);  // the prep's row-length scratch is free again
+    CL_CUDA(cudaMemsetAsync(exp, 0, (size_t)d, st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sms * 8));
+    resident_prep_kernel<<<grid, kThreads, 0, st>>>(d, (const int64_t*)(ws + L.rp2), (int32_t*)(ws + L.ci2),
+                                                    fp->res_nr, fp->res_rg, fp->res_grid == fp->res_rg ? 1 : 0, exp);
+    g_launches++;
+    if (getenv("CHEB_DEBUG"))
+        fprintf(stderr, "[chebld] resident grid %d, clusters of %d, %d rows per CTA, cap %d nnz, smem %zu\n",
+                fp->res_grid, fp->res_rg, fp->res_nr, fp->res_cap, fp->res_smem);
+    return CL_OK;
 }
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
@@ -426,6 +521,35 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         g_launches++;
     }
     if (n < 1) return CL_OK;
+
+    if constexpr ((MODE == MODE_CSR || MODE == MODE_RANK1) && K <= 64) if (fp.resident) {
+        ResArgs ra{};
+        ra.g0 = w[0];
+        ra.g1 = w[1];
+        ra.n = n;
+        ra.nr = fp.res_nr;
+        ra.cap = fp.res_cap;
+        ra.power = fp.power ? 1 : 0;
+        ra.exp = (const uint8_t*)(ws + L.cnt64);
+        ra.gpart = (double*)(ws + L.gpart);
+        ra.s_buf = sbuf;
+        ra.bar_count = (unsigned int*)(ws + L.misc + 16);
+        ra.err = (unsigned int*)(ws + L.misc + kStatusOff);
+        a.rg = fp.res_rg;
+        CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        cluster_config(&cfg, at, fp.res_grid, fp.res_rg, fp.res_smem, st, kResThreads);
+        at[1].id = cudaLaunchAttributeCooperative;  // a single cluster is co-scheduled anyway
+        at[1].val.cooperative = 1;
+        // (CHEB_RES_NOCOOP=1: profiling only -- ncu cannot replay cooperative cluster launches; the
+        // grid is the co-resident capacity, so the CTAs are co-scheduled in practice)
+        cfg.numAttrs = fp.res_grid > fp.res_rg && !env_int("CHEB_RES_NOCOOP", 0) ? 2 : 1;
+        ProfScope ps(st, 2);
+        CL_CUDA(cudaLaunchKernelEx(&cfg, cheb_resident_kernel<K, MODE>, a, ra));
+        g_launches++;
+        return CL_OK;
+    }
 
     const int tile = fp.doubling ? GD::TILE : G::TILE;
     a.ntiles = (d + tile - 1) / tile;
@@ -659,6 +783,24 @@ int cheb_set_doubling(int32_t on) {
 }
 
 int cheb_get_doubling(void) { return g_doubling.load(); }
+
+int cheb_set_resident(int32_t mode) {
+    if (mode < 0 || mode > 1) return fail(CL_EINVAL, "resident mode must be 0 or 1");
+    g_resident = mode;
+    return CL_OK;
+}
+
+int cheb_get_resident(void) { return g_resident.load(); }
+
+int cheb_last_schedule(void) { return g_last_schedule; }
+
+#if CHEB_RES_PROF
+// timing builds only (not in the header): per-CTA phase cycles of the last resident launch
+int cheb_res_prof_read(long long* out, int n) {
+    CL_CUDA(cudaMemcpyFromSymbol(out, chebld::g_res_prof, sizeof(long long) * (size_t)std::min(n, 1024 * 8)));
+    return CL_OK;
+}
+#endif
 
 // Host fp64 coefficient routine: accumulate, node by node, f(x_k)
 // times T_j(x_k) for all j with the scalar recurrence, then scale.
@@ -1014,8 +1156,22 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || fp.l2res;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
+    // shared-memory-resident kernel: csr / rank-1 Algorithm 1 (or power basis) when a probe block
+    // fits in the SMs' shared memory; only in the automatic persistent mode
+    if (op->kind != CL_OP_BTB && !fp.doubling && degree >= 1 && probe_block <= 64 && g_persistent.load() == 1 &&
+        g_resident.load() > 0) {
+        switch (probe_block) {
+            case 8: rc = resident_setup<8>(op, ws, L, st, sms, &fp); break;
+            case 16: rc = resident_setup<16>(op, ws, L, st, sms, &fp); break;
+            case 32: rc = resident_setup<32>(op, ws, L, st, sms, &fp); break;
+            default: rc = resident_setup<64>(op, ws, L, st, sms, &fp); break;
+        }
+        if (rc) return rc;
+        if (fp.resident) fp.persistent = false;
+    }
+    g_last_schedule = fp.resident ? 2 : (fp.persistent ? 1 : 0);
     // per-step csr/rank-1: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
-    fp.vbits = !fp.persistent && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
+    fp.vbits = !fp.persistent && !fp.resident && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
     if (getenv("CHEB_DEBUG"))
         fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d doubling=%d small=%d\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,

@@ -25,6 +25,9 @@ VARIANTS = {
     "r1": ["CHEB_RPG=1"],
     "r4": ["CHEB_RPG=4"],
     "checked": ["CHEB_CHECKS=1"],
+    "resprof": ["CHEB_RES_PROF=1"],
+    "resdiag1": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=1"],  # timing diagnostics: wrong results
+    "resdiag2": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=2"],  # per-CTA phase cycles of the resident kernel (scripts/res_phases.py)
     "u4c4": ["CHEB_NNZ_UNROLL=4", "CHEB_MIN_CTAS=4"],
     "u8c3": ["CHEB_NNZ_UNROLL=8", "CHEB_MIN_CTAS=3"],
     "dbl4": ["CHEB_MIN_CTAS_DBL=4"],

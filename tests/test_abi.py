@@ -96,6 +96,9 @@ def test_schedule_controls_validate(L):
     assert L.cheb_set_doubling(-1) == _lib.CL_EINVAL
     assert L.cheb_set_doubling(1) == 0 and L.cheb_get_doubling() == 1
     assert L.cheb_set_doubling(0) == 0 and L.cheb_get_doubling() == 0
+    assert L.cheb_set_resident(2) == _lib.CL_EINVAL
+    assert L.cheb_set_resident(0) == 0 and L.cheb_get_resident() == 0
+    assert L.cheb_set_resident(1) == 0 and L.cheb_get_resident() == 1
     assert L.cheb_set_persistent(3) == _lib.CL_EINVAL
     assert L.cheb_set_persistent(1) == 0
     assert L.cheb_set_small_tiles(2) == _lib.CL_EINVAL

@@ -91,13 +91,14 @@ def test_full_m_parity(orc, schedule, name, k, dbl):
     P.set_doubling(dbl)
     est = P.Estimator(op, a, b, n, m, k, seed=wl.seed)
     gp, stats = est.run(check=True)
+    sched = P.last_schedule()
     mu = est.mu.cpu().numpy()
     gp = gp.cpu().numpy()
     st = stats.cpu().numpy()
     omu, ogp, og, ose = z["mu"], z["gamma_p"], float(z["gamma"]), float(z["stderr"])
     dmu = np.abs(mu - omu)
     dgp = np.abs(gp - ogp)
-    rep = {"config": name, "notes": wl.notes, "k": k, "schedule": "doubling" if dbl else "algorithm1",
+    rep = {"config": name, "notes": wl.notes, "k": k, "schedule": "doubling" if dbl else "algorithm1", "kernel_schedule": sched,
            "m": m, "degree": n, "d": d, "gamma_gpu": float(st[0]), "gamma_oracle": og,
            "rel_err_gamma": abs(st[0] - og) / abs(og), "max_rel_err_gamma_p": float((dgp / np.abs(ogp)).max()),
            "max_abs_err_mu_over_d": float(dmu.max() / d), "rel_err_stderr": abs(st[1] - ose) / ose,
