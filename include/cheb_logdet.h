@@ -300,13 +300,14 @@ int cheb_get_doubling(void);
 
 /* Shared-memory-resident schedule for CL_OP_CSR / CL_OP_CSR_RANK1 (process-wide; default 1; env
  * CHEB_RESIDENT sets the initial value).  Applies only in the automatic persistent mode
- * (cheb_set_persistent(1)), to Algorithm 1 and the power basis (not moment doubling), k <= 64:
+ * (cheb_set_persistent(1)), to Algorithm 1, moment doubling and the power basis, k <= 64:
  *   1 = auto: when one probe block (two d x k fp64 buffers + the CTAs' matrix rows) fits in the
- *       shared memory of one CTA per SM, all n steps run in one cooperative cluster launch in
- *       which every CTA keeps its rows of w_{j-1}, w_{j-2} on chip and gathers other rows over
- *       DSMEM (same cluster) or from a global copy of the rows other clusters need
- *       (cheb_resident_kernel); w_j is bit-identical to the other schedules, the
- *       dot products follow this kernel's grid (deterministic run to run);
+ *       shared memory of one CTA per SM, all n steps run in one launch in which every CTA keeps
+ *       its rows of w_{j-1}, w_{j-2} on chip: small operators in one thread-block cluster
+ *       (other CTAs' rows over DSMEM, one cluster barrier per step), larger ones on a flat
+ *       cooperative grid (other CTAs' rows from a global copy of the rows they need, one grid
+ *       counter per step) (cheb_resident_kernel); w_j is bit-identical to the other
+ *       schedules, the dot products follow this kernel's fixed order (deterministic run to run);
  *   0 = off (the L2-resident persistent kernel or per-step launches).
  * CL_EINVAL for other values. */
 int cheb_set_resident(int32_t mode);

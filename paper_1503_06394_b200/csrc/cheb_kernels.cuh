@@ -1529,7 +1529,9 @@ __device__ long long g_res_prof[1024 * 8];
 #define RES_T(i) ((void)0)
 #endif
 
-template <int K, int MODE>
+// DBL: moment doubling (reading G25): channels w_j^T w_j and w_{j-1}^T w_j (own rows), mu_{2j-1},
+// mu_{2j} written by dbl_write
+template <int K, int MODE, bool DBL = false>
 __global__ void __launch_bounds__(kResThreads, 1)
 cheb_resident_kernel(StepArgs a, ResArgs ra) {
     using G = Geo<K>;
@@ -1541,7 +1543,8 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
     constexpr int U = CHEB_NNZ_UNROLL;
     constexpr int WORDS = G::WORDS;
     constexpr bool HAS_S = (MODE == MODE_RANK1);
-    constexpr int NCH = HAS_S ? 2 : 1;
+    constexpr int NCH = n_channels<MODE, DBL>();  // mu channel(s), then u^T w_j
+    constexpr int NMU = DBL ? 2 : 1;               // channels that make moments
     constexpr int NW = NT / 32;
     static_assert(kPPL == 4, "resident kernel: 4 probes per lane");
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1550,7 +1553,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
     __shared__ double fin[NCH][K];
     __shared__ double s_sh[HAS_S ? K : 1];
     __shared__ double red2[HAS_S ? NT / K : 1][K];  // flat grid: s_j second level
-    __shared__ double red_mu[NW];                   // flat grid: mu_j of this CTA's probe
+    __shared__ double red_mu[NMU][NW];              // flat grid: mu_j of this CTA's probe
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lg = tid % L, grp = tid / L;
@@ -1560,7 +1563,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
     const int RG = a.rg, NG = (int)gridDim.x;
     const bool single = RG == NG;
     const int crank = (int)cluster.block_rank();
-    double mu_pend = 0.0;  // flat grid: part[tid][p] of step mu_j, summed one step later
+    double mu_pend[NMU] = {};  // flat grid: part[tid][p] of step mu_j, summed one step later
     int32_t mu_j = 0;
     const int64_t r0 = (int64_t)blockIdx.x * ra.nr;
     const int nr = (int)(a.d - r0 < (int64_t)ra.nr ? (a.d - r0 > 0 ? a.d - r0 : 0) : ra.nr);
@@ -1612,14 +1615,26 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
     const double* va_g = a.va;
     asm volatile("" : "+l"(g0), "+l"(g1), "+l"(mu_out), "+l"(gpart), "+l"(bar_count), "+l"(err), "+l"(r1u));
     asm volatile("" : "+d"(r1ca), "+l"(mu_stride), "+r"(n_steps), "+r"(power), "+r"(kvalid), "+l"(ci_g), "+l"(va_g));
+    // flat grid: the moments of step j (probe blockIdx.x) from the published partials
+    auto mu_write = [&](double* row, int32_t jj, double q, double r) {
+        if (DBL) dbl_write(row, jj, mu_stride - 1, q, r);
+        else row[jj] = q;
+    };
     auto mu_flush = [&]() {  // flat grid, after the last step
-        double m = warp_sum_xor(mu_pend);
-        if (lane == 0) red_mu[warp] = m;
+#pragma unroll
+        for (int c = 0; c < NMU; c++) {
+            const double m = warp_sum_xor(mu_pend[c]);
+            if (lane == 0) red_mu[c][warp] = m;
+        }
         __syncthreads();
         if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < NW; w++) t += red_mu[w];
-            mu_out[(size_t)blockIdx.x * mu_stride + mu_j] = t;
+            double t[NMU];
+#pragma unroll
+            for (int c = 0; c < NMU; c++) {
+                t[c] = 0.0;
+                for (int w = 0; w < NW; w++) t[c] += red_mu[c][w];
+            }
+            mu_write(mu_out + (size_t)blockIdx.x * mu_stride, mu_j, t[0], t[NMU - 1]);
         }
     };
     cluster.sync();  // every peer's w_0 rows are in place
@@ -1714,9 +1729,17 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
                     }
                     *wp = nw;
                     if (ex) __stcg(reinterpret_cast<double2*>(gn + (size_t)(r0 + lr) * K + pp[sl]), nw);
-                    const uint32_t bits = sg_s[lr * WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
-                    acc[0][2 * sl] += signflip(nw.x, bits << 31);
-                    acc[0][2 * sl + 1] += signflip(nw.y, bits << 30);
+                    if (DBL) {  // w_j^T w_j and w_{j-1}^T w_j over the own rows
+                        const double2 ow = lds2(wo_s + (lr * RS + pp[sl]) * 8);
+                        acc[0][2 * sl] = fma(nw.x, nw.x, acc[0][2 * sl]);
+                        acc[0][2 * sl + 1] = fma(nw.y, nw.y, acc[0][2 * sl + 1]);
+                        acc[1][2 * sl] = fma(ow.x, nw.x, acc[1][2 * sl]);
+                        acc[1][2 * sl + 1] = fma(ow.y, nw.y, acc[1][2 * sl + 1]);
+                    } else {  // v^T w_j: the sign bit of w flipped where the probe bit is set
+                        const uint32_t bits = sg_s[lr * WORDS + (pp[sl] >> 5)] >> (pp[sl] & 31);
+                        acc[0][2 * sl] += signflip(nw.x, bits << 31);
+                        acc[0][2 * sl + 1] += signflip(nw.y, bits << 30);
+                    }
                     if (HAS_S) {
                         acc[NCH - 1][2 * sl] = fma(ui, nw.x, acc[NCH - 1][2 * sl]);
                         acc[NCH - 1][2 * sl + 1] = fma(ui, nw.y, acc[NCH - 1][2 * sl + 1]);
@@ -1742,16 +1765,23 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             }
         }
         if (!single && mu_j > 0) {  // the previous step's mu (flat grid): one butterfly, warps ascending
-            double m = warp_sum_xor(mu_pend);
-            if (lane == 0) red_mu[warp] = m;
+#pragma unroll
+            for (int c = 0; c < NMU; c++) {
+                const double m = warp_sum_xor(mu_pend[c]);
+                if (lane == 0) red_mu[c][warp] = m;
+            }
         }
         __syncthreads();
         RES_T(0);
         if (!single && mu_j > 0) {
             if (tid == 0) {
-                double m = 0.0;
-                for (int w = 0; w < NW; w++) m += red_mu[w];
-                mu_out[(size_t)blockIdx.x * mu_stride + mu_j] = m;
+                double t[NMU];
+#pragma unroll
+                for (int c = 0; c < NMU; c++) {
+                    t[c] = 0.0;
+                    for (int w = 0; w < NW; w++) t[c] += red_mu[c][w];
+                }
+                mu_write(mu_out + (size_t)blockIdx.x * mu_stride, mu_j, t[0], t[NMU - 1]);
             }
             mu_j = 0;
         }
@@ -1780,7 +1810,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             }
             __syncthreads();
             RES_T(3);
-            if (blockIdx.x == gridDim.x - 1 && tid < kvalid) mu_out[(size_t)tid * mu_stride + j] = fin[0][tid];
+            if (blockIdx.x == gridDim.x - 1 && tid < kvalid) mu_write(mu_out + (size_t)tid * mu_stride, j, fin[0][tid], fin[NMU - 1][tid]);
             if (want_s && tid < K) s_sh[tid] = fin[NCH - 1][tid];
         } else {
             // ---- flat grid (one CTA per SM, no clusters): every CTA publishes its partial, one
@@ -1798,7 +1828,9 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             // mu_j of probe blockIdx.x (CTAs < K), summed during the next step's partial reduction:
             // thread t holds part[t][p]
             if (blockIdx.x < (unsigned)kvalid) {
-                mu_pend = tid < NG ? __ldcg(pg + (size_t)tid * K + blockIdx.x) : 0.0;
+#pragma unroll
+                for (int c = 0; c < NMU; c++)
+                    mu_pend[c] = tid < NG ? __ldcg(pg + ((size_t)c * NG + tid) * K + blockIdx.x) : 0.0;
                 mu_j = j;
             }
             if (want_s) {

@@ -383,9 +383,9 @@ int persist_grid(Kern pk, int64_t ntiles, int sms, size_t smem, int* grid_out, i
 // with at most CHEB_RES_SINGLE_MAX (default 8192) row-probes per CTA: no grid-wide barrier at all
 // (configs[0]); otherwise clusters of 16/8/4/2 over the co-resident SMs, the largest cluster whose
 // grid is within 15 % of the best (configs[1] at k <= 16).  false: the block does not fit.
-template <int K, int MODE>
+template <int K, int MODE, bool DBL>
 bool resident_plan(int64_t d, int64_t nnz, bool has_u, Schedule* fp) {
-    auto kern = cheb_resident_kernel<K, MODE>;
+    auto kern = cheb_resident_kernel<K, MODE, DBL>;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -443,16 +443,20 @@ bool resident_plan(int64_t d, int64_t nnz, bool has_u, Schedule* fp) {
         cudaGetLastError();
         return false;
     }
-    const int grid = std::min(occ * sm_count(), kResThreads);
-    if (grid >= 2 && cap_for((d + grid - 1) / grid) >= 0) return take(grid, 1);
+    const int grid = std::min(occ * sm_count(), kResThreads);  // CTA p reduces probe p's moments
+    if (grid >= 2 && grid >= K && cap_for((d + grid - 1) / grid) >= 0) return take(grid, 1);
     return false;
 }
 
 template <int K>
 int resident_setup(const cl_operator* op, char* ws, const Layout& L, cudaStream_t st, int sms, Schedule* fp) {
     const int64_t d = op->A.n_cols;
-    const bool ok = op->kind == CL_OP_CSR ? resident_plan<K, MODE_CSR>(d, op->A.nnz, false, fp)
-                                          : resident_plan<K, MODE_RANK1>(d, op->A.nnz, op->r1_u != nullptr, fp);
+    const bool has_u = op->r1_u != nullptr;
+    const bool ok = op->kind == CL_OP_CSR
+                        ? (fp->doubling ? resident_plan<K, MODE_CSR, true>(d, op->A.nnz, false, fp)
+                                        : resident_plan<K, MODE_CSR, false>(d, op->A.nnz, false, fp))
+                        : (fp->doubling ? resident_plan<K, MODE_RANK1, true>(d, op->A.nnz, has_u, fp)
+                                        : resident_plan<K, MODE_RANK1, false>(d, op->A.nnz, has_u, fp));
     if (!ok) return CL_OK;
     fp->resident = true;
     uint8_t* exp = (uint8_t*)(ws + L.cnt64);  // the prep's row-length scratch is free again
@@ -526,7 +530,7 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         ResArgs ra{};
         ra.g0 = w[0];
         ra.g1 = w[1];
-        ra.n = n;
+        ra.n = fp.doubling ? (n + 1) / 2 : n;
         ra.nr = fp.res_nr;
         ra.cap = fp.res_cap;
         ra.power = fp.power ? 1 : 0;
@@ -546,7 +550,8 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         // grid is the co-resident capacity, so the CTAs are co-scheduled in practice)
         cfg.numAttrs = fp.res_grid > fp.res_rg && !env_int("CHEB_RES_NOCOOP", 0) ? 2 : 1;
         ProfScope ps(st, 2);
-        CL_CUDA(cudaLaunchKernelEx(&cfg, cheb_resident_kernel<K, MODE>, a, ra));
+        if (fp.doubling) CL_CUDA(cudaLaunchKernelEx(&cfg, cheb_resident_kernel<K, MODE, true>, a, ra));
+        else CL_CUDA(cudaLaunchKernelEx(&cfg, cheb_resident_kernel<K, MODE, false>, a, ra));
         g_launches++;
         return CL_OK;
     }
@@ -1156,9 +1161,9 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         if (g_persistent.load() > 0 && degree >= 1) fp.persistent = g_persistent.load() == 2 || fp.l2res;
         if (getenv("CHEB_DEBUG")) fprintf(stderr, "[chebld] L2=%d working set=%.0f\n", l2, wset);
     }
-    // shared-memory-resident kernel: csr / rank-1 Algorithm 1 (or power basis) when a probe block
-    // fits in the SMs' shared memory; only in the automatic persistent mode
-    if (op->kind != CL_OP_BTB && !fp.doubling && degree >= 1 && probe_block <= 64 && g_persistent.load() == 1 &&
+    // shared-memory-resident kernel: csr / rank-1 (Algorithm 1, moment doubling, power basis) when
+    // a probe block fits in the SMs' shared memory; only in the automatic persistent mode
+    if (op->kind != CL_OP_BTB && degree >= 1 && probe_block <= 64 && g_persistent.load() == 1 &&
         g_resident.load() > 0) {
         switch (probe_block) {
             case 8: rc = resident_setup<8>(op, ws, L, st, sms, &fp); break;

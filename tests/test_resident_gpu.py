@@ -109,6 +109,21 @@ def test_resident_flat_grid(orc, env, name, k):
 
 
 @pytest.mark.parametrize("single", [True, False])
+@pytest.mark.parametrize("name,k", [("gmrf_s", 16), ("torus_s", 16), ("gmrf32", 64), ("spd_csr", 8)])
+def test_resident_moment_doubling(orc, env, single, name, k):
+    """Moment doubling (reading G25) on the resident kernel: ceil(n/2) steps give mu_0..mu_n."""
+    if not single:
+        env(CHEB_RES_SINGLE_MAX=0)
+    P.set_doubling(True)
+    try:
+        wl, r, sched, mu, g, gp, se = _run(orc, name, k)
+    finally:
+        P.set_doubling(False)
+    assert sched == "resident"
+    _check(wl, r, mu, g, gp, se)
+
+
+@pytest.mark.parametrize("single", [True, False])
 def test_resident_unstaged_matrix(orc, env, single):
     """A CTA whose matrix rows exceed the staged capacity gathers col/val from global memory."""
     env(CHEB_RES_CAP=0, **({} if single else {"CHEB_RES_SINGLE_MAX": 0}))
