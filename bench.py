@@ -46,28 +46,34 @@ def _peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
-def _traffic_per_launch(workload, k, kernel="step"):
-    """dram read+write bytes per launch from the committed ncu --set full summaries."""
+def _traffic_per_launch(workload, k, kernel="step", cv=False):
+    """dram read+write bytes per launch from the committed ncu --set full summaries (key suffix
+    /cv: measured with the compressed matrix copy)."""
     p = os.path.join(ROOT, "profiles", "ncu_step_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         j = json.load(f)
-    e = j.get(f"{workload}/k{k}" + ("" if kernel == "step" else f"/{kernel}"))
+    e = j.get(f"{workload}/k{k}" + ("" if kernel == "step" else f"/{kernel}") + ("/cv" if cv else ""))
     return float(e["dram_bytes_per_launch"]) if e else None
 
 
-def step_bytes(d, nnz, k, first=False, mode="csr", doubling=False):
+CV_U = 5  # entries per row of the compressed matrix copy (CHEB_NNZ_UNROLL)
+
+
+def step_bytes(d, nnz, k, first=False, mode="csr", doubling=False, cv=False):
     """Algorithmic HBM bytes of one cheb_step_kernel launch over a block of k probes
     (SURVEY §8(d)): gather matrix (val 8 + col 4 per nnz, row_ptr 8 per
-    row) once per block; per row and probe 8 B each for the gather source read, W_prev
-    read and W_next write (no W_prev on the first step) -- plus, for B^T B, the W_cur
-    read of the -beta*w term; sign bits (4 B per row per 32 probes, >= 4; the
+    row; the compressed copy when the library used it: 3 bytes per entry of U = 5 per row, no
+    row pointer, a 2 KB value table) once per block; per row and probe 8 B each for the gather
+    source read, W_prev read and W_next write (no W_prev on the first step) -- plus, for B^T B,
+    the W_cur read of the -beta*w term; sign bits (4 B per row per 32 probes, >= 4; the
     moment-doubling schedule reads none: its dots are w_j.w_j and w_j.w_{j-1})."""
     vec = (16 if first else 24) * d * k
     if mode == "btb":
         vec += 8 * d * k
-    return 12 * nnz + 8 * (d + 1) + vec + (0 if doubling else d * max(4, k // 8))
+    mat = 3 * CV_U * d + 2048 if cv else 12 * nnz + 8 * (d + 1)
+    return mat + vec + (0 if doubling else d * max(4, k // 8))
 
 
 def spmm_bytes(d, nnz_b, k):
@@ -260,7 +266,7 @@ def timed_region(sh, steps, flush_buf, P, torch, dist, world, dev):
     return float(elapsed.item()), prof, launches, all_stats
 
 
-def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind, sched="per_step"):
+def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind, sched="per_step", cv=False):
     """Roofline of the dominant kernel from its measured launch times and algorithmic bytes."""
     d = wl.d
     gnnz = A.nnz if wl.mode != "btb" else At.nnz  # gather matrix of the step kernel
@@ -278,10 +284,10 @@ def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind, sche
         kern = f"cheb_step_kernel<{k},{wl.mode}>"
         per_block = s_n / max(blocks * steps, 1)
         if args.basis == "taylor":  # power recurrence: every launch reads w_{j-1}, writes w_j
-            tot = s_n * step_bytes(d, gnnz, k, True, wl.mode)
+            tot = s_n * step_bytes(d, gnnz, k, True, wl.mode, cv=cv)
         else:
-            tot = blocks * steps * (step_bytes(d, gnnz, k, True, wl.mode, dbl)
-                                    + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode, dbl))
+            tot = blocks * steps * (step_bytes(d, gnnz, k, True, wl.mode, dbl, cv)
+                                    + (per_block - 1) * step_bytes(d, gnnz, k, False, wl.mode, dbl, cv))
         nl = s_n
         if wl.mode == "btb" and b_n:
             # one B^T B application = spmm (Y = B w) + step (B^T Y, recurrence, dots): both halves
@@ -301,7 +307,8 @@ def roofline(wl, A, At, k, blocks, steps, t_ms, prof, args, hbm, peak_kind, sche
             "peak_kind": peak_kind, "frac_vs_nominal_8000": achieved / 8000.0, "kernel": kern,
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
             "launches": int(nl), "step_kernel_share": dom_ms / t_ms,
-            "traffic": _traffic_per_launch(wl.name, k), "gather_aware": gather_aware,
+            "matrix_format": "compressed (3 B per entry, DESIGN.md §6)" if cv else "csr (12 B per nonzero)",
+            "traffic": _traffic_per_launch(wl.name, k, cv=cv), "gather_aware": gather_aware,
             "note": ("shared-memory-resident kernel: the vectors never reach HBM; achieved = the HBM step "
                      "model's bytes / time (equivalent bandwidth)" if sched == "resident" else
                      "L2-resident persistent kernel: HBM step-model bytes / time (equivalent bandwidth)"
@@ -368,6 +375,7 @@ def run_ours(args):
     t_ms, prof, launches, all_stats = timed_region(sh, args.steps, flush_buf, P, torch, dist, world, dev)
     clk = clocks.stop() if rank == 0 else None
     sched = P.last_schedule()
+    cv = bool(P.workspace_status(sh.est.workspace) & 0x100)  # the per-step kernels read the compressed copy
     st = all_stats[-1].cpu().numpy()
 
     # ---- weak scaling beside the headline: m per GPU fixed, best single-GPU block size
@@ -380,9 +388,10 @@ def run_ours(args):
         reps = max(1, min(args.steps, 3))
         tw, profw, _, stw = timed_region(sw, reps, flush_buf, P, torch, dist, world, dev)
         sched_w = P.last_schedule()
+        cv_w = bool(P.workspace_status(sw.est.workspace) & 0x100)
         hbm, peak_kind = _peaks()
         rw = roofline(wl, A, At, k_w, math.ceil((m_w // world) / k_w), reps, tw, profw, args, hbm, peak_kind,
-                      sched_w)
+                      sched_w, cv_w)
         weak = {"scaling": "weak", "num_probes": m_w, "probes_per_gpu": m_w // world, "probe_block": k_w,
                 "value": m_w * wl.degree * reps / (tw / 1e3), "unit": UNIT, "ms_per_step": tw / reps,
                 "steps": reps, "logdet_wall_s": tw / reps / 1e3, "gamma": float(stw[-1].cpu().numpy()[0]),
@@ -408,7 +417,7 @@ def run_ours(args):
     hbm, peak_kind = _peaks()
     nnz = A.nnz + (At.nnz if At is not None else 0)
     blocks = math.ceil(m_mine / k)
-    roof = roofline(wl, A, At, k, blocks, args.steps, t_ms, prof, args, hbm, peak_kind, sched)
+    roof = roofline(wl, A, At, k, blocks, args.steps, t_ms, prof, args, hbm, peak_kind, sched, cv)
     cfg = {"workload": wl.name, "baseline_config": wl.notes, "mode": wl.mode, "d": wl.d,
            "nnz": int(nnz), "degree": wl.degree, "num_probes": m_total, "probes_per_gpu": m_mine,
            "probe_block": k, "a": a, "b": b, "basis": args.basis,

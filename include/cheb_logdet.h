@@ -193,7 +193,11 @@ int cheb_finalize(const double *mu, const double *c, int64_t m, int32_t degree,
  * that used `workspace` (DEVICE pointer; the word sits at a fixed offset of every workspace):
  *   bit 0 (1) = a grid-wide spin wait of the persistent kernel gave up after ~seconds without
  *               progress (CTAs not co-resident); that call's moments were set to NaN;
- *   bit 1 (2) = a moment of that call is not finite ([a,b] does not enclose the spectrum).
+ *   bit 1 (2) = a moment of that call is not finite ([a,b] does not enclose the spectrum);
+ *   bit 8 (0x100, informational, not an error) = the per-step kernels of that call read the
+ *               compressed matrix copy (uniform padded rows, int16 column deltas, <= 128 distinct
+ *               values: 3 bytes per entry instead of 12); moments are bit-identical
+ *               to the plain copy.  Env CHEB_CV=0 disables the compressed copy.
  * *status is a HOST uint32; synchronises `stream` (enqueue after the call, same stream). */
 int cheb_workspace_status(const void *workspace, uint32_t *status, void *stream);
 

@@ -351,7 +351,7 @@ def profile_end():
             "persistent": (pms.value, pn.value)}
 
 
-STATUS_TIMEOUT, STATUS_NONFINITE = 1, 2
+STATUS_TIMEOUT, STATUS_NONFINITE, STATUS_COMPRESSED = 1, 2, 0x100  # 0x100: informational
 
 
 def workspace_status(workspace: torch.Tensor, stream=None) -> int:

@@ -308,6 +308,13 @@ struct StepArgs {
     int64_t mu_stride;
     int32_t mu_col;
     int32_t kvalid;       // probes of this block that exist (<= K)
+    // compressed gather matrix (csr / rank-1 per-step kernels; cv_prep_kernels): usable when
+    // *cv_ok != 0 -- every prepped row has exactly CHEB_NNZ_UNROLL entries, entry e of row i is
+    // (i + cv_dc[e], cv_tab[cv_vi[e]])
+    const int32_t* cv_ok;
+    const int16_t* cv_dc;
+    const uint8_t* cv_vi;
+    const double* cv_tab;  // [kCvSlots]
 };
 
 // ---------------------------------------------------------------------------------------
@@ -578,6 +585,85 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
 }
 
 // ---------------------------------------------------------------------------------------
+// Compressed gather matrix (the "CV" format: value-indexed, delta-coded columns -- the matrix
+// compression of the SpMV literature).  When every prepped row has exactly U = CHEB_NNZ_UNROLL
+// entries, every column is within int16 of its row and the prepped values take at most
+// kCvMaxValues distinct bit patterns (stencil precisions, graph Laplacians: configs[0..3]), an
+// entry costs 3 bytes (int16 column delta + uint8 value index) instead of 12, and the row pointer
+// is implicit (row i = entries [U i, U i + U)): at configs[3], k = 16, 11.37 -> 10.05 GB per step.
+// The decoded (column, value) pairs are bit-identical to the plain copy, so are the moments.
+// The format check runs on the device (no host round trip): cv_ok stays 1 only if it holds.
+// ---------------------------------------------------------------------------------------
+constexpr int kCvSlots = 256;       // open-addressing table of value bit patterns
+constexpr int kCvMaxValues = 128;   // at most half full: short probe chains
+constexpr uint64_t kCvEmpty = ~0ull;
+
+__device__ __forceinline__ int cv_hash(uint64_t k) { return (int)((k * 0x9E3779B97F4A7C15ull) >> 56); }
+
+// Insert every prepped value into the table (tab: kCvSlots keys, set to kCvEmpty; meta[0] = ok,
+// meta[1] = distinct count).  Each thread remembers its last 4 distinct values, so a matrix with
+// a handful of values touches the table a handful of times per thread.
+__global__ void __launch_bounds__(kThreads)
+cv_values_kernel(int64_t total, const double* __restrict__ va2, unsigned long long* __restrict__ tab,
+                 int32_t* __restrict__ meta) {
+    uint64_t seen[4] = {kCvEmpty, kCvEmpty, kCvEmpty, kCvEmpty};
+    int ns = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = (uint64_t)__double_as_longlong(va2[e]);
+        if (k == seen[0] || k == seen[1] || k == seen[2] || k == seen[3]) continue;
+        if (k == kCvEmpty || *(volatile int32_t*)meta == 0) {
+            meta[0] = 0;
+            return;
+        }
+        int h = cv_hash(k), n = 0;
+        for (; n < kCvSlots; n++, h = (h + 1) & (kCvSlots - 1)) {
+            const unsigned long long prev = atomicCAS(tab + h, (unsigned long long)kCvEmpty, (unsigned long long)k);
+            if (prev == kCvEmpty) {  // inserted
+                if (atomicAdd(meta + 1, 1) + 1 > kCvMaxValues) meta[0] = 0;
+                break;
+            }
+            if (prev == k) break;  // present
+        }
+        if (n == kCvSlots) meta[0] = 0;
+        seen[ns++ & 3] = k;
+    }
+}
+
+// Encode the prepped copy: uniform rows (padded length U), int16 column deltas, value indices
+// (slots of the table).  Any violation clears meta[0].
+__global__ void __launch_bounds__(kThreads)
+cv_encode_kernel(int64_t d, const int64_t* __restrict__ rp2, const int32_t* __restrict__ ci2,
+                 const double* __restrict__ va2, const unsigned long long* __restrict__ tab,
+                 int16_t* __restrict__ dc, uint8_t* __restrict__ vi, int32_t* __restrict__ meta) {
+    constexpr int U = CHEB_NNZ_UNROLL;
+    __shared__ unsigned long long t[kCvSlots];
+    for (int x = threadIdx.x; x < kCvSlots; x += blockDim.x) t[x] = tab[x];
+    __syncthreads();
+    bool ok = true;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+        if (rp2[i] != U * i || rp2[i + 1] != U * (i + 1)) {
+            ok = false;
+            break;
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int64_t e = U * i + q;
+            const int64_t del = (int64_t)ci2[e] - i;
+            const uint64_t k = (uint64_t)__double_as_longlong(va2[e]);
+            int h = cv_hash(k), n = 0;
+            while (t[h] != k && n < kCvSlots) {
+                h = (h + 1) & (kCvSlots - 1);
+                n++;
+            }
+            ok = ok && del >= -32768 && del <= 32767 && n < kCvSlots;
+            dc[e] = (int16_t)del;
+            vi[e] = (uint8_t)h;
+        }
+    }
+    if (!ok) meta[0] = 0;
+}
+
+// ---------------------------------------------------------------------------------------
 // K1: probe initialisation.  W_cur[i][p] = v_p[i] = +-1 (global probe p0+p), sign bits,
 // mu_0 = v^T v (= d exactly), rank-1 s_0 = u^T v.
 // ---------------------------------------------------------------------------------------
@@ -663,12 +749,15 @@ __host__ __device__ constexpr int n_channels() { return (DBL ? 2 : 1) + (MODE ==
 // VB: the probe vector v = w_0 is never materialised in HBM on the per-step path, its sign bits
 // stand in for it: VB = 1 (step 1) gathers v from the bits, VB = 2 (step 2) takes w_{j-2} = v
 // from the staged bits.  x * (+-1) is exact, so results are bit-identical to reading v.
+// CV: the tile's matrix is staged in the compressed format (int16 column deltas in the col slot,
+// uint8 value indices in the val slot, table cvt in shared memory; rows of exactly U entries).
 template <int K, int MODE, bool FIRST, bool STAGED, bool CG = false, bool DBL = false,
-          bool WCS = false, int R4 = CHEB_RPG, int VB = 0>
+          bool WCS = false, int R4 = CHEB_RPG, int VB = 0, bool CV = false>
 __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char* st, int64_t r0, int rows,
                                           int64_t base_c, int64_t base_v, const double2 (&r1)[kPPL / 2],
                                           double (&acc)[n_channels<MODE, DBL>()][kPPL], const double* xg,
-                                          const double* wcur, double* wout, const double* fcoef = nullptr) {
+                                          const double* wcur, double* wout, const double* fcoef = nullptr,
+                                          const double* cvt = nullptr) {
     using G = Geo<K, R4>;
     using SL = StageLayout<K, MODE, WCS, R4>;
     constexpr int NSL = G::NSL;
@@ -698,7 +787,7 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         const int lr = grp + rr * G::GROUPS;
         if (lr >= rows) break;
         const int64_t i = r0 + lr;
-        const int64_t e_lo = rp_s[lr], e_hi = rp_s[lr + 1];
+        const int64_t e_lo = CV ? 0 : rp_s[lr], e_hi = CV ? CHEB_NNZ_UNROLL : rp_s[lr + 1];
         CHEB_ASSERT(rows <= G::TILE && i < a.d && e_lo <= e_hi);
         // 32-bit row-local offsets (a row's nnz and its staged slice fit in int32)
         const int nr = (int)(e_hi - e_lo);
@@ -724,6 +813,8 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
         CHEB_ASSERT(nr % CHEB_NNZ_UNROLL == 0);
         const int32_t* crow = STAGED ? col_s + oc : a.ci + e_lo;
         const double* vrow = STAGED ? val_s + ov : a.va + e_lo;
+        const int16_t* dcrow = reinterpret_cast<const int16_t*>(st + SL::OFF_COL) + lr * CHEB_NNZ_UNROLL;
+        const uint8_t* virow = reinterpret_cast<const uint8_t*>(st + SL::OFF_VAL) + lr * CHEB_NNZ_UNROLL;
         for (int t0 = 0; t0 < nr; t0 += CHEB_NNZ_UNROLL) {
             int32_t c[CHEB_NNZ_UNROLL];
             double v[CHEB_NNZ_UNROLL];
@@ -731,9 +822,14 @@ __device__ __forceinline__ void step_tile(const StepArgs& a, const unsigned char
             for (int q = 0; q < CHEB_NNZ_UNROLL; q++) {
                 CHEB_ASSERT(!STAGED || (oc + t0 + q >= 0 && oc + t0 + q < G::CAP + 8));
                 CHEB_ASSERT(!STAGED || (ov + t0 + q >= 0 && ov + t0 + q < G::CAP + 4));
-                c[q] = STAGED ? crow[t0 + q] : __ldg(crow + t0 + q);
+                if (CV) {
+                    c[q] = (int32_t)i + (int32_t)dcrow[t0 + q];
+                    v[q] = cvt[virow[t0 + q]];
+                } else {
+                    c[q] = STAGED ? crow[t0 + q] : __ldg(crow + t0 + q);
+                    v[q] = STAGED ? vrow[t0 + q] : __ldg(vrow + t0 + q);
+                }
                 CHEB_ASSERT(c[q] >= 0 && (int64_t)c[q] < a.d);
-                v[q] = STAGED ? vrow[t0 + q] : __ldg(vrow + t0 + q);
             }
             double2 x[CHEB_NNZ_UNROLL][NSL];
             if (VB == 1) {  // gather v = +-1 from the sign bits (4-8 B per row instead of 8K)
@@ -897,6 +993,13 @@ cheb_step_kernel(StepArgs a) {
     __shared__ __align__(16) double s_fcoef[MODE == MODE_FAM ? 3 * K : 2];
     if (MODE == MODE_FAM)
         for (int x = tid; x < 3 * K; x += kThreads) s_fcoef[x] = a.fam_coef[x];
+    // compressed matrix (csr / rank-1): decided on the device by the CV prep, uniform per launch
+    // (the value-index slice of a tile must start 16-byte aligned: U * TILE % 16 == 0)
+    constexpr bool CAN_CV = (MODE == MODE_CSR || MODE == MODE_RANK1) && G::TILE % 16 == 0;
+    __shared__ double s_cvt[CAN_CV ? kCvSlots : 1];
+    const bool cv = CAN_CV && a.cv_ok && *a.cv_ok != 0;
+    if (cv)
+        for (int x = tid; x < kCvSlots; x += kThreads) s_cvt[x] = a.cv_tab[x];
     double acc[NCH][kPPL];
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++)
@@ -924,19 +1027,26 @@ cheb_step_kernel(StepArgs a) {
         const uint32_t wbytes = (uint32_t)rows * K * 8;
         constexpr bool SIGNS = !DBL || VB != 0;  // DBL reads no sign bits, except for v itself
         const uint32_t sgbytes = SIGNS ? ((uint32_t)rows * G::WORDS * 4 + 15) & ~15u : 0u;
-        uint32_t bytes = G::RPBYTES + sgbytes;
+        // compressed: no row pointer, 2 + 1 bytes per entry (the arrays carry 16 bytes of tail padding)
+        constexpr int UCV = CHEB_NNZ_UNROLL;
+        const uint32_t dcbytes = ((uint32_t)rows * UCV * 2 + 15) & ~15u, vibytes = ((uint32_t)rows * UCV + 15) & ~15u;
+        uint32_t bytes = (cv ? 0u : (uint32_t)G::RPBYTES) + sgbytes;
         if (!FIRST && VB != 2) bytes += wbytes;
         if (SL::HAS_WC) bytes += wbytes;
-        if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
+        if (cv) bytes += dcbytes + vibytes;
+        else if (fit) bytes += (uint32_t)(c1 - c0) * 4 + (uint32_t)(v1 - v0) * 8;
         const uint32_t ubytes = ((uint32_t)rows * 8 + 15) & ~15u;
         if ((HAS_S || MODE == MODE_FAM) && a.r1u) bytes += ubytes;
         mbar_expect_tx(&bar[b], bytes);
-        bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
+        if (!cv) bulk_g2s(st + SL::OFF_RP, a.rp + r0, G::RPBYTES, &bar[b]);
         if (SIGNS) bulk_g2s(st + SL::OFF_SGN, a.sbits + (size_t)r0 * G::WORDS, sgbytes, &bar[b]);
         if (!FIRST && VB != 2)
             bulk_g2s_hint(st + SL::OFF_WPREV, a.wnext + (size_t)r0 * K, wbytes, &bar[b], policy_evict_first());
         if (SL::HAS_WC) bulk_g2s(st + SL::OFF_WCUR, a.wcur + (size_t)r0 * K, wbytes, &bar[b]);
-        if (fit) {
+        if (cv) {
+            bulk_g2s(st + SL::OFF_COL, a.cv_dc + (size_t)r0 * UCV, dcbytes, &bar[b]);
+            bulk_g2s(st + SL::OFF_VAL, a.cv_vi + (size_t)r0 * UCV, vibytes, &bar[b]);
+        } else if (fit) {
             bulk_g2s(st + SL::OFF_COL, a.ci + c0, (uint32_t)(c1 - c0) * 4, &bar[b]);
             bulk_g2s(st + SL::OFF_VAL, a.va + v0, (uint32_t)(v1 - v0) * 8, &bar[b]);
         }
@@ -986,12 +1096,18 @@ cheb_step_kernel(StepArgs a) {
             cp_async_wait_all();
             issue(tile_of(it - 1 + NS), pb, s_ne[0], s_ne[1]);
         }
-        if (tid == 0 && it + NS < nmine) bounds_async(tile_of(it + NS));  // consumed below
+        if (tid == 0 && it + NS < nmine && !cv) bounds_async(tile_of(it + NS));  // consumed below
         mbar_wait(&bar[b], phase);
         const unsigned char* st = smem + b * SL::BYTES;
         const int64_t r0 = t * G::TILE;
         const int rows = (int)imin64((int64_t)G::TILE, a.d - r0);
-        if (s_fit[b])
+        if constexpr (CAN_CV) {
+            if (cv)
+                step_tile<K, MODE, FIRST, true, false, DBL, WCS, R4, VB, true>(a, st, r0, rows, 0, 0, r1, acc, a.xg,
+                                                                         a.wcur, a.wnext, s_fcoef, s_cvt);
+        }
+        if (cv) {
+        } else if (s_fit[b])
             step_tile<K, MODE, FIRST, true, false, DBL, WCS, R4, VB>(a, st, r0, rows, s_base_c[b], s_base_v[b], r1,
                                                                acc, a.xg, a.wcur, a.wnext, s_fcoef);
         else
@@ -1130,8 +1246,9 @@ lanczos_probe_kernel(int64_t d, uint64_t seed, uint64_t p0, double* w) {
 // moment (operator spectrum outside [a,b]).  mu: the call's rows, contiguous.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
-moments_status_kernel(unsigned int* status, double* mu, int64_t nmu) {
+moments_status_kernel(unsigned int* status, double* mu, int64_t nmu, const int32_t* cv_ok) {
     const bool poison = (*reinterpret_cast<volatile unsigned int*>(status) & 1u) != 0;
+    if (cv_ok && blockIdx.x == 0 && threadIdx.x == 0 && *cv_ok) atomicOr(status, 0x100u);  // format note
     int bad = 0;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nmu; x += (int64_t)gridDim.x * blockDim.x) {
         if (poison) mu[x] = __longlong_as_double(0x7ff8000000000000ll);

@@ -153,6 +153,7 @@ int tile_rows_max(int k) { return tile_rows(k, std::max(CHEB_RPG, CHEB_RPG_DBL))
 
 struct Layout {
     size_t misc, w0, w1, y, sbits, part, gpart, sbuf, ticket;
+    size_t cv_meta, cv_tab, cv_dc, cv_vi;  // compressed gather matrix (csr / rank-1)
     size_t rp2, ci2, va2, u2, fcoef, cnt64, scan, total;
     size_t scan_bytes;
     int64_t rp2_len;
@@ -160,7 +161,8 @@ struct Layout {
 
 // Status word at the start of every cheb_moments workspace (workspace offset kStatusOff, see
 // cheb_workspace_status): bit 0 = a spin wait of the persistent kernel gave up (timeout),
-// bit 1 = a moment written by the last call is not finite.
+// bit 1 = a moment written by the last call is not finite; bit 8 (informational, not an error) =
+// the per-step kernels read the compressed matrix copy.
 constexpr size_t kStatusOff = 8;
 
 // Workspace of cheb_moments for dimension d, gather-matrix nnz, probe block k.
@@ -194,6 +196,14 @@ Layout plan(int64_t d, int64_t nnz, int k, int kind, int sms) {
     cub::DeviceScan::ExclusiveSum(nullptr, L.scan_bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(d + 1));
     L.scan = off; off += align256(L.scan_bytes);
     L.u2 = off; if (kind == CL_OP_CSR_RANK1 || kind == CL_OP_FAMILY) off += align256(((size_t)d + 2) * sizeof(double));
+    // compressed copy (CV format, cv_values_kernel / cv_encode_kernel): U entries per row, 16 bytes
+    // of tail padding for the last tile's bulk copies
+    const bool cvk = kind == CL_OP_CSR || kind == CL_OP_CSR_RANK1;
+    const size_t ucv = (size_t)CHEB_NNZ_UNROLL * (size_t)d;
+    L.cv_meta = off; if (cvk) off += 256;
+    L.cv_tab = off; if (cvk) off += align256(kCvSlots * sizeof(double));
+    L.cv_dc = off; if (cvk) off += align256(ucv * 2 + 64);
+    L.cv_vi = off; if (cvk) off += align256(ucv + 64);
     L.fcoef = off; if (kind == CL_OP_FAMILY) off += align256(3 * (size_t)k * sizeof(double));
     L.total = off;
     return L;
@@ -309,6 +319,7 @@ struct Schedule {
     bool small = false;       // 16-row tiles for the Algorithm-1 kernels (RP = 1)
     bool l2res = false;       // csr / rank-1 working set within half of L2 (persistent schedule's home)
     bool resident = false;    // shared-memory-resident kernel (cheb_resident_kernel), plan below
+    bool cv = false;          // per-step kernels may use the compressed matrix (device-checked)
     int res_grid = 0, res_rg = 1, res_nr = 0, res_cap = 0;
     size_t res_smem = 0;
     int fam_kp = 0, fam_r = 0;  // family: probes per member per block, members with output rows
@@ -509,6 +520,12 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
     a.mu_out = mu_rows;
     a.mu_stride = mu_stride;
     a.kvalid = kvalid;
+    if (fp.cv) {
+        a.cv_ok = (const int32_t*)(ws + L.cv_meta);
+        a.cv_dc = (const int16_t*)(ws + L.cv_dc);
+        a.cv_vi = (const uint8_t*)(ws + L.cv_vi);
+        a.cv_tab = (const double*)(ws + L.cv_tab);
+    }
 
     // K1
     {
@@ -1106,7 +1123,8 @@ int cheb_family_moments(const cl_csr* base, int32_t R, const double* theta, cons
     {
         const int64_t nmu = (int64_t)R * mrows * stride;
         const int grid = (int)std::min<int64_t>((nmu + kThreads - 1) / kThreads, 64);
-        moments_status_kernel<<<grid, kThreads, 0, st>>>((unsigned int*)(ws + L.misc + kStatusOff), mu_out, nmu);
+        moments_status_kernel<<<grid, kThreads, 0, st>>>((unsigned int*)(ws + L.misc + kStatusOff), mu_out, nmu,
+                                                         fp.cv ? (const int32_t*)(ws + L.cv_meta) : nullptr);
         g_launches++;
     }
     CL_CUDA(cudaGetLastError());
@@ -1177,6 +1195,26 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     g_last_schedule = fp.resident ? 2 : (fp.persistent ? 1 : 0);
     // per-step csr/rank-1: v = w_0 only as sign bits (CHEB_VBITS=0 disables)
     fp.vbits = !fp.persistent && !fp.resident && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
+    // per-step csr/rank-1: the compressed matrix copy, if the operator admits it (checked on the
+    // device; the kernels fall back to the plain copy otherwise).  CHEB_CV=0 disables.
+    const int cv_r4 = fp.small ? 1 : (fp.doubling ? CHEB_RPG_DBL : CHEB_RPG);  // the step kernels' geometry
+    if (!fp.persistent && !fp.resident && (op->kind == CL_OP_CSR || op->kind == CL_OP_CSR_RANK1) &&
+        tile_rows(probe_block, cv_r4) % 16 == 0 && env_int("CHEB_CV", 1) != 0) {
+        const int64_t d = op->A.n_cols;
+        const int32_t meta0[2] = {1, 0};
+        CL_CUDA(cudaMemcpyAsync(ws + L.cv_meta, meta0, sizeof(meta0), cudaMemcpyHostToDevice, st));
+        CL_CUDA(cudaMemsetAsync(ws + L.cv_tab, 0xFF, kCvSlots * sizeof(double), st));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sms * 8));
+        cv_values_kernel<<<grid, kThreads, 0, st>>>((int64_t)CHEB_NNZ_UNROLL * d, (const double*)(ws + L.va2),
+                                                    (unsigned long long*)(ws + L.cv_tab), (int32_t*)(ws + L.cv_meta));
+        cv_encode_kernel<<<grid, kThreads, 0, st>>>(d, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2),
+                                                    (const double*)(ws + L.va2),
+                                                    (const unsigned long long*)(ws + L.cv_tab),
+                                                    (int16_t*)(ws + L.cv_dc), (uint8_t*)(ws + L.cv_vi),
+                                                    (int32_t*)(ws + L.cv_meta));
+        g_launches += 2;
+        fp.cv = true;
+    }
     if (getenv("CHEB_DEBUG"))
         fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d doubling=%d small=%d\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
@@ -1201,7 +1239,8 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     {
         const int64_t nmu = (probe_end - probe_begin) * stride;
         const int grid = (int)std::min<int64_t>((nmu + kThreads - 1) / kThreads, 64);
-        moments_status_kernel<<<grid, kThreads, 0, st>>>((unsigned int*)(ws + L.misc + kStatusOff), mu_out, nmu);
+        moments_status_kernel<<<grid, kThreads, 0, st>>>((unsigned int*)(ws + L.misc + kStatusOff), mu_out, nmu,
+                                                         fp.cv ? (const int32_t*)(ws + L.cv_meta) : nullptr);
         g_launches++;
     }
     CL_CUDA(cudaGetLastError());

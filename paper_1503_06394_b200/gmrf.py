@@ -155,7 +155,7 @@ def likelihood_scan(family: PrecisionFamily, thetas: Sequence[float], xs: Sequen
         for r in range(R):
             moments(Operator("csr", family.at(float(th[r]))), lh[r, 0], lh[r, 1], degree, 0, num_probes, seed, k,
                     mu_out=mu[r], workspace=ws)
-            if workspace_status(ws):  # the status word is per moments call: check each member
+            if workspace_status(ws) & 3:  # the status word is per moments call: check each member
                 raise _lib.ChebError(_lib.CL_ENONFINITE, f"moments of J({th[r]}) failed (status {workspace_status(ws)})")
         family._workspace = None
     out = {"logdet": [], "stderr": [], "quad": [], "loglik": []}

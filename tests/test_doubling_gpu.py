@@ -78,8 +78,9 @@ def test_doubling_degrees_odd_even(orc, doubling, n, persist):
     steps = (n + 1) // 2
     blocks = 2
     if persist == 0:
-        # prep (count + scatter), (init + ceil(n/2) steps) per block, status epilogue, finalize
-        assert nl == 2 + blocks * (1 + steps) + 1 + 1
+        # prep (count + scatter), compressed copy (values + encode), (init + ceil(n/2) steps) per
+        # block, status epilogue, finalize
+        assert nl == 2 + 2 + blocks * (1 + steps) + 1 + 1
     mu = orc.moments(orc.Op("csr", A), wl.a, wl.b, n, 2, range(9))
     _check(r.moments, mu, wl.d)
 
@@ -128,11 +129,11 @@ def test_doubling_off_restores_algorithm1(orc):
     try:
         n0 = P.launch_count()
         P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-        assert P.launch_count() - n0 == 2 + 1 + 10 + 1 + 1  # prep, init, steps, status, finalize
+        assert P.launch_count() - n0 == 2 + 2 + 1 + 10 + 1 + 1  # prep, compressed copy, init, steps, status, finalize
         P.set_doubling(True)
         n0 = P.launch_count()
         P.logdet(op, wl.a, wl.b, 10, 16, k=16)
-        assert P.launch_count() - n0 == 2 + 1 + 5 + 1 + 1
+        assert P.launch_count() - n0 == 2 + 2 + 1 + 5 + 1 + 1
     finally:
         P.set_doubling(False)
         P.set_persistent(1)
