@@ -1201,8 +1201,9 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     if (!fp.persistent && !fp.resident && (op->kind == CL_OP_CSR || op->kind == CL_OP_CSR_RANK1) &&
         tile_rows(probe_block, cv_r4) % 16 == 0 && env_int("CHEB_CV", 1) != 0) {
         const int64_t d = op->A.n_cols;
-        const int32_t meta0[2] = {1, 0};
-        CL_CUDA(cudaMemcpyAsync(ws + L.cv_meta, meta0, sizeof(meta0), cudaMemcpyHostToDevice, st));
+        // meta = {ok = 1, count = 0} by memsets (no host source: the call stays graph-capturable)
+        CL_CUDA(cudaMemsetAsync(ws + L.cv_meta, 0, 2 * sizeof(int32_t), st));
+        CL_CUDA(cudaMemsetAsync(ws + L.cv_meta, 1, 1, st));
         CL_CUDA(cudaMemsetAsync(ws + L.cv_tab, 0xFF, kCvSlots * sizeof(double), st));
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sms * 8));
         cv_values_kernel<<<grid, kThreads, 0, st>>>((int64_t)CHEB_NNZ_UNROLL * d, (const double*)(ws + L.va2),

@@ -133,3 +133,21 @@ def test_compressed_far_columns_within_int16(orc, per_step):
     assert st1 & STATUS_COMPRESSED
     mu = orc.moments(orc.Op("csr", A), 0.3, 1.7, 20, 7, range(8))
     assert np.abs(mu1 - mu).max() <= 1e-11 * A.n_rows
+
+
+def test_compressed_cuda_graph_replay(per_step):
+    """The compressed-copy set-up (memsets + two kernels) is capturable: a CUDA-graph replay
+    reproduces the eager estimate bit for bit."""
+    wl = W.get_workload("gmrf_s")
+    A, _ = wl.matrices()
+    op = _op("csr", A)
+    est = P.Estimator(op, wl.a, wl.b, wl.degree, 32, 16, seed=wl.seed)
+    gp0, st0 = est.run()
+    torch.cuda.synchronize()
+    assert P.workspace_status(est.workspace) & STATUS_COMPRESSED
+    gp0, st0 = gp0.clone(), st0.clone()
+    replay, gp, st = est.capture()
+    for _ in range(3):
+        replay()
+    torch.cuda.synchronize()
+    assert torch.equal(st, st0) and torch.equal(gp, gp0)
