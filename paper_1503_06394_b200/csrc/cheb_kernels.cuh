@@ -594,6 +594,9 @@ prep_kernel(int64_t d, const int64_t* __restrict__ rp, const int32_t* __restrict
 // The decoded (column, value) pairs are bit-identical to the plain copy, so are the moments.
 // The format check runs on the device (no host round trip): cv_ok stays 1 only if it holds.
 // ---------------------------------------------------------------------------------------
+#ifndef CHEB_CV_KERNEL
+#define CHEB_CV_KERNEL 1  // 0: the step kernels never read the compressed copy (A/B builds)
+#endif
 constexpr int kCvSlots = 256;       // open-addressing table of value bit patterns
 constexpr int kCvMaxValues = 128;   // at most half full: short probe chains
 constexpr uint64_t kCvEmpty = ~0ull;
@@ -995,7 +998,11 @@ cheb_step_kernel(StepArgs a) {
         for (int x = tid; x < 3 * K; x += kThreads) s_fcoef[x] = a.fam_coef[x];
     // compressed matrix (csr / rank-1): decided on the device by the CV prep, uniform per launch
     // (the value-index slice of a tile must start 16-byte aligned: U * TILE % 16 == 0)
-    constexpr bool CAN_CV = (MODE == MODE_CSR || MODE == MODE_RANK1) && G::TILE % 16 == 0;
+    // Probe blocks k <= 16 only: there the matrix is 15 % of a launch's bytes and the copy saves 10 %
+    // of the time (configs[3]: 1.52 -> 1.37 s per estimate); at k = 64 it is 4 %, and the second
+    // staging path costs registers (1.308 -> 1.322 s).  Family mode: not (its registers spill).
+    constexpr bool CAN_CV = CHEB_CV_KERNEL && (MODE == MODE_CSR || MODE == MODE_RANK1) && K <= 16 &&
+                            G::TILE % 16 == 0;
     __shared__ double s_cvt[CAN_CV ? kCvSlots : 1];
     const bool cv = CAN_CV && a.cv_ok && *a.cv_ok != 0;
     if (cv)

@@ -482,6 +482,30 @@ int resident_setup(const cl_operator* op, char* ws, const Layout& L, cudaStream_
     return CL_OK;
 }
 
+// ---- compressed copy of the prepped gather matrix (CV format) --------------
+// Launches the device check + encode after the prep when the per-step kernels' tile geometry can
+// stage it (U * TILE % 16 == 0); the kernels read the verdict word and fall back to the plain copy.
+// CHEB_CV=0 disables.  Graph-capturable (memsets and kernels only).
+int cv_setup(int64_t d, int32_t probe_block, char* ws, const Layout& L, cudaStream_t st, int sms, Schedule* fp) {
+    const int r4 = fp->small ? 1 : (fp->doubling ? CHEB_RPG_DBL : CHEB_RPG);  // the step kernels' geometry
+    if (!CHEB_CV_KERNEL || probe_block > 16 || tile_rows(probe_block, r4) % 16 != 0 || env_int("CHEB_CV", 1) == 0)
+        return CL_OK;  // (the kernels' CAN_CV rule)
+    // meta = {ok = 1, count = 0} by memsets (no host source: the call stays graph-capturable)
+    CL_CUDA(cudaMemsetAsync(ws + L.cv_meta, 0, 2 * sizeof(int32_t), st));
+    CL_CUDA(cudaMemsetAsync(ws + L.cv_meta, 1, 1, st));
+    CL_CUDA(cudaMemsetAsync(ws + L.cv_tab, 0xFF, kCvSlots * sizeof(double), st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sms * 8));
+    cv_values_kernel<<<grid, kThreads, 0, st>>>((int64_t)CHEB_NNZ_UNROLL * d, (const double*)(ws + L.va2),
+                                                (unsigned long long*)(ws + L.cv_tab), (int32_t*)(ws + L.cv_meta));
+    cv_encode_kernel<<<grid, kThreads, 0, st>>>(d, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2),
+                                                (const double*)(ws + L.va2), (const unsigned long long*)(ws + L.cv_tab),
+                                                (int16_t*)(ws + L.cv_dc), (uint8_t*)(ws + L.cv_vi),
+                                                (int32_t*)(ws + L.cv_meta));
+    g_launches += 2;
+    fp->cv = true;
+    return CL_OK;
+}
+
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
 // RP: tile geometry of the Algorithm-1 kernels (0: CHEB_RPG; 1: 16-row tiles, Schedule::small)
 template <int K, int MODE, int RP = 0>
@@ -1197,25 +1221,8 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
     fp.vbits = !fp.persistent && !fp.resident && op->kind != CL_OP_BTB && env_int("CHEB_VBITS", 1) != 0;
     // per-step csr/rank-1: the compressed matrix copy, if the operator admits it (checked on the
     // device; the kernels fall back to the plain copy otherwise).  CHEB_CV=0 disables.
-    const int cv_r4 = fp.small ? 1 : (fp.doubling ? CHEB_RPG_DBL : CHEB_RPG);  // the step kernels' geometry
-    if (!fp.persistent && !fp.resident && (op->kind == CL_OP_CSR || op->kind == CL_OP_CSR_RANK1) &&
-        tile_rows(probe_block, cv_r4) % 16 == 0 && env_int("CHEB_CV", 1) != 0) {
-        const int64_t d = op->A.n_cols;
-        // meta = {ok = 1, count = 0} by memsets (no host source: the call stays graph-capturable)
-        CL_CUDA(cudaMemsetAsync(ws + L.cv_meta, 0, 2 * sizeof(int32_t), st));
-        CL_CUDA(cudaMemsetAsync(ws + L.cv_meta, 1, 1, st));
-        CL_CUDA(cudaMemsetAsync(ws + L.cv_tab, 0xFF, kCvSlots * sizeof(double), st));
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((d + kThreads - 1) / kThreads, (int64_t)sms * 8));
-        cv_values_kernel<<<grid, kThreads, 0, st>>>((int64_t)CHEB_NNZ_UNROLL * d, (const double*)(ws + L.va2),
-                                                    (unsigned long long*)(ws + L.cv_tab), (int32_t*)(ws + L.cv_meta));
-        cv_encode_kernel<<<grid, kThreads, 0, st>>>(d, (const int64_t*)(ws + L.rp2), (const int32_t*)(ws + L.ci2),
-                                                    (const double*)(ws + L.va2),
-                                                    (const unsigned long long*)(ws + L.cv_tab),
-                                                    (int16_t*)(ws + L.cv_dc), (uint8_t*)(ws + L.cv_vi),
-                                                    (int32_t*)(ws + L.cv_meta));
-        g_launches += 2;
-        fp.cv = true;
-    }
+    if (!fp.persistent && !fp.resident && (op->kind == CL_OP_CSR || op->kind == CL_OP_CSR_RANK1))
+        if ((rc = cv_setup(op->A.n_cols, probe_block, ws, L, st, sms, &fp))) return rc;
     if (getenv("CHEB_DEBUG"))
         fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d doubling=%d small=%d\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,

@@ -133,14 +133,15 @@ def likelihood_scan(family: PrecisionFamily, thetas: Sequence[float], xs: Sequen
     common probes, device quadratic forms, device Gershgorin intervals.
     batched=True: every member in the columns of each probe block (cheb_family_moments, one pass
     over the matrix for all members); False: one estimate per member, sharing a workspace.  Default:
-    batched when fewer than 32 probes per member (a separate estimate would then run at k < 32, where
-    the matrix is >= 8 % of a step's bytes); with 64 probes per member the matrix is 4 % of a k = 64
-    step and the batched kernel's per-column scalars cost more than they save (configs[3]-size scan,
-    8 members x 64 probes: 5.9 s batched vs 5.0 s separate)."""
+    separate estimates.  Since the per-step kernels read the compressed matrix copy (3 bytes per
+    entry at k <= 16) the matrix bytes a batched pass shares are small, and the
+    batched kernel's per-column scalars cost more than they save (configs[3]-size scan, 8 members:
+    64 probes each 6.16 s batched vs 5.34 s separate, 16 probes each 1.60 s vs 1.41 s;
+    profiles/r02_extras.jsonl)."""
     th = np.asarray(thetas, dtype=np.float64)
     R, d, S = th.size, family.base.n_rows, len(xs)
     if batched is None:
-        batched = num_probes < 32
+        batched = False
     lh = family.gershgorin(th)
     if not np.all(lh[:, 0] > 0):
         bad = th[~(lh[:, 0] > 0)]

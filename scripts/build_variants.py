@@ -26,6 +26,7 @@ VARIANTS = {
     "r4": ["CHEB_RPG=4"],
     "checked": ["CHEB_CHECKS=1"],
     "resprof": ["CHEB_RES_PROF=1"],
+    "nocv": ["CHEB_CV_KERNEL=0"],  # step kernels without the compressed-copy path (A/B)
     "resdiag1": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=1"],  # timing diagnostics: wrong results
     "resdiag2": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=2"],  # per-CTA phase cycles of the resident kernel (scripts/res_phases.py)
     "u4c4": ["CHEB_NNZ_UNROLL=4", "CHEB_MIN_CTAS=4"],

@@ -151,3 +151,20 @@ def test_compressed_cuda_graph_replay(per_step):
         replay()
     torch.cuda.synchronize()
     assert torch.equal(st, st0) and torch.equal(gp, gp0)
+
+
+def test_family_mode_reads_the_plain_copy(orc):
+    """Family mode (f2) keeps the plain copy (status bit clear) and matches the oracle per member."""
+    import paper_1503_06394_b200.gmrf as G
+    base = W.grid_gmrf(37, 1.0)  # I - Adj: D = I, O = -Adj
+    fam = G.PrecisionFamily(P.DeviceCSR.from_host(base))
+    thetas = [-0.24, 0.05, 0.2, 0.23]
+    lh = fam.gershgorin(thetas)
+    n, m, seed = 25, 13, 4
+    ws = P.alloc_workspace(P.Operator("family", fam.base), 64)
+    mu = fam.moments(thetas, lh, n, 0, m, seed, 64, workspace=ws).cpu().numpy()
+    assert not P.workspace_status(ws) & STATUS_COMPRESSED
+    for r, th in enumerate(thetas):
+        A = W.grid_gmrf(37, th)
+        want = orc.moments(orc.Op("csr", A), lh[r, 0], lh[r, 1], n, seed, range(m), workers=4)
+        assert np.abs(mu[r] - want).max() <= 1e-11 * A.n_rows

@@ -471,8 +471,8 @@ def test_likelihood_scan_parity(orc):
     rng = np.random.default_rng(8)
     xs = [rng.standard_normal(900) for _ in range(2)]
     thetas = [-0.24, -0.2, 0.1]
-    res = G.likelihood_scan(fam, thetas, [torch.from_numpy(x).cuda() for x in xs], 40, 16, seed=4)
-    res2 = G.likelihood_scan(fam, thetas, [torch.from_numpy(x).cuda() for x in xs], 40, 16, seed=4, batched=False)
+    res = G.likelihood_scan(fam, thetas, [torch.from_numpy(x).cuda() for x in xs], 40, 16, seed=4, batched=True)
+    res2 = G.likelihood_scan(fam, thetas, [torch.from_numpy(x).cuda() for x in xs], 40, 16, seed=4)
     assert np.allclose(res.loglik, res2.loglik, rtol=1e-12, atol=0)  # batched = separate estimates
     for th, ll in zip(thetas, res.loglik):
         A = W.grid_gmrf(30, th)
