@@ -1789,6 +1789,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             constexpr bool STAGED = decltype(staged)::value;
             for (int lr = grp; lr < nr; lr += GR) {
                 const int lo = rp_s[lr], hi = rp_s[lr + 1];
+                CHEB_ASSERT(lo <= hi && (hi - lo) % U == 0 && (!STAGED || hi <= ra.cap));
                 double2 g[NSL];
 #pragma unroll
                 for (int sl = 0; sl < NSL; sl++) g[sl] = make_double2(0.0, 0.0);
@@ -1808,12 +1809,14 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
                         } else if (CHEB_RES_DIAG == 2) {  // timing diagnostic: every gather from the own row
                             for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(wo_s + (lr * RS + pp[sl]) * 8);
                         } else if (c[q] >= 0) {
+                            CHEB_ASSERT(!single && (int64_t)c[q] < a.d);
                             const double* p = go + (size_t)c[q] * K;
 #pragma unroll
                             for (int sl = 0; sl < NSL; sl++) x[q][sl] = ldca2(p + pp[sl]);
                         } else {
                             const uint32_t e = (uint32_t)(-1 - c[q]);
                             const uint32_t rk = e >> 16;
+                            CHEB_ASSERT((int)rk < RG && (int)(e & 0xFFFFu) < ra.nr);
                             const uint32_t ad = wo_s + (e & 0xFFFFu) * (RS * 8);
                             if (rk == (uint32_t)crank) {
 #pragma unroll

@@ -1,4 +1,8 @@
-"""Tiny invocation of every kernel variant, for compute-sanitizer (one tool per run)."""
+"""Tiny invocation of every kernel variant, for compute-sanitizer (one tool per run) or the
+CHEB_CHECKS=1 build (device asserts on every gather index, staging offset and tile bound):
+
+    CHEB_LIB=build_variants/libchebld_checked.so python scripts/sanitize_smoke.py
+"""
 import os
 import sys
 
@@ -42,6 +46,16 @@ def main():
     P.set_persistent(1)
     P.logdet(op_b, a, b, 5, 9, seed=1, k=16)
     P.set_doubling(False)
+    # shared-memory-resident kernel: one cluster and the flat grid, Algorithm 1 and doubling
+    for single in ("8192", "0"):
+        os.environ["CHEB_RES_SINGLE_MAX"] = single
+        for k in (8, 16, 64):
+            P.logdet(op_g, 0.2, 1.8, 7, 11, seed=1, k=k)
+            P.logdet(op_t, 0.01, 8.5, 7, 11, seed=1, k=k)
+        P.set_doubling(True)
+        P.logdet(op_t, 0.01, 8.5, 7, 11, seed=1, k=16)
+        P.set_doubling(False)
+    os.environ.pop("CHEB_RES_SINGLE_MAX", None)
     torch.cuda.synchronize()
     print("sanitize smoke ok")
 
