@@ -1565,6 +1565,11 @@ struct ResArgs {
     const double* s_buf;      // s_0 (rank-1, from probe_init)
     unsigned int* bar_count;  // grid barrier: arrivals of cluster leaders (zeroed; monotone)
     unsigned int* err;        // wait timeout flag
+    // several probe blocks in one launch (one cluster each, single-cluster geometry only): block b
+    // is CTAs [b * G/nblk, (b+1) * G/nblk), its sign bits at sbits + b * sb_stride, its s_0 at
+    // s_buf + b * K, its moment rows from mu_out + b * K * mu_stride; kvalid counts all blocks' probes
+    int32_t nblk;             // 1: one probe block (every other geometry)
+    int64_t sb_stride;        // uint32 words between consecutive blocks' sign bits
 };
 
 // shared-memory row stride (doubles): 256-bit-lane rows (k <= 16) get a 16-byte skew so the rows
@@ -1684,12 +1689,13 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
     cg::cluster_group cluster = cg::this_cluster();
     // one cluster (RG = G: DSMEM halos and reductions) or a flat grid (RG = 1: halos through the
     // exported global rows, one grid counter per step)
-    const int RG = a.rg, NG = (int)gridDim.x;
+    const int RG = a.rg, NG = (int)gridDim.x / ra.nblk;  // NG: CTAs per probe block
     const bool single = RG == NG;
+    const int bb = (int)blockIdx.x / NG, cb = (int)blockIdx.x % NG;  // probe block, CTA within it
     const int crank = (int)cluster.block_rank();
     double mu_pend[NMU] = {};  // flat grid: part[tid][p] of step mu_j, summed one step later
     int32_t mu_j = 0;
-    const int64_t r0 = (int64_t)blockIdx.x * ra.nr;
+    const int64_t r0 = (int64_t)cb * ra.nr;
     const int nr = (int)(a.d - r0 < (int64_t)ra.nr ? (a.d - r0 > 0 ? a.d - r0 : 0) : ra.nr);
     const ResLayout ly = res_layout<K>(ra.nr, ra.cap, a.r1u != nullptr);
     double* const W0 = reinterpret_cast<double*>(smem + ly.w0);
@@ -1713,11 +1719,11 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             col_s[e] = a.ci[e0 + e];
             val_s[e] = a.va[e0 + e];
         }
-    for (int x = tid; x < nr * WORDS; x += NT) sg_s[x] = a.sbits[(size_t)r0 * WORDS + x];
+    for (int x = tid; x < nr * WORDS; x += NT) sg_s[x] = a.sbits[(size_t)bb * ra.sb_stride + (size_t)r0 * WORDS + x];
     if (a.r1u)
         for (int x = tid; x < nr; x += NT) u_s[x] = a.r1u[r0 + x];
     for (int x = tid; x < nr; x += NT) ex_s[x] = ra.exp[r0 + x];
-    if (HAS_S && tid < K) s_sh[tid] = __ldcg(ra.s_buf + tid);
+    if (HAS_S && tid < K) s_sh[tid] = __ldcg(ra.s_buf + (size_t)bb * K + tid);
     __syncthreads();
     for (int x = tid; x < nr * K; x += NT) {
         const int lr = x / K, p = x % K;
@@ -1727,14 +1733,14 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
     // bank after a barrier can miss (measured neutral, kept for predictability)
     double* g0 = ra.g0;
     double* g1 = ra.g1;
-    double* mu_out = a.mu_out;
+    double* mu_out = a.mu_out + (size_t)bb * K * a.mu_stride;
     double* gpart = ra.gpart;
     unsigned int* bar_count = ra.bar_count;
     unsigned int* err = ra.err;
     const double* r1u = a.r1u;
     double r1ca = a.r1c_alpha;
     int64_t mu_stride = a.mu_stride;
-    int32_t n_steps = ra.n, power = ra.power, kvalid = a.kvalid;
+    int32_t n_steps = ra.n, power = ra.power, kvalid = min(a.kvalid - bb * K, K);
     const int32_t* ci_g = a.ci;
     const double* va_g = a.va;
     asm volatile("" : "+l"(g0), "+l"(g1), "+l"(mu_out), "+l"(gpart), "+l"(bar_count), "+l"(err), "+l"(r1u));
@@ -1937,7 +1943,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             }
             __syncthreads();
             RES_T(3);
-            if (blockIdx.x == gridDim.x - 1 && tid < kvalid) mu_write(mu_out + (size_t)tid * mu_stride, j, fin[0][tid], fin[NMU - 1][tid]);
+            if (cb == NG - 1 && tid < kvalid) mu_write(mu_out + (size_t)tid * mu_stride, j, fin[0][tid], fin[NMU - 1][tid]);
             if (want_s && tid < K) s_sh[tid] = fin[NCH - 1][tid];
         } else {
             // ---- flat grid (one CTA per SM, no clusters): every CTA publishes its partial, one

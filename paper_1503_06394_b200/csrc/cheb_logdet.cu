@@ -321,6 +321,7 @@ struct Schedule {
     bool resident = false;    // shared-memory-resident kernel (cheb_resident_kernel), plan below
     bool cv = false;          // per-step kernels may use the compressed matrix (device-checked)
     int res_grid = 0, res_rg = 1, res_nr = 0, res_cap = 0;
+    int res_maxc = 1;         // single-cluster geometry: co-resident clusters (probe blocks per launch)
     size_t res_smem = 0;
     int fam_kp = 0, fam_r = 0;  // family: probes per member per block, members with output rows
     int64_t fam_rstride = 0;    // family: doubles between consecutive members' mu rows
@@ -446,7 +447,10 @@ bool resident_plan(int64_t d, int64_t nnz, bool has_u, Schedule* fp) {
             cudaGetLastError();
             continue;
         }
-        if (maxc >= 1) return take(rg, rg);
+        if (maxc >= 1) {
+            fp->res_maxc = env_int("CHEB_RES_MULTI", 1) ? maxc : 1;  // 0: one probe block per launch
+            return take(rg, rg);
+        }
     }
     // flat grid: one CTA per SM, every SM (no cluster stranding), at most kResThreads CTAs
     int occ = 0;
@@ -508,10 +512,12 @@ int cv_setup(int64_t d, int32_t probe_block, char* ws, const Layout& L, cudaStre
 
 // ---- one probe block: K1, then n x ([K3] K2) --------------------------------
 // RP: tile geometry of the Algorithm-1 kernels (0: CHEB_RPG; 1: 16-row tiles, Schedule::small)
+// nblk > 1 (single-cluster resident geometry only): nblk consecutive probe blocks of K probes in
+// one launch, one cluster each; kvalid counts the probes of all of them.
 template <int K, int MODE, int RP = 0>
 int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
               int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-              int64_t mu_stride, cudaStream_t st, int sms, const Schedule& fp) {
+              int64_t mu_stride, cudaStream_t st, int sms, const Schedule& fp, int nblk = 1) {
     constexpr int R4S = RP ? RP : CHEB_RPG;
     constexpr int R4D = RP ? RP : CHEB_RPG_DBL;  // doubling kernels: same RP rule
     using G = Geo<K, R4S>;  // Algorithm-1 geometry; the doubling kernels use Geo<K, R4D>
@@ -551,8 +557,13 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         a.cv_tab = (const double*)(ws + L.cv_tab);
     }
 
+    // several blocks per launch: their sign bits and s_0 in the exported-row buffers, which the
+    // single-cluster geometry never uses (every gathered row is a cluster row)
+    const int64_t sb_stride = ((int64_t)d * words_for(K) + 3) & ~int64_t(3);
+    uint32_t* sb_multi = (uint32_t*)(ws + L.w0);
+    double* s0_multi = (double*)(ws + L.w1);
     // K1
-    {
+    for (int b = 0; b < nblk; b++) {
         constexpr int groups = kThreads / (K <= 64 ? K / 2 : K / 4);
         const int64_t niter = (d + groups - 1) / groups;
         constexpr size_t init_smem = red_scratch_bytes<K, MODE == MODE_RANK1 ? 2 : 1>();
@@ -560,11 +571,19 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
                              (int)init_smem);
         const int grid = grid_for(probe_init_kernel<K, MODE>, niter, sms);
         a.mu_col = 0;
-        a.s_next = sbuf;
-        probe_init_kernel<K, MODE><<<grid, kThreads, init_smem, st>>>(a, seed, (uint64_t)p0,
-                                                                    fp.vbits ? nullptr : w[0], sbits);
+        a.s_next = nblk > 1 ? s0_multi + (size_t)b * K : sbuf;
+        a.mu_out = mu_rows + (size_t)b * K * mu_stride;
+        a.kvalid = std::min(K, kvalid - b * K);
+        if (nblk > 1)
+            probe_init_kernel<K, MODE><<<grid, kThreads, init_smem, st>>>(a, seed, (uint64_t)(p0 + (int64_t)b * K),
+                                                                        nullptr, sb_multi + (size_t)b * sb_stride);
+        else
+            probe_init_kernel<K, MODE><<<grid, kThreads, init_smem, st>>>(a, seed, (uint64_t)p0,
+                                                                        fp.vbits ? nullptr : w[0], sbits);
         g_launches++;
     }
+    a.mu_out = mu_rows;
+    a.kvalid = kvalid;
     if (n < 1) return CL_OK;
 
     if constexpr ((MODE == MODE_CSR || MODE == MODE_RANK1) && K <= 64) if (fp.resident) {
@@ -577,14 +596,17 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
         ra.power = fp.power ? 1 : 0;
         ra.exp = (const uint8_t*)(ws + L.cnt64);
         ra.gpart = (double*)(ws + L.gpart);
-        ra.s_buf = sbuf;
+        ra.s_buf = nblk > 1 ? s0_multi : sbuf;
+        ra.nblk = nblk;
+        ra.sb_stride = sb_stride;
+        if (nblk > 1) a.sbits = sb_multi;
         ra.bar_count = (unsigned int*)(ws + L.misc + 16);
         ra.err = (unsigned int*)(ws + L.misc + kStatusOff);
         a.rg = fp.res_rg;
         CL_CUDA(cudaMemsetAsync(ws + L.misc + 16, 0, 16, st));
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];
-        cluster_config(&cfg, at, fp.res_grid, fp.res_rg, fp.res_smem, st, kResThreads);
+        cluster_config(&cfg, at, fp.res_grid * nblk, fp.res_rg, fp.res_smem, st, kResThreads);
         at[1].id = cudaLaunchAttributeCooperative;  // a single cluster is co-scheduled anyway
         at[1].val.cooperative = 1;
         // (CHEB_RES_NOCOOP=1: profiling only -- ncu cannot replay cooperative cluster launches; the
@@ -706,14 +728,14 @@ int run_block(const cl_operator* op, double alpha, double beta, int32_t n, uint6
 template <int K>
 int run_block_mode(const cl_operator* op, double alpha, double beta, int32_t n, uint64_t seed,
                    int64_t p0, int kvalid, char* ws, const Layout& L, double* mu_rows,
-                   int64_t mu_stride, cudaStream_t st, int sms, const Schedule& fp) {
+                   int64_t mu_stride, cudaStream_t st, int sms, const Schedule& fp, int nblk = 1) {
     switch (op->kind) {
         case CL_OP_CSR:
-            if (fp.small) return run_block<K, MODE_CSR, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
-            return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+            if (fp.small) return run_block<K, MODE_CSR, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp, nblk);
+            return run_block<K, MODE_CSR>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp, nblk);
         case CL_OP_CSR_RANK1:
-            if (fp.small) return run_block<K, MODE_RANK1, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
-            return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
+            if (fp.small) return run_block<K, MODE_RANK1, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp, nblk);
+            return run_block<K, MODE_RANK1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp, nblk);
         case CL_OP_FAMILY:
             if constexpr (K >= 16) {  // >= 2 probes per member of an 8-member block
                 if (fp.small) return run_block<K, MODE_FAM, 1>(op, alpha, beta, n, seed, p0, kvalid, ws, L, mu_rows, mu_stride, st, sms, fp);
@@ -1227,15 +1249,29 @@ int moments_impl(const cl_operator* op, double alpha, double beta, bool power, i
         fprintf(stderr, "[chebld] d=%lld nnz=%lld k=%d kind=%d persistent=%d doubling=%d small=%d\n",
                 (long long)op->A.n_cols, (long long)op->A.nnz, probe_block, op->kind, (int)fp.persistent,
                 (int)fp.doubling, (int)fp.small);
-    for (int64_t p0 = probe_begin; p0 < probe_end; p0 += probe_block) {
-        const int kvalid = (int)std::min<int64_t>(probe_block, probe_end - p0);
+    // single-cluster resident geometry: up to res_maxc probe blocks run concurrently in one launch
+    // (one cluster each; configs[0] at k = 16: 4 blocks in one launch), as many as the exported-row
+    // buffers hold sign bits and s_0 for
+    int64_t group = 1;
+    if (fp.resident && fp.res_grid == fp.res_rg && fp.res_maxc > 1) {
+        const int64_t wb = (int64_t)(L.w1 - L.w0);
+        const int64_t sbs = (((int64_t)op->A.n_cols * words_for(probe_block) + 3) & ~int64_t(3)) * 4;
+        group = std::min<int64_t>({(int64_t)fp.res_maxc, wb / sbs, wb / ((int64_t)probe_block * 8)});
+        group = std::max<int64_t>(group, 1);
+    }
+    for (int64_t p0 = probe_begin; p0 < probe_end;) {
+        const int64_t nb = std::min<int64_t>(group, (probe_end - p0 + probe_block - 1) / probe_block);
+        const int kvalid = (int)std::min<int64_t>(probe_block * nb, probe_end - p0);
+        const int nbi = (int)nb;
         double* rows = mu_out + (size_t)(p0 - probe_begin) * stride;
+        const int64_t pb = p0;
+        p0 += probe_block * nb;
         switch (probe_block) {
-            case 8: rc = run_block_mode<8>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
-            case 16: rc = run_block_mode<16>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
-            case 32: rc = run_block_mode<32>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
-            case 64: rc = run_block_mode<64>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
-            default: rc = run_block_mode<128>(op, alpha, beta, degree, seed, p0, kvalid, ws, L, rows, stride, st, sms, fp); break;
+            case 8: rc = run_block_mode<8>(op, alpha, beta, degree, seed, pb, kvalid, ws, L, rows, stride, st, sms, fp, nbi); break;
+            case 16: rc = run_block_mode<16>(op, alpha, beta, degree, seed, pb, kvalid, ws, L, rows, stride, st, sms, fp, nbi); break;
+            case 32: rc = run_block_mode<32>(op, alpha, beta, degree, seed, pb, kvalid, ws, L, rows, stride, st, sms, fp, nbi); break;
+            case 64: rc = run_block_mode<64>(op, alpha, beta, degree, seed, pb, kvalid, ws, L, rows, stride, st, sms, fp, nbi); break;
+            default: rc = run_block_mode<128>(op, alpha, beta, degree, seed, pb, kvalid, ws, L, rows, stride, st, sms, fp); break;
         }
         if (rc) return rc;
     }

@@ -225,3 +225,42 @@ def test_resident_timeout_status(env, single):
     with pytest.raises(P.ChebError):
         P.logdet(op, wl.a, wl.b, wl.degree, 16, seed=1, k=16)
     assert P.last_schedule() == "resident"
+
+
+# several probe blocks in one launch (single-cluster geometry: one cluster per block, up to the
+# co-resident cluster count per launch; CHEB_RES_MULTI=0 runs one block per launch)
+@pytest.mark.parametrize("dbl", [False, True])
+@pytest.mark.parametrize("name,k,p0,p1", [("gmrf32", 16, 0, 64), ("gmrf32", 8, 3, 203),
+                                          ("torus_s", 8, 5, 46), ("spd_csr", 8, 0, 37)])
+def test_resident_multi_block(orc, env, dbl, name, k, p0, p1):
+    """Blocks sharing a launch give the moments of one block per launch bit for bit, and the
+    oracle's: ragged last block, a global probe offset, several launches (> the clusters that fit)."""
+    wl = _SPD() if name == "spd_csr" else W.get_workload(name)
+    A, _ = wl.matrices()
+    op = _dev_op(wl.mode, A, wl.r1_c)
+    P.set_doubling(dbl)
+    try:
+        out = {}
+        for multi in (1, 0):
+            env(CHEB_RES_MULTI=multi)
+            out[multi] = P.moments(op, wl.a, wl.b, wl.degree, p0, p1, wl.seed, k).cpu().numpy()
+            assert P.last_schedule() == "resident"
+    finally:
+        P.set_doubling(False)
+    assert np.array_equal(out[1], out[0])
+    mu = orc.moments(orc.Op(wl.mode, A, wl.r1_c), wl.a, wl.b, wl.degree, wl.seed, range(p0, p1), workers=4)
+    assert np.abs(out[1] - mu).max() <= 1e-11 * wl.d
+
+
+def test_resident_multi_block_explicit_u(orc, env):
+    T = W.torus_laplacian(21)
+    u = np.linspace(0.5, 1.5, T.n_rows)
+    op = _dev_op("rank1", T, 1e-3, u)
+    out = {}
+    for multi in (1, 0):
+        env(CHEB_RES_MULTI=multi)
+        out[multi] = P.moments(op, 1e-3, 8.5, 40, 0, 40, 3, 8).cpu().numpy()
+        assert P.last_schedule() == "resident"
+    assert np.array_equal(out[1], out[0])
+    mu = orc.moments(orc.Op("rank1", T, 1e-3, u), 1e-3, 8.5, 40, 3, range(40))
+    assert np.abs(out[1] - mu).max() <= 1e-11 * T.n_rows
