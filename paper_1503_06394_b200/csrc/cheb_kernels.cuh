@@ -1972,8 +1972,19 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
                 constexpr int UU = NT / K;
                 const double* ps = pg + (size_t)(NCH - 1) * NG * K;
                 const int p = tid % K, u = tid / K;
+                // all of a chunk's loads in flight before the (ascending) adds: one L2 round trip
+                // per 8 partials instead of one per partial (absent partials add +0.0)
                 double t = 0.0;
-                for (int c = u; c < NG; c += UU) t += __ldcg(ps + (size_t)c * K + p);
+                for (int c0 = u; c0 < NG; c0 += 8 * UU) {
+                    double v8[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const int c = c0 + q * UU;
+                        v8[q] = c < NG ? __ldcg(ps + (size_t)c * K + p) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; q++) t += v8[q];
+                }
                 red2[u][p] = t;
                 __syncthreads();
                 if (tid < K) {
