@@ -322,7 +322,12 @@ def run_ours(args):
     from paper_1503_06394_b200 import dist as pdist
     import paper_1503_06394_b200 as P
 
-    rank, world, local = pdist.init_from_env("nccl")
+    # BENCH_SHARE_GPU=1: functional check of the N > 1 code path on a one-GPU box (every rank on
+    # cuda:0, gloo instead of NCCL); the line is flagged and is never a measurement
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    rank, world, local = pdist.init_from_env("gloo" if share else "nccl")
+    if share:
+        local = 0
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     wl, A, At = build_workload(args.workload)
@@ -443,6 +448,7 @@ def run_ours(args):
            "scaling": args.scaling,
            "vs_baseline": (value / wl.paper_probe_steps_per_s) if wl.paper_probe_steps_per_s else None,
            "dtype": "f64", "data": "synthetic", "config": cfg,
+           **({"functional_check_shared_gpu": "all ranks on cuda:0 over gloo: not a measurement"} if share else {}),
            "roofline": roof, "gpu_launches": int(launches),
            "gpu_launches_per_step": launches / args.steps, "clocks": clk, "cpu_baseline": cpu,
            "e2e": e2e, "weak_scaling": weak, "alt_schedule": alt}

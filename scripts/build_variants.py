@@ -19,6 +19,7 @@ VARIANTS = {
     "wide16": ["CHEB_WIDE_MAXK=16"],
     "sus1k": ["CHEB_MBAR_SUSPEND_NS=1000"],
     "sus20k": ["CHEB_MBAR_SUSPEND_NS=20000"],
+    "s3sus1k": ["CHEB_STAGES=3", "CHEB_MBAR_SUSPEND_NS=1000"],
     "diag_r1nosync": ["CHEB_DIAG_R1_NOSYNC=1"],  # timing diagnostic: wrong rank-1 moments
     "diag_r1nosync_c4": ["CHEB_DIAG_R1_NOSYNC=1", "CHEB_MIN_CTAS_R1=4"],
     "dec3": ["CHEB_DECOUPLE=1", "CHEB_STAGES=3"],

@@ -689,3 +689,30 @@ def test_dist_entry_point_one_rank_torchrun(orc):
     og = orc.logdet(orc.Op("csr", A), wl.a, wl.b, wl.degree, wl.num_probes, wl.seed, workers=4)["gamma"]
     assert out["world"] == 1 and out["num_probes"] == wl.num_probes
     _check_gamma(out["logdet"], og)
+
+
+@pytest.mark.parametrize("workload", ["gmrf32", "gmrf1000"])
+def test_bench_two_ranks_functional(workload):
+    """bench.py's N > 1 path (torchrun, probe shards, all-reduce of the moment table, max-over-ranks
+    timing, e2e through cheb_moments_host) run as two ranks sharing cuda:0 over gloo
+    (BENCH_SHARE_GPU=1: a functional check, not a measurement): the estimate is bit-identical to the
+    one-rank line (adding the zero rows of the other shard is exact)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    flags = ["--workload", workload, "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-alt",
+             "--no-weak"]
+    out = {}
+    for n in (1, 2):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr=127.0.0.1", f"--master-port={29530 + n}", "bench.py", "--gpus", str(n)] + flags
+        env = dict(os.environ, BENCH_SHARE_GPU="1")
+        r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600, env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[n] = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out[2]["n_gpus"] == 2 and out[2]["config"]["parallelism"] == "probe-dp2"
+    assert out[2]["config"]["probes_per_gpu"] * 2 == out[1]["config"]["num_probes"]
+    assert out[2]["config"]["gamma"] == out[1]["config"]["gamma"]
+    assert out[2]["e2e"]["value"] > 0 and "functional_check_shared_gpu" in out[2]
