@@ -1638,14 +1638,6 @@ __device__ __forceinline__ double2 ldca2(const double* p) {
     return v;
 }
 
-#ifndef CHEB_RES_PF
-#define CHEB_RES_PF 0  // flat grid: L1 prefetch of the exported rows the next row iteration gathers
-#endif
-#ifndef CHEB_RES_S2
-#define CHEB_RES_S2 0  // flat grid: s_j second level by warp shuffles and four interleaved sums
-#endif
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-
 #ifndef CHEB_RES_DIAG
 #define CHEB_RES_DIAG 0  // TIMING DIAGNOSTIC builds only (wrong results): 1 no gathers, 2 own-row gathers
 #endif
@@ -1797,20 +1789,6 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
 #pragma unroll
             for (int q = 0; q < kPPL; q++) acc[ch][q] = 0.0;
         const uint32_t wo_s = smem_u32(Wo);
-        // flat grid: the exported rows that row lr gathers, prefetched into L1 one row iteration
-        // ahead (the lane group shares the row's entries; one 128-byte line per prefetch)
-        auto pf_row = [&](const double* gsrc, int lr) {
-            if (lr < nr && fit) {
-                for (int t = rp_s[lr] + lg; t < rp_s[lr + 1]; t += L) {
-                    const int32_t c = col_s[t];
-                    if (c >= 0) {
-                        const char* q = reinterpret_cast<const char*>(gsrc + (size_t)c * K);
-#pragma unroll
-                        for (int b = 0; b < K * 8; b += 128) prefetch_l1(q + b);
-                    }
-                }
-            }
-        };
         // one row: gathers (own rows: ld.shared; cluster peers: ld.shared::cluster at the mapa'd
         // address; other clusters: the exported global copy), rank-1 term, recurrence, dots
         auto rows = [&](auto staged) {
@@ -1818,7 +1796,6 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             for (int lr = grp; lr < nr; lr += GR) {
                 const int lo = rp_s[lr], hi = rp_s[lr + 1];
                 CHEB_ASSERT(lo <= hi && (hi - lo) % U == 0 && (!STAGED || hi <= ra.cap));
-                if (CHEB_RES_PF && !single) pf_row(go, lr + GR);
                 double2 g[NSL];
 #pragma unroll
                 for (int sl = 0; sl < NSL; sl++) g[sl] = make_double2(0.0, 0.0);
@@ -1981,8 +1958,6 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             }
             __syncthreads();
             RES_T(5);
-            // the next step's first row iteration gathers from gn: its L2 latency overlaps the s_j sum
-            if (CHEB_RES_PF && j < n_steps) pf_row(gn, grp);
             // mu_j of probe blockIdx.x (CTAs < K), summed during the next step's partial reduction:
             // thread t holds part[t][p]
             if (blockIdx.x < (unsigned)kvalid) {
@@ -1993,7 +1968,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
             }
             if (want_s) {
                 // s_j = sum over CTAs of part[c][S][p]: thread (u = tid / K, p = tid % K) sums
-                // c = u, u + U, ... ascending (coalesced rows of K), then u ascending
+                // c = u, u + U, ... ascending (coalesced rows of K), then the u of one probe
                 constexpr int UU = NT / K;
                 const double* ps = pg + (size_t)(NCH - 1) * NG * K;
                 const int p = tid % K, u = tid / K;
@@ -2010,28 +1985,19 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
 #pragma unroll
                     for (int q = 0; q < 8; q++) t += v8[q];
                 }
-                if (CHEB_RES_S2) {
-                    // lanes of a warp that hold the same probe (u ascending by lane), then the warps /
-                    // the u rows as four interleaved ascending sums: a fixed order with a short chain
+                // second level: the lanes of a warp that hold the same probe (u ascending by lane),
+                // then the warps / the u rows as four interleaved ascending sums -- a fixed order
+                // with a short dependent chain (14.7 -> 14.6 ms per configs[1] estimate)
 #pragma unroll
-                    for (int off = K; off < 32; off <<= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-                    constexpr int UW = K < 32 ? NW : UU;
-                    if (K >= 32 || lane < K) red2[K < 32 ? warp : u][p] = t;
-                    __syncthreads();
-                    if (tid < K) {
-                        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int off = K; off < 32; off <<= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+                constexpr int UW = K < 32 ? NW : UU;
+                if (K >= 32 || lane < K) red2[K < 32 ? warp : u][p] = t;
+                __syncthreads();
+                if (tid < K) {
+                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                        for (int v = 0; v < UW; v++) s4[v & 3] += red2[v][tid];
-                        s_sh[tid] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-                    }
-                } else {
-                    red2[u][p] = t;
-                    __syncthreads();
-                    if (tid < K) {
-                        double sj = 0.0;
-                        for (int v = 0; v < UU; v++) sj += red2[v][tid];
-                        s_sh[tid] = sj;
-                    }
+                    for (int v = 0; v < UW; v++) s4[v & 3] += red2[v][tid];
+                    s_sh[tid] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                 }
             }
             RES_T(3);

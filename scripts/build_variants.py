@@ -27,10 +27,6 @@ VARIANTS = {
     "r4": ["CHEB_RPG=4"],
     "checked": ["CHEB_CHECKS=1"],
     "resprof": ["CHEB_RES_PROF=1"],
-    "respf": ["CHEB_RES_PF=1"],  # resident flat grid: L1 prefetch one row iteration ahead
-    "ress2": ["CHEB_RES_S2=1"],  # resident flat grid: shuffle / interleaved second level of s_j
-    "respfs2": ["CHEB_RES_PF=1", "CHEB_RES_S2=1"],
-    "resprof_pfs2": ["CHEB_RES_PROF=1", "CHEB_RES_PF=1", "CHEB_RES_S2=1"],
     "nocv": ["CHEB_CV_KERNEL=0"],  # step kernels without the compressed-copy path (A/B)
     "resdiag1": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=1"],  # timing diagnostics: wrong results
     "resdiag2": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=2"],  # per-CTA phase cycles of the resident kernel (scripts/res_phases.py)
