@@ -1791,8 +1791,11 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
         const uint32_t wo_s = smem_u32(Wo);
         // one row: gathers (own rows: ld.shared; cluster peers: ld.shared::cluster at the mapa'd
         // address; other clusters: the exported global copy), rank-1 term, recurrence, dots
-        auto rows = [&](auto staged) {
+        auto rows = [&](auto staged, auto geo) {
             constexpr bool STAGED = decltype(staged)::value;
+            // the row loop is specialised on the geometry -- 1: flat grid (own rows or the exported
+            // global copy), 2: one cluster (own rows or a peer's over DSMEM)
+            constexpr int GEO = decltype(geo)::value;
             for (int lr = grp; lr < nr; lr += GR) {
                 const int lo = rp_s[lr], hi = rp_s[lr + 1];
                 CHEB_ASSERT(lo <= hi && (hi - lo) % U == 0 && (!STAGED || hi <= ra.cap));
@@ -1814,17 +1817,18 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
                             x[q][0] = x[q][NSL - 1] = make_double2(v[q], 0.0);
                         } else if (CHEB_RES_DIAG == 2) {  // timing diagnostic: every gather from the own row
                             for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(wo_s + (lr * RS + pp[sl]) * 8);
-                        } else if (c[q] >= 0) {
+                        } else if (GEO != 2 && c[q] >= 0) {
                             CHEB_ASSERT(!single && (int64_t)c[q] < a.d);
                             const double* p = go + (size_t)c[q] * K;
 #pragma unroll
                             for (int sl = 0; sl < NSL; sl++) x[q][sl] = ldca2(p + pp[sl]);
                         } else {
+                            CHEB_ASSERT(c[q] < 0);  // one cluster: every column is a cluster row
                             const uint32_t e = (uint32_t)(-1 - c[q]);
                             const uint32_t rk = e >> 16;
                             CHEB_ASSERT((int)rk < RG && (int)(e & 0xFFFFu) < ra.nr);
                             const uint32_t ad = wo_s + (e & 0xFFFFu) * (RS * 8);
-                            if (rk == (uint32_t)crank) {
+                            if (GEO == 1 || rk == (uint32_t)crank) {
 #pragma unroll
                                 for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(ad + pp[sl] * 8);
                             } else {
@@ -1880,8 +1884,15 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
                 }
             }
         };
-        if (fit) rows(std::true_type{});
-        else rows(std::false_type{});
+        using IC1 = std::integral_constant<int, 1>;
+        using IC2 = std::integral_constant<int, 2>;
+        if (single) {
+            if (fit) rows(std::true_type{}, IC2{});
+            else rows(std::false_type{}, IC2{});
+        } else {
+            if (fit) rows(std::true_type{}, IC1{});
+            else rows(std::false_type{}, IC1{});
+        }
         // ---- per-CTA partial: lanes of a warp -> warps in ascending order
 #pragma unroll
         for (int off = L; off < 32; off <<= 1)
