@@ -27,6 +27,7 @@ VARIANTS = {
     "r4": ["CHEB_RPG=4"],
     "checked": ["CHEB_CHECKS=1"],
     "resprof": ["CHEB_RES_PROF=1"],
+    "rest640": ["CHEB_RES_THREADS=640"],  # resident kernel: 20 warps per SM at 96 registers
     "nocv": ["CHEB_CV_KERNEL=0"],  # step kernels without the compressed-copy path (A/B)
     "resdiag1": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=1"],  # timing diagnostics: wrong results
     "resdiag2": ["CHEB_RES_PROF=1", "CHEB_RES_DIAG=2"],  # per-CTA phase cycles of the resident kernel (scripts/res_phases.py)

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--cases", default="torus256,gmrf32")
     ap.add_argument("--ks", default="16,32,64")
     ap.add_argument("--scheds", default="resident,persistent,per_step")
+    ap.add_argument("--doubling", action="store_true", help="also time moment doubling (G25) on each schedule")
     args = ap.parse_args()
     flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
     for name in args.cases.split(","):
@@ -51,16 +52,19 @@ def main():
         op = P.Operator(wl.mode, dA, None, wl.r1_c)
         for k in [int(x) for x in args.ks.split(",")]:
             mus = {}
-            for sname in args.scheds.split(","):
+            for sname, dbl in [(x, d) for d in ([False, True] if args.doubling else [False])
+                               for x in args.scheds.split(",")]:
                 pers, res = SCHED[sname]
                 P.set_persistent(pers)
                 P.set_resident(res)
+                P.set_doubling(dbl)
                 est = P.Estimator(op, wl.a, wl.b, wl.degree, wl.num_probes, k, seed=wl.seed)
                 ms, mu = t_est(est, args.reps, flush)
+                P.set_doubling(False)
                 mus[sname] = mu
                 ref = mus[args.scheds.split(",")[0]]
                 diff = float(np.abs(mu - ref).max() / max(1.0, np.abs(ref).max()))
-                print(json.dumps({"workload": name, "k": k, "schedule": sname, "m": wl.num_probes, "n": wl.degree,
+                print(json.dumps({"workload": name, "k": k, "schedule": sname + ("+doubling" if dbl else ""), "m": wl.num_probes, "n": wl.degree,
                                   "ms": round(ms, 4), "us_per_step": round(1e3 * ms / wl.degree / -(-wl.num_probes // k), 3),
                                   "probe_steps_per_s": wl.num_probes * wl.degree / ms * 1e3,
                                   "max_rel_diff_vs_first": diff}), flush=True)
