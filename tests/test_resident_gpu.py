@@ -100,7 +100,7 @@ def test_resident_cluster_sizes(orc, env, rg, name, k):
 
 # the flat grid (the single-cluster shortcut disabled)
 @pytest.mark.parametrize("name,k", [("gmrf_s", 16), ("torus_s", 32), ("gmrf32", 64), ("spd_csr", 16),
-                                    ("torus_s", 8), ("gmrf_s", 64)])
+                                    ("torus_s", 8), ("gmrf_s", 64), ("torus_s", 16), ("torus_s", 64)])
 def test_resident_flat_grid(orc, env, name, k):
     env(CHEB_RES_SINGLE_MAX=0)
     wl, r, sched, mu, g, gp, se = _run(orc, name, k)
