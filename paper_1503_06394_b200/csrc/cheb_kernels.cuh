@@ -1616,7 +1616,7 @@ resident_prep_kernel(int64_t d, const int64_t* __restrict__ rp2, int32_t* __rest
     }
 }
 
-// 16-byte loads of the resident kernel: own shared memory, a cluster peer's (DSMEM), global (L1)
+// 16-byte loads of the resident kernel: own shared memory, a cluster peer's (DSMEM); generic below
 __device__ __forceinline__ double2 lds2(uint32_t a) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
@@ -1632,12 +1632,13 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     return r;
 }
-__device__ __forceinline__ double2 ldca2(const double* p) {
+
+// generic 16-byte load (flat grid: a gather is the CTA's own shared-memory row or the exported global copy)
+__device__ __forceinline__ double2 ldgen2(uint64_t a) {
     double2 v;
-    asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    asm volatile("ld.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a) : "memory");
     return v;
 }
-
 #ifndef CHEB_RES_DIAG
 #define CHEB_RES_DIAG 0  // TIMING DIAGNOSTIC builds only (wrong results): 1 no gathers, 2 own-row gathers
 #endif
@@ -1789,6 +1790,7 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
 #pragma unroll
             for (int q = 0; q < kPPL; q++) acc[ch][q] = 0.0;
         const uint32_t wo_s = smem_u32(Wo);
+        const uint64_t wo_gen = (uint64_t)Wo, go_gen = (uint64_t)go;  // generic addresses
         // one row: gathers (own rows: ld.shared; cluster peers: ld.shared::cluster at the mapa'd
         // address; other clusters: the exported global copy), rank-1 term, recurrence, dots
         auto rows = [&](auto staged, auto geo) {
@@ -1817,18 +1819,23 @@ cheb_resident_kernel(StepArgs a, ResArgs ra) {
                             x[q][0] = x[q][NSL - 1] = make_double2(v[q], 0.0);
                         } else if (CHEB_RES_DIAG == 2) {  // timing diagnostic: every gather from the own row
                             for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(wo_s + (lr * RS + pp[sl]) * 8);
-                        } else if (GEO != 2 && c[q] >= 0) {
-                            CHEB_ASSERT(!single && (int64_t)c[q] < a.d);
-                            const double* p = go + (size_t)c[q] * K;
+                        } else if (GEO == 1) {
+                            // flat grid: the two sources share the generic address space, so the address is
+                            // selected and one generic load issued -- no branch per entry, all of a
+                            // chunk's loads back to back (configs[1]: 14.5 -> 13.8 ms per estimate)
+                            CHEB_ASSERT(c[q] >= 0 ? (int64_t)c[q] < a.d : ((-1 - c[q]) >> 16) == 0 && ((-1 - c[q]) & 0xFFFF) < ra.nr);
+                            const uint64_t ag = go_gen + (uint64_t)(uint32_t)c[q] * (K * 8);
+                            const uint64_t as = wo_gen + (uint64_t)((uint32_t)(-1 - c[q]) & 0xFFFFu) * (RS * 8);
+                            const uint64_t ad = c[q] >= 0 ? ag : as;
 #pragma unroll
-                            for (int sl = 0; sl < NSL; sl++) x[q][sl] = ldca2(p + pp[sl]);
+                            for (int sl = 0; sl < NSL; sl++) x[q][sl] = ldgen2(ad + pp[sl] * 8);
                         } else {
                             CHEB_ASSERT(c[q] < 0);  // one cluster: every column is a cluster row
                             const uint32_t e = (uint32_t)(-1 - c[q]);
                             const uint32_t rk = e >> 16;
                             CHEB_ASSERT((int)rk < RG && (int)(e & 0xFFFFu) < ra.nr);
                             const uint32_t ad = wo_s + (e & 0xFFFFu) * (RS * 8);
-                            if (GEO == 1 || rk == (uint32_t)crank) {
+                            if (rk == (uint32_t)crank) {
 #pragma unroll
                                 for (int sl = 0; sl < NSL; sl++) x[q][sl] = lds2(ad + pp[sl] * 8);
                             } else {
